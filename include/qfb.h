@@ -1,0 +1,308 @@
+/*
+ * qfb.h — C-ABI of the B200-native fused fake-quantization path ("qfb").
+ *
+ * This is the drop-in boundary for the DPVO-QAT++ accelerator path
+ * (arxiv 2511.12653). Every entry point replaces one operator of the
+ * reference library `quantfuse` (namespace qf, /root/reference/proj); the
+ * reference interface each one replaces is cited as file:line (paths relative
+ * to proj/include/quantfuse/).
+ *
+ * Conventions
+ *  - Plain C types only: pointers, sizes, enums, POD structs. No torch types.
+ *  - Every function returns qfb_status; on failure qfb_last_error() holds a
+ *    thread-local message. Status codes mirror the reference exception
+ *    taxonomy (errors.hpp:11-33, exec.hpp:51-53).
+ *  - Device entry points (qfb_fq_*, qfb_int8_codes, qfb_fill_*) take DEVICE
+ *    pointers, validate arguments on the host before anything is enqueued
+ *    (validation-before-compute, as in quant.hpp:124-157), then enqueue
+ *    asynchronously on the context's stream. They never allocate on the hot
+ *    path except to grow the context workspace. Device-detected conditions
+ *    (non-finite values where the reference throws NonFiniteError) are
+ *    latched in the context and reported by qfb_ctx_sync().
+ *  - Host entry points (*_host) mirror the reference's value-semantics API:
+ *    host buffers in, host buffers out, synchronous, all copies inside.
+ *  - Layout: every tensor is viewed as [outer, channels, inner] row-major.
+ *    Element i uses scale index (i / inner) % channels. Per-tensor scale is
+ *    channels == 1. The reference's per-channel axis-0 form
+ *    (quant.hpp:150-170, [C_out, per]) is outer=1, channels=C_out,
+ *    inner=per; a batch of CHW frames with per-channel activation scales is
+ *    outer=frames, channels=C, inner=H*W.
+ *  - A context is externally single-threaded (exec.hpp:180-181); distinct
+ *    contexts may be used from distinct threads.
+ */
+#ifndef QFB_H_
+#define QFB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QFB_VERSION_MAJOR 0
+#define QFB_VERSION_MINOR 1
+
+/* ---------------------------------------------------------------------- */
+/* Status codes: errors.hpp:11-33 (ShapeError, ValueError, IoError,        */
+/* NonFiniteError, InsufficientMatchesError) + exec.hpp:51 FusedPathError. */
+/* ---------------------------------------------------------------------- */
+typedef enum qfb_status {
+  QFB_OK = 0,
+  QFB_ERR_SHAPE = 1,          /* qf::ShapeError               errors.hpp:11 */
+  QFB_ERR_VALUE = 2,          /* qf::ValueError               errors.hpp:16 */
+  QFB_ERR_IO = 3,             /* qf::IoError                  errors.hpp:21 */
+  QFB_ERR_NONFINITE = 4,      /* qf::NonFiniteError           errors.hpp:26 */
+  QFB_ERR_INSUFFICIENT = 5,   /* qf::InsufficientMatchesError errors.hpp:31 */
+  QFB_ERR_FUSED_PATH = 6,     /* qf::FusedPathError           exec.hpp:51   */
+  QFB_ERR_CUDA = 7,           /* CUDA runtime / launch failure              */
+  QFB_ERR_NCCL = 8,           /* collective failure                         */
+  QFB_ERR_UNSUPPORTED = 9     /* argument combination not supported         */
+} qfb_status;
+
+/* Thread-local message of the last failing call on this thread. */
+const char* qfb_last_error(void);
+const char* qfb_status_name(qfb_status s);
+/* Library build string (arch, version). */
+const char* qfb_build_info(void);
+
+/* Storage type of device tensors. */
+typedef enum qfb_dtype {
+  QFB_F32 = 0, /* float32 storage                                        */
+  QFB_F16 = 1  /* IEEE binary16 storage (the reference's EmulatedHalf     */
+               /* values are exactly these, tensor.hpp:25, half.hpp:1-5) */
+} qfb_dtype;
+
+/* qf::Precision (tensor.hpp:23). Selects the activation scale lower bound
+ * (quant.hpp:45-47) and, for float32 storage, whether results are re-rounded
+ * onto the binary16 grid (quant.hpp:141-143). */
+typedef enum qfb_precision {
+  QFB_PREC_FULL = 0,
+  QFB_PREC_HALF = 1
+} qfb_precision;
+
+/* Kernel flags. */
+#define QFB_FLAG_HALF_GRID 0x1u /* f32 storage: round outputs to binary16 */
+                                /* grid (round_to_half, half.hpp:72-82)   */
+#define QFB_FLAG_STREAMING 0x2u /* evict-first loads/stores (data >> L2)  */
+
+/* ---------------------------------------------------------------------- */
+/* Quantization config: qf::QuantConfig (quant.hpp:35-61).                */
+/* ---------------------------------------------------------------------- */
+typedef struct qfb_quant_config {
+  int32_t bits;       /* default 8 -> q_max 127                          */
+  int32_t reserved;
+  double s_min;       /* 1e-6, Full path lower clamp                     */
+  double s_min_half;  /* 1e-4, FP16 path lower clamp                     */
+  double s_max;       /* 64                                              */
+  double eps;         /* 1e-8                                            */
+} qfb_quant_config;
+
+void qfb_quant_config_default(qfb_quant_config* cfg);          /* quant.hpp:35-43 */
+qfb_status qfb_quant_config_validate(const qfb_quant_config*); /* quant.hpp:49-60 */
+int32_t qfb_q_max(const qfb_quant_config* cfg);                /* quant.hpp:45    */
+
+/* ---------------------------------------------------------------------- */
+/* Host scale math — computed with the host libm so the resolved scales are */
+/* bit-identical to the reference on the same machine.                     */
+/* ---------------------------------------------------------------------- */
+double qfb_softplus(double x);                           /* quant.hpp:71-75 */
+double qfb_sigmoid(double x);                            /* quant.hpp:77-84 */
+qfb_status qfb_softplus_inv(double y, double* out);      /* quant.hpp:87-91 */
+/* s = clip(softplus(log_s)+eps, s_min_for(prec), s_max); quant.hpp:95-109.
+ * Non-finite log_s -> QFB_ERR_NONFINITE. */
+qfb_status qfb_resolve_scales(const double* log_s, int64_t n,
+                              const qfb_quant_config* cfg, qfb_precision prec,
+                              double* s_out);
+/* Backward factors per scale: s (double, quant.hpp:241/281) and
+ * chain = clamped ? 0 : sigmoid(log_s) (quant.hpp:242-244, 282-284). */
+qfb_status qfb_scale_grad_factors(const double* log_s, int64_t n,
+                                  const qfb_quant_config* cfg,
+                                  qfb_precision prec, double* s_out,
+                                  double* chain_out);
+/* Forward scale contract: reject s <= 0 (ValueError, quant.hpp:124-129) and
+ * cast to float (quant.hpp:138, 162; exec.hpp:250-254). */
+qfb_status qfb_cast_scales_f32(const double* s, int64_t n, float* out);
+
+/* ---------------------------------------------------------------------- */
+/* Context: one per (device, stream); owns the reduction workspace and the */
+/* device status latch.                                                     */
+/* ---------------------------------------------------------------------- */
+typedef struct qfb_ctx qfb_ctx;
+
+/* stream: a cudaStream_t (NULL = the legacy default stream). */
+qfb_status qfb_ctx_create(int32_t device, void* stream, qfb_ctx** out);
+qfb_status qfb_ctx_destroy(qfb_ctx* ctx);
+qfb_status qfb_ctx_set_stream(qfb_ctx* ctx, void* stream);
+void* qfb_ctx_stream(qfb_ctx* ctx);
+int32_t qfb_ctx_sm_count(qfb_ctx* ctx);
+/* Synchronize the stream; report (and clear) latched device conditions.
+ * Returns QFB_ERR_NONFINITE if a kernel saw a non-finite value where the
+ * reference throws (demote_half, tensor.hpp:160). */
+qfb_status qfb_ctx_sync(qfb_ctx* ctx);
+/* Number of kernels this context has launched (for launch accounting). */
+int64_t qfb_ctx_launch_count(qfb_ctx* ctx);
+
+/* ---------------------------------------------------------------------- */
+/* Device operators (async on the context stream, device pointers).        */
+/* ---------------------------------------------------------------------- */
+
+/* Fake-quant forward, y = s*rint(clip(x/s, -q, q)) in float32 with IEEE
+ * division, round-half-even, NaN-propagating clip and signed zero.
+ * Replaces qf::fake_quantize per-tensor (quant.hpp:136-146) and per-channel
+ * (quant.hpp:150-170), scalar kernel quant.hpp:114-121.
+ * scale: device float[channels] (already cast, see qfb_cast_scales_f32).
+ * x == y (in place) is allowed. */
+qfb_status qfb_fq_fwd(qfb_ctx* ctx, qfb_dtype dtype, const void* x, void* y,
+                      int64_t outer, int64_t channels, int64_t inner,
+                      const float* scale, int32_t q_max, uint32_t flags);
+
+/* Integer image: codes = (int8)rint(clip(x/s)). qf::int8_codes
+ * (quant.hpp:174-207). NaN -> 0. */
+qfb_status qfb_int8_codes(qfb_ctx* ctx, qfb_dtype dtype, const void* x,
+                          int8_t* codes, int64_t outer, int64_t channels,
+                          int64_t inner, const float* scale, int32_t q_max);
+
+/* STE/LSQ backward with the reference's fixed pairwise reduction tree
+ * (tensor.hpp:100-109) reproduced exactly on the device.
+ * Replaces qf::fake_quantize_backward per-tensor (quant.hpp:233-257) and
+ * per-channel (quant.hpp:261-294).
+ *  dx (nullable, frozen weights, frontend.hpp:221-225): mask * up.
+ *  scale64 / chain: device double[channels] from qfb_scale_grad_factors.
+ *  d_log_s: device double[channels]. Row (o,c) yields
+ *    r[o][c] = pairwise_sum(d_ds * up over the row) * chain[c].
+ *  accumulate == 0: d_log_s[c] = ((r[0][c] + r[1][c]) + ...)
+ *  accumulate != 0: d_log_s[c] = ((d_log_s[c] + r[0][c]) + r[1][c]) + ...
+ *    (the trainer's `g += grad` accumulation, frontend.hpp:222-228). */
+qfb_status qfb_fq_bwd(qfb_ctx* ctx, qfb_dtype dtype, const void* x,
+                      const void* up, void* dx, int64_t outer,
+                      int64_t channels, int64_t inner, const double* scale64,
+                      const double* chain, int32_t q_max, double* d_log_s,
+                      int32_t accumulate);
+
+/* Activation applied inside a fused chain. */
+typedef enum qfb_act {
+  QFB_ACT_NONE = 0,
+  QFB_ACT_RELU = 1, /* v > 0 ? v : 0, tensor.hpp:147-151               */
+  QFB_ACT_GELU = 2  /* portable tanh-GELU, include/qfb_portable.h      */
+} qfb_act;
+
+#define QFB_MAX_CHAIN_OUT 2
+
+/* Fused quant->act->quant chain over one tensor (one HBM pass):
+ *   v = a (+ b); v = act(v); if half: v = demote(v) (non-finite latched,
+ *   tensor.hpp:159-170); preact = v (optional);
+ *   y[k] = FQ(v, scale[k]) (+ half re-round) for k < n_out.
+ * Semantics: the residual joins maybe_half(relu(add(a,b))) of
+ * exec.hpp:438,443,447 followed by the next layers' fused activation
+ * sweep exec.hpp:353-361, including multi-consumer points exec.hpp:440-451. */
+typedef struct qfb_chain_desc {
+  const void* a;
+  const void* b;         /* nullable */
+  void* preact;          /* nullable */
+  void* y[QFB_MAX_CHAIN_OUT];
+  const float* scale[QFB_MAX_CHAIN_OUT]; /* device float[channels] each */
+  int64_t outer, channels, inner;
+  int32_t n_out;         /* 0..2 */
+  int32_t act;           /* qfb_act */
+  int32_t dtype;         /* qfb_dtype */
+  int32_t q_max;
+  uint32_t flags;        /* QFB_FLAG_* */
+  uint32_t reserved;
+} qfb_chain_desc;
+
+qfb_status qfb_fq_chain(qfb_ctx* ctx, const qfb_chain_desc* desc);
+
+/* Batched launches: one kernel over a table of quant points (all the
+ * activation quant points of a frame or window). The table is passed by
+ * value in kernel parameters, so calls are CUDA-graph capturable. */
+typedef struct qfb_fq_desc {
+  const void* x;
+  void* y[QFB_MAX_CHAIN_OUT];            /* y[1] used when n_out == 2 */
+  const float* scale[QFB_MAX_CHAIN_OUT];
+  int64_t outer, channels, inner;
+  int32_t n_out;   /* 1 or 2 (multi-consumer quant point, one read of x) */
+  int32_t q_max;
+  uint32_t flags;
+  uint32_t reserved;
+} qfb_fq_desc;
+
+qfb_status qfb_fq_fwd_multi(qfb_ctx* ctx, qfb_dtype dtype,
+                            const qfb_fq_desc* table, int32_t n);
+
+typedef struct qfb_bwd_desc {
+  const void* x;
+  const void* up;
+  void* dx;                 /* nullable */
+  const double* scale64;
+  const double* chain;
+  double* d_log_s;
+  int64_t outer, channels, inner;
+  int32_t q_max;
+  int32_t accumulate;
+} qfb_bwd_desc;
+
+qfb_status qfb_fq_bwd_multi(qfb_ctx* ctx, qfb_dtype dtype,
+                            const qfb_bwd_desc* table, int32_t n);
+
+qfb_status qfb_fq_chain_multi(qfb_ctx* ctx, const qfb_chain_desc* table,
+                              int32_t n);
+
+/* Device-side scale resolution (the paper's scale kernel):
+ * CUDA libm, may differ from the host libm by <= 1-2 ulp in double.
+ * Any output pointer may be NULL. Non-finite log_s is latched
+ * (QFB_ERR_NONFINITE at qfb_ctx_sync). */
+qfb_status qfb_resolve_scales_dev(qfb_ctx* ctx, const double* log_s,
+                                  int64_t n, const qfb_quant_config* cfg,
+                                  qfb_precision prec, float* s32,
+                                  double* s64, double* chain);
+
+/* Synthetic input generation on the device with the reference counter RNG
+ * (rng.hpp:24-50), so host and device see identical bytes without H2D:
+ * out[i] = (dtype)(lo + (hi - lo) * uniform(i))   (kind 0)
+ * out[i] = (dtype)(scale * normal(i))              (kind 1; lo = scale)
+ * with index i + index_offset. */
+qfb_status qfb_fill_rng(qfb_ctx* ctx, qfb_dtype dtype, void* out, int64_t n,
+                        uint64_t seed, uint64_t stream, uint64_t index_offset,
+                        int32_t kind, double lo, double hi);
+
+/* ---------------------------------------------------------------------- */
+/* Per-operator plan (ablation + fused-path fallback), exec.hpp:276-342:   */
+/* four sweeps divide -> clip -> round -> multiply with materialized       */
+/* float temporaries (z, c, r), bit-identical to the fused sweep.          */
+/* tmp: device float[3 * numel] scratch.                                   */
+/* ---------------------------------------------------------------------- */
+qfb_status qfb_fq_fwd_perop(qfb_ctx* ctx, qfb_dtype dtype, const void* x,
+                            void* y, int64_t outer, int64_t channels,
+                            int64_t inner, const float* scale, int32_t q_max,
+                            uint32_t flags, float* tmp);
+
+/* ---------------------------------------------------------------------- */
+/* Host-level operators with reference value semantics (quant.hpp).        */
+/* Float32 host buffers; prec == QFB_PREC_HALF means the input is an       */
+/* EmulatedHalf tensor (values on the binary16 grid) and the output is     */
+/* re-rounded onto that grid; a non-finite result -> QFB_ERR_NONFINITE as  */
+/* demote_half would throw (tensor.hpp:160). Synchronous.                  */
+/* ---------------------------------------------------------------------- */
+/* s: host double[channels] (validated > 0 and cast to float). */
+qfb_status qfb_fake_quantize_host(qfb_ctx* ctx, qfb_precision prec,
+                                  const float* x, float* y, int64_t outer,
+                                  int64_t channels, int64_t inner,
+                                  const double* s,
+                                  const qfb_quant_config* cfg);
+qfb_status qfb_int8_codes_host(qfb_ctx* ctx, const float* x, int8_t* codes,
+                               int64_t outer, int64_t channels, int64_t inner,
+                               const double* s, const qfb_quant_config* cfg);
+/* log_s: host double[channels]; d_log_s: host double[channels] (written,
+ * or accumulated into when accumulate != 0); dx nullable. */
+qfb_status qfb_fake_quantize_backward_host(
+    qfb_ctx* ctx, qfb_precision prec, const float* x, const float* up,
+    float* dx, int64_t outer, int64_t channels, int64_t inner,
+    const double* log_s, const qfb_quant_config* cfg, double* d_log_s,
+    int32_t accumulate);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* QFB_H_ */

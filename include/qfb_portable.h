@@ -1,0 +1,93 @@
+/*
+ * qfb_portable.h — arithmetic that must give identical bits on the host
+ * (gcc, x86-64, -ffp-contract=off) and on the device (nvcc, sm_100a).
+ *
+ * Only IEEE-754 basic operations with round-to-nearest-even are used (add,
+ * mul, div, fma, rint), each spelled through a macro that maps to the
+ * correctly rounded intrinsic on the device and to the plain operator /
+ * libm fmaf on the host. No libm transcendental is called, so the result
+ * does not depend on either side's libm.
+ *
+ * GELU: the reference has no GELU (parity unpinned). This
+ * header DEFINES the GELU of the fused chain (tanh form,
+ * 0.5*x*(1+tanh(sqrt(2/pi)*(x+0.044715*x^3)))) with a portable expf, and the
+ * CPU oracle includes this same header, so oracle and kernel agree bitwise
+ * by construction. It is the only code shared by oracle and product.
+ */
+#ifndef QFB_PORTABLE_H_
+#define QFB_PORTABLE_H_
+
+#include <stdint.h>
+
+#if defined(__CUDACC__)
+#define QFB_HD __host__ __device__ __forceinline__
+#else
+#define QFB_HD static inline
+#include <math.h>
+#include <string.h>
+#endif
+
+#if defined(__CUDA_ARCH__)
+#define QFB_P_ADD(a, b) __fadd_rn((a), (b))
+#define QFB_P_MUL(a, b) __fmul_rn((a), (b))
+#define QFB_P_DIV(a, b) __fdiv_rn((a), (b))
+#define QFB_P_FMA(a, b, c) __fmaf_rn((a), (b), (c))
+#define QFB_P_RINT(a) rintf(a)
+#define QFB_P_AS_FLOAT(u) __uint_as_float(u)
+#else
+#define QFB_P_ADD(a, b) ((a) + (b))
+#define QFB_P_MUL(a, b) ((a) * (b))
+#define QFB_P_DIV(a, b) ((a) / (b))
+#define QFB_P_FMA(a, b, c) fmaf((a), (b), (c))
+#define QFB_P_RINT(a) rintf(a)
+QFB_HD float qfb_p_as_float_(uint32_t u) {
+  float f;
+  memcpy(&f, &u, sizeof f);
+  return f;
+}
+#define QFB_P_AS_FLOAT(u) qfb_p_as_float_(u)
+#endif
+
+/* 2^j for j in [-126, 127], built from the exponent field. */
+QFB_HD float qfb_p_exp2i(int32_t j) {
+  return QFB_P_AS_FLOAT((uint32_t)(j + 127) << 23);
+}
+
+/* e^x, < 2 ulp, deterministic: Cody-Waite reduction + degree-7 Taylor/Horner
+ * on |r| <= ln2/2, exponent applied in two exact-range steps. */
+QFB_HD float qfb_p_expf(float x) {
+  if (!(x == x)) return QFB_P_ADD(x, x); /* NaN */
+  if (x > 88.72283935546875f) return QFB_P_AS_FLOAT(0x7f800000u);
+  if (x < -103.97208404541015625f) return 0.0f;
+  const float kf = QFB_P_RINT(QFB_P_MUL(x, 1.44269502162933349609375f));
+  float r = QFB_P_FMA(kf, -0.693145751953125f, x);      /* ln2 hi (exact k*hi) */
+  r = QFB_P_FMA(kf, -1.428606765330187045e-06f, r);     /* ln2 lo */
+  float p = 1.98412701e-4f;                              /* 1/5040 */
+  p = QFB_P_FMA(p, r, 1.38888892e-3f);                   /* 1/720  */
+  p = QFB_P_FMA(p, r, 8.33333377e-3f);                   /* 1/120  */
+  p = QFB_P_FMA(p, r, 4.16666679e-2f);                   /* 1/24   */
+  p = QFB_P_FMA(p, r, 1.66666672e-1f);                   /* 1/6    */
+  p = QFB_P_FMA(p, r, 0.5f);
+  p = QFB_P_FMA(p, r, 1.0f);
+  p = QFB_P_FMA(p, r, 1.0f);
+  const int32_t k = (int32_t)kf;
+  const int32_t k1 = k >> 1; /* floor(k/2) */
+  const int32_t k2 = k - k1;
+  return QFB_P_MUL(QFB_P_MUL(p, qfb_p_exp2i(k1)), qfb_p_exp2i(k2));
+}
+
+/* tanh-form GELU. +-inf map to +inf / -0. */
+QFB_HD float qfb_p_gelu(float x) {
+  const float x3 = QFB_P_MUL(QFB_P_MUL(x, x), x);
+  const float u = QFB_P_MUL(0.7978845834732055664f, QFB_P_FMA(0.044715f, x3, x));
+  const float au = u < 0.0f ? -u : u;
+  const float e = qfb_p_expf(QFB_P_MUL(2.0f, au));
+  /* tanh(|u|) = 1 - 2/(e^{2|u|}+1) */
+  float t = QFB_P_ADD(1.0f, -QFB_P_DIV(2.0f, QFB_P_ADD(e, 1.0f)));
+  if (u < 0.0f) t = -t;
+  const float hx = QFB_P_MUL(0.5f, x);
+  if (x < -3.0e38f) return -0.0f; /* 0.5*(-inf)*0 would be NaN */
+  return QFB_P_MUL(hx, QFB_P_ADD(1.0f, t));
+}
+
+#endif /* QFB_PORTABLE_H_ */

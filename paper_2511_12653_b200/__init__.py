@@ -1,0 +1,505 @@
+"""paper_2511_12653_b200 — B200-native fused fake-quantization (qfb).
+
+Python mirror of the reference operator API (quantfuse, namespace ``qf``,
+/root/reference/proj/include/quantfuse/quant.hpp) on top of the C-ABI in
+``include/qfb.h``. Every call goes through ``libqfb.so`` (hand-written
+sm_100a kernels). There is no CPU or eager-PyTorch fallback: if the library
+is missing, importing this package raises.
+
+PyTorch is used only as plumbing: device memory (``torch.Tensor`` on
+``cuda``) and the current CUDA stream.
+
+Reference names kept: ``QuantConfig``, ``resolve_scale``, ``softplus``,
+``sigmoid``, ``softplus_inv``, ``fake_quantize``, ``int8_codes``,
+``fake_quantize_backward`` (returning ``FakeQuantGrad``), and the error
+taxonomy ``ShapeError``/``ValueError``/``IoError``/``NonFiniteError``/
+``FusedPathError`` (errors.hpp:11-33, exec.hpp:51).
+"""
+from __future__ import annotations
+
+import builtins
+import ctypes
+import dataclasses
+import os
+from typing import Optional, Sequence, Union
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libqfb.so")
+
+# ---------------------------------------------------------------- errors --
+
+
+class QfError(RuntimeError):
+    """Base of the qf error taxonomy."""
+
+
+class ShapeError(QfError):
+    """qf::ShapeError (errors.hpp:11)."""
+
+
+class ValueError(QfError, builtins.ValueError):  # noqa: A001 - mirrors qf::ValueError
+    """qf::ValueError (errors.hpp:16)."""
+
+
+class IoError(QfError):
+    """qf::IoError (errors.hpp:21)."""
+
+
+class NonFiniteError(QfError):
+    """qf::NonFiniteError (errors.hpp:26)."""
+
+
+class InsufficientMatchesError(QfError):
+    """qf::InsufficientMatchesError (errors.hpp:31)."""
+
+
+class FusedPathError(QfError):
+    """qf::FusedPathError (exec.hpp:51)."""
+
+
+class CudaError(QfError):
+    pass
+
+
+class NcclError(QfError):
+    pass
+
+
+class UnsupportedError(QfError):
+    pass
+
+
+_STATUS = {
+    1: ShapeError,
+    2: ValueError,
+    3: IoError,
+    4: NonFiniteError,
+    5: InsufficientMatchesError,
+    6: FusedPathError,
+    7: CudaError,
+    8: NcclError,
+    9: UnsupportedError,
+}
+
+F32, F16 = 0, 1
+PREC_FULL, PREC_HALF = 0, 1
+FLAG_HALF_GRID, FLAG_STREAMING = 0x1, 0x2
+ACT_NONE, ACT_RELU, ACT_GELU = 0, 1, 2
+
+# ------------------------------------------------------------ library --
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"libqfb.so not found at {LIB_PATH}: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+        " (there is no CPU fallback)")
+_lib = ctypes.CDLL(LIB_PATH)
+
+_vp = ctypes.c_void_p
+_i32 = ctypes.c_int32
+_u32 = ctypes.c_uint32
+_i64 = ctypes.c_int64
+_u64 = ctypes.c_uint64
+_dbl = ctypes.c_double
+_pd = ctypes.POINTER(ctypes.c_double)
+_pf = ctypes.POINTER(ctypes.c_float)
+
+
+class CQuantConfig(ctypes.Structure):
+    _fields_ = [("bits", _i32), ("reserved", _i32), ("s_min", _dbl), ("s_min_half", _dbl),
+                ("s_max", _dbl), ("eps", _dbl)]
+
+
+class CFqDesc(ctypes.Structure):
+    _fields_ = [("x", _vp), ("y", _vp * 2), ("scale", _vp * 2), ("outer", _i64),
+                ("channels", _i64), ("inner", _i64), ("n_out", _i32), ("q_max", _i32),
+                ("flags", _u32), ("reserved", _u32)]
+
+
+class CBwdDesc(ctypes.Structure):
+    _fields_ = [("x", _vp), ("up", _vp), ("dx", _vp), ("scale64", _vp), ("chain", _vp),
+                ("d_log_s", _vp), ("outer", _i64), ("channels", _i64), ("inner", _i64),
+                ("q_max", _i32), ("accumulate", _i32)]
+
+
+class CChainDesc(ctypes.Structure):
+    _fields_ = [("a", _vp), ("b", _vp), ("preact", _vp), ("y", _vp * 2), ("scale", _vp * 2),
+                ("outer", _i64), ("channels", _i64), ("inner", _i64), ("n_out", _i32),
+                ("act", _i32), ("dtype", _i32), ("q_max", _i32), ("flags", _u32),
+                ("reserved", _u32)]
+
+
+def _sig(name, res, args):
+    f = getattr(_lib, name)
+    f.restype = res
+    f.argtypes = args
+    return f
+
+
+_lib.qfb_last_error.restype = ctypes.c_char_p
+_lib.qfb_status_name.restype = ctypes.c_char_p
+_lib.qfb_build_info.restype = ctypes.c_char_p
+_sig("qfb_quant_config_default", None, [ctypes.POINTER(CQuantConfig)])
+_sig("qfb_quant_config_validate", _i32, [ctypes.POINTER(CQuantConfig)])
+_sig("qfb_q_max", _i32, [ctypes.POINTER(CQuantConfig)])
+_sig("qfb_softplus", _dbl, [_dbl])
+_sig("qfb_sigmoid", _dbl, [_dbl])
+_sig("qfb_softplus_inv", _i32, [_dbl, _pd])
+_sig("qfb_resolve_scales", _i32, [_pd, _i64, ctypes.POINTER(CQuantConfig), _i32, _pd])
+_sig("qfb_scale_grad_factors", _i32, [_pd, _i64, ctypes.POINTER(CQuantConfig), _i32, _pd, _pd])
+_sig("qfb_cast_scales_f32", _i32, [_pd, _i64, _pf])
+_sig("qfb_ctx_create", _i32, [_i32, _vp, ctypes.POINTER(_vp)])
+_sig("qfb_ctx_destroy", _i32, [_vp])
+_sig("qfb_ctx_set_stream", _i32, [_vp, _vp])
+_sig("qfb_ctx_stream", _vp, [_vp])
+_sig("qfb_ctx_sm_count", _i32, [_vp])
+_sig("qfb_ctx_sync", _i32, [_vp])
+_sig("qfb_ctx_launch_count", _i64, [_vp])
+_sig("qfb_fq_fwd", _i32, [_vp, _i32, _vp, _vp, _i64, _i64, _i64, _vp, _i32, _u32])
+_sig("qfb_int8_codes", _i32, [_vp, _i32, _vp, _vp, _i64, _i64, _i64, _vp, _i32])
+_sig("qfb_fq_bwd", _i32, [_vp, _i32, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _i32, _vp, _i32])
+_sig("qfb_fq_chain", _i32, [_vp, ctypes.POINTER(CChainDesc)])
+_sig("qfb_fq_chain_multi", _i32, [_vp, ctypes.POINTER(CChainDesc), _i32])
+_sig("qfb_fq_fwd_multi", _i32, [_vp, _i32, ctypes.POINTER(CFqDesc), _i32])
+_sig("qfb_fq_bwd_multi", _i32, [_vp, _i32, ctypes.POINTER(CBwdDesc), _i32])
+_sig("qfb_resolve_scales_dev", _i32, [_vp, _vp, _i64, ctypes.POINTER(CQuantConfig), _i32, _vp, _vp, _vp])
+_sig("qfb_fill_rng", _i32, [_vp, _i32, _vp, _i64, _u64, _u64, _u64, _i32, _dbl, _dbl])
+_sig("qfb_fq_fwd_perop", _i32, [_vp, _i32, _vp, _vp, _i64, _i64, _i64, _vp, _i32, _u32, _vp])
+_sig("qfb_fake_quantize_host", _i32, [_vp, _i32, _vp, _vp, _i64, _i64, _i64, _pd, ctypes.POINTER(CQuantConfig)])
+_sig("qfb_int8_codes_host", _i32, [_vp, _vp, _vp, _i64, _i64, _i64, _pd, ctypes.POINTER(CQuantConfig)])
+_sig("qfb_fake_quantize_backward_host", _i32, [_vp, _i32, _vp, _vp, _vp, _i64, _i64, _i64, _pd,
+                                                ctypes.POINTER(CQuantConfig), _pd, _i32])
+
+
+def lib() -> ctypes.CDLL:
+    """The loaded libqfb.so handle (raw C-ABI)."""
+    return _lib
+
+
+def check(status: int) -> None:
+    """Raise the qf exception mirroring a qfb_status."""
+    if status != 0:
+        msg = _lib.qfb_last_error().decode(errors="replace")
+        raise _STATUS.get(status, QfError)(msg)
+
+
+def build_info() -> str:
+    return _lib.qfb_build_info().decode()
+
+# ------------------------------------------------------------- config --
+
+
+@dataclasses.dataclass
+class QuantConfig:
+    """qf::QuantConfig (quant.hpp:35-61)."""
+    bits: int = 8
+    s_min: float = 1e-6
+    s_min_half: float = 1e-4
+    s_max: float = 64.0
+    eps: float = 1e-8
+
+    def q_max(self) -> int:
+        return (1 << (self.bits - 1)) - 1
+
+    def s_min_for(self, precision: int) -> float:
+        return self.s_min_half if precision == PREC_HALF else self.s_min
+
+    def to_c(self) -> CQuantConfig:
+        return CQuantConfig(self.bits, 0, self.s_min, self.s_min_half, self.s_max, self.eps)
+
+    def validate(self) -> None:
+        c = self.to_c()
+        check(_lib.qfb_quant_config_validate(ctypes.byref(c)))
+
+
+def _cfg(cfg: Optional[QuantConfig]) -> QuantConfig:
+    return cfg if cfg is not None else QuantConfig()
+
+
+def _darr(vals: Sequence[float]):
+    arr = (ctypes.c_double * max(len(vals), 1))(*vals)
+    return arr
+
+# ------------------------------------------------------ host scale math --
+
+
+def softplus(x: float) -> float:
+    return _lib.qfb_softplus(float(x))
+
+
+def sigmoid(x: float) -> float:
+    return _lib.qfb_sigmoid(float(x))
+
+
+def softplus_inv(y: float) -> float:
+    out = ctypes.c_double()
+    check(_lib.qfb_softplus_inv(float(y), ctypes.byref(out)))
+    return out.value
+
+
+def resolve_scale(log_s: Union[float, Sequence[float]], cfg: Optional[QuantConfig] = None,
+                  precision: int = PREC_FULL):
+    """quant.hpp:95-109. Scalar in -> float out; sequence in -> list out."""
+    scalar = not isinstance(log_s, (list, tuple)) and not hasattr(log_s, "__len__")
+    vals = [float(log_s)] if scalar else [float(v) for v in log_s]
+    c = _cfg(cfg).to_c()
+    out = _darr([0.0] * len(vals))
+    check(_lib.qfb_resolve_scales(_darr(vals), len(vals), ctypes.byref(c), precision, out))
+    res = [out[i] for i in range(len(vals))]
+    return res[0] if scalar else res
+
+
+def scale_grad_factors(log_s: Sequence[float], cfg: Optional[QuantConfig] = None,
+                       precision: int = PREC_FULL):
+    """(s, chain) per scale, quant.hpp:241-244 / 281-284."""
+    vals = [float(v) for v in log_s]
+    c = _cfg(cfg).to_c()
+    s = _darr([0.0] * len(vals))
+    ch = _darr([0.0] * len(vals))
+    check(_lib.qfb_scale_grad_factors(_darr(vals), len(vals), ctypes.byref(c), precision, s, ch))
+    return [s[i] for i in range(len(vals))], [ch[i] for i in range(len(vals))]
+
+
+def cast_scales_f32(s: Sequence[float]):
+    vals = [float(v) for v in s]
+    out = (ctypes.c_float * max(len(vals), 1))()
+    check(_lib.qfb_cast_scales_f32(_darr(vals), len(vals), out))
+    return [out[i] for i in range(len(vals))]
+
+# ------------------------------------------------------------- context --
+
+
+class Context:
+    """qfb_ctx: one per (device, stream). Externally single-threaded."""
+
+    def __init__(self, device: int = 0, stream: Optional[int] = None):
+        self.device = device
+        h = _vp()
+        check(_lib.qfb_ctx_create(device, _vp(stream or 0), ctypes.byref(h)))
+        self.handle = h
+
+    def set_stream(self, stream: Optional[int]) -> None:
+        check(_lib.qfb_ctx_set_stream(self.handle, _vp(stream or 0)))
+
+    def sync(self) -> None:
+        check(_lib.qfb_ctx_sync(self.handle))
+
+    @property
+    def launch_count(self) -> int:
+        return _lib.qfb_ctx_launch_count(self.handle)
+
+    @property
+    def sm_count(self) -> int:
+        return _lib.qfb_ctx_sm_count(self.handle)
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            _lib.qfb_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_CTX = {}
+
+
+def default_context(device: Optional[int] = None) -> Context:
+    """Per-device context bound to torch's current stream of that device."""
+    import torch
+    if device is None:
+        device = torch.cuda.current_device()
+    ctx = _CTX.get(device)
+    if ctx is None:
+        ctx = _CTX[device] = Context(device)
+    ctx.set_stream(torch.cuda.current_stream(device).cuda_stream)
+    return ctx
+
+# -------------------------------------------------- tensor-level ops --
+
+
+def _dtype_code(t) -> int:
+    import torch
+    if t.dtype == torch.float32:
+        return F32
+    if t.dtype == torch.float16:
+        return F16
+    raise ValueError(f"unsupported dtype {t.dtype} (float32 / float16 only)")
+
+
+def _layout(x, nscale: int, channel_axis: int):
+    """[outer, channels, inner] view of x for a scale vector of nscale."""
+    shape = list(x.shape)
+    if nscale == 1 and channel_axis is None:
+        return 1, 1, x.numel()
+    ax = 0 if channel_axis is None else channel_axis
+    if len(shape) == 0 or shape[ax] != nscale:
+        raise ShapeError(f"fake_quantize: per-channel scale length {nscale} != dim {ax} of {shape}")
+    outer = 1
+    for d in shape[:ax]:
+        outer *= d
+    inner = 1
+    for d in shape[ax + 1:]:
+        inner *= d
+    return outer, nscale, inner
+
+
+def _scale_list(s) -> list:
+    if isinstance(s, (list, tuple)):
+        return [float(v) for v in s]
+    if hasattr(s, "tolist") and not isinstance(s, float):
+        v = s.tolist()
+        return [float(a) for a in (v if isinstance(v, list) else [v])]
+    return [float(s)]
+
+
+def fake_quantize(x, s, cfg: Optional[QuantConfig] = None, precision: Optional[int] = None,
+                  channel_axis: Optional[int] = None, out=None, ctx: Optional[Context] = None):
+    """qf::fake_quantize (quant.hpp:136 per-tensor, :150 per-channel).
+
+    ``s``: a positive float (per-tensor) or a sequence of positive floats
+    (per-channel along ``channel_axis``, default axis 0 like the reference).
+    float16 tensors are EmulatedHalf; ``precision=PREC_HALF`` on a float32
+    tensor re-rounds the result onto the binary16 grid. A non-finite result
+    on the half path raises NonFiniteError (tensor.hpp:160).
+    """
+    import torch
+    cfg = _cfg(cfg)
+    svals = _scale_list(s)
+    per_channel = isinstance(s, (list, tuple)) or (hasattr(s, "__len__") and len(svals) != 1) \
+        or channel_axis is not None
+    sf = cast_scales_f32(svals)
+    outer, ch, inner = _layout(x, len(svals), channel_axis if per_channel else None)
+    if not x.is_cuda:
+        raise ValueError("fake_quantize: tensor must live on a CUDA device")
+    x = x.contiguous()
+    y = torch.empty_like(x) if out is None else out
+    ctx = ctx or default_context(x.device.index)
+    ds = torch.tensor(sf, dtype=torch.float32, device=x.device)
+    dt = _dtype_code(x)
+    half = dt == F16 or precision == PREC_HALF
+    flags = FLAG_HALF_GRID if (half and dt == F32) else 0
+    check(_lib.qfb_fq_fwd(ctx.handle, dt, _vp(x.data_ptr()), _vp(y.data_ptr()), outer, ch, inner,
+                          _vp(ds.data_ptr()), cfg.q_max(), flags))
+    if half:
+        ctx.sync()
+    return y
+
+
+def int8_codes(x, s, cfg: Optional[QuantConfig] = None, channel_axis: Optional[int] = None,
+               ctx: Optional[Context] = None):
+    """qf::int8_codes (quant.hpp:174-207)."""
+    import torch
+    cfg = _cfg(cfg)
+    svals = _scale_list(s)
+    per_channel = isinstance(s, (list, tuple)) or channel_axis is not None
+    sf = cast_scales_f32(svals)
+    outer, ch, inner = _layout(x, len(svals), channel_axis if per_channel else None)
+    x = x.contiguous()
+    codes = torch.empty(x.shape, dtype=torch.int8, device=x.device)
+    ctx = ctx or default_context(x.device.index)
+    ds = torch.tensor(sf, dtype=torch.float32, device=x.device)
+    check(_lib.qfb_int8_codes(ctx.handle, _dtype_code(x), _vp(x.data_ptr()), _vp(codes.data_ptr()),
+                              outer, ch, inner, _vp(ds.data_ptr()), cfg.q_max()))
+    return codes
+
+
+@dataclasses.dataclass
+class FakeQuantGrad:
+    """qf::FakeQuantGrad (quant.hpp:209-212)."""
+    d_input: object
+    d_log_scale: list
+
+
+def fake_quantize_backward(x, log_s, cfg: Optional[QuantConfig], upstream,
+                           precision: int = PREC_FULL, channel_axis: Optional[int] = None,
+                           need_d_input: bool = True, ctx: Optional[Context] = None):
+    """qf::fake_quantize_backward (quant.hpp:233 per-tensor, :261 per-channel).
+
+    Bit-identical to the reference: per-element terms in double and the
+    fixed pairwise reduction tree. With channel_axis > 0 (outer > 1 rows per
+    channel) the per-row results are accumulated in row order like the
+    trainer's ``g += grad`` (frontend.hpp:222-228).
+    """
+    import torch
+    cfg = _cfg(cfg)
+    if tuple(x.shape) != tuple(upstream.shape):
+        raise ShapeError(f"fake_quantize_backward: x {list(x.shape)} vs upstream {list(upstream.shape)}")
+    lvals = _scale_list(log_s)
+    per_channel = isinstance(log_s, (list, tuple)) or channel_axis is not None
+    outer, ch, inner = _layout(x, len(lvals), channel_axis if per_channel else None)
+    s64, chain = scale_grad_factors(lvals, cfg, precision)
+    dev = x.device
+    fac = torch.tensor(s64 + chain, dtype=torch.float64, device=dev)
+    dls = torch.zeros(ch, dtype=torch.float64, device=dev)
+    x = x.contiguous()
+    upstream = upstream.contiguous()
+    if upstream.dtype != x.dtype:
+        raise ValueError("fake_quantize_backward: x and upstream must share a dtype")
+    dx = torch.empty_like(x) if need_d_input else None
+    ctx = ctx or default_context(dev.index)
+    check(_lib.qfb_fq_bwd(ctx.handle, _dtype_code(x), _vp(x.data_ptr()), _vp(upstream.data_ptr()),
+                          _vp(dx.data_ptr() if dx is not None else 0), outer, ch, inner,
+                          _vp(fac.data_ptr()), _vp(fac.data_ptr() + 8 * ch), cfg.q_max(),
+                          _vp(dls.data_ptr()), 0))
+    return FakeQuantGrad(dx, dls.cpu().tolist())
+
+
+def fq_chain(a, b=None, scales=(), act: int = ACT_RELU, half: bool = False, preact: bool = False,
+             cfg: Optional[QuantConfig] = None, channel_axis: Optional[int] = None,
+             ctx: Optional[Context] = None):
+    """Fused maybe_half(act(a + b)) -> FQ x len(scales) (exec.hpp:438-451).
+
+    ``scales``: up to two entries, each a float (per-tensor) or a sequence
+    (per-channel along channel_axis). Returns (outputs, preact-or-None).
+    """
+    import torch
+    cfg = _cfg(cfg)
+    if len(scales) > 2:
+        raise ValueError("fq_chain: at most 2 outputs")
+    a = a.contiguous()
+    if b is not None:
+        if tuple(b.shape) != tuple(a.shape):
+            raise ShapeError(f"add: shape mismatch {list(a.shape)} vs {list(b.shape)}")
+        b = b.contiguous()
+    nscale = len(_scale_list(scales[0])) if scales else 1
+    per_channel = channel_axis is not None or (scales and isinstance(scales[0], (list, tuple)))
+    outer, ch, inner = _layout(a, nscale, channel_axis if per_channel else None)
+    ctx = ctx or default_context(a.device.index)
+    d = CChainDesc()
+    d.a = a.data_ptr()
+    d.b = b.data_ptr() if b is not None else None
+    pre = torch.empty_like(a) if preact else None
+    d.preact = pre.data_ptr() if pre is not None else None
+    outs, keep = [], []
+    for k, s in enumerate(scales):
+        sv = cast_scales_f32(_scale_list(s))
+        if len(sv) != ch:
+            raise ShapeError("fq_chain: scale vectors must have the same length")
+        ds = torch.tensor(sv, dtype=torch.float32, device=a.device)
+        keep.append(ds)
+        y = torch.empty_like(a)
+        outs.append(y)
+        d.y[k] = y.data_ptr()
+        d.scale[k] = ds.data_ptr()
+    d.outer, d.channels, d.inner = outer, ch, inner
+    d.n_out = len(scales)
+    d.act = act
+    d.dtype = _dtype_code(a)
+    d.q_max = cfg.q_max()
+    d.flags = FLAG_HALF_GRID if (half and d.dtype == F32) else 0
+    check(_lib.qfb_fq_chain(ctx.handle, ctypes.byref(d)))
+    if half or d.dtype == F16:
+        ctx.sync()
+    return outs, pre
+
+
+def fill_rng(t, seed: int, stream: int, kind: int = 1, lo: float = 1.0, hi: float = 0.0,
+             offset: int = 0, ctx: Optional[Context] = None):
+    """Counter-RNG synthetic data on the device (rng.hpp:24-50)."""
+    ctx = ctx or default_context(t.device.index)
+    check(_lib.qfb_fill_rng(ctx.handle, _dtype_code(t), _vp(t.data_ptr()), t.numel(), seed, stream,
+                            offset, kind, lo, hi))
+    return t

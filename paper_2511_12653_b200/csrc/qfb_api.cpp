@@ -1,0 +1,799 @@
+// qfb_api.cpp — the C-ABI (include/qfb.h): argument validation (before
+// anything is enqueued, like the reference's throw-before-compute),
+// host-side scale math with the host libm, the per-(device, stream)
+// context with its self-resetting reduction workspace, and launch planning
+// (vector/scalar path choice, descriptor tables, grid sizing).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/qfb.h"
+#include "qfb_kernels.h"
+
+using namespace qfb;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+qfb_status fail(qfb_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return st;
+}
+
+qfb_status cuda_fail(cudaError_t e, const char* where) {
+  return fail(QFB_ERR_CUDA, "%s: %s (%s)", where, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+#define QFB_CUDA(call)                                  \
+  do {                                                  \
+    cudaError_t e_ = (call);                            \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+  } while (0)
+
+// Scoped device switch so calls from any thread land on the ctx device.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// Device buffer that only grows.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace
+
+struct qfb_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int sm_count = 148;
+  int ew_blocks_per_sm = 4;
+  uint32_t* d_status = nullptr;
+  uint32_t* h_status = nullptr;  // pinned
+  DevBuf ws_f64;                 // partials / segment results
+  DevBuf ws_u32;                 // tickets (kept zero between launches)
+  DevBuf host_io[6];             // scratch for the *_host entry points
+  int64_t launches = 0;
+};
+
+namespace {
+
+qfb_status grow(qfb_ctx* ctx, DevBuf& b, size_t bytes, bool zero) {
+  if (b.bytes >= bytes) return QFB_OK;
+  size_t nb = std::max(bytes, b.bytes * 2);
+  nb = (nb + 255) & ~size_t(255);
+  if (b.p) {
+    // In-flight kernels may still read the old buffer.
+    QFB_CUDA(cudaStreamSynchronize(ctx->stream));
+    QFB_CUDA(cudaFree(b.p));
+    b.p = nullptr;
+    b.bytes = 0;
+  }
+  QFB_CUDA(cudaMalloc(&b.p, nb));
+  if (zero) QFB_CUDA(cudaMemsetAsync(b.p, 0, nb, ctx->stream));
+  b.bytes = nb;
+  return QFB_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+qfb_status check_ctx(qfb_ctx* ctx) {
+  if (!ctx) return fail(QFB_ERR_VALUE, "null qfb_ctx");
+  return QFB_OK;
+}
+
+// tensor.hpp:58-64: every dim must be positive.
+qfb_status check_dims(int64_t outer, int64_t channels, int64_t inner, const char* who) {
+  if (outer <= 0 || channels <= 0 || inner <= 0) {
+    return fail(QFB_ERR_SHAPE, "%s: non-positive dim in shape [%lld,%lld,%lld]", who,
+                (long long)outer, (long long)channels, (long long)inner);
+  }
+  if (outer > INT64_MAX / channels || outer * channels > INT64_MAX / inner) {
+    return fail(QFB_ERR_SHAPE, "%s: element count overflows", who);
+  }
+  return QFB_OK;
+}
+
+qfb_status check_dtype(int dtype) {
+  if (dtype != QFB_F32 && dtype != QFB_F16) return fail(QFB_ERR_VALUE, "unknown dtype %d", dtype);
+  return QFB_OK;
+}
+
+int elem_size(int dtype) { return dtype == QFB_F32 ? 4 : 2; }
+int per_vec(int dtype) { return dtype == QFB_F32 ? 4 : 8; }
+
+constexpr uint64_t kMaxUnits = 1ull << 31;
+
+// One logical elementwise job, before splitting into <2^31-unit pieces.
+struct EwJob {
+  const void* a;
+  const void* b;
+  void* preact;
+  void* y[2];
+  const float* s[2];
+  int64_t outer, channels, inner;
+  int n_out, act;
+  uint32_t flags;
+  float q;
+};
+
+// Split a job into descriptors: vector path when every pointer is 16-byte
+// aligned and a vector never straddles a channel boundary.
+qfb_status plan_ew(int dtype, const EwJob& j, std::vector<EwDesc>& out) {
+  const int V = per_vec(dtype);
+  const int es = elem_size(dtype);
+  const int64_t row = j.channels * j.inner;  // elements per outer index
+  const int64_t n = j.outer * row;
+  bool vec = (j.channels == 1 ? (n % V == 0) : (j.inner % V == 0));
+  vec = vec && aligned16(j.a) && (!j.b || aligned16(j.b)) && (!j.preact || aligned16(j.preact));
+  for (int k = 0; k < j.n_out; ++k) vec = vec && aligned16(j.y[k]);
+  const int64_t unit = vec ? V : 1;
+  // Rows per piece so a piece stays below 2^31 units.
+  int64_t rows_per_piece = j.outer;
+  if ((uint64_t)(n / unit) >= kMaxUnits) {
+    rows_per_piece = (int64_t)(kMaxUnits * (uint64_t)unit / (uint64_t)row);
+    if (rows_per_piece == 0) {
+      if (j.channels != 1) return fail(QFB_ERR_UNSUPPORTED, "row of %lld elements too large", (long long)row);
+    }
+  }
+  auto emit = [&](int64_t elem_off, int64_t elems, int64_t inner_units, int64_t chans) {
+    EwDesc d{};
+    const char* base = nullptr;
+    (void)base;
+    d.a = static_cast<const char*>(j.a) + elem_off * es;
+    d.b = j.b ? static_cast<const char*>(j.b) + elem_off * es : nullptr;
+    d.preact = j.preact ? static_cast<char*>(j.preact) + elem_off * es : nullptr;
+    for (int k = 0; k < 2; ++k) {
+      d.y[k] = k < j.n_out ? static_cast<char*>(j.y[k]) + elem_off * es : nullptr;
+      d.s[k] = k < j.n_out ? j.s[k] : nullptr;
+    }
+    d.nunits = (uint32_t)(elems / unit);
+    d.vec = (uint32_t)unit;
+    d.inner_u = make_fastdiv((uint32_t)std::max<int64_t>(inner_units, 1));
+    d.chans = make_fastdiv((uint32_t)chans);
+    d.n_out = j.n_out;
+    d.act = j.act;
+    d.flags = j.flags;
+    d.q = j.q;
+    out.push_back(d);
+  };
+  if (j.channels == 1) {
+    // per-tensor: split anywhere on a unit boundary
+    const int64_t max_elems = (int64_t)(kMaxUnits / 2) * unit;
+    for (int64_t off = 0; off < n; off += max_elems) {
+      emit(off, std::min(max_elems, n - off), 1, 1);
+    }
+    return QFB_OK;
+  }
+  if (j.inner / unit >= (int64_t)UINT32_MAX || j.channels >= (int64_t)UINT32_MAX) {
+    return fail(QFB_ERR_UNSUPPORTED, "inner/channels too large");
+  }
+  for (int64_t r = 0; r < j.outer; r += rows_per_piece) {
+    const int64_t rows = std::min(rows_per_piece, j.outer - r);
+    emit(r * row, rows * row, j.inner / unit, j.channels);
+  }
+  return QFB_OK;
+}
+
+qfb_status run_ew(qfb_ctx* ctx, int dtype, const std::vector<EwDesc>& descs) {
+  size_t i = 0;
+  while (i < descs.size()) {
+    EwBatch b;
+    std::memset(&b, 0, sizeof b);
+    uint32_t chunks = 0;
+    int n = 0;
+    for (; i < descs.size() && n < kMaxEwDesc; ++i, ++n) {
+      b.d[n] = descs[i];
+      b.chunk_begin[n] = chunks;
+      chunks += (descs[i].nunits + kEwChunk - 1) / kEwChunk;
+    }
+    b.n = n;
+    b.chunk_begin[n] = chunks;
+    if (chunks == 0) continue;
+    const int grid = (int)std::min<uint64_t>(chunks, (uint64_t)ctx->sm_count * ctx->ew_blocks_per_sm);
+    cudaError_t e = launch_ew(dtype, b, ctx->d_status, grid, ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "ew_kernel launch");
+    ctx->launches++;
+  }
+  return QFB_OK;
+}
+
+qfb_status q_of(int32_t q_max, float* q) {
+  if (q_max < 1 || q_max > 32767) return fail(QFB_ERR_VALUE, "q_max %d out of range", q_max);
+  *q = (float)q_max;
+  return QFB_OK;
+}
+
+}  // namespace
+
+// =====================================================================
+extern "C" {
+
+const char* qfb_last_error(void) { return g_last_error.c_str(); }
+
+const char* qfb_status_name(qfb_status s) {
+  switch (s) {
+    case QFB_OK: return "OK";
+    case QFB_ERR_SHAPE: return "ShapeError";
+    case QFB_ERR_VALUE: return "ValueError";
+    case QFB_ERR_IO: return "IoError";
+    case QFB_ERR_NONFINITE: return "NonFiniteError";
+    case QFB_ERR_INSUFFICIENT: return "InsufficientMatchesError";
+    case QFB_ERR_FUSED_PATH: return "FusedPathError";
+    case QFB_ERR_CUDA: return "CudaError";
+    case QFB_ERR_NCCL: return "NcclError";
+    case QFB_ERR_UNSUPPORTED: return "Unsupported";
+  }
+  return "Unknown";
+}
+
+const char* qfb_build_info(void) {
+  return "qfb 0.1 sm_100a (compute_100a) ieee-div ftz=off no-fast-math";
+}
+
+// ----------------------------------------------------------- config ---
+void qfb_quant_config_default(qfb_quant_config* c) {
+  if (!c) return;
+  c->bits = 8;
+  c->reserved = 0;
+  c->s_min = 1e-6;
+  c->s_min_half = 1e-4;
+  c->s_max = 64.0;
+  c->eps = 1e-8;
+}
+
+qfb_status qfb_quant_config_validate(const qfb_quant_config* c) {
+  if (!c) return fail(QFB_ERR_VALUE, "null config");
+  if (c->bits < 2 || c->bits > 16) return fail(QFB_ERR_VALUE, "QuantConfig: bits out of range");
+  if (!(c->s_min > 0.0) || !(c->s_min < c->s_max))
+    return fail(QFB_ERR_VALUE, "QuantConfig: require 0 < s_min < s_max");
+  if (!(c->eps > 0.0) || !(c->eps < c->s_min))
+    return fail(QFB_ERR_VALUE, "QuantConfig: require 0 < eps < s_min");
+  if (!(c->s_min_half > 0.0) || !(c->s_min_half < c->s_max))
+    return fail(QFB_ERR_VALUE, "QuantConfig: require 0 < s_min_half < s_max");
+  return QFB_OK;
+}
+
+int32_t qfb_q_max(const qfb_quant_config* c) { return c ? (1 << (c->bits - 1)) - 1 : 127; }
+
+// ------------------------------------------------------- scale math ---
+// Same expressions as quant.hpp:71-109 evaluated with the host libm, so the
+// doubles are bit-identical to the reference's on the same machine.
+double qfb_softplus(double x) {
+  if (x > 30.0) return x + std::log1p(std::exp(-x));
+  return std::log1p(std::exp(x));
+}
+
+double qfb_sigmoid(double x) {
+  if (x >= 0.0) return 1.0 / (1.0 + std::exp(-x));
+  const double e = std::exp(x);
+  return e / (1.0 + e);
+}
+
+qfb_status qfb_softplus_inv(double y, double* out) {
+  if (!out) return fail(QFB_ERR_VALUE, "null output");
+  if (!(y > 0.0)) return fail(QFB_ERR_VALUE, "softplus_inv: argument must be positive");
+  *out = y > 30.0 ? y : std::log(std::expm1(y));
+  return QFB_OK;
+}
+
+static double lower_for(const qfb_quant_config* c, qfb_precision p) {
+  return p == QFB_PREC_HALF ? c->s_min_half : c->s_min;
+}
+
+qfb_status qfb_resolve_scales(const double* log_s, int64_t n, const qfb_quant_config* cfg,
+                              qfb_precision prec, double* s_out) {
+  if (n < 0 || (n > 0 && (!log_s || !s_out)) || !cfg) return fail(QFB_ERR_VALUE, "resolve_scales: bad args");
+  const double lo = lower_for(cfg, prec);
+  for (int64_t i = 0; i < n; ++i) {
+    if (!std::isfinite(log_s[i]))
+      return fail(QFB_ERR_NONFINITE, "resolve_scale: non-finite log scale at %lld", (long long)i);
+    const double raw = qfb_softplus(log_s[i]) + cfg->eps;
+    s_out[i] = std::min(std::max(raw, lo), cfg->s_max);
+  }
+  return QFB_OK;
+}
+
+qfb_status qfb_scale_grad_factors(const double* log_s, int64_t n, const qfb_quant_config* cfg,
+                                  qfb_precision prec, double* s_out, double* chain_out) {
+  qfb_status st = qfb_resolve_scales(log_s, n, cfg, prec, s_out);
+  if (st != QFB_OK) return st;
+  if (!chain_out) return fail(QFB_ERR_VALUE, "scale_grad_factors: null chain");
+  const double lo = lower_for(cfg, prec);
+  for (int64_t i = 0; i < n; ++i) {
+    const double raw = qfb_softplus(log_s[i]) + cfg->eps;  // quant.hpp:242-244
+    const bool clamped = !(raw > lo && raw < cfg->s_max);
+    chain_out[i] = clamped ? 0.0 : qfb_sigmoid(log_s[i]);
+  }
+  return QFB_OK;
+}
+
+qfb_status qfb_cast_scales_f32(const double* s, int64_t n, float* out) {
+  if (n < 0 || (n > 0 && (!s || !out))) return fail(QFB_ERR_VALUE, "cast_scales: bad args");
+  for (int64_t i = 0; i < n; ++i) {
+    if (!(s[i] > 0.0))
+      return fail(QFB_ERR_VALUE, "fake_quantize: scale must be positive, got %f", s[i]);
+    out[i] = static_cast<float>(s[i]);
+  }
+  return QFB_OK;
+}
+
+// ---------------------------------------------------------- context ---
+qfb_status qfb_ctx_create(int32_t device, void* stream, qfb_ctx** out) {
+  if (!out) return fail(QFB_ERR_VALUE, "null out");
+  *out = nullptr;
+  int ndev = 0;
+  QFB_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(QFB_ERR_VALUE, "device %d out of range (%d)", device, ndev);
+  DeviceGuard g(device);
+  qfb_ctx* c = new qfb_ctx();
+  c->device = device;
+  c->stream = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+  if (e == cudaSuccess) {
+    int per = 0;
+    // occupancy of the elementwise kernel decides the persistent grid
+    if (ew_occupancy(&per) == cudaSuccess && per > 0) c->ew_blocks_per_sm = per;
+  }
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_status, sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMallocHost(&c->h_status, sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMemsetAsync(c->d_status, 0, sizeof(uint32_t), c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) {
+    qfb_ctx_destroy(c);
+    return cuda_fail(e, "qfb_ctx_create");
+  }
+  *out = c;
+  return QFB_OK;
+}
+
+qfb_status qfb_ctx_destroy(qfb_ctx* ctx) {
+  if (!ctx) return QFB_OK;
+  DeviceGuard g(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->d_status) cudaFree(ctx->d_status);
+  if (ctx->h_status) cudaFreeHost(ctx->h_status);
+  if (ctx->ws_f64.p) cudaFree(ctx->ws_f64.p);
+  if (ctx->ws_u32.p) cudaFree(ctx->ws_u32.p);
+  for (auto& b : ctx->host_io)
+    if (b.p) cudaFree(b.p);
+  delete ctx;
+  return QFB_OK;
+}
+
+qfb_status qfb_ctx_set_stream(qfb_ctx* ctx, void* stream) {
+  if (qfb_status st = check_ctx(ctx)) return st;
+  ctx->stream = static_cast<cudaStream_t>(stream);
+  return QFB_OK;
+}
+
+void* qfb_ctx_stream(qfb_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
+int32_t qfb_ctx_sm_count(qfb_ctx* ctx) { return ctx ? ctx->sm_count : 0; }
+int64_t qfb_ctx_launch_count(qfb_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+qfb_status qfb_ctx_sync(qfb_ctx* ctx) {
+  if (qfb_status st = check_ctx(ctx)) return st;
+  DeviceGuard g(ctx->device);
+  QFB_CUDA(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  QFB_CUDA(cudaStreamSynchronize(ctx->stream));
+  const uint32_t flags = *ctx->h_status;
+  if (flags != 0) {
+    QFB_CUDA(cudaMemsetAsync(ctx->d_status, 0, sizeof(uint32_t), ctx->stream));
+    QFB_CUDA(cudaStreamSynchronize(ctx->stream));
+    return fail(QFB_ERR_NONFINITE, "demote_half: non-finite value on the binary16 path");
+  }
+  return QFB_OK;
+}
+
+// --------------------------------------------------- forward ops ---
+qfb_status qfb_fq_fwd(qfb_ctx* ctx, qfb_dtype dtype, const void* x, void* y, int64_t outer,
+                      int64_t channels, int64_t inner, const float* scale, int32_t q_max,
+                      uint32_t flags) {
+  if (qfb_status st = check_ctx(ctx)) return st;
+  if (qfb_status st = check_dtype(dtype)) return st;
+  if (qfb_status st = check_dims(outer, channels, inner, "fake_quantize")) return st;
+  if (!x || !y || !scale) return fail(QFB_ERR_VALUE, "fake_quantize: null pointer");
+  float q;
+  if (qfb_status st = q_of(q_max, &q)) return st;
+  EwJob j{x, nullptr, nullptr, {y, nullptr}, {scale, nullptr}, outer, channels, inner,
+          1, QFB_ACT_NONE, flags & (kEwHalfGrid | kEwStreaming), q};
+  std::vector<EwDesc> d;
+  if (qfb_status st = plan_ew(dtype, j, d)) return st;
+  DeviceGuard g(ctx->device);
+  return run_ew(ctx, dtype, d);
+}
+
+qfb_status qfb_fq_fwd_multi(qfb_ctx* ctx, qfb_dtype dtype, const qfb_fq_desc* table, int32_t n) {
+  if (qfb_status st = check_ctx(ctx)) return st;
+  if (qfb_status st = check_dtype(dtype)) return st;
+  if (n < 0 || (n > 0 && !table)) return fail(QFB_ERR_VALUE, "fq_fwd_multi: bad table");
+  std::vector<EwDesc> d;
+  for (int32_t i = 0; i < n; ++i) {
+    const qfb_fq_desc& t = table[i];
+    if (qfb_status st = check_dims(t.outer, t.channels, t.inner, "fq_fwd_multi")) return st;
+    if (t.n_out < 1 || t.n_out > 2) return fail(QFB_ERR_VALUE, "fq_fwd_multi: n_out must be 1 or 2");
+    if (!t.x || !t.y[0] || !t.scale[0] || (t.n_out == 2 && (!t.y[1] || !t.scale[1])))
+      return fail(QFB_ERR_VALUE, "fq_fwd_multi: null pointer in entry %d", i);
+    float q;
+    if (qfb_status st = q_of(t.q_max, &q)) return st;
+    EwJob j{t.x, nullptr, nullptr, {t.y[0], t.y[1]}, {t.scale[0], t.scale[1]}, t.outer,
+            t.channels, t.inner, t.n_out, QFB_ACT_NONE, t.flags & (kEwHalfGrid | kEwStreaming), q};
+    if (qfb_status st = plan_ew(dtype, j, d)) return st;
+  }
+  DeviceGuard g(ctx->device);
+  return run_ew(ctx, dtype, d);
+}
+
+static qfb_status chain_job(const qfb_chain_desc& t, EwJob& j) {
+  if (qfb_status st = check_dtype(t.dtype)) return st;
+  if (qfb_status st = check_dims(t.outer, t.channels, t.inner, "fq_chain")) return st;
+  if (t.n_out < 0 || t.n_out > 2) return fail(QFB_ERR_VALUE, "fq_chain: n_out must be 0..2");
+  if (t.act < 0 || t.act > 2) return fail(QFB_ERR_VALUE, "fq_chain: unknown activation %d", t.act);
+  if (!t.a) return fail(QFB_ERR_VALUE, "fq_chain: null input");
+  for (int k = 0; k < t.n_out; ++k)
+    if (!t.y[k] || !t.scale[k]) return fail(QFB_ERR_VALUE, "fq_chain: null output %d", k);
+  if (t.n_out == 0 && !t.preact) return fail(QFB_ERR_VALUE, "fq_chain: no outputs");
+  float q;
+  if (qfb_status st = q_of(t.q_max, &q)) return st;
+  const bool half = t.dtype == QFB_F16 || (t.flags & QFB_FLAG_HALF_GRID);
+  uint32_t flags = t.flags & (kEwHalfGrid | kEwStreaming);
+  if (half) flags |= kEwDemoteIn;
+  j = EwJob{t.a, t.b, t.preact, {t.y[0], t.y[1]}, {t.scale[0], t.scale[1]}, t.outer,
+            t.channels, t.inner, t.n_out, t.act, flags, q};
+  return QFB_OK;
+}
+
+qfb_status qfb_fq_chain(qfb_ctx* ctx, const qfb_chain_desc* desc) {
+  if (qfb_status st = check_ctx(ctx)) return st;
+  if (!desc) return fail(QFB_ERR_VALUE, "fq_chain: null desc");
+  return qfb_fq_chain_multi(ctx, desc, 1);
+}
+
+qfb_status qfb_fq_chain_multi(qfb_ctx* ctx, const qfb_chain_desc* table, int32_t n) {
+  if (qfb_status st = check_ctx(ctx)) return st;
+  if (n < 0 || (n > 0 && !table)) return fail(QFB_ERR_VALUE, "fq_chain_multi: bad table");
+  // one launch per dtype group (a batch shares the element type)
+  for (int dt = 0; dt < 2; ++dt) {
+    std::vector<EwDesc> d;
+    for (int32_t i = 0; i < n; ++i) {
+      EwJob j;
+      if (qfb_status st = chain_job(table[i], j)) return st;
+      if (table[i].dtype != dt) continue;
+      if (qfb_status st = plan_ew(dt, j, d)) return st;
+    }
+    if (d.empty()) continue;
+    DeviceGuard g(ctx->device);
+    if (qfb_status st = run_ew(ctx, dt, d)) return st;
+  }
+  return QFB_OK;
+}
+
+qfb_status qfb_int8_codes(qfb_ctx* ctx, qfb_dtype dtype, const void* x, int8_t* codes,
+                          int64_t outer, int64_t channels, int64_t inner, const float* scale,
+                          int32_t q_max) {
+  if (qfb_status st = check_ctx(ctx)) return st;
+  if (qfb_status st = check_dtype(dtype)) return st;
+  if (qfb_status st = check_dims(outer, channels, inner, "int8_codes")) return st;
+  if (!x || !codes || !scale) return fail(QFB_ERR_VALUE, "int8_codes: null pointer");
+  float q;
+  if (qfb_status st = q_of(q_max, &q)) return st;
+  const int V = per_vec(dtype);
+  const int64_t n = outer * channels * inner;
+  if (n >= (int64_t)kMaxUnits) return fail(QFB_ERR_UNSUPPORTED, "int8_codes: tensor too large");
+  const bool vec = (channels == 1 ? n % V == 0 : inner % V == 0) && aligned16(x) &&
+                   ((reinterpret_cast<uintptr_t>(codes) & (V - 1)) == 0);
+  const int64_t unit = vec ? V : 1;
+  CodesDesc d{};
+  d.x = x;
+  d.codes = codes;
+  d.s = scale;
+  d.nunits = (uint32_t)(n / unit);
+  d.vec = (uint32_t)unit;
+  d.inner_u = make_fastdiv((uint32_t)(inner / unit > 0 ? inner / unit : 1));
+  d.chans = make_fastdiv((uint32_t)channels);
+  d.q = q;
+  DeviceGuard g(ctx->device);
+  const int grid = (int)std::min<int64_t>((d.nunits + kEwThreads - 1) / kEwThreads,
+                                          (int64_t)ctx->sm_count * 8);
+  cudaError_t e = launch_codes(dtype, d, std::max(grid, 1), ctx->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "codes_kernel launch");
+  ctx->launches++;
+  return QFB_OK;
+}
+
+qfb_status qfb_fq_fwd_perop(qfb_ctx* ctx, qfb_dtype dtype, const void* x, void* y,
+                            int64_t outer, int64_t channels, int64_t inner, const float* scale,
+                            int32_t q_max, uint32_t flags, float* tmp) {
+  if (qfb_status st = check_ctx(ctx)) return st;
+  if (qfb_status st = check_dtype(dtype)) return st;
+  if (qfb_status st = check_dims(outer, channels, inner, "fake_quantize_perop")) return st;
+  if (!x || !y || !scale || !tmp) return fail(QFB_ERR_VALUE, "fake_quantize_perop: null pointer");
+  float q;
+  if (qfb_status st = q_of(q_max, &q)) return st;
+  const uint64_t n = (uint64_t)(outer * channels * inner);
+  float* t1 = tmp;
+  float* t2 = tmp + n;
+  float* t3 = tmp + 2 * n;
+  const void* ins[4] = {x, t1, t2, t3};
+  void* outs[4] = {t1, t2, t3, y};
+  DeviceGuard g(ctx->device);
+  const int grid = (int)std::min<uint64_t>((n + kEwThreads - 1) / kEwThreads,
+                                           (uint64_t)ctx->sm_count * 8);
+  for (int op = 0; op < 4; ++op) {
+    PerOpDesc d{ins[op], outs[op], scale, n, (uint64_t)inner, (uint64_t)channels, q,
+                flags & kEwHalfGrid};
+    cudaError_t e = launch_perop(dtype, op, d, ctx->d_status, std::max(grid, 1), ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "perop_kernel launch");
+    ctx->launches++;
+  }
+  return QFB_OK;
+}
+
+qfb_status qfb_fill_rng(qfb_ctx* ctx, qfb_dtype dtype, void* out, int64_t n, uint64_t seed,
+                        uint64_t stream, uint64_t index_offset, int32_t kind, double lo,
+                        double hi) {
+  if (qfb_status st = check_ctx(ctx)) return st;
+  if (qfb_status st = check_dtype(dtype)) return st;
+  if (n < 0 || (n > 0 && !out)) return fail(QFB_ERR_VALUE, "fill_rng: bad args");
+  if (kind != 0 && kind != 1) return fail(QFB_ERR_VALUE, "fill_rng: kind must be 0 or 1");
+  if (n == 0) return QFB_OK;
+  DeviceGuard g(ctx->device);
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->sm_count * 16);
+  cudaError_t e = launch_fill_rng(dtype, out, n, seed, stream, index_offset, kind, lo, hi, grid,
+                                  ctx->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "fill_rng launch");
+  ctx->launches++;
+  return QFB_OK;
+}
+
+qfb_status qfb_resolve_scales_dev(qfb_ctx* ctx, const double* log_s, int64_t n,
+                                  const qfb_quant_config* cfg, qfb_precision prec, float* s32,
+                                  double* s64, double* chain) {
+  if (qfb_status st = check_ctx(ctx)) return st;
+  if (qfb_status st = qfb_quant_config_validate(cfg)) return st;
+  if (n < 0 || (n > 0 && !log_s)) return fail(QFB_ERR_VALUE, "resolve_scales_dev: bad args");
+  if (n == 0) return QFB_OK;
+  ResolveDesc d{log_s, s32, s64, chain, n, lower_for(cfg, prec), cfg->s_max, cfg->eps};
+  DeviceGuard g(ctx->device);
+  cudaError_t e = launch_resolve(d, ctx->d_status, ctx->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "resolve launch");
+  ctx->launches++;
+  return QFB_OK;
+}
+
+// -------------------------------------------------- backward ops ---
+namespace {
+
+struct BwdPlan {
+  BwdDesc d;
+  uint64_t tiles;
+  size_t f64_need;  // doubles
+  size_t u32_need;  // counters
+};
+
+// Depth D of the 16-bounded leaf groups: smallest D with ceil(n/2^D) <= 16.
+uint32_t leaf_depth(uint64_t n) {
+  uint32_t d = 0;
+  while (((n + (1ull << d) - 1) >> d) > (uint64_t)kLeafMax) ++d;
+  return d;
+}
+
+qfb_status plan_bwd(const qfb_bwd_desc& t, BwdPlan& p) {
+  if (qfb_status st = check_dims(t.outer, t.channels, t.inner, "fake_quantize_backward")) return st;
+  if (!t.x || !t.up || !t.scale64 || !t.chain || !t.d_log_s)
+    return fail(QFB_ERR_VALUE, "fake_quantize_backward: null pointer");
+  if (t.q_max < 1 || t.q_max > 32767) return fail(QFB_ERR_VALUE, "q_max out of range");
+  const uint64_t segs = (uint64_t)t.outer * (uint64_t)t.channels;
+  if (segs >= (1ull << 32)) return fail(QFB_ERR_UNSUPPORTED, "too many rows");
+  std::memset(&p, 0, sizeof p);
+  BwdDesc& d = p.d;
+  d.x = t.x;
+  d.up = t.up;
+  d.dx = t.dx;
+  d.s64 = t.scale64;
+  d.chain = t.chain;
+  d.d_log_s = t.d_log_s;
+  d.inner = (uint64_t)t.inner;
+  d.outer = (uint32_t)t.outer;
+  d.chans = (uint32_t)t.channels;
+  d.depth = leaf_depth((uint64_t)t.inner);
+  d.g = std::min<uint32_t>(d.depth, (uint32_t)kBwdGroupsLog);
+  d.tps_log = d.depth - d.g;
+  d.accumulate = t.accumulate ? 1 : 0;
+  d.q = (double)t.q_max;
+  const uint64_t tps = 1ull << d.tps_log;
+  p.tiles = segs * tps;
+  if (p.tiles >= (1ull << 31)) return fail(QFB_ERR_UNSUPPORTED, "too many tiles");
+  if (tps > 1) {
+    p.f64_need += segs * tps;
+    p.u32_need += segs;
+  }
+  if (t.outer > 1) {
+    p.f64_need += segs;
+    p.u32_need += (size_t)t.channels;
+  }
+  return QFB_OK;
+}
+
+}  // namespace
+
+qfb_status qfb_fq_bwd_multi(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc* table, int32_t n) {
+  if (qfb_status st = check_ctx(ctx)) return st;
+  if (qfb_status st = check_dtype(dtype)) return st;
+  if (n < 0 || (n > 0 && !table)) return fail(QFB_ERR_VALUE, "fq_bwd_multi: bad table");
+  std::vector<BwdPlan> plans((size_t)n);
+  for (int32_t i = 0; i < n; ++i)
+    if (qfb_status st = plan_bwd(table[i], plans[i])) return st;
+  DeviceGuard g(ctx->device);
+  int32_t i = 0;
+  while (i < n) {
+    // Batch up to kMaxBwdDesc entries; each gets its own workspace slice.
+    int32_t cnt = 0;
+    size_t f64 = 0, u32 = 0;
+    uint64_t tiles = 0;
+    while (i + cnt < n && cnt < kMaxBwdDesc) {
+      const BwdPlan& p = plans[i + cnt];
+      if (cnt > 0 && tiles + p.tiles >= (1ull << 31)) break;
+      f64 += p.f64_need;
+      u32 += p.u32_need;
+      tiles += p.tiles;
+      ++cnt;
+    }
+    if (qfb_status st = grow(ctx, ctx->ws_f64, std::max<size_t>(f64, 1) * 8, false)) return st;
+    if (qfb_status st = grow(ctx, ctx->ws_u32, std::max<size_t>(u32, 1) * 4, true)) return st;
+    BwdBatch b;
+    std::memset(&b, 0, sizeof b);
+    double* fp = static_cast<double*>(ctx->ws_f64.p);
+    uint32_t* up = static_cast<uint32_t*>(ctx->ws_u32.p);
+    uint64_t tb = 0;
+    for (int32_t k = 0; k < cnt; ++k) {
+      BwdDesc d = plans[i + k].d;
+      const uint64_t segs = (uint64_t)d.outer * d.chans;
+      const uint64_t tps = 1ull << d.tps_log;
+      if (tps > 1) {
+        d.partials = fp;
+        fp += segs * tps;
+        d.seg_counters = up;
+        up += segs;
+      }
+      if (d.outer > 1) {
+        d.seg_results = fp;
+        fp += segs;
+        d.chan_counters = up;
+        up += d.chans;
+      }
+      b.d[k] = d;
+      b.tile_begin[k] = (uint32_t)tb;
+      tb += plans[i + k].tiles;
+    }
+    b.n = cnt;
+    b.tile_begin[cnt] = (uint32_t)tb;
+    cudaError_t e = launch_bwd(dtype, b, ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "bwd_kernel launch");
+    ctx->launches++;
+    i += cnt;
+  }
+  return QFB_OK;
+}
+
+qfb_status qfb_fq_bwd(qfb_ctx* ctx, qfb_dtype dtype, const void* x, const void* up, void* dx,
+                      int64_t outer, int64_t channels, int64_t inner, const double* scale64,
+                      const double* chain, int32_t q_max, double* d_log_s, int32_t accumulate) {
+  qfb_bwd_desc t{x, up, dx, scale64, chain, d_log_s, outer, channels, inner, q_max, accumulate};
+  return qfb_fq_bwd_multi(ctx, dtype, &t, 1);
+}
+
+// ------------------------------------------------ host-level ops ---
+namespace {
+
+qfb_status h2d(qfb_ctx* ctx, DevBuf& b, const void* src, size_t bytes) {
+  if (qfb_status st = grow(ctx, b, bytes, false)) return st;
+  QFB_CUDA(cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  return QFB_OK;
+}
+
+}  // namespace
+
+qfb_status qfb_fake_quantize_host(qfb_ctx* ctx, qfb_precision prec, const float* x, float* y,
+                                  int64_t outer, int64_t channels, int64_t inner,
+                                  const double* s, const qfb_quant_config* cfg) {
+  if (qfb_status st = check_ctx(ctx)) return st;
+  if (qfb_status st = qfb_quant_config_validate(cfg)) return st;
+  if (qfb_status st = check_dims(outer, channels, inner, "fake_quantize")) return st;
+  if (!x || !y || !s) return fail(QFB_ERR_VALUE, "fake_quantize: null pointer");
+  std::vector<float> sf((size_t)channels);
+  if (qfb_status st = qfb_cast_scales_f32(s, channels, sf.data())) return st;
+  const size_t bytes = (size_t)(outer * channels * inner) * sizeof(float);
+  DeviceGuard g(ctx->device);
+  if (qfb_status st = h2d(ctx, ctx->host_io[0], x, bytes)) return st;
+  if (qfb_status st = h2d(ctx, ctx->host_io[2], sf.data(), sf.size() * sizeof(float))) return st;
+  if (qfb_status st = grow(ctx, ctx->host_io[1], bytes, false)) return st;
+  const uint32_t flags = prec == QFB_PREC_HALF ? QFB_FLAG_HALF_GRID : 0u;
+  if (qfb_status st = qfb_fq_fwd(ctx, QFB_F32, ctx->host_io[0].p, ctx->host_io[1].p, outer,
+                                 channels, inner, static_cast<const float*>(ctx->host_io[2].p),
+                                 qfb_q_max(cfg), flags))
+    return st;
+  QFB_CUDA(cudaMemcpyAsync(y, ctx->host_io[1].p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  return qfb_ctx_sync(ctx);
+}
+
+qfb_status qfb_int8_codes_host(qfb_ctx* ctx, const float* x, int8_t* codes, int64_t outer,
+                               int64_t channels, int64_t inner, const double* s,
+                               const qfb_quant_config* cfg) {
+  if (qfb_status st = check_ctx(ctx)) return st;
+  if (qfb_status st = qfb_quant_config_validate(cfg)) return st;
+  if (qfb_status st = check_dims(outer, channels, inner, "int8_codes")) return st;
+  if (!x || !codes || !s) return fail(QFB_ERR_VALUE, "int8_codes: null pointer");
+  std::vector<float> sf((size_t)channels);
+  if (qfb_status st = qfb_cast_scales_f32(s, channels, sf.data())) return st;
+  const size_t n = (size_t)(outer * channels * inner);
+  DeviceGuard g(ctx->device);
+  if (qfb_status st = h2d(ctx, ctx->host_io[0], x, n * sizeof(float))) return st;
+  if (qfb_status st = h2d(ctx, ctx->host_io[2], sf.data(), sf.size() * sizeof(float))) return st;
+  if (qfb_status st = grow(ctx, ctx->host_io[1], n, false)) return st;
+  if (qfb_status st = qfb_int8_codes(ctx, QFB_F32, ctx->host_io[0].p,
+                                     static_cast<int8_t*>(ctx->host_io[1].p), outer, channels,
+                                     inner, static_cast<const float*>(ctx->host_io[2].p),
+                                     qfb_q_max(cfg)))
+    return st;
+  QFB_CUDA(cudaMemcpyAsync(codes, ctx->host_io[1].p, n, cudaMemcpyDeviceToHost, ctx->stream));
+  return qfb_ctx_sync(ctx);
+}
+
+qfb_status qfb_fake_quantize_backward_host(qfb_ctx* ctx, qfb_precision prec, const float* x,
+                                           const float* up, float* dx, int64_t outer,
+                                           int64_t channels, int64_t inner,
+                                           const double* log_s, const qfb_quant_config* cfg,
+                                           double* d_log_s, int32_t accumulate) {
+  if (qfb_status st = check_ctx(ctx)) return st;
+  if (qfb_status st = qfb_quant_config_validate(cfg)) return st;
+  if (qfb_status st = check_dims(outer, channels, inner, "fake_quantize_backward")) return st;
+  if (!x || !up || !log_s || !d_log_s) return fail(QFB_ERR_VALUE, "fake_quantize_backward: null pointer");
+  std::vector<double> fac((size_t)channels * 3);
+  double* s64 = fac.data();
+  double* chain = fac.data() + channels;
+  double* acc = fac.data() + 2 * channels;
+  if (qfb_status st = qfb_scale_grad_factors(log_s, channels, cfg, prec, s64, chain)) return st;
+  for (int64_t c = 0; c < channels; ++c) acc[c] = accumulate ? d_log_s[c] : 0.0;
+  const size_t bytes = (size_t)(outer * channels * inner) * sizeof(float);
+  DeviceGuard g(ctx->device);
+  if (qfb_status st = h2d(ctx, ctx->host_io[0], x, bytes)) return st;
+  if (qfb_status st = h2d(ctx, ctx->host_io[1], up, bytes)) return st;
+  if (qfb_status st = h2d(ctx, ctx->host_io[3], fac.data(), fac.size() * sizeof(double))) return st;
+  if (dx)
+    if (qfb_status st = grow(ctx, ctx->host_io[4], bytes, false)) return st;
+  const double* dfac = static_cast<const double*>(ctx->host_io[3].p);
+  double* dacc = static_cast<double*>(ctx->host_io[3].p) + 2 * channels;
+  if (qfb_status st = qfb_fq_bwd(ctx, QFB_F32, ctx->host_io[0].p, ctx->host_io[1].p,
+                                 dx ? ctx->host_io[4].p : nullptr, outer, channels, inner, dfac,
+                                 dfac + channels, qfb_q_max(cfg), dacc, accumulate))
+    return st;
+  if (dx) QFB_CUDA(cudaMemcpyAsync(dx, ctx->host_io[4].p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  QFB_CUDA(cudaMemcpyAsync(d_log_s, dacc, (size_t)channels * sizeof(double),
+                           cudaMemcpyDeviceToHost, ctx->stream));
+  return qfb_ctx_sync(ctx);
+}
+
+}  // extern "C"

@@ -1,0 +1,178 @@
+// qfb_device.cuh — device-side scalar contract of the fake-quant path.
+//
+// Every function here restates one reference scalar operation bit-exactly
+// (paths relative to /root/reference/proj/include/quantfuse/). Compiled
+// without fast-math, with FTZ off and IEEE division (nvcc defaults); the
+// arithmetic that must not be contracted is spelled with _rn intrinsics.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+#include "qfb_kernels.h"
+
+namespace qfb {
+
+// Status latch bits (qfb_ctx_sync maps them to qfb_status).
+constexpr uint32_t kStatusNonFinite = 1u;
+
+// ---------------------------------------------------------------- FQ ---
+// quant.hpp:114-121:  s * nearbyintf(min(max(x / s, -q), q))
+//  - IEEE round-to-nearest division (__fdiv_rn), never x * (1/s);
+//  - the clip is a pair of compare-selects exactly like std::max/std::min,
+//    so NaN propagates (fmaxf/fminf would drop it);
+//  - rintf == nearbyintf under round-to-nearest-even (FRND);
+//  - the product keeps the sign of zero (no integer round trip).
+__device__ __forceinline__ float fq_clip(float z, float q) {
+  z = (z < -q) ? -q : z;  // std::max(z, -q)
+  z = (q < z) ? q : z;    // std::min(z, q)
+  return z;
+}
+
+__device__ __forceinline__ float fq_value(float x, float s, float q) {
+  const float z = __fdiv_rn(x, s);
+  return __fmul_rn(s, rintf(fq_clip(z, q)));
+}
+
+// ----------------------------------------------------------- binary16 ---
+// half.hpp:72-82 round_to_half: |v| > 65504 saturates to +-65504 (never
+// inf); NaN maps to +-65504 through the exponent guard of f32_to_f16_rne
+// (half.hpp:24-26) with the sign of the NaN. On the device a NaN produced
+// by arithmetic is canonical (+), while the host propagates the operand's
+// sign, so callers pass the sign source (the offending input).
+// For non-NaN v: RNE(clamp(v)) == __float2half_rn(clamp(v)) for every float
+// (verified exhaustively).
+__device__ __forceinline__ __half half_store(float v, float sign_src, bool& nonfinite) {
+  if (!isfinite(v)) nonfinite = true;
+  if (isnan(v)) return __ushort_as_half(signbit(sign_src) ? 0xfbffu : 0x7bffu);
+  v = fminf(fmaxf(v, -65504.0f), 65504.0f);
+  return __float2half_rn(v);
+}
+
+__device__ __forceinline__ float half_grid(float v, float sign_src, bool& nonfinite) {
+  return __half2float(half_store(v, sign_src, nonfinite));
+}
+
+// ---------------------------------------------------- int8 code ---
+// quant.hpp:186: static_cast<int8_t>(nearbyintf(clip(x/s))). NaN -> 0
+// (the x86 reference truncates through int32 0x80000000, low byte 0).
+__device__ __forceinline__ int8_t fq_code(float x, float s, float q) {
+  const float r = rintf(fq_clip(__fdiv_rn(x, s), q));
+  const int32_t w = isnan(r) ? 0 : __float2int_rz(r);
+  return (int8_t)(uint8_t)(uint32_t)w;
+}
+
+// ----------------------------------------------- STE / LSQ terms ---
+// quant.hpp:217-228 in double: z = x/s, mask = |z| <= q,
+// d_ds = mask ? rint(z) - z : (z > 0 ? q : -q).
+struct GradTerm {
+  bool mask;
+  double d_ds;
+};
+
+__device__ __forceinline__ GradTerm grad_term(float x, double s, double q) {
+  const double z = __ddiv_rn((double)x, s);
+  GradTerm t;
+  t.mask = fabs(z) <= q;
+  t.d_ds = t.mask ? __dadd_rn(rint(z), -z) : (z > 0.0 ? q : -q);
+  return t;
+}
+
+// ------------------------------------------------------ fast divide ---
+// Unsigned 32-bit division by a runtime-invariant divisor (round-up
+// multiplier method); exact for every n < 2^32.
+using FastDiv = FastDivHost;
+
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
+  if (f.d == 1) return n;
+  const uint32_t hi = __umulhi(n, f.m);
+  return (uint32_t)(((uint64_t)hi + n) >> f.s);
+}
+
+// -------------------------------------------------------- memory ---
+__device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void st_v4(void* p, uint4 v, bool streaming) {
+  if (streaming) {
+    asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+  } else {
+    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+  }
+}
+
+// Element <-> float conversions for the two storage types. A "unit" is
+// one 16-byte vector: 4 floats or 8 halves.
+template <typename T>
+struct Elem;
+
+template <>
+struct Elem<float> {
+  static constexpr int kPerVec = 4;
+  __device__ __forceinline__ static void unpack(const uint4& r, float* v) {
+    v[0] = __uint_as_float(r.x);
+    v[1] = __uint_as_float(r.y);
+    v[2] = __uint_as_float(r.z);
+    v[3] = __uint_as_float(r.w);
+  }
+  // half_grid: re-round onto the binary16 grid (EmulatedHalf in f32).
+  __device__ __forceinline__ static uint4 pack(const float* v, const float* sign_src,
+                                               bool half_grid_out, bool& nf) {
+    float o[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o[i] = half_grid_out ? half_grid(v[i], sign_src[i], nf) : v[i];
+    return make_uint4(__float_as_uint(o[0]), __float_as_uint(o[1]), __float_as_uint(o[2]),
+                      __float_as_uint(o[3]));
+  }
+  __device__ __forceinline__ static float load1(const void* p, uint64_t i) {
+    return __ldg(static_cast<const float*>(p) + i);
+  }
+  __device__ __forceinline__ static void store1(void* p, uint64_t i, float v, float sign_src,
+                                                bool half_grid_out, bool& nf) {
+    static_cast<float*>(p)[i] = half_grid_out ? half_grid(v, sign_src, nf) : v;
+  }
+};
+
+template <>
+struct Elem<__half> {
+  static constexpr int kPerVec = 8;
+  __device__ __forceinline__ static void unpack(const uint4& r, float* v) {
+    const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
+      v[2 * i] = f.x;
+      v[2 * i + 1] = f.y;
+    }
+  }
+  // f16 storage always rounds through half_store (RNE + saturation).
+  __device__ __forceinline__ static uint4 pack(const float* v, const float* sign_src,
+                                               bool /*half_grid_out*/, bool& nf) {
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t lo = __half_as_ushort(half_store(v[2 * i], sign_src[2 * i], nf));
+      const uint32_t hi = __half_as_ushort(half_store(v[2 * i + 1], sign_src[2 * i + 1], nf));
+      w[i] = lo | (hi << 16);
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  __device__ __forceinline__ static float load1(const void* p, uint64_t i) {
+    return __half2float(static_cast<const __half*>(p)[i]);
+  }
+  __device__ __forceinline__ static void store1(void* p, uint64_t i, float v, float sign_src,
+                                                bool /*half_grid_out*/, bool& nf) {
+    static_cast<__half*>(p)[i] = half_store(v, sign_src, nf);
+  }
+};
+
+}  // namespace qfb

@@ -1,0 +1,335 @@
+// qfb_fwd.cu — forward-side sm_100a kernels: fused fake-quant forward /
+// quant->act->quant chains (one HBM pass over a table of quant points),
+// int8 code emission, the per-operator ablation sweeps, device scale
+// resolution and the counter-RNG synthetic generator.
+//
+// All of these are HBM-bound elementwise sweeps (SURVEY.md §8 d): 16-byte
+// vectorized, coalesced loads (ld.global.nc.L1::no_allocate) and stores,
+// kEwUnroll independent loads in flight per thread, a grid of
+// (SM count x resident CTAs) persistent CTAs striding over 1024-unit chunks.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include "../../include/qfb_portable.h"
+#include "qfb_device.cuh"
+#include "qfb_kernels.h"
+
+namespace qfb {
+
+namespace {
+
+__device__ __forceinline__ uint32_t channel_of(uint32_t unit, const FastDiv& inner_u,
+                                               const FastDiv& chans) {
+  if (chans.d == 1) return 0;
+  const uint32_t row = fdiv(unit, inner_u);
+  return row - fdiv(row, chans) * chans.d;
+}
+
+__device__ __forceinline__ float apply_act(float v, int act) {
+  if (act == 1) return v > 0.0f ? v : 0.0f;  // relu, tensor.hpp:147-151
+  if (act == 2) return qfb_p_gelu(v);
+  return v;
+}
+
+// Vector path: every unit is one 16-byte vector, all its elements share a
+// channel (host guarantees inner % kPerVec == 0 and 16-byte alignment).
+template <typename T>
+__device__ __forceinline__ void ew_vec(const EwDesc& d, uint32_t ubase, bool& nf) {
+  constexpr int V = Elem<T>::kPerVec;
+  const bool has_b = d.b != nullptr;
+  const bool streaming = (d.flags & kEwStreaming) != 0;
+  const bool half_out = (d.flags & kEwHalfGrid) != 0;
+  const bool demote_in = (d.flags & kEwDemoteIn) != 0;
+  uint4 ra[kEwUnroll], rb[kEwUnroll];
+#pragma unroll
+  for (int k = 0; k < kEwUnroll; ++k) {
+    const uint32_t u = ubase + k * kEwThreads;
+    if (u < d.nunits) {
+      ra[k] = ld_nc_v4(static_cast<const uint4*>(d.a) + u);
+      if (has_b) rb[k] = ld_nc_v4(static_cast<const uint4*>(d.b) + u);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kEwUnroll; ++k) {
+    const uint32_t u = ubase + k * kEwThreads;
+    if (u >= d.nunits) break;
+    const uint32_t ch = channel_of(u, d.inner_u, d.chans);
+    float v[V];
+    Elem<T>::unpack(ra[k], v);
+    if (has_b) {
+      float w[V];
+      Elem<T>::unpack(rb[k], w);
+#pragma unroll
+      for (int i = 0; i < V; ++i) v[i] = __fadd_rn(v[i], w[i]);  // tensor.hpp:126-134
+    }
+    if (d.act != 0) {
+#pragma unroll
+      for (int i = 0; i < V; ++i) v[i] = apply_act(v[i], d.act);
+    }
+    if (demote_in) {
+#pragma unroll
+      for (int i = 0; i < V; ++i) v[i] = half_grid(v[i], v[i], nf);  // tensor.hpp:159-170
+    }
+    if (d.preact != nullptr) {
+      st_v4(static_cast<uint4*>(d.preact) + u, Elem<T>::pack(v, v, false, nf), streaming);
+    }
+    for (int j = 0; j < d.n_out; ++j) {
+      const float s = __ldg(d.s[j] + ch);
+      float o[V];
+#pragma unroll
+      for (int i = 0; i < V; ++i) o[i] = fq_value(v[i], s, d.q);
+      st_v4(static_cast<uint4*>(d.y[j]) + u, Elem<T>::pack(o, v, half_out, nf), streaming);
+    }
+  }
+}
+
+// Scalar path (unaligned or inner % kPerVec != 0): unit == element.
+template <typename T>
+__device__ __forceinline__ void ew_scalar(const EwDesc& d, uint32_t ubase, bool& nf) {
+  const bool has_b = d.b != nullptr;
+  const bool half_out = (d.flags & kEwHalfGrid) != 0;
+  const bool demote_in = (d.flags & kEwDemoteIn) != 0;
+  float va[kEwUnroll], vb[kEwUnroll];
+#pragma unroll
+  for (int k = 0; k < kEwUnroll; ++k) {
+    const uint32_t u = ubase + k * kEwThreads;
+    if (u < d.nunits) {
+      va[k] = Elem<T>::load1(d.a, u);
+      vb[k] = has_b ? Elem<T>::load1(d.b, u) : 0.0f;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kEwUnroll; ++k) {
+    const uint32_t u = ubase + k * kEwThreads;
+    if (u >= d.nunits) break;
+    const uint32_t ch = channel_of(u, d.inner_u, d.chans);
+    float v = va[k];
+    if (has_b) v = __fadd_rn(v, vb[k]);
+    v = apply_act(v, d.act);
+    if (demote_in) v = half_grid(v, v, nf);
+    if (d.preact != nullptr) Elem<T>::store1(d.preact, u, v, v, false, nf);
+    for (int j = 0; j < d.n_out; ++j) {
+      const float s = __ldg(d.s[j] + ch);
+      Elem<T>::store1(d.y[j], u, fq_value(v, s, d.q), v, half_out, nf);
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kEwThreads) ew_kernel(const __grid_constant__ EwBatch bt,
+                                                        uint32_t* __restrict__ status) {
+  bool nf = false;
+  const uint32_t total = bt.chunk_begin[bt.n];
+  for (uint32_t chunk = blockIdx.x; chunk < total; chunk += gridDim.x) {
+    int lo = 0, hi = bt.n - 1;  // last descriptor with chunk_begin <= chunk
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (bt.chunk_begin[mid] <= chunk) lo = mid;
+      else hi = mid - 1;
+    }
+    const EwDesc& d = bt.d[lo];
+    const uint32_t ubase = (chunk - bt.chunk_begin[lo]) * kEwChunk + threadIdx.x;
+    if (d.vec > 1) ew_vec<T>(d, ubase, nf);
+    else ew_scalar<T>(d, ubase, nf);
+  }
+  if (nf) atomicOr(status, kStatusNonFinite);
+}
+
+// ------------------------------------------------------------ codes ---
+template <typename T>
+__global__ void __launch_bounds__(kEwThreads) codes_kernel(const __grid_constant__ CodesDesc d) {
+  constexpr int V = Elem<T>::kPerVec;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < d.nunits; u += stride) {
+    const uint32_t ch = channel_of(u, d.inner_u, d.chans);
+    const float s = __ldg(d.s + ch);
+    if (d.vec > 1) {
+      float v[V];
+      Elem<T>::unpack(ld_nc_v4(static_cast<const uint4*>(d.x) + u), v);
+      uint32_t w[V / 4];
+#pragma unroll
+      for (int i = 0; i < V / 4; ++i) {
+        w[i] = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          w[i] |= (uint32_t)(uint8_t)fq_code(v[4 * i + b], s, d.q) << (8 * b);
+      }
+      if (V == 4) {
+        reinterpret_cast<uint32_t*>(d.codes)[u] = w[0];
+      } else {
+        reinterpret_cast<uint2*>(d.codes)[u] = make_uint2(w[0], w[V / 4 - 1]);
+      }
+    } else {
+      d.codes[u] = fq_code(Elem<T>::load1(d.x, u), s, d.q);
+    }
+  }
+}
+
+// --------------------------------------------------- per-operator ---
+// exec.hpp:276-342: four sweeps, float temporaries. op0 reads dtype,
+// op3 writes dtype (with the half re-round of exec.hpp:306-307).
+template <typename T, int OP>
+__global__ void __launch_bounds__(kEwThreads)
+    perop_kernel(const __grid_constant__ PerOpDesc d, uint32_t* __restrict__ status) {
+  bool nf = false;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < d.n; i += stride) {
+    const uint64_t ch = d.chans == 1 ? 0 : (i / d.inner) % d.chans;
+    // NaNs are carried through the temporaries with the input's sign, as
+    // the host reference does, so a half re-round in op 3 sees the same sign.
+    if (OP == 0) {
+      const float x = Elem<T>::load1(d.in, i);
+      static_cast<float*>(d.out)[i] =
+          isnan(x) ? __uint_as_float(__float_as_uint(x) | 0x400000u) : __fdiv_rn(x, __ldg(d.s + ch));
+    } else if (OP == 1) {
+      static_cast<float*>(d.out)[i] = fq_clip(static_cast<const float*>(d.in)[i], d.q);
+    } else if (OP == 2) {
+      const float c = static_cast<const float*>(d.in)[i];
+      static_cast<float*>(d.out)[i] = isnan(c) ? c : rintf(c);
+    } else {
+      const float r = static_cast<const float*>(d.in)[i];
+      const float v = __fmul_rn(__ldg(d.s + ch), r);
+      // sign source: NaN results come from a NaN input; r carries its sign
+      Elem<T>::store1(d.out, i, v, r, (d.flags & kEwHalfGrid) != 0, nf);
+    }
+  }
+  if (nf) atomicOr(status, kStatusNonFinite);
+}
+
+// ------------------------------------------------------------- rng ---
+// rng.hpp:15-50, identical integer/double arithmetic.
+__device__ __forceinline__ uint64_t smix(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+
+template <typename T>
+__global__ void fill_rng_kernel(T* out, int64_t n, uint64_t seed_mix, uint64_t stream_term,
+                                uint64_t offset, int kind, double lo, double hi) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t idx = offset + (uint64_t)i;
+    double v;
+    if (kind == 0) {
+      const uint64_t w = smix(seed_mix ^ smix(stream_term + idx));
+      const double u = __dmul_rn((double)(w >> 11), 0x1.0p-53);
+      v = __dadd_rn(lo, __dmul_rn(__dadd_rn(hi, -lo), u));
+    } else {
+      double acc = 0.0;
+      for (uint64_t k = 0; k < 12; ++k) {
+        const uint64_t w = smix(seed_mix ^ smix(stream_term + idx * 12 + k));
+        acc = __dadd_rn(acc, __dmul_rn((double)(w >> 11), 0x1.0p-53));
+      }
+      v = __dmul_rn(lo, __dadd_rn(acc, -6.0));
+    }
+    const float f = __double2float_rn(v);
+    if constexpr (sizeof(T) == 4) {
+      out[i] = f;
+    } else {
+      bool nf = false;
+      out[i] = half_store(f, f, nf);
+    }
+  }
+}
+
+// ------------------------------------------------------- resolve ---
+// quant.hpp:71-109 and :241-244 with the CUDA double libm (the paper's
+// scale kernel). May differ from glibc by <= 1-2 ulp.
+__global__ void resolve_kernel(const __grid_constant__ ResolveDesc d, uint32_t* status) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= d.n) return;
+  const double ls = d.log_s[i];
+  if (!isfinite(ls)) {
+    atomicOr(status, kStatusNonFinite);
+    return;
+  }
+  const double sp = ls > 30.0 ? ls + log1p(exp(-ls)) : log1p(exp(ls));
+  const double raw = sp + d.eps;
+  double s = raw < d.lo ? d.lo : raw;
+  s = d.s_max < s ? d.s_max : s;
+  if (d.s32) d.s32[i] = (float)s;
+  if (d.s64) d.s64[i] = s;
+  if (d.chain) {
+    const bool clamped = !(raw > d.lo && raw < d.s_max);
+    double sg;
+    if (ls >= 0.0) {
+      sg = 1.0 / (1.0 + exp(-ls));
+    } else {
+      const double e = exp(ls);
+      sg = e / (1.0 + e);
+    }
+    d.chain[i] = clamped ? 0.0 : sg;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_ew(int dtype, const EwBatch& b, uint32_t* status, int grid,
+                      cudaStream_t st) {
+  if (dtype == 0) ew_kernel<float><<<grid, kEwThreads, 0, st>>>(b, status);
+  else ew_kernel<__half><<<grid, kEwThreads, 0, st>>>(b, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_codes(int dtype, const CodesDesc& d, int grid, cudaStream_t st) {
+  if (dtype == 0) codes_kernel<float><<<grid, kEwThreads, 0, st>>>(d);
+  else codes_kernel<__half><<<grid, kEwThreads, 0, st>>>(d);
+  return cudaGetLastError();
+}
+
+template <typename T>
+static void perop_dispatch(int op, const PerOpDesc& d, uint32_t* status, int grid,
+                           cudaStream_t st) {
+  switch (op) {
+    case 0: perop_kernel<T, 0><<<grid, kEwThreads, 0, st>>>(d, status); break;
+    case 1: perop_kernel<T, 1><<<grid, kEwThreads, 0, st>>>(d, status); break;
+    case 2: perop_kernel<T, 2><<<grid, kEwThreads, 0, st>>>(d, status); break;
+    default: perop_kernel<T, 3><<<grid, kEwThreads, 0, st>>>(d, status); break;
+  }
+}
+
+cudaError_t launch_perop(int dtype, int op, const PerOpDesc& d, uint32_t* status, int grid,
+                         cudaStream_t st) {
+  if (dtype == 0) perop_dispatch<float>(op, d, status, grid, st);
+  else perop_dispatch<__half>(op, d, status, grid, st);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_rng(int dtype, void* out, int64_t n, uint64_t seed, uint64_t stream,
+                            uint64_t offset, int kind, double lo, double hi, int grid,
+                            cudaStream_t st) {
+  // word(i) = mix(mix(seed ^ K) ^ mix(stream * G + i)), rng.hpp:29-32
+  const uint64_t seed_mix = [] (uint64_t x) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+  }(seed ^ 0x243f6a8885a308d3ull);
+  const uint64_t stream_term = stream * 0x9e3779b97f4a7c15ull;
+  if (dtype == 0)
+    fill_rng_kernel<float><<<grid, 256, 0, st>>>(static_cast<float*>(out), n, seed_mix,
+                                                 stream_term, offset, kind, lo, hi);
+  else
+    fill_rng_kernel<__half><<<grid, 256, 0, st>>>(static_cast<__half*>(out), n, seed_mix,
+                                                  stream_term, offset, kind, lo, hi);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_resolve(const ResolveDesc& d, uint32_t* status, cudaStream_t st) {
+  const int threads = 128;
+  const int grid = (int)((d.n + threads - 1) / threads);
+  if (grid > 0) resolve_kernel<<<grid, threads, 0, st>>>(d, status);
+  return cudaGetLastError();
+}
+
+}  // namespace qfb
+
+namespace qfb {
+// Occupancy of the elementwise kernel (sizes the persistent grid).
+cudaError_t ew_occupancy(int* blocks_per_sm) {
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, ew_kernel<float>,
+                                                       kEwThreads, 0);
+}
+}  // namespace qfb

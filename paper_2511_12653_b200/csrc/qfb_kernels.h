@@ -1,0 +1,153 @@
+// qfb_kernels.h — launch-level interface between the C-ABI host code
+// (qfb_api.cpp) and the sm_100a kernels (qfb_fwd.cu, qfb_bwd.cu).
+// Parameter tables are passed BY VALUE as __grid_constant__ kernel
+// parameters (<= 32 KB), so every launch is self-contained and CUDA-graph
+// capturable; nothing is staged through host-pinned memory.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace qfb {
+
+struct FastDivHost {
+  uint32_t d, m, s, pad;
+};
+
+inline FastDivHost make_fastdiv(uint32_t d) {
+  FastDivHost f{d, 0u, 0u, 0u};
+  if (d <= 1) {
+    f.d = 1;
+    return f;
+  }
+  uint32_t s = 0;
+  while ((1ull << s) < d) ++s;  // s = ceil(log2 d)
+  const uint64_t m = ((1ull << 32) * ((1ull << s) - d)) / d + 1;
+  f.m = (uint32_t)m;
+  f.s = s;
+  return f;
+}
+
+// ------------------------------------------------------ elementwise ----
+constexpr int kEwThreads = 256;
+constexpr int kEwUnroll = 4;
+constexpr int kEwChunk = kEwThreads * kEwUnroll;  // units per chunk
+constexpr int kMaxEwDesc = 96;
+
+constexpr uint32_t kEwHalfGrid = 0x1u;   // == QFB_FLAG_HALF_GRID
+constexpr uint32_t kEwStreaming = 0x2u;  // == QFB_FLAG_STREAMING
+constexpr uint32_t kEwDemoteIn = 0x100u; // chain: demote v before FQ
+
+// One fused elementwise job: v = act(a (+ b)) [demote]; preact = v;
+// y[j] = FQ(v, s[j][ch]) [half]. Plain FQ forward: b = preact = NULL,
+// act = none, no demote.
+struct EwDesc {
+  const void* a;
+  const void* b;
+  void* preact;
+  void* y[2];
+  const float* s[2];
+  uint32_t nunits;  // vector units (vec elements each) or elements (vec 1)
+  uint32_t vec;
+  FastDivHost inner_u;  // units per [inner] row
+  FastDivHost chans;    // channels
+  int32_t n_out;
+  int32_t act;
+  uint32_t flags;
+  float q;
+};
+
+struct EwBatch {
+  int32_t n;
+  int32_t pad;
+  uint32_t chunk_begin[kMaxEwDesc + 1];
+  EwDesc d[kMaxEwDesc];
+};
+
+// dtype: 0 f32, 1 f16.
+cudaError_t ew_occupancy(int* blocks_per_sm);
+cudaError_t launch_ew(int dtype, const EwBatch& b, uint32_t* status, int grid,
+                      cudaStream_t st);
+
+// int8 codes (vec path when aligned).
+struct CodesDesc {
+  const void* x;
+  int8_t* codes;
+  const float* s;
+  uint32_t nunits;
+  uint32_t vec;
+  FastDivHost inner_u;
+  FastDivHost chans;
+  float q;
+  uint32_t pad;
+};
+cudaError_t launch_codes(int dtype, const CodesDesc& d, int grid, cudaStream_t st);
+
+// Per-operator sweeps (exec.hpp:276-342): op 0 divide, 1 clip, 2 round,
+// 3 multiply. Elements are scalar; in/out float except op 0 input and
+// op 3 output which use dtype.
+struct PerOpDesc {
+  const void* in;
+  void* out;
+  const float* s;
+  uint64_t n;
+  uint64_t inner;
+  uint64_t chans;
+  float q;
+  uint32_t flags;
+};
+cudaError_t launch_perop(int dtype, int op, const PerOpDesc& d, uint32_t* status,
+                         int grid, cudaStream_t st);
+
+cudaError_t launch_fill_rng(int dtype, void* out, int64_t n, uint64_t seed, uint64_t stream,
+                            uint64_t offset, int kind, double lo, double hi, int grid,
+                            cudaStream_t st);
+
+struct ResolveDesc {
+  const double* log_s;
+  float* s32;
+  double* s64;
+  double* chain;
+  int64_t n;
+  double lo, s_max, eps;
+};
+cudaError_t launch_resolve(const ResolveDesc& d, uint32_t* status, cudaStream_t st);
+
+// --------------------------------------------------------- backward ----
+constexpr int kBwdThreads = 256;
+constexpr int kBwdGroupsLog = 8;  // leaf groups per full tile (= threads)
+constexpr int kLeafMax = 16;      // leaf-group size bound (two <=8 folds)
+constexpr int kBwdTileMax = kLeafMax << kBwdGroupsLog;  // 4096 elements
+constexpr int kMaxBwdDesc = 64;
+
+struct BwdDesc {
+  const void* x;
+  const void* up;
+  void* dx;
+  const double* s64;
+  const double* chain;
+  double* d_log_s;
+  double* partials;         // [segments * tps] when tps > 1
+  double* seg_results;      // [segments] when outer > 1
+  uint32_t* seg_counters;   // [segments] when tps > 1 (zero, self-resetting)
+  uint32_t* chan_counters;  // [channels] when outer > 1 (zero, self-resetting)
+  uint64_t inner;           // row (segment) length n
+  uint32_t outer;
+  uint32_t chans;
+  uint32_t tps_log;  // tiles per segment = 2^(depth - g)
+  uint32_t depth;    // tree depth of the 16-bounded leaf groups
+  uint32_t g;        // tile depth = min(depth, kBwdGroupsLog)
+  int32_t accumulate;
+  double q;
+};
+
+struct BwdBatch {
+  int32_t n;
+  int32_t pad;
+  uint32_t tile_begin[kMaxBwdDesc + 1];
+  BwdDesc d[kMaxBwdDesc];
+};
+
+cudaError_t launch_bwd(int dtype, const BwdBatch& b, cudaStream_t st);
+
+}  // namespace qfb

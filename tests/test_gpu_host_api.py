@@ -1,0 +1,59 @@
+"""GPU parity of the host-level (value-semantics) C-ABI entry points — the
+exact calls a reference user makes with host buffers (quant.hpp:136-294)."""
+import ctypes
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from test_gpu_fwd import bits32  # noqa: E402
+
+
+def _p(a):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def test_host_fwd_codes_bwd(qfb, orc, ref, cuda):
+    L = qfb.lib()
+    ctx = qfb.Context(0)
+    cfg = qfb.QuantConfig().to_c()
+    rng = np.random.default_rng(3)
+    C, H, W = 32, 60, 80
+    x = rng.normal(0, 1, (C, H, W)).astype(np.float32)
+    up = rng.normal(0, 1, (C, H, W)).astype(np.float32)
+    s = np.exp(rng.uniform(np.log(1e-3), np.log(0.1), C))
+    y = np.empty_like(x)
+    qfb.check(L.qfb_fake_quantize_host(ctx.handle, 0, _p(x), _p(y), 1, C, H * W,
+                                       s.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(cfg)))
+    _, want = ref.fake_quantize(x, [C, H, W], s, per_channel=True)
+    assert np.array_equal(bits32(y.ravel()), bits32(want))
+    codes = np.empty(x.size, dtype=np.int8)
+    qfb.check(L.qfb_int8_codes_host(ctx.handle, _p(x), _p(codes), 1, C, H * W,
+                                    s.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(cfg)))
+    _, cw = ref.int8_codes(x, [C, H, W], s, per_channel=True)
+    assert np.array_equal(codes, cw)
+    ls = np.log(np.expm1(s))
+    dx = np.empty_like(x)
+    dls = np.zeros(C)
+    qfb.check(L.qfb_fake_quantize_backward_host(
+        ctx.handle, 0, _p(x), _p(up), _p(dx), 1, C, H * W,
+        ls.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(cfg),
+        dls.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), 0))
+    _, wdx, wdls = ref.fq_backward(x, up, [C, H, W], ls, per_channel=True)
+    assert np.array_equal(bits32(dx.ravel()), bits32(wdx))
+    assert dls.tobytes() == wdls.tobytes()     # bit-identical to the reference itself
+    # half path: NaN -> NonFiniteError like demote_half
+    xh = x.astype(np.float16).astype(np.float32)
+    xh[0, 0, 0] = np.nan
+    st = L.qfb_fake_quantize_host(ctx.handle, 1, _p(xh), _p(y), 1, C, H * W,
+                                  s.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(cfg))
+    assert st == 4
+    # bad scale -> ValueError before any compute
+    s_bad = s.copy()
+    s_bad[1] = 0.0
+    st = L.qfb_fake_quantize_host(ctx.handle, 0, _p(x), _p(y), 1, C, H * W,
+                                  s_bad.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(cfg))
+    assert st == 2
+    ctx.close()
