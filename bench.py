@@ -1,0 +1,469 @@
+#!/usr/bin/env python3
+"""bench.py — DPVO front-end fused fake-quant throughput on B200.
+
+Metric (BASELINE.json): "fake-quant GB/s (% of HBM peak) and front-end
+frames/sec at 1/2/4/8 B200 vs CPU ref". One STEP = the hot path over one
+480x640 frame of BASELINE config 2: per-channel fake-quant forward over the
+22 activation quant points of both DPVO encoders (19 tensors, one fused
+launch) + the scale-only LSQ/STE backward over the same 22 points (one
+launch, bit-exact pairwise-tree scale gradients) [+ at N>1 the NCCL
+all-reduce of the 902 per-channel scale gradients, the QAT exchange step].
+`value` = frames/s of the whole job; GB/s and the HBM-roofline fraction are
+reported beside it.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--dtype f32|f16]
+  python bench.py --impl reference ...   # the reference's own CPU code
+
+Under torchrun each rank drives one GPU; frames shard across ranks (weak
+scaling, no data-path collective). Timing: CUDA events on the library's
+stream, barrier + synchronize on both sides, max over ranks. Inputs are
+rotated over >= 2 independent frame sets (> 1.2 GB, >> 126 MB L2).
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fake-quant GB/s (% of HBM peak) and front-end frames/sec at 1/2/4/8 B200 vs CPU ref"
+UNIT = "frames/s"
+WORKLOAD = ("BASELINE config 2: per-channel fake-quant fwd + scale-only LSQ/STE bwd over the 22 "
+            "DPVO encoder activation quant points of one 480x640 frame (41,164,800 quant-point elems)")
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=1000)
+    p.add_argument("--warmup", type=int, default=20)
+    p.add_argument("--impl", default="qfb", choices=["qfb", "reference"])
+    p.add_argument("--dtype", default="f32", choices=["f32", "f16"])
+    p.add_argument("--sets", type=int, default=2, help="rotating input sets (L2 defeat)")
+    p.add_argument("--e2e-steps", type=int, default=10)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=15.0)
+    return p.parse_args()
+
+
+# ------------------------------------------------------------- helpers --
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic():
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu
+    capture summary (profiles/ncu_traffic.json), else None."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons DURING the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.06)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------ reference (CPU) --
+
+class RefCpuWorkload:
+    """The reference's own per-channel fake_quantize (quant.hpp:150) and
+    fake_quantize_backward (quant.hpp:261), compiled -O3 from its sources
+    (oracle/_ref), over the frame's 22 quant points. Work items are
+    4-channel blocks (the per-channel ops are independent per channel, so
+    blocking does not change the work), pulled by `threads` host threads.
+    A bounded sample (a fixed subset of blocks, sized to `budget_s`) is
+    timed and converted to frames/s = frames-worth of elements / seconds."""
+
+    def __init__(self, consumers, threads, dtype="f32", seed=7):
+        import numpy as np
+        import oracle
+        self.ref = oracle.Reference()
+        self.threads = threads
+        self.half = 1 if dtype == "f16" else 0
+        rng = np.random.default_rng(seed)
+        self.items = []
+        self.frame_elems = sum(p.numel for (p, _c) in consumers)
+        xs = {}
+        for (p, _c) in consumers:
+            if p.name not in xs:
+                xs[p.name] = rng.standard_normal((p.channels, p.inner), dtype=np.float32)
+            x = xs[p.name]
+            up = rng.standard_normal((p.channels, p.inner), dtype=np.float32)
+            ls = np.log(np.expm1(np.exp(rng.uniform(np.log(1e-3), np.log(0.1), p.channels))))
+            for c0 in range(0, p.channels, 4):
+                c1 = min(c0 + 4, p.channels)
+                self.items.append((np.ascontiguousarray(x[c0:c1]), np.ascontiguousarray(up[c0:c1]),
+                                   c1 - c0, p.inner, np.ascontiguousarray(ls[c0:c1])))
+        order = list(range(len(self.items)))
+        rng.shuffle(order)
+        self.order = order
+        self.sel = order
+
+    def _run(self, idx):
+        sel = [self.items[i] for i in idx]
+        st, secs, _ = self.ref.bench_points([s[0] for s in sel], [s[1] for s in sel],
+                                            [s[2] for s in sel], [s[3] for s in sel],
+                                            [s[4] for s in sel], half=self.half,
+                                            threads=self.threads, reps=1)
+        assert st == 0, f"reference bench failed: {st}"
+        return secs, sum(s[2] * s[3] for s in sel)
+
+    def size(self, budget_s):
+        probe = self.order[:max(2 * self.threads, 8)]
+        secs, elems = self._run(probe)
+        want = elems / max(secs, 1e-9) * budget_s
+        acc, k = 0, 0
+        while k < len(self.order) and acc < want:
+            it = self.items[self.order[k]]
+            acc += it[2] * it[3]
+            k += 1
+        self.sel = self.order[:max(k, min(len(self.order), self.threads))]
+        return self
+
+    def run(self):
+        secs, elems = self._run(self.sel)
+        return secs, elems / self.frame_elems
+
+    def describe(self, secs, frames):
+        return (f"{frames:.3f} frames-worth of quant-point elements ({len(self.sel)} of "
+                f"{len(self.items)} 4-channel blocks) in {secs:.2f} s on {self.threads} threads; "
+                f"reference quant.hpp fake_quantize + fake_quantize_backward, -O3 from its sources")
+
+
+def cpu_reference_frames_per_s(consumers, budget_s, threads, dtype="f32"):
+    import oracle
+    if not oracle.reference_available():
+        return None
+    w = RefCpuWorkload(consumers, threads, dtype).size(budget_s)
+    secs, frames = w.run()
+    return {"value": frames / secs, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": w.describe(secs, frames)}
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference_arm(args):
+    """--impl reference: the reference CPU implementation on the host cores,
+    same metric/unit/config; each step a bounded sample of the workload."""
+    import oracle
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    if not oracle.reference_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libqfref.so missing"}))
+        return 0
+    from paper_2511_12653_b200.frontend import dpvo_quant_points
+    pts = dpvo_quant_points()
+    consumers = [(p, c) for p in pts for c in p.consumers]
+    threads = host_threads()
+    per_step = max(0.02, min(2.0, 120.0 / max(1, args.steps + args.warmup)))
+    w = RefCpuWorkload(consumers, threads, args.dtype).size(per_step)
+    for _ in range(args.warmup):
+        w.run()
+    tot_s, tot_f = 0.0, 0.0
+    for _ in range(args.steps):
+        s, f = w.run()
+        tot_s += s
+        tot_f += f
+    fps = tot_f / tot_s
+    line = {"metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1000.0 / fps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+            "config": {"workload": WORKLOAD, "host_threads": threads},
+            "impl": "reference",
+            "cpu_baseline": {"value": fps, "unit": UNIT, "cores": threads, "kind": "reference",
+                             "sample": "per step: " + w.describe(tot_s / args.steps,
+                                                                 tot_f / args.steps)},
+            "e2e": {"value": fps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+# --------------------------------------------------------- our arm (GPU) --
+
+def run_qfb(args):
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    import paper_2511_12653_b200 as q
+    from paper_2511_12653_b200.dist import gather_fold
+    from paper_2511_12653_b200.frontend import FrontendQuantPass
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    ctx = q.Context(local, stream.cuda_stream)
+    fp = FrontendQuantPass(ctx, frames=1, dtype=args.dtype, sets=max(1, args.sets),
+                           seed=1 + 7919 * rank, device=dev)
+    grads = fp.scale_grads()
+    nsets = len(fp.sets)
+
+    def step(i, ev=None):
+        si = i % nsets
+        if ev is not None:
+            ev[0].record(stream)
+        fp.forward(si)
+        if ev is not None:
+            ev[1].record(stream)
+        fp.backward(si)
+        if ev is not None:
+            ev[2].record(stream)
+        if pg is not None:
+            # QAT exchange: per-frame scale-gradient rows, all-gathered and
+            # folded in frame order (bit-identical at any GPU count)
+            gather_fold(torch.cat(fp.dls).unsqueeze(0))
+
+    for i in range(args.warmup):
+        step(i)
+    ctx.sync()
+    if pg is not None:
+        pg.barrier()
+    torch.cuda.synchronize(dev)
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.15)  # let the sampler attach before the timed region
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    launches0 = ctx.launch_count
+    wall0 = time.perf_counter()
+    t_start.record(stream)
+    for i in range(args.steps):
+        step(i, evs[i])
+    t_end.record(stream)
+    torch.cuda.synchronize(dev)
+    wall1 = time.perf_counter()
+    clocks = sampler.stop()
+    launches = ctx.launch_count - launches0
+    ctx.sync()
+    ms_total = t_start.elapsed_time(t_end)
+    fwd_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
+    bwd_ms = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
+    if pg is not None:
+        t = torch.tensor([ms_total], device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        ms_total = t.item()
+        pg.barrier()
+    ms_step = ms_total / args.steps
+    frames_total = ws * args.steps * fp.frames
+    fps = frames_total / (ms_total / 1000.0)
+    b = fp.bytes_per_step()
+    step_bytes = b["fwd"] + b["bwd"]
+    gbps = ws * step_bytes / (ms_step / 1000.0) / 1e9
+    peak, peak_src = load_peaks()
+    fwd_gbps = b["fwd"] / (fwd_ms / 1000.0) / 1e9
+    bwd_gbps = b["bwd"] / (bwd_ms / 1000.0) / 1e9
+    traffic = load_traffic()
+    dominant = "bwd" if b["bwd"] >= b["fwd"] else "fwd"
+    roofline = {"bound": "hbm", "kernel": "qfb::bwd_kernel (scale-only LSQ/STE backward)",
+                "achieved": bwd_gbps, "peak": peak, "unit": "GB/s", "frac": bwd_gbps / peak,
+                "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": b["bwd"],
+                "traffic": (traffic or {}).get(args.dtype, {}).get("bwd_bytes_per_launch"),
+                "fwd_kernel": {"kernel": "qfb::ew_kernel (fused multi-point forward)",
+                               "achieved": fwd_gbps, "frac": fwd_gbps / peak,
+                               "algorithmic_bytes_per_launch": b["fwd"],
+                               "traffic": (traffic or {}).get(args.dtype, {}).get("fwd_bytes_per_launch")},
+                "step_gbps": gbps / ws, "step_frac": (gbps / ws) / peak}
+
+    # ---------------------------------------------------- e2e (host API) --
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, q, ctx, fp, stream, dev, pg, ws)
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        cons = [(p, c) for p in fp.points for c in p.consumers]
+        try:
+            cpu = cpu_reference_frames_per_s(cons, args.cpu_seconds, host_threads(), args.dtype)
+        except Exception as exc:  # pragma: no cover
+            cpu = {"value": None, "unit": UNIT, "cores": host_threads(), "kind": "reference",
+                   "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
+                "data": "synthetic (CounterRng normal, rng.hpp:24-50, generated on device)",
+                "config": {"workload": WORKLOAD, "frames_per_step_per_gpu": fp.frames,
+                           "quant_points": len(fp.consumers), "tensors": len(fp.points),
+                           "scales": "per-channel, log-uniform [1e-3, 0.1]",
+                           "l2_policy": f"inputs > L2: {nsets} rotating frame sets, "
+                                        f"{step_bytes / 1e6:.0f} MB moved per step vs 126 MB L2",
+                           "parallelism": f"frames sharded over {ws} GPU(s); NCCL all-gather + frame-order fold "
+                                          f"of {int(grads.numel())} fp64 scale grads per step" if ws > 1
+                           else "1 GPU"},
+                "gbps": gbps, "hbm_frac": (gbps / ws) / peak,
+                "kernel_ms": {"fwd": fwd_ms, "bwd": bwd_ms},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches, "clocks": clocks,
+                "wall_ms_per_step": (wall1 - wall0) * 1000.0 / args.steps}
+        print(json.dumps(line))
+    if pg is not None:
+        pg.barrier()
+        pg.destroy_process_group()
+    ctx.close()
+    return 0
+
+
+def run_e2e(args, q, ctx, fp, stream, dev, pg, ws):
+    """Same workload through the reference-facing host C-ABI
+    (qfb_fake_quantize_host / qfb_fake_quantize_backward_host): host (pinned)
+    buffers in, host buffers out, every copy inside the timed region."""
+    import ctypes
+
+    import numpy as np
+    import torch
+    L = q.lib()
+    cfg = q.QuantConfig().to_c()
+    hx = {p.name: torch.empty(p.numel, dtype=torch.float32).pin_memory() for p in fp.points}
+    for pi, p in enumerate(fp.points):
+        hx[p.name].copy_(fp.sets[0]["x"][pi].reshape(-1).float().cpu())
+    hup, hy, hdx, ls, sc, dls = [], [], [], [], [], []
+    for ci, (p, _c) in enumerate(fp.consumers):
+        hup.append(fp.sets[0]["up"][ci].reshape(-1).float().cpu().pin_memory())
+        hy.append(torch.empty(p.numel, dtype=torch.float32).pin_memory())
+        hdx.append(torch.empty(p.numel, dtype=torch.float32).pin_memory())
+        lsv = np.ascontiguousarray(fp.log_s[ci], dtype=np.float64)
+        ls.append(lsv)
+        sc.append(np.array(q.resolve_scale(lsv.tolist()), dtype=np.float64))
+        dls.append(np.zeros(p.channels, dtype=np.float64))
+    dp = ctypes.POINTER(ctypes.c_double)
+    prec = 1 if args.dtype == "f16" else 0
+
+    def e2e_step():
+        for ci, (p, _c) in enumerate(fp.consumers):
+            x = hx[p.name]
+            q.check(L.qfb_fake_quantize_host(ctx.handle, prec, x.data_ptr(), hy[ci].data_ptr(), 1,
+                                             p.channels, p.inner, sc[ci].ctypes.data_as(dp),
+                                             ctypes.byref(cfg)))
+            q.check(L.qfb_fake_quantize_backward_host(
+                ctx.handle, prec, x.data_ptr(), hup[ci].data_ptr(), hdx[ci].data_ptr(), 1,
+                p.channels, p.inner, ls[ci].ctypes.data_as(dp), ctypes.byref(cfg),
+                dls[ci].ctypes.data_as(dp), 0))
+        if pg is not None:
+            from paper_2511_12653_b200.dist import gather_fold
+            gather_fold(torch.from_numpy(np.concatenate(dls)).to(dev).unsqueeze(0))
+
+    e2e_step()
+    if pg is not None:
+        pg.barrier()
+    torch.cuda.synchronize(dev)
+    k = max(3, args.e2e_steps)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(k):
+        e2e_step()
+    t1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = t0.elapsed_time(t1)
+    if pg is not None:
+        t = torch.tensor([ms], device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        ms = t.item()
+    h2d = sum(p.numel * 4 * 3 for (p, _c) in fp.consumers)   # x (fwd), x + up (bwd)
+    d2h = sum(p.numel * 4 * 2 + p.channels * 8 for (p, _c) in fp.consumers)
+    return {"value": ws * k / (ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "steps": k,
+            "api": "qfb_fake_quantize_host + qfb_fake_quantize_backward_host per quant point "
+                   "(float32 pinned host buffers)"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_qfb(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

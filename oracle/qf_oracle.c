@@ -121,7 +121,9 @@ float orc_f16_bits_to_f32(uint16_t h) {
   if (e == 0) {
     mag = ldexpf((float)m, -24);
   } else if (e == 31) {
-    mag = m ? NAN : INFINITY;
+    /* inf / NaN: keep the payload bits (half.hpp:62-63) */
+    const uint32_t u = 0x7f800000u | ((uint32_t)m << 13);
+    memcpy(&mag, &u, sizeof mag);
   } else {
     mag = ldexpf((float)(1024 + m), e - 25);
   }

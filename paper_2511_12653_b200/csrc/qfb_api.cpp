@@ -68,7 +68,8 @@ struct qfb_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   int sm_count = 148;
-  int ew_blocks_per_sm = 4;
+  int ew_blocks_per_sm[2][2] = {{4, 4}, {4, 4}};  // [dtype][chain]
+  int bwd_blocks_per_sm[2] = {4, 4};
   uint32_t* d_status = nullptr;
   uint32_t* h_status = nullptr;  // pinned
   DevBuf ws_f64;                 // partials / segment results
@@ -196,7 +197,7 @@ qfb_status plan_ew(int dtype, const EwJob& j, std::vector<EwDesc>& out) {
   return QFB_OK;
 }
 
-qfb_status run_ew(qfb_ctx* ctx, int dtype, const std::vector<EwDesc>& descs) {
+qfb_status run_ew(qfb_ctx* ctx, int dtype, const std::vector<EwDesc>& descs, bool chain) {
   size_t i = 0;
   while (i < descs.size()) {
     EwBatch b;
@@ -211,8 +212,9 @@ qfb_status run_ew(qfb_ctx* ctx, int dtype, const std::vector<EwDesc>& descs) {
     b.n = n;
     b.chunk_begin[n] = chunks;
     if (chunks == 0) continue;
-    const int grid = (int)std::min<uint64_t>(chunks, (uint64_t)ctx->sm_count * ctx->ew_blocks_per_sm);
-    cudaError_t e = launch_ew(dtype, b, ctx->d_status, grid, ctx->stream);
+    const int grid = (int)std::min<uint64_t>(
+        chunks, (uint64_t)ctx->sm_count * ctx->ew_blocks_per_sm[dtype][chain ? 1 : 0]);
+    cudaError_t e = launch_ew(dtype, chain, b, ctx->d_status, grid, ctx->stream);
     if (e != cudaSuccess) return cuda_fail(e, "ew_kernel launch");
     ctx->launches++;
   }
@@ -352,9 +354,16 @@ qfb_status qfb_ctx_create(int32_t device, void* stream, qfb_ctx** out) {
   c->stream = static_cast<cudaStream_t>(stream);
   cudaError_t e = cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
   if (e == cudaSuccess) {
-    int per = 0;
-    // occupancy of the elementwise kernel decides the persistent grid
-    if (ew_occupancy(&per) == cudaSuccess && per > 0) c->ew_blocks_per_sm = per;
+    // occupancy of each elementwise kernel variant sizes its persistent grid
+    for (int dt = 0; dt < 2; ++dt)
+      for (int ch = 0; ch < 2; ++ch) {
+        int per = 0;
+        if (ew_occupancy(dt, ch != 0, &per) == cudaSuccess && per > 0) c->ew_blocks_per_sm[dt][ch] = per;
+      }
+    for (int dt = 0; dt < 2; ++dt) {
+      int per = 0;
+      if (bwd_occupancy(dt, &per) == cudaSuccess && per > 0) c->bwd_blocks_per_sm[dt] = per;
+    }
   }
   if (e == cudaSuccess) e = cudaMalloc(&c->d_status, sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMallocHost(&c->h_status, sizeof(uint32_t));
@@ -422,7 +431,7 @@ qfb_status qfb_fq_fwd(qfb_ctx* ctx, qfb_dtype dtype, const void* x, void* y, int
   std::vector<EwDesc> d;
   if (qfb_status st = plan_ew(dtype, j, d)) return st;
   DeviceGuard g(ctx->device);
-  return run_ew(ctx, dtype, d);
+  return run_ew(ctx, dtype, d, false);
 }
 
 qfb_status qfb_fq_fwd_multi(qfb_ctx* ctx, qfb_dtype dtype, const qfb_fq_desc* table, int32_t n) {
@@ -443,7 +452,7 @@ qfb_status qfb_fq_fwd_multi(qfb_ctx* ctx, qfb_dtype dtype, const qfb_fq_desc* ta
     if (qfb_status st = plan_ew(dtype, j, d)) return st;
   }
   DeviceGuard g(ctx->device);
-  return run_ew(ctx, dtype, d);
+  return run_ew(ctx, dtype, d, false);
 }
 
 static qfb_status chain_job(const qfb_chain_desc& t, EwJob& j) {
@@ -485,7 +494,7 @@ qfb_status qfb_fq_chain_multi(qfb_ctx* ctx, const qfb_chain_desc* table, int32_t
     }
     if (d.empty()) continue;
     DeviceGuard g(ctx->device);
-    if (qfb_status st = run_ew(ctx, dt, d)) return st;
+    if (qfb_status st = run_ew(ctx, dt, d, true)) return st;
   }
   return QFB_OK;
 }
@@ -623,6 +632,7 @@ qfb_status plan_bwd(const qfb_bwd_desc& t, BwdPlan& p) {
   d.tps_log = d.depth - d.g;
   d.accumulate = t.accumulate ? 1 : 0;
   d.q = (double)t.q_max;
+  d.vec = (aligned16(t.x) && aligned16(t.up) && (!t.dx || aligned16(t.dx))) ? 1u : 0u;
   const uint64_t tps = 1ull << d.tps_log;
   p.tiles = segs * tps;
   if (p.tiles >= (1ull << 31)) return fail(QFB_ERR_UNSUPPORTED, "too many tiles");
@@ -690,7 +700,8 @@ qfb_status qfb_fq_bwd_multi(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc* t
     }
     b.n = cnt;
     b.tile_begin[cnt] = (uint32_t)tb;
-    cudaError_t e = launch_bwd(dtype, b, ctx->stream);
+    const int grid = ctx->sm_count * ctx->bwd_blocks_per_sm[dtype];
+    cudaError_t e = launch_bwd(dtype, b, grid, ctx->stream);
     if (e != cudaSuccess) return cuda_fail(e, "bwd_kernel launch");
     ctx->launches++;
     i += cnt;

@@ -29,9 +29,61 @@ __device__ __forceinline__ float fq_clip(float z, float q) {
   return z;
 }
 
+// x86 NaN propagation (the reference's host semantics): an operation with
+// one NaN operand returns that operand quieted (sign and payload kept); an
+// invalid operation (inf - inf, 0 * inf) returns the x86 default NaN
+// 0xffc00000. The GPU instead returns a canonical 0x7fffffff, so the paths
+// whose NaN bits are observable emulate the host rule explicitly.
+__device__ __forceinline__ float quiet_nan(float v) {
+  return __uint_as_float(__float_as_uint(v) | 0x400000u);
+}
+constexpr uint32_t kX86DefaultNaN = 0xffc00000u;
+
+__device__ __forceinline__ float x86_add(float a, float b) {
+  const float r = __fadd_rn(a, b);
+  if (!isnan(r)) return r;
+  return isnan(a) ? quiet_nan(a) : isnan(b) ? quiet_nan(b) : __uint_as_float(kX86DefaultNaN);
+}
+
+// NaN in -> the same NaN (quieted) out, exactly as x/s, the selects,
+// nearbyintf and s*r propagate it on the host.
 __device__ __forceinline__ float fq_value(float x, float s, float q) {
+  if (isnan(x)) return quiet_nan(x);
   const float z = __fdiv_rn(x, s);
   return __fmul_rn(s, rintf(fq_clip(z, q)));
+}
+
+// Division shortcut for the hot forward: Markstein-corrected quotient with
+// a hoisted correctly rounded reciprocal y = __frcp_rn(s) — one FMUL + two
+// FFMA per element instead of MUFU.RCP + refinement + FCHK + branch.
+// Bit-identical to __fdiv_rn for every normal x, s with a normal quotient:
+// proven by exhaustion over all 2^46 significand pairs (tools/verify_div.cu,
+// result in profiles/).
+__device__ __forceinline__ float markstein_div(float x, float s, float y) {
+  const float q0 = __fmul_rn(x, y);
+  const float r = __fmaf_rn(-s, q0, x);
+  return __fmaf_rn(r, y, q0);
+}
+
+// Scales for which the shortcut is used (y finite and normal).
+__device__ __forceinline__ bool fast_div_ok(float s) {
+  return s >= 0x1p-100f && s <= 0x1p100f;
+}
+
+// fq_value via the shortcut; requires fast_div_ok(s) and y = __frcp_rn(s).
+// Outside the proven range the quotient only feeds rint(clip(.)):
+//  - |q0| >= 2^100 (incl. inf): clip saturates to +-q for both paths;
+//  - subnormal/tiny quotients: |z| < 0.5 rounds to +-0 for both paths, and
+//    copysign restores the sign of x that FMA-based correction can lose on
+//    signed zeros. tools/verify_div.cu test 2 checks every 2^32 x.
+__device__ __forceinline__ float fq_value_fast(float x, float s, float y, float q) {
+  if (isnan(x)) return quiet_nan(x);
+  const float q0 = __fmul_rn(x, y);
+  float z = __fmaf_rn(__fmaf_rn(-s, q0, x), y, q0);
+  z = fabsf(q0) < 0x1p100f ? z : q0;
+  z = copysignf(z, x);
+  z = fminf(fmaxf(z, -q), q);  // never NaN here: select clip == min/max
+  return __fmul_rn(s, rintf(z));
 }
 
 // ----------------------------------------------------------- binary16 ---
@@ -65,6 +117,15 @@ __device__ __forceinline__ int8_t fq_code(float x, float s, float q) {
 // ----------------------------------------------- STE / LSQ terms ---
 // quant.hpp:217-228 in double: z = x/s, mask = |z| <= q,
 // d_ds = mask ? rint(z) - z : (z > 0 ? q : -q).
+// d_input = float(mask * double(up)) with host NaN rules: NaN upstream
+// propagates (quieted); a masked-out inf gives 0*inf = default NaN.
+__device__ __forceinline__ float masked_upstream(bool mask, float up) {
+  if (isnan(up)) return quiet_nan(up);
+  if (mask) return up;
+  if (isinf(up)) return __uint_as_float(kX86DefaultNaN);
+  return __fmul_rn(0.0f, up);  // +-0 with the sign of up
+}
+
 struct GradTerm {
   bool mask;
   double d_ds;

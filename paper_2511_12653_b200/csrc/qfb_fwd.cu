@@ -31,22 +31,40 @@ __device__ __forceinline__ float apply_act(float v, int act) {
   return v;
 }
 
+// FQ of one unit (V elements sharing scale s): division shortcut with the
+// reciprocal hoisted per unit when the scale is in the proven range.
+template <int V>
+__device__ __forceinline__ void fq_unit(const float* v, float s, float q, float* o) {
+  if (fast_div_ok(s)) {
+    const float y = __frcp_rn(s);
+#pragma unroll
+    for (int i = 0; i < V; ++i) o[i] = fq_value_fast(v[i], s, y, q);
+  } else {
+#pragma unroll
+    for (int i = 0; i < V; ++i) o[i] = fq_value(v[i], s, q);
+  }
+}
+
 // Vector path: every unit is one 16-byte vector, all its elements share a
 // channel (host guarantees inner % kPerVec == 0 and 16-byte alignment).
-template <typename T>
+// kChain = false is the plain multi-output fake-quant forward (no b, no
+// activation, no preact, no demotion): fewer live registers, more CTAs/SM.
+template <typename T, bool kChain>
 __device__ __forceinline__ void ew_vec(const EwDesc& d, uint32_t ubase, bool& nf) {
   constexpr int V = Elem<T>::kPerVec;
-  const bool has_b = d.b != nullptr;
   const bool streaming = (d.flags & kEwStreaming) != 0;
   const bool half_out = (d.flags & kEwHalfGrid) != 0;
-  const bool demote_in = (d.flags & kEwDemoteIn) != 0;
-  uint4 ra[kEwUnroll], rb[kEwUnroll];
+  uint4 ra[kEwUnroll];
+  uint4 rb[kChain ? kEwUnroll : 1];
+  const bool has_b = kChain && d.b != nullptr;
 #pragma unroll
   for (int k = 0; k < kEwUnroll; ++k) {
     const uint32_t u = ubase + k * kEwThreads;
     if (u < d.nunits) {
       ra[k] = ld_nc_v4(static_cast<const uint4*>(d.a) + u);
-      if (has_b) rb[k] = ld_nc_v4(static_cast<const uint4*>(d.b) + u);
+      if constexpr (kChain) {
+        if (has_b) rb[k] = ld_nc_v4(static_cast<const uint4*>(d.b) + u);
+      }
     }
   }
 #pragma unroll
@@ -56,28 +74,28 @@ __device__ __forceinline__ void ew_vec(const EwDesc& d, uint32_t ubase, bool& nf
     const uint32_t ch = channel_of(u, d.inner_u, d.chans);
     float v[V];
     Elem<T>::unpack(ra[k], v);
-    if (has_b) {
-      float w[V];
-      Elem<T>::unpack(rb[k], w);
+    if constexpr (kChain) {
+      if (has_b) {
+        float w[V];
+        Elem<T>::unpack(rb[k], w);
 #pragma unroll
-      for (int i = 0; i < V; ++i) v[i] = __fadd_rn(v[i], w[i]);  // tensor.hpp:126-134
-    }
-    if (d.act != 0) {
+        for (int i = 0; i < V; ++i) v[i] = x86_add(v[i], w[i]);  // tensor.hpp:126-134
+      }
+      if (d.act != 0) {
 #pragma unroll
-      for (int i = 0; i < V; ++i) v[i] = apply_act(v[i], d.act);
-    }
-    if (demote_in) {
+        for (int i = 0; i < V; ++i) v[i] = apply_act(v[i], d.act);
+      }
+      if (d.flags & kEwDemoteIn) {
 #pragma unroll
-      for (int i = 0; i < V; ++i) v[i] = half_grid(v[i], v[i], nf);  // tensor.hpp:159-170
-    }
-    if (d.preact != nullptr) {
-      st_v4(static_cast<uint4*>(d.preact) + u, Elem<T>::pack(v, v, false, nf), streaming);
+        for (int i = 0; i < V; ++i) v[i] = half_grid(v[i], v[i], nf);  // tensor.hpp:159-170
+      }
+      if (d.preact != nullptr) {
+        st_v4(static_cast<uint4*>(d.preact) + u, Elem<T>::pack(v, v, false, nf), streaming);
+      }
     }
     for (int j = 0; j < d.n_out; ++j) {
-      const float s = __ldg(d.s[j] + ch);
       float o[V];
-#pragma unroll
-      for (int i = 0; i < V; ++i) o[i] = fq_value(v[i], s, d.q);
+      fq_unit<V>(v, __ldg(d.s[j] + ch), d.q, o);
       st_v4(static_cast<uint4*>(d.y[j]) + u, Elem<T>::pack(o, v, half_out, nf), streaming);
     }
   }
@@ -104,19 +122,20 @@ __device__ __forceinline__ void ew_scalar(const EwDesc& d, uint32_t ubase, bool&
     if (u >= d.nunits) break;
     const uint32_t ch = channel_of(u, d.inner_u, d.chans);
     float v = va[k];
-    if (has_b) v = __fadd_rn(v, vb[k]);
+    if (has_b) v = x86_add(v, vb[k]);
     v = apply_act(v, d.act);
     if (demote_in) v = half_grid(v, v, nf);
     if (d.preact != nullptr) Elem<T>::store1(d.preact, u, v, v, false, nf);
     for (int j = 0; j < d.n_out; ++j) {
-      const float s = __ldg(d.s[j] + ch);
-      Elem<T>::store1(d.y[j], u, fq_value(v, s, d.q), v, half_out, nf);
+      float o;
+      fq_unit<1>(&v, __ldg(d.s[j] + ch), d.q, &o);
+      Elem<T>::store1(d.y[j], u, o, v, half_out, nf);
     }
   }
 }
 
-template <typename T>
-__global__ void __launch_bounds__(kEwThreads) ew_kernel(const __grid_constant__ EwBatch bt,
+template <typename T, bool kChain>
+__global__ void __launch_bounds__(kEwThreads, kChain ? 3 : 4) ew_kernel(const __grid_constant__ EwBatch bt,
                                                         uint32_t* __restrict__ status) {
   bool nf = false;
   const uint32_t total = bt.chunk_begin[bt.n];
@@ -129,7 +148,7 @@ __global__ void __launch_bounds__(kEwThreads) ew_kernel(const __grid_constant__ 
     }
     const EwDesc& d = bt.d[lo];
     const uint32_t ubase = (chunk - bt.chunk_begin[lo]) * kEwChunk + threadIdx.x;
-    if (d.vec > 1) ew_vec<T>(d, ubase, nf);
+    if (d.vec > 1) ew_vec<T, kChain>(d, ubase, nf);
     else ew_scalar<T>(d, ubase, nf);
   }
   if (nf) atomicOr(status, kStatusNonFinite);
@@ -188,7 +207,7 @@ __global__ void __launch_bounds__(kEwThreads)
       static_cast<float*>(d.out)[i] = isnan(c) ? c : rintf(c);
     } else {
       const float r = static_cast<const float*>(d.in)[i];
-      const float v = __fmul_rn(__ldg(d.s + ch), r);
+      const float v = isnan(r) ? r : __fmul_rn(__ldg(d.s + ch), r);
       // sign source: NaN results come from a NaN input; r carries its sign
       Elem<T>::store1(d.out, i, v, r, (d.flags & kEwHalfGrid) != 0, nf);
     }
@@ -266,10 +285,15 @@ __global__ void resolve_kernel(const __grid_constant__ ResolveDesc d, uint32_t* 
 
 }  // namespace
 
-cudaError_t launch_ew(int dtype, const EwBatch& b, uint32_t* status, int grid,
+cudaError_t launch_ew(int dtype, bool chain, const EwBatch& b, uint32_t* status, int grid,
                       cudaStream_t st) {
-  if (dtype == 0) ew_kernel<float><<<grid, kEwThreads, 0, st>>>(b, status);
-  else ew_kernel<__half><<<grid, kEwThreads, 0, st>>>(b, status);
+  if (chain) {
+    if (dtype == 0) ew_kernel<float, true><<<grid, kEwThreads, 0, st>>>(b, status);
+    else ew_kernel<__half, true><<<grid, kEwThreads, 0, st>>>(b, status);
+  } else {
+    if (dtype == 0) ew_kernel<float, false><<<grid, kEwThreads, 0, st>>>(b, status);
+    else ew_kernel<__half, false><<<grid, kEwThreads, 0, st>>>(b, status);
+  }
   return cudaGetLastError();
 }
 
@@ -328,8 +352,9 @@ cudaError_t launch_resolve(const ResolveDesc& d, uint32_t* status, cudaStream_t 
 
 namespace qfb {
 // Occupancy of the elementwise kernel (sizes the persistent grid).
-cudaError_t ew_occupancy(int* blocks_per_sm) {
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, ew_kernel<float>,
-                                                       kEwThreads, 0);
+cudaError_t ew_occupancy(int dtype, bool chain, int* blocks_per_sm) {
+  const void* f = chain ? (dtype == 0 ? (const void*)ew_kernel<float, true> : (const void*)ew_kernel<__half, true>)
+                        : (dtype == 0 ? (const void*)ew_kernel<float, false> : (const void*)ew_kernel<__half, false>);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, kEwThreads, 0);
 }
 }  // namespace qfb

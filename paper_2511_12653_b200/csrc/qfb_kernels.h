@@ -65,8 +65,8 @@ struct EwBatch {
 };
 
 // dtype: 0 f32, 1 f16.
-cudaError_t ew_occupancy(int* blocks_per_sm);
-cudaError_t launch_ew(int dtype, const EwBatch& b, uint32_t* status, int grid,
+cudaError_t ew_occupancy(int dtype, bool chain, int* blocks_per_sm);
+cudaError_t launch_ew(int dtype, bool chain, const EwBatch& b, uint32_t* status, int grid,
                       cudaStream_t st);
 
 // int8 codes (vec path when aligned).
@@ -139,6 +139,8 @@ struct BwdDesc {
   uint32_t g;        // tile depth = min(depth, kBwdGroupsLog)
   int32_t accumulate;
   double q;
+  uint32_t vec;  // x/up/dx 16-byte aligned: vector-window loads
+  uint32_t pad;
 };
 
 struct BwdBatch {
@@ -148,6 +150,7 @@ struct BwdBatch {
   BwdDesc d[kMaxBwdDesc];
 };
 
-cudaError_t launch_bwd(int dtype, const BwdBatch& b, cudaStream_t st);
+cudaError_t bwd_occupancy(int dtype, int* blocks_per_sm);
+cudaError_t launch_bwd(int dtype, const BwdBatch& b, int grid, cudaStream_t st);
 
 }  // namespace qfb

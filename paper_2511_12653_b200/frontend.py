@@ -1,0 +1,166 @@
+"""DPVO front-end quant pass: every activation quant point of the two
+BasicEncoder4 encoders (fnet, inet) for a batch of 480x640 frames, run as ONE
+fused forward launch and ONE backward launch through the C-ABI tables.
+
+This is the B200 counterpart of the quant portion of the reference's
+front-end walk (exec.hpp:416-460 run_frontend / frontend.hpp:170-258
+forward_train + backward_train): per quant point the activation fake-quant
+forward (exec.hpp:353-361) and the scale-only backward
+(frontend.hpp:226-229 -> quant.hpp:261-294). The convolutions themselves are
+out of scope (cuDNN territory).
+
+Shapes: the reference ships only a 10-layer toy roster
+(model.hpp:134-143); the DPVO encoder shapes are the public BasicEncoder4's
+(22 convs, quant point = conv input). Multi-consumer points read
+their tensor once and write one output per consumer (exec.hpp:440-451):
+the image feeds both encoders' conv1; each layer2.0 input feeds conv1 and
+downsample.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import List
+
+import numpy as np
+
+from . import (CBwdDesc, CFqDesc, F16, F32, Context, check, lib, scale_grad_factors)
+
+H, W = 480, 640
+
+
+@dataclass
+class QuantPoint:
+    name: str
+    channels: int
+    height: int
+    width: int
+    consumers: List[str] = field(default_factory=list)
+
+    @property
+    def inner(self) -> int:
+        return self.height * self.width
+
+    @property
+    def numel(self) -> int:
+        return self.channels * self.inner
+
+
+def dpvo_quant_points(h: int = H, w: int = W) -> List[QuantPoint]:
+    """The 19 activation tensors / 22 quant points of one frame."""
+    pts = [QuantPoint("image", 3, h, w, ["fnet.conv1", "inet.conv1"])]
+    h2, w2, h4, w4 = h // 2, w // 2, h // 4, w // 4
+    for enc in ("fnet", "inet"):
+        for blk in ("layer1.0", "layer1.1"):
+            for cv in ("conv1", "conv2"):
+                pts.append(QuantPoint(f"{enc}.{blk}.{cv}.in", 32, h2, w2, [f"{enc}.{blk}.{cv}"]))
+        pts.append(QuantPoint(f"{enc}.layer2.0.in", 32, h2, w2,
+                              [f"{enc}.layer2.0.conv1", f"{enc}.layer2.0.downsample"]))
+        pts.append(QuantPoint(f"{enc}.layer2.0.conv2.in", 64, h4, w4, [f"{enc}.layer2.0.conv2"]))
+        for cv in ("conv1", "conv2"):
+            pts.append(QuantPoint(f"{enc}.layer2.1.{cv}.in", 64, h4, w4, [f"{enc}.layer2.1.{cv}"]))
+        pts.append(QuantPoint(f"{enc}.conv2.in", 64, h4, w4, [f"{enc}.conv2"]))
+    return pts
+
+
+def frame_bytes(points: List[QuantPoint], esize: int) -> dict:
+    """Algorithmic HBM bytes per frame: forward reads each
+    tensor once and writes one output per consumer; backward reads x and
+    upstream and writes d_input per consumer."""
+    uniq = sum(p.numel for p in points)
+    qp = sum(p.numel * len(p.consumers) for p in points)
+    return {"fwd": (uniq + qp) * esize, "bwd": 3 * qp * esize, "unique_elems": uniq,
+            "quant_point_elems": qp}
+
+
+class FrontendQuantPass:
+    """Device buffers + C-ABI descriptor tables for `frames` frames of the
+    DPVO activation set, per-channel scales (log-uniform [1e-3, 0.1],
+    SURVEY §8d C2). `sets` independent input sets rotate so consecutive
+    steps never hit L2-resident inputs."""
+
+    def __init__(self, ctx: Context, frames: int = 1, dtype: str = "f32", sets: int = 1,
+                 seed: int = 1, device=None, h: int = H, w: int = W):
+        import torch
+        self.ctx = ctx
+        self.frames = frames
+        self.dtype_code = F32 if dtype == "f32" else F16
+        tdt = torch.float32 if dtype == "f32" else torch.float16
+        self.esize = 4 if dtype == "f32" else 2
+        dev = device if device is not None else torch.device("cuda", ctx.device)
+        self.points = dpvo_quant_points(h, w)
+        self.consumers = [(p, c) for p in self.points for c in p.consumers]
+        rng = np.random.default_rng(seed)
+        L = lib()
+        # scales: per consumer, per channel
+        self.log_s, self.s32, self.fac, self.dls = [], [], [], []
+        for p, _ in self.consumers:
+            s = np.exp(rng.uniform(np.log(1e-3), np.log(0.1), p.channels))
+            ls = np.log(np.expm1(s))
+            s64, chain = scale_grad_factors(ls.tolist())
+            self.log_s.append(ls)
+            self.s32.append(torch.tensor(np.array(s64, dtype=np.float64).astype(np.float32), device=dev))
+            self.fac.append(torch.tensor(s64 + chain, dtype=torch.float64, device=dev))
+            self.dls.append(torch.zeros(p.channels, dtype=torch.float64, device=dev))
+        # outputs shared across sets (written every step)
+        self.y = [torch.empty((frames, p.channels, p.height, p.width), dtype=tdt, device=dev)
+                  for p, _ in self.consumers]
+        self.dx = [torch.empty_like(t) for t in self.y]
+        self.sets = []
+        for si in range(sets):
+            xs = []
+            for pi, p in enumerate(self.points):
+                t = torch.empty((frames, p.channels, p.height, p.width), dtype=tdt, device=dev)
+                check(L.qfb_fill_rng(ctx.handle, self.dtype_code, t.data_ptr(), t.numel(),
+                                     seed + 1000 * si, pi, 0, 1, 1.0, 0.0))
+                xs.append(t)
+            ups = []
+            for ci, (p, _) in enumerate(self.consumers):
+                t = torch.empty((frames, p.channels, p.height, p.width), dtype=tdt, device=dev)
+                check(L.qfb_fill_rng(ctx.handle, self.dtype_code, t.data_ptr(), t.numel(),
+                                     seed + 1000 * si + 500, ci, 0, 1, 1.0, 0.0))
+                ups.append(t)
+            self.sets.append(self._tables(xs, ups))
+        ctx.sync()
+
+    def _tables(self, xs, ups):
+        fwd, bwd = [], []
+        ci = 0
+        for pi, p in enumerate(self.points):
+            d = CFqDesc()
+            d.x = xs[pi].data_ptr()
+            d.outer, d.channels, d.inner = self.frames, p.channels, p.inner
+            d.n_out, d.q_max, d.flags = len(p.consumers), 127, 0
+            for k in range(len(p.consumers)):
+                d.y[k] = self.y[ci + k].data_ptr()
+                d.scale[k] = self.s32[ci + k].data_ptr()
+            fwd.append(d)
+            for k in range(len(p.consumers)):
+                b = CBwdDesc()
+                b.x, b.up, b.dx = xs[pi].data_ptr(), ups[ci + k].data_ptr(), self.dx[ci + k].data_ptr()
+                b.scale64 = self.fac[ci + k].data_ptr()
+                b.chain = self.fac[ci + k].data_ptr() + 8 * p.channels
+                b.d_log_s = self.dls[ci + k].data_ptr()
+                b.outer, b.channels, b.inner = self.frames, p.channels, p.inner
+                b.q_max, b.accumulate = 127, 0
+                bwd.append(b)
+            ci += len(p.consumers)
+        ft = (CFqDesc * len(fwd))(*fwd)
+        bt = (CBwdDesc * len(bwd))(*bwd)
+        return {"x": xs, "up": ups, "fwd": ft, "nf": len(fwd), "bwd": bt, "nb": len(bwd)}
+
+    def forward(self, set_index: int = 0) -> None:
+        s = self.sets[set_index]
+        check(lib().qfb_fq_fwd_multi(self.ctx.handle, self.dtype_code, s["fwd"], s["nf"]))
+
+    def backward(self, set_index: int = 0) -> None:
+        s = self.sets[set_index]
+        check(lib().qfb_fq_bwd_multi(self.ctx.handle, self.dtype_code, s["bwd"], s["nb"]))
+
+    def scale_grads(self):
+        import torch
+        return torch.cat(self.dls)
+
+    def bytes_per_step(self) -> dict:
+        b = frame_bytes(self.points, self.esize)
+        return {k: v * self.frames for k, v in b.items()}

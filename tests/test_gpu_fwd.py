@@ -131,7 +131,8 @@ def test_unaligned_and_inplace(qfb, orc, cuda):
 
 def test_half_nonfinite_latched(qfb, cuda):
     import torch
-    x = torch.tensor([1.0, float("nan"), -float("nan"), 2.0], device=cuda, dtype=torch.float16)
+    # half bit patterns: 1.0, +NaN, -NaN (payload 0x201), 2.0
+    x = torch.tensor([0x3c00, 0x7e01, -0x1ff, 0x4000], dtype=torch.int16).view(torch.float16).to(cuda)
     with pytest.raises(qfb.NonFiniteError):
         qfb.fake_quantize(x, 0.5)
     # the store follows round_to_half: NaN -> +-65504 with the input's sign

@@ -26,13 +26,12 @@ def bits32(a):
 
 
 def same_bits_or_both_nan(a, b):
+    """Bitwise equality INCLUDING NaN sign and payload: the device emulates
+    the host's x86 NaN propagation (qfb_device.cuh quiet_nan / x86_add)."""
     a = np.asarray(a, dtype=np.float32)
     b = np.asarray(b, dtype=np.float32)
-    nan = np.isnan(a)
-    assert np.array_equal(nan, np.isnan(b))
-    # NaN: the sign is observable through the half path; keep it pinned too
-    assert np.array_equal(np.signbit(a[nan]), np.signbit(b[nan]))
-    assert np.array_equal(bits32(a[~nan]), bits32(b[~nan]))
+    assert a.shape == b.shape
+    assert np.array_equal(bits32(a), bits32(b))
 
 
 # --------------------------------------------------------------- scales --
