@@ -14,10 +14,13 @@
 // boundaries follow the recursive floor split, located per group by
 // descending the bits of its index. A perfect tree is exactly what an xor
 // butterfly computes (IEEE addition is commutative), so:
-//   tile    = 2^g consecutive leaf groups (g = min(D, 8)), <= 4096 elements:
-//             16-byte vector window loads (coalesced) -> per-element term
-//             (double) in padded smem, d_input straight to HBM -> one leaf
-//             group per thread -> warp/CTA butterfly = the subtree's sum;
+//   tile    = 2^g consecutive leaf groups (g = min(D, 8)), <= 4096 elements,
+//             staged into shared memory by the TMA engine (cp.async.bulk +
+//             mbarrier, double-buffered: tile i+1 lands while tile i
+//             computes); each thread owns one leaf group, computes its
+//             elements' terms in registers and folds them in reference order,
+//             writing d_input back into the stage; a coalesced 16-byte copy
+//             moves d_input to HBM; warp/CTA butterfly = the subtree's sum;
 //   segment = one row: its 2^(D-g) tile partials are reduced in tree order
 //             by the last CTA to finish (threadfence + atomic ticket);
 //   channel = rows of the same channel over `outer` are accumulated in row
@@ -35,10 +38,8 @@ namespace qfb {
 
 namespace {
 
-constexpr int kPadShift = 4;  // one pad double every 16: conflict-light leaf reads
-constexpr int kSmemDoubles = kBwdTileMax + (kBwdTileMax >> kPadShift);
-
-__device__ __forceinline__ int pad_idx(int e) { return e + (e >> kPadShift); }
+constexpr int kStages = 2;
+constexpr int kWinPad = 32;  // window slack: 16-byte rounding at both ends
 
 // Descend `levels` levels of the reference split from node (lo, m) along
 // the bits of `path` (MSB first): bit 0 = left child [lo, lo + m/2),
@@ -54,16 +55,6 @@ __device__ __forceinline__ void descend(I& lo, I& m, uint32_t path, int levels) 
       m = h;
     }
   }
-}
-
-// Left fold from 0.0 over smem[start, start + len), len <= 8
-// (tensor.hpp:101-104), as a fixed-trip predicated loop.
-__device__ __forceinline__ double fold8(const double* sm, int start, int len) {
-  double acc = 0.0;
-#pragma unroll
-  for (int k = 0; k < 8; ++k)
-    if (k < len) acc = __dadd_rn(acc, sm[pad_idx(start + k)]);
-  return acc;
 }
 
 // Butterfly over the first `lanes` (power of two) threads of the CTA; the
@@ -114,233 +105,314 @@ __device__ void finish_segment(const BwdDesc& d, uint32_t seg, uint32_t c, doubl
   d.chan_counters[c] = 0;  // self-reset for the next launch
 }
 
-// Per-element terms of one element (quant.hpp:217-228 + :250-251).
-struct ElemOut {
-  float dx;
-  double term;
-};
-
-__device__ __forceinline__ ElemOut elem_terms(float xv, float uv, double s, double q) {
-  const GradTerm gt = grad_term(xv, s, q);
-  return {masked_upstream(gt.mask, uv), __dmul_rn(gt.d_ds, (double)uv)};
-}
-
 template <typename T>
-struct VecIO;
-
-template <>
-struct VecIO<float> {
-  static constexpr int V = 4;
-  __device__ __forceinline__ static void unpack(const uint4& r, float* v) { Elem<float>::unpack(r, v); }
-  __device__ __forceinline__ static uint4 pack(const float* v) {
-    return make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]),
-                      __float_as_uint(v[3]));
-  }
-  __device__ __forceinline__ static void store1(void* p, uint64_t i, float v) {
-    static_cast<float*>(p)[i] = v;
-  }
-};
-
-template <>
-struct VecIO<__half> {
-  static constexpr int V = 8;
-  __device__ __forceinline__ static void unpack(const uint4& r, float* v) { Elem<__half>::unpack(r, v); }
-  // dx values are +-up, +-0 or NaN of a half upstream: exact in binary16
-  __device__ __forceinline__ static uint4 pack(const float* v) {
-    uint32_t w[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      w[i] = (uint32_t)__half_as_ushort(__float2half_rn(v[2 * i])) |
-             ((uint32_t)__half_as_ushort(__float2half_rn(v[2 * i + 1])) << 16);
-    }
-    return make_uint4(w[0], w[1], w[2], w[3]);
-  }
-  __device__ __forceinline__ static void store1(void* p, uint64_t i, float v) {
-    static_cast<__half*>(p)[i] = __float2half_rn(v);
-  }
+struct Stage {
+  T x[kBwdTileMax + kWinPad];
+  T up[kBwdTileMax + kWinPad];
 };
 
 template <typename T>
-__device__ __forceinline__ float load1(const void* p, uint64_t i) {
-  if constexpr (sizeof(T) == 4) {
-    return __ldg(static_cast<const float*>(p) + i);
-  } else {
-    return __half2float(static_cast<const __half*>(p)[i]);
+__device__ __forceinline__ float to_f(T v) {
+  if constexpr (sizeof(T) == 4) return v;
+  else return __half2float(v);
+}
+template <typename T>
+__device__ __forceinline__ T from_f(float v) {
+  if constexpr (sizeof(T) == 4) return v;
+  else return __float2half_rn(v);  // d_input of a half upstream: exact
+}
+
+// Where one tile lives: descriptor, row segment, tree node.
+struct TileRef {
+  int di;
+  uint32_t seg, t, c;
+  uint64_t A;  // first element (descriptor-relative)
+  int m;       // elements
+};
+
+__device__ __forceinline__ TileRef locate(const BwdBatch& bt, uint32_t tile_id) {
+  TileRef r;
+  int hi = bt.n - 1;
+  r.di = 0;
+  while (r.di < hi) {
+    const int mid = (r.di + hi + 1) >> 1;
+    if (bt.tile_begin[mid] <= tile_id) r.di = mid;
+    else hi = mid - 1;
+  }
+  const BwdDesc& d = bt.d[r.di];
+  const uint32_t local = tile_id - bt.tile_begin[r.di];
+  r.seg = local >> d.tps_log;
+  r.t = local & ((1u << d.tps_log) - 1u);
+  r.c = r.seg % d.chans;
+  // tile root: node t at depth D - g of the row's tree (64-bit: rows may
+  // exceed 2^32 elements); everything inside a tile fits 32 bits
+  uint64_t lo = 0, mm = d.inner;
+  descend<uint64_t>(lo, mm, r.t, (int)d.tps_log);
+  r.A = (uint64_t)r.seg * d.inner + lo;
+  r.m = (int)mm;
+  return r;
+}
+
+// 16-byte window [w0, w1) (bytes) of a tile that a bulk copy may fetch:
+// never past the last full 16 bytes of the tensor (the few elements beyond
+// are loaded by threads).
+template <typename T>
+__device__ __forceinline__ void window(const BwdDesc& d, const TileRef& r, uint64_t& w0,
+                                       uint64_t& w1) {
+  const uint64_t b0 = r.A * sizeof(T), b1 = (r.A + (uint64_t)r.m) * sizeof(T);
+  const uint64_t tot = (uint64_t)d.outer * d.chans * d.inner * sizeof(T);
+  w0 = b0 & ~uint64_t(15);
+  w1 = (b1 + 15) & ~uint64_t(15);
+  const uint64_t cap = tot & ~uint64_t(15);
+  if (w1 > cap) w1 = cap > w0 ? cap : w0;
+}
+
+// Thread 0: arm the stage's mbarrier and launch the two bulk copies.
+template <typename T>
+__device__ __forceinline__ void issue_tile(const BwdDesc& d, const TileRef& r, Stage<T>& st,
+                                           uint64_t* bar) {
+  uint64_t w0, w1;
+  window<T>(d, r, w0, w1);
+  const uint32_t bytes = (uint32_t)(w1 - w0);
+  fence_proxy_async_smem();
+  mbar_arrive_expect_tx(bar, 2 * bytes);
+  if (bytes) {
+    bulk_g2s(st.x, static_cast<const char*>(d.x) + w0, bytes, bar);
+    bulk_g2s(st.up, static_cast<const char*>(d.up) + w0, bytes, bar);
   }
 }
 
-// Pass 1, vector window: units of V elements aligned to 16 bytes covering
-// [A, A + m); elements outside the tile are loaded but ignored.
-template <typename T>
-__device__ __forceinline__ void pass1_vec(const BwdDesc& d, uint64_t A, int m, double s, double q,
-                                          double* sm) {
-  constexpr int V = VecIO<T>::V;
-  const int off = (int)(A & (V - 1));
-  const uint64_t ubase = A >> (V == 4 ? 2 : 3);
-  const int U = (off + m + V - 1) / V;
-  const uint4* xv = static_cast<const uint4*>(d.x) + ubase;
-  const uint4* uv = static_cast<const uint4*>(d.up) + ubase;
-  uint4* dxv = d.dx ? static_cast<uint4*>(d.dx) + ubase : nullptr;
-  for (int u0 = threadIdx.x; u0 < U; u0 += 2 * kBwdThreads) {
-    uint4 rx[2], ru[2];
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const int u = u0 + k * kBwdThreads;
-      if (u < U) {
-        rx[k] = ld_nc_v4(xv + u);
-        ru[k] = ld_nc_v4(uv + u);
-      }
+// Group (leaf) of this thread inside a tile of m elements: depends only on
+// (m, g), and a descriptor's tiles take at most two sizes -> 2-slot cache.
+struct GroupCache {
+  int k0 = -1, lo0 = 0, len0 = 0;
+  int k1 = -1, lo1 = 0, len1 = 0;
+
+  __device__ __forceinline__ void get(int m, int g, int tid, int& glo, int& glen) {
+    const int k = m | (g << 16);
+    if (k0 == k) {
+      glo = lo0;
+      glen = len0;
+      return;
     }
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const int u = u0 + k * kBwdThreads;
-      if (u >= U) break;
-      float x[V], up[V], dx[V];
-      VecIO<T>::unpack(rx[k], x);
-      VecIO<T>::unpack(ru[k], up);
-      const int e0 = u * V - off;  // tile-relative index of element 0
-      const bool full = e0 >= 0 && e0 + V <= m;
-#pragma unroll
-      for (int j = 0; j < V; ++j) {
-        const ElemOut eo = elem_terms(x[j], up[j], s, q);
-        dx[j] = eo.dx;
-        const int e = e0 + j;
-        if (full || (unsigned)e < (unsigned)m) sm[pad_idx(e)] = eo.term;
-      }
-      if (dxv != nullptr) {
-        if (full) {
-          st_v4(dxv + u, VecIO<T>::pack(dx), false);
-        } else {
-#pragma unroll
-          for (int j = 0; j < V; ++j)
-            if ((unsigned)(e0 + j) < (unsigned)m) VecIO<T>::store1(d.dx, A + e0 + j, dx[j]);
-        }
-      }
+    if (k1 == k) {
+      glo = lo1;
+      glen = len1;
+      return;
     }
+    int l = 0, mm = m;
+    if (tid < (1 << g)) descend<int>(l, mm, (uint32_t)tid, g);
+    else mm = 0;
+    k1 = k0;
+    lo1 = lo0;
+    len1 = len0;
+    k0 = k;
+    lo0 = l;
+    len0 = mm;
+    glo = l;
+    glen = mm;
   }
+};
+
+// Terms of one element: d_ds * up (double) and d_input (x86 NaN rules).
+template <typename T>
+__device__ __forceinline__ double elem(T* sx, const T* su, int k, const DivCtx& dc, double q,
+                                       bool want_dx) {
+  const float xv = to_f<T>(sx[k]);
+  const float uv = to_f<T>(su[k]);
+  const GradTerm gt = grad_term_fast(xv, dc, q);
+  if (want_dx) sx[k] = from_f<T>(masked_upstream(gt.mask, uv));
+  return __dmul_rn(gt.d_ds, (double)uv);
 }
 
-// Pass 1, scalar (unaligned buffers).
 template <typename T>
-__device__ __forceinline__ void pass1_scalar(const BwdDesc& d, uint64_t A, int m, double s,
-                                             double q, double* sm) {
-  for (int e = threadIdx.x; e < m; e += kBwdThreads) {
-    const ElemOut eo = elem_terms(load1<T>(d.x, A + e), load1<T>(d.up, A + e), s, q);
-    if (d.dx != nullptr) VecIO<T>::store1(d.dx, A + e, eo.dx);
-    sm[pad_idx(e)] = eo.term;
-  }
-}
-
-template <typename T>
-__global__ void __launch_bounds__(kBwdThreads, 4)
-    bwd_kernel(const __grid_constant__ BwdBatch bt) {
-  __shared__ double sm[kSmemDoubles];
+__global__ void __launch_bounds__(kBwdThreads, 3) bwd_kernel(const __grid_constant__ BwdBatch bt) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Stage<T>* stages = reinterpret_cast<Stage<T>*>(smem_raw);
+  __shared__ __align__(8) uint64_t bars[kStages];
+  __shared__ TileRef sh_tile[2];
   __shared__ double red[kBwdThreads / 32];
   __shared__ int last_flag;
   const int tid = threadIdx.x;
   const uint32_t total = bt.tile_begin[bt.n];
+  if (blockIdx.x >= total) return;
 
-  for (uint32_t tile_id = blockIdx.x; tile_id < total; tile_id += gridDim.x) {
-    int di = 0, hi = bt.n - 1;
-    while (di < hi) {
-      const int mid = (di + hi + 1) >> 1;
-      if (bt.tile_begin[mid] <= tile_id) di = mid;
-      else hi = mid - 1;
+  // Thread 0 is the producer: it locates tiles and issues their bulk copies
+  // one tile ahead; everyone reads the tile descriptors from smem.
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+    sh_tile[0] = locate(bt, blockIdx.x);
+    if (bt.d[sh_tile[0].di].vec) issue_tile<T>(bt.d[sh_tile[0].di], sh_tile[0], stages[0], &bars[0]);
+  }
+  __syncthreads();
+
+  uint32_t phase_bits = 0;  // per-stage mbarrier parity
+  GroupCache gc;
+  int it = 0;
+  for (uint32_t tile_id = blockIdx.x; tile_id < total; tile_id += gridDim.x, ++it) {
+    const int sidx = it & (kStages - 1);
+    Stage<T>& st = stages[sidx];
+    const TileRef cur = sh_tile[it & 1];
+    const BwdDesc& d = bt.d[cur.di];
+
+    // Producer: next tile into the other stage (freed by the barrier that
+    // ended the previous iteration).
+    const uint32_t next_id = tile_id + gridDim.x;
+    if (tid == 0 && next_id < total) {
+      const TileRef nxt = locate(bt, next_id);
+      sh_tile[(it + 1) & 1] = nxt;
+      if (bt.d[nxt.di].vec) issue_tile<T>(bt.d[nxt.di], nxt, stages[sidx ^ 1], &bars[sidx ^ 1]);
     }
-    const BwdDesc& d = bt.d[di];
-    const uint32_t local = tile_id - bt.tile_begin[di];
-    const uint32_t seg = local >> d.tps_log;
-    const uint32_t t = local & ((1u << d.tps_log) - 1u);
-    const uint32_t c = seg % d.chans;
 
-    // Tile root: node t at depth D - g of the row's tree (64-bit: rows may
-    // exceed 2^32 elements); everything inside a tile fits 32 bits.
-    uint64_t lo = 0, mm = d.inner;
-    descend<uint64_t>(lo, mm, t, (int)d.tps_log);
-    const int m = (int)mm;  // <= kBwdTileMax
-    const uint64_t A = (uint64_t)seg * d.inner + lo;
-    const double s = d.s64[c];
-    const double q = d.q;
-
-    if (d.vec) pass1_vec<T>(d, A, m, s, q, sm);
-    else pass1_scalar<T>(d, A, m, s, q, sm);
-    __syncthreads();
-
-    // Pass 2: one leaf group per thread, then the perfect-tree butterfly.
-    const int groups = 1 << d.g;
-    double v = 0.0;
-    if (tid < groups) {
-      int glo = 0, gm = m;
-      descend<int>(glo, gm, (uint32_t)tid, (int)d.g);
-      const int h = gm > 8 ? gm >> 1 : gm;
-      v = fold8(sm, glo, h);
-      if (gm > 8) v = __dadd_rn(v, fold8(sm, glo + h, gm - h));
-    }
-    const double tile_sum = cta_tree_sum(v, groups, red);
-
-    const uint32_t tps = 1u << d.tps_log;
-    if (tps == 1) {
-      if (tid == 0) finish_segment(d, seg, c, __dmul_rn(tile_sum, d.chain[c]));
+    uint64_t w0, w1;
+    window<T>(d, cur, w0, w1);
+    const int off = (int)((cur.A * sizeof(T) - w0) / sizeof(T));  // tile start in stage
+    if (d.vec) {
+      mbar_wait(&bars[sidx], (phase_bits >> sidx) & 1u);
+      phase_bits ^= 1u << sidx;
+      // elements past the bulk window (only at the very end of a tensor)
+      const uint64_t e_end = cur.A + (uint64_t)cur.m;
+      const uint64_t e_w1 = w1 / sizeof(T);
+      if (e_w1 < e_end) {
+        for (uint64_t e = e_w1 + tid; e < e_end; e += kBwdThreads) {
+          st.x[e - w0 / sizeof(T)] = static_cast<const T*>(d.x)[e];
+          st.up[e - w0 / sizeof(T)] = static_cast<const T*>(d.up)[e];
+        }
+        __syncthreads();
+      }
     } else {
-      // Pass 3: segment completion by the last tile (atomic ticket).
-      if (tid == 0) {
-        d.partials[(uint64_t)seg * tps + t] = tile_sum;
-        __threadfence();
-        const uint32_t ticket = atomicAdd(d.seg_counters + seg, 1u);
-        last_flag = (ticket == tps - 1);
+      for (int e = tid; e < cur.m; e += kBwdThreads) {
+        st.x[off + e] = static_cast<const T*>(d.x)[cur.A + e];
+        st.up[off + e] = static_cast<const T*>(d.up)[cur.A + e];
       }
       __syncthreads();
-      if (last_flag) {
+    }
+
+    // This thread's leaf group: two left folds from 0.0 over its halves (or
+    // one fold if <= 8 elements), in registers, then their sum.
+    int glo, glen;
+    gc.get(cur.m, (int)d.g, tid, glo, glen);
+    const DivCtx dc = make_div(d.s64[cur.c]);
+    const double q = d.q;
+    const bool want_dx = d.dx != nullptr;
+    T* sx = st.x + off + glo;
+    const T* su = st.up + off + glo;
+    const int h = glen > 8 ? glen >> 1 : glen;
+    double acc_l = 0.0, acc_r = 0.0;
+    int k = 0;
+    for (; k < h; ++k) acc_l = __dadd_rn(acc_l, elem<T>(sx, su, k, dc, q, want_dx));
+    for (; k < glen; ++k) acc_r = __dadd_rn(acc_r, elem<T>(sx, su, k, dc, q, want_dx));
+    const double v = glen > 8 ? __dadd_rn(acc_l, acc_r) : acc_l;
+    __syncthreads();  // stage.x now holds d_input for the whole tile
+
+    const int groups = 1 << d.g;
+    const double tile_sum = cta_tree_sum(v, groups, red);
+    const uint32_t tps = 1u << d.tps_log;
+    // Thread 0 publishes the tile result first so its fence/ticket overlaps
+    // the d_input copy-out of the other threads.
+    if (tid == 0) {
+      if (tps == 1) {
+        finish_segment(d, cur.seg, cur.c, __dmul_rn(tile_sum, d.chain[cur.c]));
+        last_flag = 0;
+      } else {
+        d.partials[(uint64_t)cur.seg * tps + cur.t] = tile_sum;
         __threadfence();
-        const double* p = d.partials + (uint64_t)seg * tps;
-        // Each thread reduces `per` consecutive partials as a perfect
-        // subtree, then the CTA butterfly combines the subtrees in order.
-        const uint32_t lanes = tps < (uint32_t)kBwdThreads ? tps : (uint32_t)kBwdThreads;
-        const uint32_t per = tps / lanes;
-        double w = 0.0;
-        if ((uint32_t)tid < lanes) {
-          const double* mine = p + (uint64_t)tid * per;
-          switch (per) {
-            case 1: w = tree_load<1>(mine); break;
-            case 2: w = tree_load<2>(mine); break;
-            case 4: w = tree_load<4>(mine); break;
-            case 8: w = tree_load<8>(mine); break;
-            case 16: w = tree_load<16>(mine); break;
-            default: {
-              // per > 16 (rows > 2^26 elements): level-by-level in place
-              // over the thread's own slice, still the perfect-tree order.
-              double* q2 = const_cast<double*>(mine);
-              for (uint32_t width = per; width > 1; width >>= 1)
-                for (uint32_t k = 0; k < width / 2; ++k)
-                  q2[k] = __dadd_rn(__ldcg(q2 + 2 * k), __ldcg(q2 + 2 * k + 1));
-              w = __ldcg(q2);
-            }
+        const uint32_t ticket = atomicAdd(d.seg_counters + cur.seg, 1u);
+        last_flag = (ticket == tps - 1);
+      }
+    }
+
+    // d_input -> HBM: 16-byte copies for units fully inside the tile,
+    // element copies at the two ragged ends.
+    if (want_dx) {
+      const uint64_t b0 = cur.A * sizeof(T), b1 = (cur.A + (uint64_t)cur.m) * sizeof(T);
+      const int nunits = (int)((b1 - w0 + 15) / 16);
+      for (int u = tid; u < nunits; u += kBwdThreads) {
+        const uint64_t ub = w0 + 16ull * (uint64_t)u;
+        if (ub >= b0 && ub + 16 <= b1) {
+          const uint4 val = *reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(st.x) + 16 * u);
+          st_v4(static_cast<char*>(d.dx) + ub, val, false);
+        } else {
+          constexpr int kPer = 16 / (int)sizeof(T);
+#pragma unroll
+          for (int j = 0; j < kPer; ++j) {
+            const uint64_t eb = ub + (uint64_t)j * sizeof(T);
+            if (eb >= b0 && eb < b1) static_cast<T*>(d.dx)[eb / sizeof(T)] = st.x[u * kPer + j];
           }
-        }
-        const double seg_sum = cta_tree_sum(w, (int)lanes, red);
-        if (tid == 0) {
-          d.seg_counters[seg] = 0;  // self-reset
-          finish_segment(d, seg, c, __dmul_rn(seg_sum, d.chain[c]));
         }
       }
     }
-    __syncthreads();  // smem / red / last_flag are reused by the next tile
+    __syncthreads();  // stage reads done; last_flag visible
+
+    if (last_flag) {
+      __threadfence();
+      const double* p = d.partials + (uint64_t)cur.seg * tps;
+      // each thread reduces `per` consecutive partials as a perfect
+      // subtree, then the CTA butterfly combines the subtrees in order
+      const uint32_t lanes = tps < (uint32_t)kBwdThreads ? tps : (uint32_t)kBwdThreads;
+      const uint32_t per = tps / lanes;
+      double w = 0.0;
+      if ((uint32_t)tid < lanes) {
+        const double* mine = p + (uint64_t)tid * per;
+        switch (per) {
+          case 1: w = tree_load<1>(mine); break;
+          case 2: w = tree_load<2>(mine); break;
+          case 4: w = tree_load<4>(mine); break;
+          case 8: w = tree_load<8>(mine); break;
+          case 16: w = tree_load<16>(mine); break;
+          default: {
+            // per > 16 (rows > 2^26 elements): level-by-level in place over
+            // the thread's own slice, still the perfect-tree order
+            double* q2 = const_cast<double*>(mine);
+            for (uint32_t width = per; width > 1; width >>= 1)
+              for (uint32_t kk = 0; kk < width / 2; ++kk)
+                q2[kk] = __dadd_rn(__ldcg(q2 + 2 * kk), __ldcg(q2 + 2 * kk + 1));
+            w = __ldcg(q2);
+          }
+        }
+      }
+      const double seg_sum = cta_tree_sum(w, (int)lanes, red);
+      if (tid == 0) {
+        d.seg_counters[cur.seg] = 0;  // self-reset
+        finish_segment(d, cur.seg, cur.c, __dmul_rn(seg_sum, d.chain[cur.c]));
+      }
+      __syncthreads();  // red reused by the next tile
+    }
   }
+}
+
+template <typename T>
+constexpr size_t stage_bytes() {
+  return sizeof(Stage<T>) * kStages;
 }
 
 }  // namespace
 
 cudaError_t bwd_occupancy(int dtype, int* blocks_per_sm) {
-  const void* f = dtype == 0 ? (const void*)bwd_kernel<float> : (const void*)bwd_kernel<__half>;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, kBwdThreads, 0);
+  cudaError_t e;
+  if (dtype == 0) {
+    e = cudaFuncSetAttribute(bwd_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)stage_bytes<float>());
+    if (e != cudaSuccess) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, bwd_kernel<float>,
+                                                         kBwdThreads, stage_bytes<float>());
+  }
+  e = cudaFuncSetAttribute(bwd_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)stage_bytes<__half>());
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, bwd_kernel<__half>,
+                                                       kBwdThreads, stage_bytes<__half>());
 }
 
 cudaError_t launch_bwd(int dtype, const BwdBatch& b, int grid, cudaStream_t st) {
   const uint32_t tiles = b.tile_begin[b.n];
   if (tiles == 0) return cudaSuccess;
   if ((uint32_t)grid > tiles) grid = (int)tiles;
-  if (dtype == 0) bwd_kernel<float><<<grid, kBwdThreads, 0, st>>>(b);
-  else bwd_kernel<__half><<<grid, kBwdThreads, 0, st>>>(b);
+  if (dtype == 0)
+    bwd_kernel<float><<<grid, kBwdThreads, stage_bytes<float>(), st>>>(b);
+  else
+    bwd_kernel<__half><<<grid, kBwdThreads, stage_bytes<__half>(), st>>>(b);
   return cudaGetLastError();
 }
 

@@ -120,10 +120,12 @@ __device__ __forceinline__ int8_t fq_code(float x, float s, float q) {
 // d_input = float(mask * double(up)) with host NaN rules: NaN upstream
 // propagates (quieted); a masked-out inf gives 0*inf = default NaN.
 __device__ __forceinline__ float masked_upstream(bool mask, float up) {
-  if (isnan(up)) return quiet_nan(up);
-  if (mask) return up;
-  if (isinf(up)) return __uint_as_float(kX86DefaultNaN);
-  return __fmul_rn(0.0f, up);  // +-0 with the sign of up
+  const uint32_t ub = __float_as_uint(up);
+  float d = mask ? up : __uint_as_float(ub & 0x80000000u);  // +-0 with the sign of up
+  if ((ub & 0x7f800000u) == 0x7f800000u) {                   // inf / NaN (rare)
+    d = (ub & 0x7fffffu) ? quiet_nan(up) : (mask ? up : __uint_as_float(kX86DefaultNaN));
+  }
+  return d;
 }
 
 struct GradTerm {
@@ -133,6 +135,51 @@ struct GradTerm {
 
 __device__ __forceinline__ GradTerm grad_term(float x, double s, double q) {
   const double z = __ddiv_rn((double)x, s);
+  GradTerm t;
+  t.mask = fabs(z) <= q;
+  t.d_ds = t.mask ? __dadd_rn(rint(z), -z) : (z > 0.0 ? q : -q);
+  return t;
+}
+
+// Certified fast double division for the backward: z = RN(x / s) with a
+// hoisted y = RN(1/s). Markstein's correction gives a candidate q1; it is
+// ACCEPTED only if the exact-or-larger residual proves it is the unique
+// nearest double: |x - s*q1| < s*ulp(q1)/2 (threshold exactly representable,
+// so rounding of the residual can never sneak under it) and q1 is not a
+// power of two (where the ulp below is smaller). Anything else — ties,
+// binade edges, inf/NaN/zero x — takes __ddiv_rn. Correct by construction.
+struct DivCtx {
+  double s;
+  double y;     // __drcp_rn(s)
+  bool usable;  // s normal and far from over/underflow
+};
+
+__device__ __forceinline__ DivCtx make_div(double s) {
+  DivCtx c;
+  c.s = s;
+  c.y = __drcp_rn(s);
+  c.usable = s >= 0x1p-900 && s <= 0x1p900;
+  return c;
+}
+
+__device__ __forceinline__ double certified_div(float xf, const DivCtx& c) {
+  const double x = (double)xf;
+  const double q0 = __dmul_rn(x, c.y);
+  const double q1 = __fma_rn(__fma_rn(-c.s, q0, x), c.y, q0);
+  const double r1 = __fma_rn(-c.s, q1, x);
+  const unsigned long long qb = (unsigned long long)__double_as_longlong(q1);
+  const unsigned long long e = (qb >> 52) & 0x7ffull;
+  // s * ulp(q1) / 2 = s * 2^(e - 1023 - 53): exact power-of-two scaling
+  const double half_ulp_s = __dmul_rn(c.s, __longlong_as_double((long long)((e - 53ull) << 52)));
+  const bool ok = c.usable && (qb & 0x000fffffffffffffull) != 0ull && e > 160ull && e < 1900ull &&
+                  fabs(r1) < half_ulp_s;
+  if (__builtin_expect(ok, 1)) return q1;
+  return __ddiv_rn(x, c.s);
+}
+
+// grad_term with the certified division.
+__device__ __forceinline__ GradTerm grad_term_fast(float x, const DivCtx& c, double q) {
+  const double z = certified_div(x, c);
   GradTerm t;
   t.mask = fabs(z) <= q;
   t.d_ds = t.mask ? __dadd_rn(rint(z), -z) : (z > 0.0 ? q : -q);
@@ -171,6 +218,51 @@ __device__ __forceinline__ void st_v4(void* p, uint4 v, bool streaming) {
   }
 }
 
+// ------------------------------------------- TMA bulk copy + mbarrier ---
+// 1-D bulk async copies (cp.async.bulk, the TMA engine without a tensor
+// map) into shared memory, completion tracked by an mbarrier transaction
+// count. Addresses and sizes must be 16-byte aligned / multiples of 16.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// Orders this thread's generic-proxy shared accesses (after a CTA barrier:
+// everyone's) before subsequent async-proxy (bulk copy) writes.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
 // Element <-> float conversions for the two storage types. A "unit" is
 // one 16-byte vector: 4 floats or 8 halves.
 template <typename T>
@@ -203,6 +295,15 @@ struct Elem<float> {
   }
 };
 
+// binary16 bits -> float bits with NaN sign/payload kept (f16_to_f32,
+// half.hpp:62-63); the hardware conversion returns a canonical NaN.
+__device__ __forceinline__ float half_bits_to_float_exact(uint32_t h) {
+  const float f = __half2float(__ushort_as_half((unsigned short)h));
+  if ((h & 0x7c00u) == 0x7c00u && (h & 0x3ffu))
+    return __uint_as_float(((h & 0x8000u) << 16) | 0x7f800000u | ((h & 0x3ffu) << 13));
+  return f;
+}
+
 template <>
 struct Elem<__half> {
   static constexpr int kPerVec = 8;
@@ -213,6 +314,16 @@ struct Elem<__half> {
       const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
       v[2 * i] = f.x;
       v[2 * i + 1] = f.y;
+    }
+    // rare path: any all-ones exponent (inf/NaN) in the unit
+    const uint32_t e = (__vcmpeq2(r.x & 0x7c007c00u, 0x7c007c00u) | __vcmpeq2(r.y & 0x7c007c00u, 0x7c007c00u) |
+                        __vcmpeq2(r.z & 0x7c007c00u, 0x7c007c00u) | __vcmpeq2(r.w & 0x7c007c00u, 0x7c007c00u));
+    if (e) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        v[2 * i] = half_bits_to_float_exact(w[i] & 0xffffu);
+        v[2 * i + 1] = half_bits_to_float_exact(w[i] >> 16);
+      }
     }
   }
   // f16 storage always rounds through half_store (RNE + saturation).
@@ -228,7 +339,7 @@ struct Elem<__half> {
     return make_uint4(w[0], w[1], w[2], w[3]);
   }
   __device__ __forceinline__ static float load1(const void* p, uint64_t i) {
-    return __half2float(static_cast<const __half*>(p)[i]);
+    return half_bits_to_float_exact(static_cast<const unsigned short*>(p)[i]);
   }
   __device__ __forceinline__ static void store1(void* p, uint64_t i, float v, float sign_src,
                                                 bool /*half_grid_out*/, bool& nf) {

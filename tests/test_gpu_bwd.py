@@ -202,3 +202,29 @@ def test_bwd_multi_table_and_determinism(qfb, orc, cuda):
             assert np.array_equal(bits32(host(dx).ravel()), bits32(wdx))
             check_grads(dls.cpu().numpy(), wdls, TOL_F32)
     assert results[0] == results[1]
+
+
+def test_special_values_bitwise(qfb, orc, cuda):
+    """inf / NaN / +-0 / subnormal / huge x and +-inf / NaN upstream through
+    the certified division and the x86 NaN rules of d_input."""
+    rng = np.random.default_rng(77)
+    sp = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 1e-45, -1e-45, 1.17e-38, 3.4e38, -3.4e38,
+                   0.5, -0.5, 1.5, 127.0, 127.5, -127.5, 126.5, 1e-8], dtype=np.float32)
+    for s in (1e-6, 0.0315, 1.0, 2.0, 64.0, 0.5):
+        x = np.concatenate([sp * np.float32(s), sp, rng.normal(0, 50 * s, 5000).astype(np.float32)])
+        up = rng.normal(0, 1, x.size).astype(np.float32)
+        up[::97] = np.inf
+        up[1::97] = -np.inf
+        up[2::97] = np.nan
+        up[3::97] = -0.0
+        ls = float(np.log(np.expm1(s))) if s < 30 else s
+        g = qfb.fake_quantize_backward(to_dev(x, cuda), ls, None, to_dev(up, cuda))
+        _, dx, dls = orc.fq_backward(x, up, [ls], 1, 1, x.size)
+        assert np.array_equal(bits32(host(g.d_input)), bits32(dx)), s
+        assert np.isnan(g.d_log_scale[0]) and np.isnan(dls[0])
+        # finite upstream: gradient bitwise too
+        up2 = np.nan_to_num(up, nan=0.5, posinf=2.0, neginf=-2.0)
+        g = qfb.fake_quantize_backward(to_dev(x, cuda), ls, None, to_dev(up2, cuda))
+        _, dx, dls = orc.fq_backward(x, up2, [ls], 1, 1, x.size)
+        assert np.array_equal(bits32(host(g.d_input)), bits32(dx)), s
+        check_grads(g.d_log_scale, dls, TOL_F32)
