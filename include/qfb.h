@@ -301,6 +301,33 @@ qfb_status qfb_fake_quantize_backward_host(
     const double* log_s, const qfb_quant_config* cfg, double* d_log_s,
     int32_t accumulate);
 
+/* ---------------------------------------------------------------------- */
+/* Frame-level host pass: the quant portion of run_frontend +             */
+/* backward_train (exec.hpp:435-451, frontend.hpp:236-258) for a set of    */
+/* quant points given as HOST float32 buffers. Each input tensor is copied */
+/* once even when it feeds two consumers; host->device copies, kernels and */
+/* device->host copies are pipelined per point over two copy engines and  */
+/* the compute stream. Pinned host buffers get full PCIe bandwidth;        */
+/* pageable ones work too (driver-staged). Synchronous. Results are        */
+/* identical to the per-point *_host calls.                                 */
+/* ---------------------------------------------------------------------- */
+typedef struct qfb_host_point {
+  const float* x;                              /* [outer, channels, inner] */
+  int64_t outer, channels, inner;
+  int32_t n_out;                               /* consumers: 1 or 2        */
+  int32_t reserved;
+  const double* s[QFB_MAX_CHAIN_OUT];          /* fwd scales [channels]    */
+  float* y[QFB_MAX_CHAIN_OUT];                 /* fwd outputs (nullable)   */
+  const double* log_s[QFB_MAX_CHAIN_OUT];      /* bwd log scales (nullable: no bwd) */
+  const float* up[QFB_MAX_CHAIN_OUT];          /* bwd upstream             */
+  float* dx[QFB_MAX_CHAIN_OUT];                /* d_input (nullable)       */
+  double* d_log_s[QFB_MAX_CHAIN_OUT];          /* scale gradients [channels] */
+} qfb_host_point;
+
+qfb_status qfb_quant_pass_host(qfb_ctx* ctx, qfb_precision prec,
+                               const qfb_host_point* points, int32_t n,
+                               const qfb_quant_config* cfg);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

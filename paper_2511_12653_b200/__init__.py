@@ -128,6 +128,12 @@ class CChainDesc(ctypes.Structure):
                 ("reserved", _u32)]
 
 
+class CHostPoint(ctypes.Structure):
+    _fields_ = [("x", _vp), ("outer", _i64), ("channels", _i64), ("inner", _i64),
+                ("n_out", _i32), ("reserved", _i32), ("s", _vp * 2), ("y", _vp * 2),
+                ("log_s", _vp * 2), ("up", _vp * 2), ("dx", _vp * 2), ("d_log_s", _vp * 2)]
+
+
 def _sig(name, res, args):
     f = getattr(_lib, name)
     f.restype = res
@@ -166,6 +172,7 @@ _sig("qfb_fill_rng", _i32, [_vp, _i32, _vp, _i64, _u64, _u64, _u64, _i32, _dbl, 
 _sig("qfb_fq_fwd_perop", _i32, [_vp, _i32, _vp, _vp, _i64, _i64, _i64, _vp, _i32, _u32, _vp])
 _sig("qfb_fake_quantize_host", _i32, [_vp, _i32, _vp, _vp, _i64, _i64, _i64, _pd, ctypes.POINTER(CQuantConfig)])
 _sig("qfb_int8_codes_host", _i32, [_vp, _vp, _vp, _i64, _i64, _i64, _pd, ctypes.POINTER(CQuantConfig)])
+_sig("qfb_quant_pass_host", _i32, [_vp, _i32, ctypes.POINTER(CHostPoint), _i32, ctypes.POINTER(CQuantConfig)])
 _sig("qfb_fake_quantize_backward_host", _i32, [_vp, _i32, _vp, _vp, _vp, _i64, _i64, _i64, _pd,
                                                 ctypes.POINTER(CQuantConfig), _pd, _i32])
 

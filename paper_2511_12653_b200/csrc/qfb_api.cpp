@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -70,12 +71,18 @@ struct qfb_ctx {
   int sm_count = 148;
   int ew_blocks_per_sm[2][2] = {{4, 4}, {4, 4}};  // [dtype][chain]
   int bwd_blocks_per_sm[2] = {4, 4};
+  int tma_blocks_per_sm[2] = {0, 0};  // 0: TMA forward unavailable
   uint32_t* d_status = nullptr;
   uint32_t* h_status = nullptr;  // pinned
   DevBuf ws_f64;                 // partials / segment results
   DevBuf ws_u32;                 // tickets (kept zero between launches)
   DevBuf host_io[6];             // scratch for the *_host entry points
   int64_t launches = 0;
+  // qfb_quant_pass_host: copy streams, events and per-point device buffers
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  std::vector<cudaEvent_t> ev;
+  std::vector<DevBuf> pass_bufs;
+  DevBuf pass_params;
 };
 
 namespace {
@@ -212,9 +219,17 @@ qfb_status run_ew(qfb_ctx* ctx, int dtype, const std::vector<EwDesc>& descs, boo
     b.n = n;
     b.chunk_begin[n] = chunks;
     if (chunks == 0) continue;
-    const int grid = (int)std::min<uint64_t>(
-        chunks, (uint64_t)ctx->sm_count * ctx->ew_blocks_per_sm[dtype][chain ? 1 : 0]);
-    cudaError_t e = launch_ew(dtype, chain, b, ctx->d_status, grid, ctx->stream);
+    bool all_vec = !chain && ctx->tma_blocks_per_sm[dtype] > 0;
+    for (int k = 0; k < n && all_vec; ++k) all_vec = b.d[k].vec > 1;
+    cudaError_t e;
+    if (all_vec) {
+      const int grid = (int)std::min<uint64_t>(chunks, (uint64_t)ctx->sm_count * ctx->tma_blocks_per_sm[dtype]);
+      e = launch_ew_tma(dtype, b, ctx->d_status, grid, ctx->stream);
+    } else {
+      const int grid = (int)std::min<uint64_t>(
+          chunks, (uint64_t)ctx->sm_count * ctx->ew_blocks_per_sm[dtype][chain ? 1 : 0]);
+      e = launch_ew(dtype, chain, b, ctx->d_status, grid, ctx->stream);
+    }
     if (e != cudaSuccess) return cuda_fail(e, "ew_kernel launch");
     ctx->launches++;
   }
@@ -363,7 +378,11 @@ qfb_status qfb_ctx_create(int32_t device, void* stream, qfb_ctx** out) {
     for (int dt = 0; dt < 2; ++dt) {
       int per = 0;
       if (bwd_occupancy(dt, &per) == cudaSuccess && per > 0) c->bwd_blocks_per_sm[dt] = per;
+      per = 0;
+      if (ew_tma_occupancy(dt, &per) == cudaSuccess && per > 0) c->tma_blocks_per_sm[dt] = per;
     }
+    if (const char* env = getenv("QFB_DISABLE_TMA_FWD"))
+      if (env[0] == '1') c->tma_blocks_per_sm[0] = c->tma_blocks_per_sm[1] = 0;
   }
   if (e == cudaSuccess) e = cudaMalloc(&c->d_status, sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMallocHost(&c->h_status, sizeof(uint32_t));
@@ -387,6 +406,12 @@ qfb_status qfb_ctx_destroy(qfb_ctx* ctx) {
   if (ctx->ws_u32.p) cudaFree(ctx->ws_u32.p);
   for (auto& b : ctx->host_io)
     if (b.p) cudaFree(b.p);
+  for (auto& b : ctx->pass_bufs)
+    if (b.p) cudaFree(b.p);
+  if (ctx->pass_params.p) cudaFree(ctx->pass_params.p);
+  for (auto e : ctx->ev) cudaEventDestroy(e);
+  if (ctx->s_in) cudaStreamDestroy(ctx->s_in);
+  if (ctx->s_out) cudaStreamDestroy(ctx->s_out);
   delete ctx;
   return QFB_OK;
 }
@@ -636,14 +661,8 @@ qfb_status plan_bwd(const qfb_bwd_desc& t, BwdPlan& p) {
   const uint64_t tps = 1ull << d.tps_log;
   p.tiles = segs * tps;
   if (p.tiles >= (1ull << 31)) return fail(QFB_ERR_UNSUPPORTED, "too many tiles");
-  if (tps > 1) {
-    p.f64_need += segs * tps;
-    p.u32_need += segs;
-  }
-  if (t.outer > 1) {
-    p.f64_need += segs;
-    p.u32_need += (size_t)t.channels;
-  }
+  p.f64_need = segs * tps;  // tile partials, reduced by the finisher
+  p.u32_need = 0;
   return QFB_OK;
 }
 
@@ -671,29 +690,18 @@ qfb_status qfb_fq_bwd_multi(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc* t
       tiles += p.tiles;
       ++cnt;
     }
+    (void)u32;
     if (qfb_status st = grow(ctx, ctx->ws_f64, std::max<size_t>(f64, 1) * 8, false)) return st;
-    if (qfb_status st = grow(ctx, ctx->ws_u32, std::max<size_t>(u32, 1) * 4, true)) return st;
     BwdBatch b;
     std::memset(&b, 0, sizeof b);
     double* fp = static_cast<double*>(ctx->ws_f64.p);
-    uint32_t* up = static_cast<uint32_t*>(ctx->ws_u32.p);
     uint64_t tb = 0;
     for (int32_t k = 0; k < cnt; ++k) {
       BwdDesc d = plans[i + k].d;
       const uint64_t segs = (uint64_t)d.outer * d.chans;
       const uint64_t tps = 1ull << d.tps_log;
-      if (tps > 1) {
-        d.partials = fp;
-        fp += segs * tps;
-        d.seg_counters = up;
-        up += segs;
-      }
-      if (d.outer > 1) {
-        d.seg_results = fp;
-        fp += segs;
-        d.chan_counters = up;
-        up += d.chans;
-      }
+      d.partials = fp;
+      fp += segs * tps;
       b.d[k] = d;
       b.tile_begin[k] = (uint32_t)tb;
       tb += plans[i + k].tiles;
@@ -703,7 +711,7 @@ qfb_status qfb_fq_bwd_multi(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc* t
     const int grid = ctx->sm_count * ctx->bwd_blocks_per_sm[dtype];
     cudaError_t e = launch_bwd(dtype, b, grid, ctx->stream);
     if (e != cudaSuccess) return cuda_fail(e, "bwd_kernel launch");
-    ctx->launches++;
+    ctx->launches += 2;  // main pass + finisher
     i += cnt;
   }
   return QFB_OK;
@@ -804,6 +812,142 @@ qfb_status qfb_fake_quantize_backward_host(qfb_ctx* ctx, qfb_precision prec, con
   if (dx) QFB_CUDA(cudaMemcpyAsync(dx, ctx->host_io[4].p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
   QFB_CUDA(cudaMemcpyAsync(d_log_s, dacc, (size_t)channels * sizeof(double),
                            cudaMemcpyDeviceToHost, ctx->stream));
+  return qfb_ctx_sync(ctx);
+}
+
+qfb_status qfb_quant_pass_host(qfb_ctx* ctx, qfb_precision prec, const qfb_host_point* pts,
+                               int32_t n, const qfb_quant_config* cfg) {
+  if (qfb_status st = check_ctx(ctx)) return st;
+  if (qfb_status st = qfb_quant_config_validate(cfg)) return st;
+  if (n < 0 || (n > 0 && !pts)) return fail(QFB_ERR_VALUE, "quant_pass_host: bad table");
+  if (n == 0) return QFB_OK;
+  const int32_t q = qfb_q_max(cfg);
+  // ---- validate everything and build the parameter block on the host
+  // layout per point k: [s32 (2*C floats padded)...] then doubles; keep it
+  // simple: one double block {s64|chain|acc} x 2 consumers, one float block
+  std::vector<size_t> foff((size_t)n), doff((size_t)n);
+  size_t fcount = 0, dcount = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    const qfb_host_point& p = pts[i];
+    if (qfb_status st = check_dims(p.outer, p.channels, p.inner, "quant_pass_host")) return st;
+    if (!p.x || p.n_out < 1 || p.n_out > 2) return fail(QFB_ERR_VALUE, "quant_pass_host: point %d", i);
+    for (int k = 0; k < p.n_out; ++k) {
+      if (p.y[k] && !p.s[k]) return fail(QFB_ERR_VALUE, "quant_pass_host: point %d needs scales", i);
+      if (p.log_s[k] && (!p.up[k] || !p.d_log_s[k]))
+        return fail(QFB_ERR_VALUE, "quant_pass_host: point %d backward needs up/d_log_s", i);
+    }
+    foff[i] = fcount;
+    fcount += (size_t)(2 * p.channels + 4);   // 16-byte aligned float slots
+    fcount = (fcount + 3) & ~size_t(3);
+    doff[i] = dcount;
+    dcount += (size_t)(6 * p.channels);
+  }
+  std::vector<float> fblk(fcount, 0.0f);
+  std::vector<double> dblk(dcount, 0.0);
+  for (int32_t i = 0; i < n; ++i) {
+    const qfb_host_point& p = pts[i];
+    for (int k = 0; k < p.n_out; ++k) {
+      if (p.y[k])
+        if (qfb_status st = qfb_cast_scales_f32(p.s[k], p.channels, fblk.data() + foff[i] + k * p.channels))
+          return st;
+      if (p.log_s[k]) {
+        double* b = dblk.data() + doff[i] + (size_t)k * 3 * p.channels;
+        if (qfb_status st = qfb_scale_grad_factors(p.log_s[k], p.channels, cfg, prec, b, b + p.channels))
+          return st;
+      }
+    }
+  }
+  DeviceGuard g(ctx->device);
+  if (!ctx->s_in) {
+    QFB_CUDA(cudaStreamCreateWithFlags(&ctx->s_in, cudaStreamNonBlocking));
+    QFB_CUDA(cudaStreamCreateWithFlags(&ctx->s_out, cudaStreamNonBlocking));
+  }
+  while ((int32_t)ctx->ev.size() < 2 * n + 1) {
+    cudaEvent_t e;
+    QFB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx->ev.push_back(e);
+  }
+  const size_t pbytes = fcount * sizeof(float) + dcount * sizeof(double);
+  if (qfb_status st = grow(ctx, ctx->pass_params, pbytes, false)) return st;
+  float* dF = static_cast<float*>(ctx->pass_params.p);
+  double* dD = reinterpret_cast<double*>(static_cast<char*>(ctx->pass_params.p) + fcount * sizeof(float));
+  // all streams start after prior work on the context stream
+  QFB_CUDA(cudaEventRecord(ctx->ev[2 * n], ctx->stream));
+  QFB_CUDA(cudaStreamWaitEvent(ctx->s_in, ctx->ev[2 * n], 0));
+  QFB_CUDA(cudaMemcpyAsync(dF, fblk.data(), fcount * sizeof(float), cudaMemcpyHostToDevice, ctx->s_in));
+  QFB_CUDA(cudaMemcpyAsync(dD, dblk.data(), dcount * sizeof(double), cudaMemcpyHostToDevice, ctx->s_in));
+  // per point: buffers x, up[2], y[2], dx[2]
+  if (ctx->pass_bufs.size() < (size_t)n * 7) ctx->pass_bufs.resize((size_t)n * 7);
+  for (int32_t i = 0; i < n; ++i) {
+    const qfb_host_point& p = pts[i];
+    const size_t bytes = (size_t)(p.outer * p.channels * p.inner) * sizeof(float);
+    DevBuf* B = &ctx->pass_bufs[(size_t)i * 7];
+    if (qfb_status st = grow(ctx, B[0], bytes, false)) return st;
+    for (int k = 0; k < p.n_out; ++k) {
+      if (p.log_s[k])
+        if (qfb_status st = grow(ctx, B[1 + k], bytes, false)) return st;
+      if (p.y[k])
+        if (qfb_status st = grow(ctx, B[3 + k], bytes, false)) return st;
+      if (p.log_s[k] && p.dx[k])
+        if (qfb_status st = grow(ctx, B[5 + k], bytes, false)) return st;
+    }
+  }
+  // ---- pipeline: H2D (s_in) -> kernels (ctx->stream) -> D2H (s_out)
+  const uint32_t flags = prec == QFB_PREC_HALF ? QFB_FLAG_HALF_GRID : 0u;
+  for (int32_t i = 0; i < n; ++i) {
+    const qfb_host_point& p = pts[i];
+    const size_t bytes = (size_t)(p.outer * p.channels * p.inner) * sizeof(float);
+    DevBuf* B = &ctx->pass_bufs[(size_t)i * 7];
+    QFB_CUDA(cudaMemcpyAsync(B[0].p, p.x, bytes, cudaMemcpyHostToDevice, ctx->s_in));
+    for (int k = 0; k < p.n_out; ++k)
+      if (p.log_s[k])
+        QFB_CUDA(cudaMemcpyAsync(B[1 + k].p, p.up[k], bytes, cudaMemcpyHostToDevice, ctx->s_in));
+    QFB_CUDA(cudaEventRecord(ctx->ev[2 * i], ctx->s_in));
+    QFB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev[2 * i], 0));
+    // forward: one launch for all consumers of this tensor
+    bool any_y = false;
+    qfb_fq_desc fd{};
+    fd.x = B[0].p;
+    fd.outer = p.outer;
+    fd.channels = p.channels;
+    fd.inner = p.inner;
+    fd.q_max = q;
+    fd.flags = flags;
+    int no = 0;
+    for (int k = 0; k < p.n_out; ++k) {
+      if (!p.y[k]) continue;
+      fd.y[no] = B[3 + k].p;
+      fd.scale[no] = dF + foff[i] + k * p.channels;
+      ++no;
+      any_y = true;
+    }
+    fd.n_out = no;
+    if (any_y)
+      if (qfb_status st = qfb_fq_fwd_multi(ctx, QFB_F32, &fd, 1)) return st;
+    // backward per consumer
+    qfb_bwd_desc bd[2];
+    int nb = 0;
+    for (int k = 0; k < p.n_out; ++k) {
+      if (!p.log_s[k]) continue;
+      const double* f = dD + doff[i] + (size_t)k * 3 * p.channels;
+      bd[nb] = qfb_bwd_desc{B[0].p, B[1 + k].p, p.dx[k] ? B[5 + k].p : nullptr, f, f + p.channels,
+                            const_cast<double*>(f + 2 * p.channels), p.outer, p.channels, p.inner, q, 0};
+      ++nb;
+    }
+    if (nb)
+      if (qfb_status st = qfb_fq_bwd_multi(ctx, QFB_F32, bd, nb)) return st;
+    QFB_CUDA(cudaEventRecord(ctx->ev[2 * i + 1], ctx->stream));
+    QFB_CUDA(cudaStreamWaitEvent(ctx->s_out, ctx->ev[2 * i + 1], 0));
+    for (int k = 0; k < p.n_out; ++k) {
+      if (p.y[k]) QFB_CUDA(cudaMemcpyAsync(p.y[k], B[3 + k].p, bytes, cudaMemcpyDeviceToHost, ctx->s_out));
+      if (p.log_s[k]) {
+        if (p.dx[k]) QFB_CUDA(cudaMemcpyAsync(p.dx[k], B[5 + k].p, bytes, cudaMemcpyDeviceToHost, ctx->s_out));
+        QFB_CUDA(cudaMemcpyAsync(p.d_log_s[k], dD + doff[i] + (size_t)k * 3 * p.channels + 2 * p.channels,
+                                 (size_t)p.channels * sizeof(double), cudaMemcpyDeviceToHost, ctx->s_out));
+      }
+    }
+  }
+  QFB_CUDA(cudaStreamSynchronize(ctx->s_out));
   return qfb_ctx_sync(ctx);
 }
 

@@ -22,9 +22,11 @@
 //             writing d_input back into the stage; a coalesced 16-byte copy
 //             moves d_input to HBM; warp/CTA butterfly = the subtree's sum;
 //   segment = one row: its 2^(D-g) tile partials are reduced in tree order
-//             by the last CTA to finish (threadfence + atomic ticket);
-//   channel = rows of the same channel over `outer` are accumulated in row
-//             order by the last segment to finish (the trainer's `g += ...`).
+//             by a small stream-ordered finisher kernel (one warp per
+//             channel: per-lane perfect subtrees + xor butterfly), which also
+//             applies the chain factor and folds the rows of a channel over
+//             `outer` in row order (the trainer's `g += ...`). No fences,
+//             atomics or tickets on the hot path.
 // CTAs are persistent (grid = SMs x resident CTAs) and stride over tiles.
 // The result is bit-identical to the reference for any grid size.
 // tests/test_tree_model.py executes this exact schedule on the CPU.
@@ -55,54 +57,6 @@ __device__ __forceinline__ void descend(I& lo, I& m, uint32_t path, int levels) 
       m = h;
     }
   }
-}
-
-// Butterfly over the first `lanes` (power of two) threads of the CTA; the
-// result (sum in perfect-tree order) is returned to thread 0.
-__device__ __forceinline__ double cta_tree_sum(double v, int lanes, double* red) {
-  const int tid = threadIdx.x;
-  const int wl = lanes < 32 ? lanes : 32;
-  for (int off = 1; off < wl; off <<= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
-  if (lanes <= 32) return v;
-  const int nw = lanes >> 5;
-  if ((tid & 31) == 0 && (tid >> 5) < nw) red[tid >> 5] = v;
-  __syncthreads();
-  double r = 0.0;
-  if (tid < 32) {
-    r = tid < nw ? red[tid] : 0.0;
-    for (int off = 1; off < nw; off <<= 1) r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, off));
-  }
-  return r;
-}
-
-// Perfect-tree sum of P consecutive partials (L2 loads: written by other CTAs).
-template <int P>
-__device__ __forceinline__ double tree_load(const double* p) {
-  if constexpr (P == 1) {
-    return __ldcg(p);
-  } else {
-    return __dadd_rn(tree_load<P / 2>(p), tree_load<P / 2>(p + P / 2));
-  }
-}
-
-// Channel-level completion: fold the per-row results of channel c in row
-// order (frontend.hpp:222-228 accumulation).
-__device__ void finish_segment(const BwdDesc& d, uint32_t seg, uint32_t c, double r) {
-  if (d.outer == 1) {
-    d.d_log_s[c] = d.accumulate ? __dadd_rn(d.d_log_s[c], r) : r;
-    return;
-  }
-  d.seg_results[seg] = r;
-  __threadfence();
-  const uint32_t ticket = atomicAdd(d.chan_counters + c, 1u);
-  if (ticket != d.outer - 1) return;
-  __threadfence();
-  double acc = d.accumulate ? __dadd_rn(d.d_log_s[c], __ldcg(d.seg_results + c))
-                            : __ldcg(d.seg_results + c);
-  for (uint32_t o = 1; o < d.outer; ++o)
-    acc = __dadd_rn(acc, __ldcg(d.seg_results + (uint64_t)o * d.chans + c));
-  d.d_log_s[c] = acc;
-  d.chan_counters[c] = 0;  // self-reset for the next launch
 }
 
 template <typename T>
@@ -232,7 +186,6 @@ __global__ void __launch_bounds__(kBwdThreads, 3) bwd_kernel(const __grid_consta
   __shared__ __align__(8) uint64_t bars[kStages];
   __shared__ TileRef sh_tile[2];
   __shared__ double red[kBwdThreads / 32];
-  __shared__ int last_flag;
   const int tid = threadIdx.x;
   const uint32_t total = bt.tile_begin[bt.n];
   if (blockIdx.x >= total) return;
@@ -306,22 +259,12 @@ __global__ void __launch_bounds__(kBwdThreads, 3) bwd_kernel(const __grid_consta
     const double v = glen > 8 ? __dadd_rn(acc_l, acc_r) : acc_l;
     __syncthreads();  // stage.x now holds d_input for the whole tile
 
+    // Warp-level butterfly now; the cross-warp step after the copy-out.
     const int groups = 1 << d.g;
-    const double tile_sum = cta_tree_sum(v, groups, red);
-    const uint32_t tps = 1u << d.tps_log;
-    // Thread 0 publishes the tile result first so its fence/ticket overlaps
-    // the d_input copy-out of the other threads.
-    if (tid == 0) {
-      if (tps == 1) {
-        finish_segment(d, cur.seg, cur.c, __dmul_rn(tile_sum, d.chain[cur.c]));
-        last_flag = 0;
-      } else {
-        d.partials[(uint64_t)cur.seg * tps + cur.t] = tile_sum;
-        __threadfence();
-        const uint32_t ticket = atomicAdd(d.seg_counters + cur.seg, 1u);
-        last_flag = (ticket == tps - 1);
-      }
-    }
+    const int wl = groups < 32 ? groups : 32;
+    double wv = v;
+    for (int o = 1; o < wl; o <<= 1) wv = __dadd_rn(wv, __shfl_xor_sync(0xffffffffu, wv, o));
+    if ((tid & 31) == 0) red[tid >> 5] = wv;
 
     // d_input -> HBM: 16-byte copies for units fully inside the tile,
     // element copies at the two ragged ends.
@@ -343,43 +286,71 @@ __global__ void __launch_bounds__(kBwdThreads, 3) bwd_kernel(const __grid_consta
         }
       }
     }
-    __syncthreads();  // stage reads done; last_flag visible
+    __syncthreads();  // stage reads done (producer may refill it); red complete
 
-    if (last_flag) {
-      __threadfence();
-      const double* p = d.partials + (uint64_t)cur.seg * tps;
-      // each thread reduces `per` consecutive partials as a perfect
-      // subtree, then the CTA butterfly combines the subtrees in order
-      const uint32_t lanes = tps < (uint32_t)kBwdThreads ? tps : (uint32_t)kBwdThreads;
-      const uint32_t per = tps / lanes;
-      double w = 0.0;
-      if ((uint32_t)tid < lanes) {
-        const double* mine = p + (uint64_t)tid * per;
-        switch (per) {
-          case 1: w = tree_load<1>(mine); break;
-          case 2: w = tree_load<2>(mine); break;
-          case 4: w = tree_load<4>(mine); break;
-          case 8: w = tree_load<8>(mine); break;
-          case 16: w = tree_load<16>(mine); break;
-          default: {
-            // per > 16 (rows > 2^26 elements): level-by-level in place over
-            // the thread's own slice, still the perfect-tree order
-            double* q2 = const_cast<double*>(mine);
-            for (uint32_t width = per; width > 1; width >>= 1)
-              for (uint32_t kk = 0; kk < width / 2; ++kk)
-                q2[kk] = __dadd_rn(__ldcg(q2 + 2 * kk), __ldcg(q2 + 2 * kk + 1));
-            w = __ldcg(q2);
-          }
-        }
-      }
-      const double seg_sum = cta_tree_sum(w, (int)lanes, red);
-      if (tid == 0) {
-        d.seg_counters[cur.seg] = 0;  // self-reset
-        finish_segment(d, cur.seg, cur.c, __dmul_rn(seg_sum, d.chain[cur.c]));
-      }
-      __syncthreads();  // red reused by the next tile
+    // Perfect-tree combine of the warp sums (groups > 32) -> tile partial.
+    if (tid < 32) {
+      const int nw = groups > 32 ? groups >> 5 : 1;
+      double r = tid < nw ? red[tid] : 0.0;
+      for (int o = 1; o < nw; o <<= 1) r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, o));
+      if (tid == 0) d.partials[((uint64_t)cur.seg << d.tps_log) + cur.t] = r;
     }
   }
+}
+
+// Finisher: one warp per (descriptor, channel). Each row's 2^tps_log tile
+// partials are reduced in perfect-tree order (lane slices + xor butterfly),
+// times chain[c]; rows of the channel are folded in row order.
+constexpr int kFinSmem = 4096;  // partials per row staged in smem (32 KB)
+
+__global__ void __launch_bounds__(32) bwd_finish_kernel(const __grid_constant__ BwdBatch bt,
+                                                        uint32_t warp_base_mul) {
+  __shared__ double sp[kFinSmem];
+  // locate (descriptor, channel) of this warp: warps are laid out per
+  // descriptor as chans consecutive warps
+  uint32_t w = blockIdx.x;
+  int di = 0;
+  while (di < bt.n && w >= bt.d[di].chans) {
+    w -= bt.d[di].chans;
+    ++di;
+  }
+  if (di >= bt.n) return;
+  const BwdDesc& d = bt.d[di];
+  const uint32_t c = w;
+  const int lane = threadIdx.x;
+  const uint32_t tps = 1u << d.tps_log;
+  const uint32_t lanes = tps < 32u ? tps : 32u;
+  const uint32_t per = tps / lanes;
+  const double chain = d.chain[c];
+  double acc = 0.0;
+  for (uint32_t o = 0; o < d.outer; ++o) {
+    const double* p = d.partials + (((uint64_t)o * d.chans + c) << d.tps_log);
+    double v = 0.0;
+    if (per == 1) {
+      v = (uint32_t)lane < lanes ? p[lane] : 0.0;
+    } else if (tps <= (uint32_t)kFinSmem) {
+      for (uint32_t i = lane; i < tps; i += 32) sp[i] = p[i];
+      __syncwarp();
+      double* mine = sp + (uint32_t)lane * per;
+      for (uint32_t width = per; width > 1; width >>= 1)
+        for (uint32_t k = 0; k < width / 2; ++k) mine[k] = __dadd_rn(mine[2 * k], mine[2 * k + 1]);
+      v = mine[0];
+      __syncwarp();
+    } else {
+      // huge rows: in place over the lane's own global slice
+      double* mine = const_cast<double*>(p) + (uint64_t)lane * per;
+      for (uint32_t width = per; width > 1; width >>= 1)
+        for (uint32_t k = 0; k < width / 2; ++k) mine[k] = __dadd_rn(mine[2 * k], mine[2 * k + 1]);
+      v = mine[0];
+    }
+    for (uint32_t off = 1; off < lanes; off <<= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+    const double r = __dmul_rn(v, chain);
+    // accumulate == 0: ((r0 + r1) + ...); else ((d_log_s + r0) + r1) + ...
+    if (o == 0) acc = d.accumulate ? __dadd_rn(d.d_log_s[c], r) : r;
+    else acc = __dadd_rn(acc, r);
+  }
+  if (lane == 0) d.d_log_s[c] = acc;
+  (void)warp_base_mul;
 }
 
 template <typename T>
@@ -413,6 +384,11 @@ cudaError_t launch_bwd(int dtype, const BwdBatch& b, int grid, cudaStream_t st) 
     bwd_kernel<float><<<grid, kBwdThreads, stage_bytes<float>(), st>>>(b);
   else
     bwd_kernel<__half><<<grid, kBwdThreads, stage_bytes<__half>(), st>>>(b);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  uint32_t warps = 0;
+  for (int i = 0; i < b.n; ++i) warps += b.d[i].chans;
+  bwd_finish_kernel<<<warps, 32, 0, st>>>(b, 0u);
   return cudaGetLastError();
 }
 

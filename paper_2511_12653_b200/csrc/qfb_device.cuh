@@ -162,6 +162,10 @@ __device__ __forceinline__ DivCtx make_div(double s) {
   return c;
 }
 
+// Out of line so the compiler cannot if-convert (speculate) the full IEEE
+// division onto the fast path.
+static __device__ __noinline__ double slow_ddiv(double x, double s) { return __ddiv_rn(x, s); }
+
 __device__ __forceinline__ double certified_div(float xf, const DivCtx& c) {
   const double x = (double)xf;
   const double q0 = __dmul_rn(x, c.y);
@@ -174,7 +178,7 @@ __device__ __forceinline__ double certified_div(float xf, const DivCtx& c) {
   const bool ok = c.usable && (qb & 0x000fffffffffffffull) != 0ull && e > 160ull && e < 1900ull &&
                   fabs(r1) < half_ulp_s;
   if (__builtin_expect(ok, 1)) return q1;
-  return __ddiv_rn(x, c.s);
+  return slow_ddiv(x, c.s);
 }
 
 // grad_term with the certified division.

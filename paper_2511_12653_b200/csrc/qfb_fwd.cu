@@ -154,6 +154,101 @@ __global__ void __launch_bounds__(kEwThreads, kChain ? 3 : 4) ew_kernel(const __
   if (nf) atomicOr(status, kStatusNonFinite);
 }
 
+// ------------------------------------------- TMA-staged plain forward ---
+// Plain multi-output FQ forward (aligned descriptors): chunks of 1024
+// 16-byte units are brought into a kFwdStages-deep shared-memory ring by the
+// TMA engine (cp.async.bulk + mbarrier), issued by thread 0 kFwdStages-1
+// chunks ahead, so the bytes in flight no longer depend on registers or
+// occupancy; threads read conflict-free 16-byte vectors from smem and write
+// outputs with 16-byte stores.
+constexpr int kFwdStages = 3;
+constexpr int kFwdChunkBytes = kEwChunk * 16;  // 16 KB
+
+struct ChunkRef {
+  int di;
+  uint32_t u0;     // first unit of the chunk within the descriptor
+  uint32_t units;  // units in this chunk
+};
+
+__device__ __forceinline__ ChunkRef locate_chunk(const EwBatch& bt, uint32_t chunk) {
+  int lo = 0, hi = bt.n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (bt.chunk_begin[mid] <= chunk) lo = mid;
+    else hi = mid - 1;
+  }
+  ChunkRef r;
+  r.di = lo;
+  r.u0 = (chunk - bt.chunk_begin[lo]) * kEwChunk;
+  const uint32_t left = bt.d[lo].nunits - r.u0;
+  r.units = left < (uint32_t)kEwChunk ? left : (uint32_t)kEwChunk;
+  return r;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kEwThreads, 4)
+    ew_tma_kernel(const __grid_constant__ EwBatch bt, uint32_t* __restrict__ status) {
+  constexpr int V = Elem<T>::kPerVec;
+  extern __shared__ __align__(128) unsigned char fsmem[];
+  uint4* ring = reinterpret_cast<uint4*>(fsmem);
+  __shared__ __align__(8) uint64_t bars[kFwdStages];
+  __shared__ ChunkRef refs[kFwdStages];
+  const int tid = threadIdx.x;
+  const uint32_t total = bt.chunk_begin[bt.n];
+  if (blockIdx.x >= total) return;
+
+  auto issue = [&](uint32_t chunk, int s) {
+    const ChunkRef r = locate_chunk(bt, chunk);
+    refs[s] = r;
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(&bars[s], r.units * 16u);
+    bulk_g2s(ring + s * kEwChunk, static_cast<const uint4*>(bt.d[r.di].a) + r.u0, r.units * 16u,
+             &bars[s]);
+  };
+  if (tid == 0) {
+    for (int s = 0; s < kFwdStages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+    for (int s = 0; s < kFwdStages - 1; ++s) {
+      const uint32_t c = blockIdx.x + (uint32_t)s * gridDim.x;
+      if (c < total) issue(c, s);
+    }
+  }
+  __syncthreads();
+
+  bool nf = false;
+  uint32_t phase_bits = 0;
+  int it = 0;
+  for (uint32_t chunk = blockIdx.x; chunk < total; chunk += gridDim.x, ++it) {
+    const int s = it % kFwdStages;
+    // producer: keep kFwdStages-1 chunks in flight (the target stage was
+    // released by the barrier at the end of the previous iteration)
+    if (tid == 0) {
+      const uint32_t c = chunk + (uint32_t)(kFwdStages - 1) * gridDim.x;
+      if (c < total) issue(c, (it + kFwdStages - 1) % kFwdStages);
+    }
+    mbar_wait(&bars[s], (phase_bits >> s) & 1u);
+    phase_bits ^= 1u << s;
+    const ChunkRef r = refs[s];
+    const EwDesc& d = bt.d[r.di];
+    const bool streaming = (d.flags & kEwStreaming) != 0;
+    const bool half_out = (d.flags & kEwHalfGrid) != 0;
+    const uint4* src = ring + s * kEwChunk;
+    for (uint32_t k = tid; k < r.units; k += kEwThreads) {
+      const uint32_t u = r.u0 + k;
+      const uint32_t ch = channel_of(u, d.inner_u, d.chans);
+      float v[V];
+      Elem<T>::unpack(src[k], v);
+      for (int j = 0; j < d.n_out; ++j) {
+        float o[V];
+        fq_unit<V>(v, __ldg(d.s[j] + ch), d.q, o);
+        st_v4(static_cast<uint4*>(d.y[j]) + u, Elem<T>::pack(o, v, half_out, nf), streaming);
+      }
+    }
+    __syncthreads();  // stage s free for the producer
+  }
+  if (nf) atomicOr(status, kStatusNonFinite);
+}
+
 // ------------------------------------------------------------ codes ---
 template <typename T>
 __global__ void __launch_bounds__(kEwThreads) codes_kernel(const __grid_constant__ CodesDesc d) {
@@ -284,6 +379,21 @@ __global__ void resolve_kernel(const __grid_constant__ ResolveDesc d, uint32_t* 
 }
 
 }  // namespace
+
+size_t ew_tma_smem() { return (size_t)kFwdStages * kFwdChunkBytes; }
+
+cudaError_t ew_tma_occupancy(int dtype, int* blocks_per_sm) {
+  const void* f = dtype == 0 ? (const void*)ew_tma_kernel<float> : (const void*)ew_tma_kernel<__half>;
+  cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ew_tma_smem());
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, kEwThreads, ew_tma_smem());
+}
+
+cudaError_t launch_ew_tma(int dtype, const EwBatch& b, uint32_t* status, int grid, cudaStream_t st) {
+  if (dtype == 0) ew_tma_kernel<float><<<grid, kEwThreads, ew_tma_smem(), st>>>(b, status);
+  else ew_tma_kernel<__half><<<grid, kEwThreads, ew_tma_smem(), st>>>(b, status);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_ew(int dtype, bool chain, const EwBatch& b, uint32_t* status, int grid,
                       cudaStream_t st) {

@@ -68,6 +68,9 @@ struct EwBatch {
 cudaError_t ew_occupancy(int dtype, bool chain, int* blocks_per_sm);
 cudaError_t launch_ew(int dtype, bool chain, const EwBatch& b, uint32_t* status, int grid,
                       cudaStream_t st);
+// TMA-staged plain forward: every descriptor must be on the vector path.
+cudaError_t ew_tma_occupancy(int dtype, int* blocks_per_sm);
+cudaError_t launch_ew_tma(int dtype, const EwBatch& b, uint32_t* status, int grid, cudaStream_t st);
 
 // int8 codes (vec path when aligned).
 struct CodesDesc {
@@ -127,11 +130,8 @@ struct BwdDesc {
   const double* s64;
   const double* chain;
   double* d_log_s;
-  double* partials;         // [segments * tps] when tps > 1
-  double* seg_results;      // [segments] when outer > 1
-  uint32_t* seg_counters;   // [segments] when tps > 1 (zero, self-resetting)
-  uint32_t* chan_counters;  // [channels] when outer > 1 (zero, self-resetting)
-  uint64_t inner;           // row (segment) length n
+  double* partials;  // [segments * tps] tile sums, reduced by bwd_finish
+  uint64_t inner;    // row (segment) length n
   uint32_t outer;
   uint32_t chans;
   uint32_t tps_log;  // tiles per segment = 2^(depth - g)
@@ -139,7 +139,7 @@ struct BwdDesc {
   uint32_t g;        // tile depth = min(depth, kBwdGroupsLog)
   int32_t accumulate;
   double q;
-  uint32_t vec;  // x/up/dx 16-byte aligned: vector-window loads
+  uint32_t vec;  // x/up/dx 16-byte aligned: TMA bulk staging
   uint32_t pad;
 };
 
@@ -151,6 +151,8 @@ struct BwdBatch {
 };
 
 cudaError_t bwd_occupancy(int dtype, int* blocks_per_sm);
+// Main pass (tile partials) + finisher (segment trees, chain, outer fold);
+// stream order replaces fences and tickets.
 cudaError_t launch_bwd(int dtype, const BwdBatch& b, int grid, cudaStream_t st);
 
 }  // namespace qfb

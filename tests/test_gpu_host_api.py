@@ -57,3 +57,47 @@ def test_host_fwd_codes_bwd(qfb, orc, ref, cuda):
                                   s_bad.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(cfg))
     assert st == 2
     ctx.close()
+
+
+def test_quant_pass_host_matches_reference(qfb, orc, ref, cuda):
+    """Frame-level pipelined host pass == per-point reference calls, bitwise
+    (forward outputs, d_input and scale gradients)."""
+    import torch
+    rng = np.random.default_rng(11)
+    shapes = [(3, 48, 64, 2), (32, 24, 32, 1), (32, 24, 32, 2), (64, 12, 16, 1), (7, 5, 9, 1)]
+    keep, pts, checks = [], [], []
+    D = ctypes.POINTER(ctypes.c_double)
+    for C, H, W, n_out in shapes:
+        x = torch.from_numpy(rng.normal(0, 1, C * H * W).astype(np.float32)).pin_memory()
+        p = qfb.CHostPoint()
+        p.x = x.data_ptr()
+        p.outer, p.channels, p.inner, p.n_out = 1, C, H * W, n_out
+        keep.append(x)
+        for k in range(n_out):
+            s = np.exp(rng.uniform(np.log(1e-3), np.log(0.1), C))
+            ls = np.log(np.expm1(s))
+            up = torch.from_numpy(rng.normal(0, 1, C * H * W).astype(np.float32)).pin_memory()
+            y = torch.empty(C * H * W).pin_memory()
+            dx = torch.empty(C * H * W).pin_memory()
+            dls = np.zeros(C)
+            keep += [s, ls, up, y, dx, dls]
+            p.s[k] = s.ctypes.data
+            p.y[k] = y.data_ptr()
+            p.log_s[k] = ls.ctypes.data
+            p.up[k] = up.data_ptr()
+            p.dx[k] = dx.data_ptr()
+            p.d_log_s[k] = dls.ctypes.data
+            checks.append((x.numpy(), s, ls, up.numpy(), y, dx, dls, C, H * W))
+        pts.append(p)
+    ctx = qfb.Context(0)
+    cfg = qfb.QuantConfig().to_c()
+    table = (qfb.CHostPoint * len(pts))(*pts)
+    for _ in range(2):
+        qfb.check(qfb.lib().qfb_quant_pass_host(ctx.handle, 0, table, len(pts), ctypes.byref(cfg)))
+        for x, s, ls, up, y, dx, dls, C, HW in checks:
+            _, wy = ref.fake_quantize(x, [C, HW], s, per_channel=True)
+            assert np.array_equal(bits32(y.numpy()), bits32(wy))
+            _, wdx, wdls = ref.fq_backward(x, up, [C, HW], ls, per_channel=True)
+            assert np.array_equal(bits32(dx.numpy()), bits32(wdx))
+            assert dls.tobytes() == wdls.tobytes()
+    ctx.close()

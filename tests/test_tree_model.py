@@ -73,8 +73,8 @@ def device_schedule_sum(a):
         partials.append(butterfly(leaves))
     if len(partials) == 1:
         return partials[0]
-    # last CTA: each lane tree-reduces `per` consecutive partials, then butterfly
-    lanes = min(len(partials), 256)
+    # finisher warp: each lane tree-reduces `per` consecutive partials, then butterfly
+    lanes = min(len(partials), 32)
     per = len(partials) // lanes
     sub = []
     for i in range(lanes):
