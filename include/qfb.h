@@ -302,6 +302,69 @@ qfb_status qfb_fake_quantize_backward_host(
     int32_t accumulate);
 
 /* ---------------------------------------------------------------------- */
+/* Execution plan: the quant part of qf::run_quant_conv (exec.hpp:222-405) */
+/* — scale pass, activation FQ, weight FQ — under a PerOperator (four      */
+/* materialized sweeps each) or Fused (one sweep each) plan, with the      */
+/* fused-path fault hook and fallback, the frozen-weight cache and the     */
+/* modeled pass/byte counters (exec.hpp:199-216). The convolution itself   */
+/* stays with the caller (cuDNN).                            */
+/* ---------------------------------------------------------------------- */
+typedef enum qfb_exec_mode { QFB_MODE_PER_OPERATOR = 0, QFB_MODE_FUSED = 1 } qfb_exec_mode; /* exec.hpp:43 */
+typedef enum qfb_precision_policy {
+  QFB_POLICY_FULL_ONLY = 0, QFB_POLICY_HALF_ACTIVATIONS = 1                              /* exec.hpp:44 */
+} qfb_precision_policy;
+
+typedef struct qfb_exec_plan {   /* qf::ExecutionPlan, exec.hpp:55-65 */
+  int32_t mode;                  /* qfb_exec_mode */
+  int32_t policy;                /* qfb_precision_policy */
+  int32_t fallback_enabled;      /* fused failure -> per-operator rerun */
+  int32_t cache_weights;         /* quantize frozen weights once per plan */
+  int32_t fault_inject_layer;    /* test hook: fused path fails at this layer (-1 off) */
+  int32_t reserved;
+} qfb_exec_plan;
+
+typedef struct qfb_exec_trace {  /* qf::ExecutionTrace counters, exec.hpp:75-98 */
+  int64_t pass_count;            /* modeled sweeps (scale + quant; conv is the caller's) */
+  int64_t bytes_read;
+  int64_t bytes_written;
+  int64_t launches;              /* device kernels actually launched */
+  int64_t peak_scratch_bytes;    /* per-operator temporaries (allocated peak) */
+  int32_t fell_back;
+  int32_t layers;
+} qfb_exec_trace;
+
+/* One layer's quantization state (qf::ConvLayer quant fields, model.hpp). */
+typedef struct qfb_quant_layer {
+  int32_t index;                 /* roster index: fault hook + cache key */
+  int32_t reserved;
+  const float* weight;           /* device [c_out, per], float32 */
+  int64_t c_out, per;
+  const double* log_w;           /* host [c_out] log weight scales */
+  double log_a;                  /* log activation scale */
+} qfb_quant_layer;
+
+typedef struct qfb_exec qfb_exec;
+qfb_status qfb_exec_create(qfb_ctx* ctx, const qfb_exec_plan* plan, qfb_exec** out);
+qfb_status qfb_exec_destroy(qfb_exec* ex);
+/* Quantize one layer's activation x (device, dtype, [outer, channels,
+ * inner] viewed per-tensor as in the reference) into qa (device, same
+ * dtype) and its weights into *qw (device float[c_out*per]; points at the
+ * plan's cache when cache_weights, else at qw_buf which the caller owns).
+ * Returns QFB_ERR_FUSED_PATH when the injected fault fires without
+ * fallback. */
+qfb_status qfb_exec_quant_layer(qfb_exec* ex, const qfb_quant_layer* layer,
+                                const qfb_quant_config* cfg, qfb_dtype dtype,
+                                const void* x, int64_t n_act, void* qa,
+                                float* qw_buf, const float** qw);
+qfb_status qfb_exec_trace_get(const qfb_exec* ex, qfb_exec_trace* out);
+qfb_status qfb_exec_trace_reset(qfb_exec* ex);
+/* The modeled counter increments of one layer, exec.hpp:203-214 byte rules
+ * (host only, no GPU): for the schedule-walker tests (test_exec.cpp:31-92). */
+qfb_status qfb_exec_model_layer(const qfb_exec_plan* plan, int64_t n_act, int64_t c_out,
+                                int64_t per, int32_t weights_cached, int32_t fused_fails,
+                                qfb_exec_trace* delta);
+
+/* ---------------------------------------------------------------------- */
 /* Frame-level host pass: the quant portion of run_frontend +             */
 /* backward_train (exec.hpp:435-451, frontend.hpp:236-258) for a set of    */
 /* quant points given as HOST float32 buffers. Each input tensor is copied */

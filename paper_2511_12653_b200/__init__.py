@@ -134,6 +134,22 @@ class CHostPoint(ctypes.Structure):
                 ("log_s", _vp * 2), ("up", _vp * 2), ("dx", _vp * 2), ("d_log_s", _vp * 2)]
 
 
+class CExecPlan(ctypes.Structure):
+    _fields_ = [("mode", _i32), ("policy", _i32), ("fallback_enabled", _i32),
+                ("cache_weights", _i32), ("fault_inject_layer", _i32), ("reserved", _i32)]
+
+
+class CExecTrace(ctypes.Structure):
+    _fields_ = [("pass_count", _i64), ("bytes_read", _i64), ("bytes_written", _i64),
+                ("launches", _i64), ("peak_scratch_bytes", _i64), ("fell_back", _i32),
+                ("layers", _i32)]
+
+
+class CQuantLayer(ctypes.Structure):
+    _fields_ = [("index", _i32), ("reserved", _i32), ("weight", _vp), ("c_out", _i64),
+                ("per", _i64), ("log_w", _vp), ("log_a", _dbl)]
+
+
 def _sig(name, res, args):
     f = getattr(_lib, name)
     f.restype = res
@@ -172,6 +188,14 @@ _sig("qfb_fill_rng", _i32, [_vp, _i32, _vp, _i64, _u64, _u64, _u64, _i32, _dbl, 
 _sig("qfb_fq_fwd_perop", _i32, [_vp, _i32, _vp, _vp, _i64, _i64, _i64, _vp, _i32, _u32, _vp])
 _sig("qfb_fake_quantize_host", _i32, [_vp, _i32, _vp, _vp, _i64, _i64, _i64, _pd, ctypes.POINTER(CQuantConfig)])
 _sig("qfb_int8_codes_host", _i32, [_vp, _vp, _vp, _i64, _i64, _i64, _pd, ctypes.POINTER(CQuantConfig)])
+_sig("qfb_exec_create", _i32, [_vp, ctypes.POINTER(CExecPlan), ctypes.POINTER(_vp)])
+_sig("qfb_exec_destroy", _i32, [_vp])
+_sig("qfb_exec_quant_layer", _i32, [_vp, ctypes.POINTER(CQuantLayer), ctypes.POINTER(CQuantConfig), _i32,
+                                    _vp, _i64, _vp, _vp, ctypes.POINTER(_vp)])
+_sig("qfb_exec_trace_get", _i32, [_vp, ctypes.POINTER(CExecTrace)])
+_sig("qfb_exec_trace_reset", _i32, [_vp])
+_sig("qfb_exec_model_layer", _i32, [ctypes.POINTER(CExecPlan), _i64, _i64, _i64, _i32, _i32,
+                                    ctypes.POINTER(CExecTrace)])
 _sig("qfb_quant_pass_host", _i32, [_vp, _i32, ctypes.POINTER(CHostPoint), _i32, ctypes.POINTER(CQuantConfig)])
 _sig("qfb_fake_quantize_backward_host", _i32, [_vp, _i32, _vp, _vp, _vp, _i64, _i64, _i64, _pd,
                                                 ctypes.POINTER(CQuantConfig), _pd, _i32])
@@ -509,4 +533,99 @@ def fill_rng(t, seed: int, stream: int, kind: int = 1, lo: float = 1.0, hi: floa
     ctx = ctx or default_context(t.device.index)
     check(_lib.qfb_fill_rng(ctx.handle, _dtype_code(t), _vp(t.data_ptr()), t.numel(), seed, stream,
                             offset, kind, lo, hi))
+    return t
+
+
+# ------------------------------------------------------ execution plan --
+
+MODE_PER_OPERATOR, MODE_FUSED = 0, 1
+POLICY_FULL_ONLY, POLICY_HALF_ACTIVATIONS = 0, 1
+
+
+@dataclasses.dataclass
+class ExecutionPlan:
+    """qf::ExecutionPlan (exec.hpp:55-65); `threads` has no GPU meaning."""
+    mode: int = MODE_FUSED
+    policy: int = POLICY_FULL_ONLY
+    fallback_enabled: bool = True
+    cache_weights: bool = False
+    fault_inject_layer: int = -1
+
+    def to_c(self) -> CExecPlan:
+        return CExecPlan(self.mode, self.policy, int(self.fallback_enabled), int(self.cache_weights),
+                         self.fault_inject_layer, 0)
+
+
+class ExecutionContext:
+    """The quantization part of qf::ExecutionContext + run_quant_conv
+    (exec.hpp:182-405) on the GPU: `quant_layer` returns (qa, qw) for the
+    caller's convolution; `trace` holds the modeled counters."""
+
+    def __init__(self, plan: ExecutionPlan, ctx: Optional[Context] = None, device: int = 0):
+        self.plan = plan
+        self.ctx = ctx or default_context(device)
+        h = _vp()
+        c = plan.to_c()
+        check(_lib.qfb_exec_create(self.ctx.handle, ctypes.byref(c), ctypes.byref(h)))
+        self.handle = h
+
+    def quant_layer(self, index: int, x, weight, log_w: Sequence[float], log_a: float,
+                    cfg: Optional[QuantConfig] = None):
+        import torch
+        cfg = _cfg(cfg)
+        w = weight.contiguous().float()
+        c_out = w.shape[0]
+        per = w.numel() // c_out
+        lw = (ctypes.c_double * c_out)(*[float(v) for v in log_w])
+        L = CQuantLayer(index, 0, w.data_ptr(), c_out, per, ctypes.cast(lw, _vp), float(log_a))
+        x = x.contiguous()
+        qa = torch.empty_like(x)
+        qw_buf = None if self.plan.cache_weights else torch.empty_like(w)
+        out = _vp()
+        cc = cfg.to_c()
+        check(_lib.qfb_exec_quant_layer(self.handle, ctypes.byref(L), ctypes.byref(cc), _dtype_code(x),
+                                        _vp(x.data_ptr()), x.numel(), _vp(qa.data_ptr()),
+                                        _vp(qw_buf.data_ptr() if qw_buf is not None else 0),
+                                        ctypes.byref(out)))
+        self.ctx.sync()
+        if qw_buf is not None and out.value == qw_buf.data_ptr():
+            return qa, qw_buf
+        # plan-owned cache buffer: return a copy (the cache stays private)
+        return qa, _device_view(out.value, w.numel() * 4, w.device).view(torch.float32).view_as(w).clone()
+
+    @property
+    def trace(self) -> CExecTrace:
+        t = CExecTrace()
+        check(_lib.qfb_exec_trace_get(self.handle, ctypes.byref(t)))
+        return t
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _lib.qfb_exec_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _device_view(ptr: int, nbytes: int, device):
+    """uint8 torch view of a library-owned device buffer."""
+    import torch
+
+    class _View:
+        __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, True),
+                                    "version": 2}
+    return torch.as_tensor(_View(), device=device)
+
+
+def model_layer_counts(plan: ExecutionPlan, n_act: int, c_out: int, per: int, weights_cached: bool = False,
+                       fused_fails: bool = False) -> CExecTrace:
+    """Host-only modeled counter increments of one layer (exec.hpp:199-216)."""
+    t = CExecTrace()
+    c = plan.to_c()
+    check(_lib.qfb_exec_model_layer(ctypes.byref(c), n_act, c_out, per, int(weights_cached),
+                                    int(fused_fails), ctypes.byref(t)))
     return t

@@ -634,7 +634,7 @@ uint32_t leaf_depth(uint64_t n) {
   return d;
 }
 
-qfb_status plan_bwd(const qfb_bwd_desc& t, BwdPlan& p) {
+qfb_status plan_bwd(const qfb_bwd_desc& t, BwdPlan& p, int dtype_of_plan) {
   if (qfb_status st = check_dims(t.outer, t.channels, t.inner, "fake_quantize_backward")) return st;
   if (!t.x || !t.up || !t.scale64 || !t.chain || !t.d_log_s)
     return fail(QFB_ERR_VALUE, "fake_quantize_backward: null pointer");
@@ -658,6 +658,8 @@ qfb_status plan_bwd(const qfb_bwd_desc& t, BwdPlan& p) {
   d.accumulate = t.accumulate ? 1 : 0;
   d.q = (double)t.q_max;
   d.vec = (aligned16(t.x) && aligned16(t.up) && (!t.dx || aligned16(t.dx))) ? 1u : 0u;
+  d.total_bytes = (uint64_t)t.outer * (uint64_t)t.channels * (uint64_t)t.inner *
+                  (uint64_t)elem_size(dtype_of_plan);
   const uint64_t tps = 1ull << d.tps_log;
   p.tiles = segs * tps;
   if (p.tiles >= (1ull << 31)) return fail(QFB_ERR_UNSUPPORTED, "too many tiles");
@@ -674,7 +676,7 @@ qfb_status qfb_fq_bwd_multi(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc* t
   if (n < 0 || (n > 0 && !table)) return fail(QFB_ERR_VALUE, "fq_bwd_multi: bad table");
   std::vector<BwdPlan> plans((size_t)n);
   for (int32_t i = 0; i < n; ++i)
-    if (qfb_status st = plan_bwd(table[i], plans[i])) return st;
+    if (qfb_status st = plan_bwd(table[i], plans[i], dtype)) return st;
   DeviceGuard g(ctx->device);
   int32_t i = 0;
   while (i < n) {

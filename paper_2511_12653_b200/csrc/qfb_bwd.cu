@@ -76,12 +76,17 @@ __device__ __forceinline__ T from_f(float v) {
   else return __float2half_rn(v);  // d_input of a half upstream: exact
 }
 
-// Where one tile lives: descriptor, row segment, tree node.
+// Where one tile lives: descriptor, row segment, tree node, its 16-byte
+// window and the division context — computed once by the producer thread.
 struct TileRef {
   int di;
   uint32_t seg, t, c;
-  uint64_t A;  // first element (descriptor-relative)
-  int m;       // elements
+  uint64_t A;   // first element (descriptor-relative)
+  int m;        // elements
+  int off;      // tile start inside the staged window (elements)
+  uint64_t w0;  // window [w0, w1) in bytes
+  uint64_t w1;
+  double s, y;  // scale and RN(1/s)
 };
 
 __device__ __forceinline__ TileRef locate(const BwdBatch& bt, uint32_t tile_id) {
@@ -107,6 +112,22 @@ __device__ __forceinline__ TileRef locate(const BwdBatch& bt, uint32_t tile_id) 
   return r;
 }
 
+template <typename T>
+__device__ __forceinline__ void window(const BwdDesc& d, const TileRef& r, uint64_t& w0,
+                                       uint64_t& w1);
+
+// Producer-side completion of a TileRef: window, in-stage offset, s, 1/s.
+template <typename T>
+__device__ __forceinline__ TileRef locate_full(const BwdBatch& bt, uint32_t tile_id) {
+  TileRef r = locate(bt, tile_id);
+  const BwdDesc& d = bt.d[r.di];
+  window<T>(d, r, r.w0, r.w1);
+  r.off = (int)((r.A * sizeof(T) - r.w0) / sizeof(T));
+  r.s = d.s64[r.c];
+  r.y = __drcp_rn(r.s);
+  return r;
+}
+
 // 16-byte window [w0, w1) (bytes) of a tile that a bulk copy may fetch:
 // never past the last full 16 bytes of the tensor (the few elements beyond
 // are loaded by threads).
@@ -114,7 +135,7 @@ template <typename T>
 __device__ __forceinline__ void window(const BwdDesc& d, const TileRef& r, uint64_t& w0,
                                        uint64_t& w1) {
   const uint64_t b0 = r.A * sizeof(T), b1 = (r.A + (uint64_t)r.m) * sizeof(T);
-  const uint64_t tot = (uint64_t)d.outer * d.chans * d.inner * sizeof(T);
+  const uint64_t tot = d.total_bytes;
   w0 = b0 & ~uint64_t(15);
   w1 = (b1 + 15) & ~uint64_t(15);
   const uint64_t cap = tot & ~uint64_t(15);
@@ -125,14 +146,12 @@ __device__ __forceinline__ void window(const BwdDesc& d, const TileRef& r, uint6
 template <typename T>
 __device__ __forceinline__ void issue_tile(const BwdDesc& d, const TileRef& r, Stage<T>& st,
                                            uint64_t* bar) {
-  uint64_t w0, w1;
-  window<T>(d, r, w0, w1);
-  const uint32_t bytes = (uint32_t)(w1 - w0);
+  const uint32_t bytes = (uint32_t)(r.w1 - r.w0);
   fence_proxy_async_smem();
   mbar_arrive_expect_tx(bar, 2 * bytes);
   if (bytes) {
-    bulk_g2s(st.x, static_cast<const char*>(d.x) + w0, bytes, bar);
-    bulk_g2s(st.up, static_cast<const char*>(d.up) + w0, bytes, bar);
+    bulk_g2s(st.x, static_cast<const char*>(d.x) + r.w0, bytes, bar);
+    bulk_g2s(st.up, static_cast<const char*>(d.up) + r.w0, bytes, bar);
   }
 }
 
@@ -169,14 +188,38 @@ struct GroupCache {
 };
 
 // Terms of one element: d_ds * up (double) and d_input (x86 NaN rules).
-template <typename T>
-__device__ __forceinline__ double elem(T* sx, const T* su, int k, const DivCtx& dc, double q,
-                                       bool want_dx) {
+template <typename T, bool kDx>
+__device__ __forceinline__ double elem(T* sx, const T* su, int k, const DivCtx& dc, double q) {
   const float xv = to_f<T>(sx[k]);
   const float uv = to_f<T>(su[k]);
   const GradTerm gt = grad_term_fast(xv, dc, q);
-  if (want_dx) sx[k] = from_f<T>(masked_upstream(gt.mask, uv));
+  if (kDx) sx[k] = from_f<T>(masked_upstream(gt.mask, uv));
   return __dmul_rn(gt.d_ds, (double)uv);
+}
+
+// A leaf group's sum in the reference order: fold(left half) + fold(right
+// half) from 0.0 each (or one fold if <= 8 elements). The two folds are
+// independent chains, so they are interleaved for ILP.
+template <typename T, bool kDx>
+__device__ __forceinline__ double group_sum(T* sx, const T* su, int glen, const DivCtx& dc,
+                                            double q) {
+  if (glen <= 8) {
+    double acc = 0.0;
+    for (int k = 0; k < glen; ++k) acc = __dadd_rn(acc, elem<T, kDx>(sx, su, k, dc, q));
+    return acc;
+  }
+  const int h = glen >> 1;  // left; right has glen - h >= h elements
+  T* rx = sx + h;
+  const T* ru = su + h;
+  double acc_l = 0.0, acc_r = 0.0;
+  for (int k = 0; k < h; ++k) {
+    const double tl = elem<T, kDx>(sx, su, k, dc, q);
+    const double tr = elem<T, kDx>(rx, ru, k, dc, q);
+    acc_l = __dadd_rn(acc_l, tl);
+    acc_r = __dadd_rn(acc_r, tr);
+  }
+  if (glen - h > h) acc_r = __dadd_rn(acc_r, elem<T, kDx>(rx, ru, h, dc, q));
+  return __dadd_rn(acc_l, acc_r);
 }
 
 template <typename T>
@@ -195,7 +238,7 @@ __global__ void __launch_bounds__(kBwdThreads, 3) bwd_kernel(const __grid_consta
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
-    sh_tile[0] = locate(bt, blockIdx.x);
+    sh_tile[0] = locate_full<T>(bt, blockIdx.x);
     if (bt.d[sh_tile[0].di].vec) issue_tile<T>(bt.d[sh_tile[0].di], sh_tile[0], stages[0], &bars[0]);
   }
   __syncthreads();
@@ -213,14 +256,13 @@ __global__ void __launch_bounds__(kBwdThreads, 3) bwd_kernel(const __grid_consta
     // ended the previous iteration).
     const uint32_t next_id = tile_id + gridDim.x;
     if (tid == 0 && next_id < total) {
-      const TileRef nxt = locate(bt, next_id);
+      const TileRef nxt = locate_full<T>(bt, next_id);
       sh_tile[(it + 1) & 1] = nxt;
       if (bt.d[nxt.di].vec) issue_tile<T>(bt.d[nxt.di], nxt, stages[sidx ^ 1], &bars[sidx ^ 1]);
     }
 
-    uint64_t w0, w1;
-    window<T>(d, cur, w0, w1);
-    const int off = (int)((cur.A * sizeof(T) - w0) / sizeof(T));  // tile start in stage
+    const uint64_t w0 = cur.w0, w1 = cur.w1;
+    const int off = cur.off;  // tile start in stage
     if (d.vec) {
       mbar_wait(&bars[sidx], (phase_bits >> sidx) & 1u);
       phase_bits ^= 1u << sidx;
@@ -246,17 +288,16 @@ __global__ void __launch_bounds__(kBwdThreads, 3) bwd_kernel(const __grid_consta
     // one fold if <= 8 elements), in registers, then their sum.
     int glo, glen;
     gc.get(cur.m, (int)d.g, tid, glo, glen);
-    const DivCtx dc = make_div(d.s64[cur.c]);
+    DivCtx dc;
+    dc.s = cur.s;
+    dc.y = cur.y;
+    dc.usable = cur.s >= 0x1p-900 && cur.s <= 0x1p900;
     const double q = d.q;
     const bool want_dx = d.dx != nullptr;
     T* sx = st.x + off + glo;
     const T* su = st.up + off + glo;
-    const int h = glen > 8 ? glen >> 1 : glen;
-    double acc_l = 0.0, acc_r = 0.0;
-    int k = 0;
-    for (; k < h; ++k) acc_l = __dadd_rn(acc_l, elem<T>(sx, su, k, dc, q, want_dx));
-    for (; k < glen; ++k) acc_r = __dadd_rn(acc_r, elem<T>(sx, su, k, dc, q, want_dx));
-    const double v = glen > 8 ? __dadd_rn(acc_l, acc_r) : acc_l;
+    const double v = want_dx ? group_sum<T, true>(sx, su, glen, dc, q)
+                             : group_sum<T, false>(sx, su, glen, dc, q);
     __syncthreads();  // stage.x now holds d_input for the whole tile
 
     // Warp-level butterfly now; the cross-warp step after the copy-out.

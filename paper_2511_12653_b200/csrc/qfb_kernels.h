@@ -141,6 +141,7 @@ struct BwdDesc {
   double q;
   uint32_t vec;  // x/up/dx 16-byte aligned: TMA bulk staging
   uint32_t pad;
+  uint64_t total_bytes;  // outer * chans * inner * sizeof(T)
 };
 
 struct BwdBatch {
