@@ -616,7 +616,7 @@ def _device_view(ptr: int, nbytes: int, device):
     import torch
 
     class _View:
-        __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, True),
+        __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
                                     "version": 2}
     return torch.as_tensor(_View(), device=device)
 

@@ -83,6 +83,8 @@ struct qfb_ctx {
   std::vector<cudaEvent_t> ev;
   std::vector<DevBuf> pass_bufs;
   DevBuf pass_params;
+  void* pinned = nullptr;  // pinned staging for params and scale gradients
+  size_t pinned_bytes = 0;
 };
 
 namespace {
@@ -409,6 +411,7 @@ qfb_status qfb_ctx_destroy(qfb_ctx* ctx) {
   for (auto& b : ctx->pass_bufs)
     if (b.p) cudaFree(b.p);
   if (ctx->pass_params.p) cudaFree(ctx->pass_params.p);
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
   for (auto e : ctx->ev) cudaEventDestroy(e);
   if (ctx->s_in) cudaStreamDestroy(ctx->s_in);
   if (ctx->s_out) cudaStreamDestroy(ctx->s_out);
@@ -873,11 +876,23 @@ qfb_status qfb_quant_pass_host(qfb_ctx* ctx, qfb_precision prec, const qfb_host_
   if (qfb_status st = grow(ctx, ctx->pass_params, pbytes, false)) return st;
   float* dF = static_cast<float*>(ctx->pass_params.p);
   double* dD = reinterpret_cast<double*>(static_cast<char*>(ctx->pass_params.p) + fcount * sizeof(float));
+  // Pinned staging: a copy from/to pageable memory is synchronous for the
+  // issuing thread and would serialize the pipeline.
+  if (ctx->pinned_bytes < pbytes) {
+    if (ctx->pinned) QFB_CUDA(cudaFreeHost(ctx->pinned));
+    ctx->pinned = nullptr;
+    ctx->pinned_bytes = 0;
+    QFB_CUDA(cudaMallocHost(&ctx->pinned, pbytes));
+    ctx->pinned_bytes = pbytes;
+  }
+  float* hF = static_cast<float*>(ctx->pinned);
+  double* hD = reinterpret_cast<double*>(static_cast<char*>(ctx->pinned) + fcount * sizeof(float));
+  std::memcpy(hF, fblk.data(), fcount * sizeof(float));
+  std::memcpy(hD, dblk.data(), dcount * sizeof(double));
   // all streams start after prior work on the context stream
   QFB_CUDA(cudaEventRecord(ctx->ev[2 * n], ctx->stream));
   QFB_CUDA(cudaStreamWaitEvent(ctx->s_in, ctx->ev[2 * n], 0));
-  QFB_CUDA(cudaMemcpyAsync(dF, fblk.data(), fcount * sizeof(float), cudaMemcpyHostToDevice, ctx->s_in));
-  QFB_CUDA(cudaMemcpyAsync(dD, dblk.data(), dcount * sizeof(double), cudaMemcpyHostToDevice, ctx->s_in));
+  QFB_CUDA(cudaMemcpyAsync(dF, hF, pbytes, cudaMemcpyHostToDevice, ctx->s_in));
   // per point: buffers x, up[2], y[2], dx[2]
   if (ctx->pass_bufs.size() < (size_t)n * 7) ctx->pass_bufs.resize((size_t)n * 7);
   for (int32_t i = 0; i < n; ++i) {
@@ -944,13 +959,22 @@ qfb_status qfb_quant_pass_host(qfb_ctx* ctx, qfb_precision prec, const qfb_host_
       if (p.y[k]) QFB_CUDA(cudaMemcpyAsync(p.y[k], B[3 + k].p, bytes, cudaMemcpyDeviceToHost, ctx->s_out));
       if (p.log_s[k]) {
         if (p.dx[k]) QFB_CUDA(cudaMemcpyAsync(p.dx[k], B[5 + k].p, bytes, cudaMemcpyDeviceToHost, ctx->s_out));
-        QFB_CUDA(cudaMemcpyAsync(p.d_log_s[k], dD + doff[i] + (size_t)k * 3 * p.channels + 2 * p.channels,
-                                 (size_t)p.channels * sizeof(double), cudaMemcpyDeviceToHost, ctx->s_out));
+        const size_t o = doff[i] + (size_t)k * 3 * p.channels + 2 * p.channels;
+        QFB_CUDA(cudaMemcpyAsync(hD + o, dD + o, (size_t)p.channels * sizeof(double),
+                                 cudaMemcpyDeviceToHost, ctx->s_out));
       }
     }
   }
   QFB_CUDA(cudaStreamSynchronize(ctx->s_out));
-  return qfb_ctx_sync(ctx);
+  if (qfb_status st = qfb_ctx_sync(ctx)) return st;
+  for (int32_t i = 0; i < n; ++i) {
+    const qfb_host_point& p = pts[i];
+    for (int k = 0; k < p.n_out; ++k)
+      if (p.log_s[k])
+        std::memcpy(p.d_log_s[k], hD + doff[i] + (size_t)k * 3 * p.channels + 2 * p.channels,
+                    (size_t)p.channels * sizeof(double));
+  }
+  return QFB_OK;
 }
 
 }  // extern "C"

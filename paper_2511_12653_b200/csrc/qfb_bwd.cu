@@ -188,13 +188,37 @@ struct GroupCache {
 };
 
 // Terms of one element: d_ds * up (double) and d_input (x86 NaN rules).
+// Exact reference semantics for the rare elements the fast path cannot
+// certify (zeros, inf/NaN, ties, binade edges): IEEE division, quant.hpp
+// :217-228 verbatim. Out of line so it never bloats the hot loop.
+static __device__ __noinline__ void slow_elem(float xv, float uv, double s, double q, double* term,
+                                              float* dx) {
+  const GradTerm gt = grad_term(xv, s, q);
+  *dx = masked_upstream(gt.mask, uv);
+  *term = __dmul_rn(gt.d_ds, (double)uv);
+}
+
+// One element: term = d_ds * up (double) and d_input, with z = RN(x/s)
+// from certified_quotient (qfb_device.cuh); uncertified elements take the
+// exact IEEE path in slow_elem.
 template <typename T, bool kDx>
 __device__ __forceinline__ double elem(T* sx, const T* su, int k, const DivCtx& dc, double q) {
   const float xv = to_f<T>(sx[k]);
   const float uv = to_f<T>(su[k]);
-  const GradTerm gt = grad_term_fast(xv, dc, q);
-  if (kDx) sx[k] = from_f<T>(masked_upstream(gt.mask, uv));
-  return __dmul_rn(gt.d_ds, (double)uv);
+  double z;
+  const bool ok = certified_quotient((double)xv, dc, z);
+  double term;
+  float dx;
+  if (__builtin_expect(ok, 1)) {
+    const bool mask = fabs(z) <= q;
+    const double d_ds = mask ? __dadd_rn(rint(z), -z) : copysign(q, z);  // z finite, nonzero
+    term = __dmul_rn(d_ds, (double)uv);
+    dx = masked_upstream(mask, uv);
+  } else {
+    slow_elem(xv, uv, dc.s, q, &term, &dx);
+  }
+  if (kDx) sx[k] = from_f<T>(dx);
+  return term;
 }
 
 // A leaf group's sum in the reference order: fold(left half) + fold(right
@@ -291,7 +315,7 @@ __global__ void __launch_bounds__(kBwdThreads, 3) bwd_kernel(const __grid_consta
     DivCtx dc;
     dc.s = cur.s;
     dc.y = cur.y;
-    dc.usable = cur.s >= 0x1p-900 && cur.s <= 0x1p900;
+    dc.usable = cur.s >= 0x1p-100 && cur.s <= 0x1p100;
     const double q = d.q;
     const bool want_dx = d.dx != nullptr;
     T* sx = st.x + off + glo;

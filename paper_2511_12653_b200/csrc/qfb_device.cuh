@@ -142,24 +142,37 @@ __device__ __forceinline__ GradTerm grad_term(float x, double s, double q) {
 }
 
 // Certified fast double division for the backward: z = RN(x / s) with a
-// hoisted y = RN(1/s). Markstein's correction gives a candidate q1; it is
-// ACCEPTED only if the exact-or-larger residual proves it is the unique
-// nearest double: |x - s*q1| < s*ulp(q1)/2 (threshold exactly representable,
-// so rounding of the residual can never sneak under it) and q1 is not a
-// power of two (where the ulp below is smaller). Anything else — ties,
-// binade edges, inf/NaN/zero x — takes __ddiv_rn. Correct by construction.
+// hoisted y = RN(1/s). Markstein's correction gives a candidate z; it is
+// ACCEPTED only if its exact-or-larger residual proves it is the unique
+// nearest double: |x - s*z| < s*ulp(z)/2, with the threshold a power of
+// two times s (exactly representable, so a rounded residual can never pass
+// wrongly), and z not a power of two (where the ulp below is smaller).
+// With s in [2^-100, 2^100] (DivCtx::usable) every nonzero finite float x
+// gives normal z and threshold; zeros, inf/NaN, ties and binade edges fail
+// and the caller takes the IEEE path. Correct by construction; exercised
+// over all 2^32 x by tools/verify_div.cu.
 struct DivCtx {
   double s;
-  double y;     // __drcp_rn(s)
-  bool usable;  // s normal and far from over/underflow
+  double y;     // RN(1/s)
+  bool usable;  // s in [2^-100, 2^100]
 };
 
 __device__ __forceinline__ DivCtx make_div(double s) {
   DivCtx c;
   c.s = s;
   c.y = __drcp_rn(s);
-  c.usable = s >= 0x1p-900 && s <= 0x1p900;
+  c.usable = s >= 0x1p-100 && s <= 0x1p100;
   return c;
+}
+
+__device__ __forceinline__ bool certified_quotient(double x, const DivCtx& c, double& z) {
+  const double q0 = __dmul_rn(x, c.y);
+  z = __fma_rn(__fma_rn(-c.s, q0, x), c.y, q0);
+  const double r1 = __fma_rn(-c.s, z, x);
+  const int hi = __double2hiint(z);
+  const int lo = __double2loint(z);
+  const double thr = __dmul_rn(c.s, __hiloint2double((hi & 0x7ff00000) - (53 << 20), 0));
+  return c.usable && ((hi & 0x000fffff) | lo) != 0 && fabs(r1) < thr;
 }
 
 // Out of line so the compiler cannot if-convert (speculate) the full IEEE
@@ -168,26 +181,9 @@ static __device__ __noinline__ double slow_ddiv(double x, double s) { return __d
 
 __device__ __forceinline__ double certified_div(float xf, const DivCtx& c) {
   const double x = (double)xf;
-  const double q0 = __dmul_rn(x, c.y);
-  const double q1 = __fma_rn(__fma_rn(-c.s, q0, x), c.y, q0);
-  const double r1 = __fma_rn(-c.s, q1, x);
-  const unsigned long long qb = (unsigned long long)__double_as_longlong(q1);
-  const unsigned long long e = (qb >> 52) & 0x7ffull;
-  // s * ulp(q1) / 2 = s * 2^(e - 1023 - 53): exact power-of-two scaling
-  const double half_ulp_s = __dmul_rn(c.s, __longlong_as_double((long long)((e - 53ull) << 52)));
-  const bool ok = c.usable && (qb & 0x000fffffffffffffull) != 0ull && e > 160ull && e < 1900ull &&
-                  fabs(r1) < half_ulp_s;
-  if (__builtin_expect(ok, 1)) return q1;
+  double z;
+  if (__builtin_expect(certified_quotient(x, c, z), 1)) return z;
   return slow_ddiv(x, c.s);
-}
-
-// grad_term with the certified division.
-__device__ __forceinline__ GradTerm grad_term_fast(float x, const DivCtx& c, double q) {
-  const double z = certified_div(x, c);
-  GradTerm t;
-  t.mask = fabs(z) <= q;
-  t.d_ds = t.mask ? __dadd_rn(rint(z), -z) : (z > 0.0 ? q : -q);
-  return t;
 }
 
 // ------------------------------------------------------ fast divide ---
@@ -275,6 +271,14 @@ struct Elem;
 template <>
 struct Elem<float> {
   static constexpr int kPerVec = 4;
+  __device__ __forceinline__ static bool unpack_flag(const uint4& r, float* v) {
+    unpack(r, v);
+    return true;  // not tracked for f32: callers take the general pack
+  }
+  __device__ __forceinline__ static uint4 pack_in_range(const float* v) {
+    return make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]),
+                      __float_as_uint(v[3]));
+  }
   __device__ __forceinline__ static void unpack(const uint4& r, float* v) {
     v[0] = __uint_as_float(r.x);
     v[1] = __uint_as_float(r.y);
@@ -311,7 +315,8 @@ __device__ __forceinline__ float half_bits_to_float_exact(uint32_t h) {
 template <>
 struct Elem<__half> {
   static constexpr int kPerVec = 8;
-  __device__ __forceinline__ static void unpack(const uint4& r, float* v) {
+  // Returns true when the unit holds an inf/NaN (all-ones exponent).
+  __device__ __forceinline__ static bool unpack_flag(const uint4& r, float* v) {
     const uint32_t w[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -329,6 +334,18 @@ struct Elem<__half> {
         v[2 * i + 1] = half_bits_to_float_exact(w[i] >> 16);
       }
     }
+    return e != 0;
+  }
+  __device__ __forceinline__ static void unpack(const uint4& r, float* v) { (void)unpack_flag(r, v); }
+  // Finite values known to lie within +-65504: plain packed RNE conversion.
+  __device__ __forceinline__ static uint4 pack_in_range(const float* v) {
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const __half2 h = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
+      w[i] = *reinterpret_cast<const uint32_t*>(&h);
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
   }
   // f16 storage always rounds through half_store (RNE + saturation).
   __device__ __forceinline__ static uint4 pack(const float* v, const float* sign_src,

@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(kEwThreads, kChain ? 3 : 4) ew_kernel(const __
 // chunks ahead, so the bytes in flight no longer depend on registers or
 // occupancy; threads read conflict-free 16-byte vectors from smem and write
 // outputs with 16-byte stores.
-constexpr int kFwdStages = 3;
+constexpr int kFwdStages = 2;
 constexpr int kFwdChunkBytes = kEwChunk * 16;  // 16 KB
 
 struct ChunkRef {
@@ -186,7 +186,7 @@ __device__ __forceinline__ ChunkRef locate_chunk(const EwBatch& bt, uint32_t chu
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kEwThreads, 4)
+__global__ void __launch_bounds__(kEwThreads, 5)
     ew_tma_kernel(const __grid_constant__ EwBatch bt, uint32_t* __restrict__ status) {
   constexpr int V = Elem<T>::kPerVec;
   extern __shared__ __align__(128) unsigned char fsmem[];
@@ -233,15 +233,45 @@ __global__ void __launch_bounds__(kEwThreads, 4)
     const bool streaming = (d.flags & kEwStreaming) != 0;
     const bool half_out = (d.flags & kEwHalfGrid) != 0;
     const uint4* src = ring + s * kEwChunk;
+    // Per-thread scale cache: units of a chunk mostly share a channel, so
+    // the channel, its scales and reciprocals are recomputed only when the
+    // row changes.
+    uint32_t last_row = 0xffffffffu;
+    float sc[2] = {1.0f, 1.0f}, rc[2] = {1.0f, 1.0f};
+    bool fast[2] = {true, true};
     for (uint32_t k = tid; k < r.units; k += kEwThreads) {
       const uint32_t u = r.u0 + k;
-      const uint32_t ch = channel_of(u, d.inner_u, d.chans);
+      const uint32_t row = d.chans.d == 1 ? 0u : fdiv(u, d.inner_u);
+      if (row != last_row) {
+        last_row = row;
+        const uint32_t ch = d.chans.d == 1 ? 0u : row - fdiv(row, d.chans) * d.chans.d;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          if (j < d.n_out) {
+            sc[j] = __ldg(d.s[j] + ch);
+            fast[j] = fast_div_ok(sc[j]);
+            rc[j] = fast[j] ? __frcp_rn(sc[j]) : 1.0f;
+          }
+        }
+      }
       float v[V];
-      Elem<T>::unpack(src[k], v);
-      for (int j = 0; j < d.n_out; ++j) {
+      const bool special = Elem<T>::unpack_flag(src[k], v);
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        if (j >= d.n_out) break;
         float o[V];
-        fq_unit<V>(v, __ldg(d.s[j] + ch), d.q, o);
-        st_v4(static_cast<uint4*>(d.y[j]) + u, Elem<T>::pack(o, v, half_out, nf), streaming);
+        if (fast[j]) {
+#pragma unroll
+          for (int i = 0; i < V; ++i) o[i] = fq_value_fast(v[i], sc[j], rc[j], d.q);
+        } else {
+#pragma unroll
+          for (int i = 0; i < V; ++i) o[i] = fq_value(v[i], sc[j], d.q);
+        }
+        // f16 store: FQ outputs of finite inputs are bounded by q*s; when
+        // that is within the half range a plain packed conversion is exact
+        const bool plain = sizeof(T) == 2 ? (!special && sc[j] * d.q <= 65504.0f) : !half_out;
+        const uint4 packed = plain ? Elem<T>::pack_in_range(o) : Elem<T>::pack(o, v, half_out, nf);
+        st_v4(static_cast<uint4*>(d.y[j]) + u, packed, streaming);
       }
     }
     __syncthreads();  // stage s free for the producer

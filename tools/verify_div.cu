@@ -100,6 +100,8 @@ __global__ void certified_kernel(const double* scales, int ns, uint64_t base) {
   for (int i = 0; i < ns; ++i) {
     const DivCtx c = make_div(scales[i]);
     const double a = __ddiv_rn((double)x, c.s);
+    double z;
+    if (certified_quotient((double)x, c, z) && __double_as_longlong(a) != __double_as_longlong(z)) ++bad;
     const double b = certified_div(x, c);
     if (__double_as_longlong(a) != __double_as_longlong(b) && !(isnan(a) && isnan(b))) ++bad;
   }
