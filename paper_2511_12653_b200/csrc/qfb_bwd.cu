@@ -207,16 +207,13 @@ __device__ __forceinline__ double elem(T* sx, const T* su, int k, const DivCtx& 
   const float uv = to_f<T>(su[k]);
   double z;
   const bool ok = certified_quotient((double)xv, dc, z);
-  double term;
-  float dx;
-  if (__builtin_expect(ok, 1)) {
-    const bool mask = fabs(z) <= q;
-    const double d_ds = mask ? __dadd_rn(rint(z), -z) : copysign(q, z);  // z finite, nonzero
-    term = __dmul_rn(d_ds, (double)uv);
-    dx = masked_upstream(mask, uv);
-  } else {
-    slow_elem(xv, uv, dc.s, q, &term, &dx);
-  }
+  // Branch-free fast path computed speculatively (shorter dependency chain);
+  // an uncertified element is recomputed exactly and overrides it.
+  const bool mask = fabs(z) <= q;
+  const double d_ds = mask ? __dadd_rn(rint(z), -z) : copysign(q, z);
+  double term = __dmul_rn(d_ds, (double)uv);
+  float dx = masked_upstream(mask, uv);
+  if (__builtin_expect(!ok, 0)) slow_elem(xv, uv, dc.s, q, &term, &dx);
   if (kDx) sx[k] = from_f<T>(dx);
   return term;
 }
@@ -280,6 +277,7 @@ __global__ void __launch_bounds__(kBwdThreads, 3) bwd_kernel(const __grid_consta
     // ended the previous iteration).
     const uint32_t next_id = tile_id + gridDim.x;
     if (tid == 0 && next_id < total) {
+      bulk_wait_read_all();  // the stage's last bulk store has read it
       const TileRef nxt = locate_full<T>(bt, next_id);
       sh_tile[(it + 1) & 1] = nxt;
       if (bt.d[nxt.di].vec) issue_tile<T>(bt.d[nxt.di], nxt, stages[sidx ^ 1], &bars[sidx ^ 1]);
@@ -331,27 +329,26 @@ __global__ void __launch_bounds__(kBwdThreads, 3) bwd_kernel(const __grid_consta
     for (int o = 1; o < wl; o <<= 1) wv = __dadd_rn(wv, __shfl_xor_sync(0xffffffffu, wv, o));
     if ((tid & 31) == 0) red[tid >> 5] = wv;
 
-    // d_input -> HBM: 16-byte copies for units fully inside the tile,
-    // element copies at the two ragged ends.
+    // d_input -> HBM. The 16-byte-aligned interior of the tile goes out as
+    // ONE bulk store (TMA) issued by thread 0 after the barrier below; the
+    // ragged head/tail elements are stored by threads.
+    const uint64_t b0 = cur.A * sizeof(T), b1 = (cur.A + (uint64_t)cur.m) * sizeof(T);
+    const uint64_t i0 = (b0 + 15) & ~uint64_t(15), i1 = b1 & ~uint64_t(15);
     if (want_dx) {
-      const uint64_t b0 = cur.A * sizeof(T), b1 = (cur.A + (uint64_t)cur.m) * sizeof(T);
-      const int nunits = (int)((b1 - w0 + 15) / 16);
-      for (int u = tid; u < nunits; u += kBwdThreads) {
-        const uint64_t ub = w0 + 16ull * (uint64_t)u;
-        if (ub >= b0 && ub + 16 <= b1) {
-          const uint4 val = *reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(st.x) + 16 * u);
-          st_v4(static_cast<char*>(d.dx) + ub, val, false);
-        } else {
-          constexpr int kPer = 16 / (int)sizeof(T);
-#pragma unroll
-          for (int j = 0; j < kPer; ++j) {
-            const uint64_t eb = ub + (uint64_t)j * sizeof(T);
-            if (eb >= b0 && eb < b1) static_cast<T*>(d.dx)[eb / sizeof(T)] = st.x[u * kPer + j];
-          }
-        }
-      }
+      const int head = (int)((i0 > b1 ? b1 : i0) - b0) / (int)sizeof(T);
+      const int tail0 = i1 > i0 ? (int)((i1 - b0) / sizeof(T)) : head;
+      for (int e = tid; e < head; e += kBwdThreads)
+        static_cast<T*>(d.dx)[cur.A + e] = st.x[off + e];
+      for (int e = tail0 + tid; e < cur.m; e += kBwdThreads)
+        static_cast<T*>(d.dx)[cur.A + e] = st.x[off + e];
     }
-    __syncthreads();  // stage reads done (producer may refill it); red complete
+    __syncthreads();  // d_input complete in the stage; red complete
+    if (tid == 0 && want_dx && i1 > i0) {
+      fence_proxy_async_smem();  // generic-proxy smem writes -> async proxy
+      bulk_s2g(static_cast<char*>(d.dx) + i0, reinterpret_cast<const char*>(st.x) + (i0 - w0),
+               (uint32_t)(i1 - i0));
+      bulk_commit();
+    }
 
     // Perfect-tree combine of the warp sums (groups > 32) -> tile partial.
     if (tid < 32) {
@@ -361,6 +358,7 @@ __global__ void __launch_bounds__(kBwdThreads, 3) bwd_kernel(const __grid_consta
       if (tid == 0) d.partials[((uint64_t)cur.seg << d.tps_log) + cur.t] = r;
     }
   }
+  if (tid == 0) bulk_wait_all();  // d_input bulk stores complete before exit
 }
 
 // Finisher: one warp per (descriptor, channel). Each row's 2^tps_log tile
