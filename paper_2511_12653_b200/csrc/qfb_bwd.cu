@@ -14,22 +14,22 @@
 // boundaries follow the recursive floor split, located per group by
 // descending the bits of its index. A perfect tree is exactly what an xor
 // butterfly computes (IEEE addition is commutative), so:
-//   warp tile = 2^g consecutive leaf groups (g = min(D, 5), <= 512
-//             elements), owned by ONE warp with its own TMA ring: lane 0
-//             issues cp.async.bulk copies of the next tile's x/up windows
-//             (mbarrier completion) while the warp computes the current one;
-//             each lane owns one leaf group, computes its terms in registers
-//             and folds them in reference order (the two half-folds
-//             interleaved), writes d_input back into the stage; a shuffle
-//             butterfly gives the subtree sum; d_input leaves as one bulk
-//             store (aligned interior) + lane stores (ragged ends). Warps
-//             never wait on each other: no CTA barrier on the hot path.
-//   row     = its 2^(D-g) warp-tile partials are reduced in tree order by a
-//             stream-ordered finisher kernel (one warp per channel), which
-//             also applies the chain factor and folds the rows of a channel
-//             over `outer` in row order (the trainer's `g += ...`).
+//   tile    = 2^g consecutive leaf groups (g = min(D, 8)), <= 4096 elements,
+//             staged into shared memory by the TMA engine (cp.async.bulk +
+//             mbarrier, double-buffered: tile i+1 lands while tile i
+//             computes); each thread owns one leaf group, computes its
+//             elements' terms in registers and folds them in reference order,
+//             writing d_input back into the stage; a coalesced 16-byte copy
+//             moves d_input to HBM; warp/CTA butterfly = the subtree's sum;
+//   segment = one row: its 2^(D-g) tile partials are reduced in tree order
+//             by a small stream-ordered finisher kernel (one warp per
+//             channel: per-lane perfect subtrees + xor butterfly), which also
+//             applies the chain factor and folds the rows of a channel over
+//             `outer` in row order (the trainer's `g += ...`). No fences,
+//             atomics or tickets on the hot path.
+// CTAs are persistent (grid = SMs x resident CTAs) and stride over tiles.
 // The result is bit-identical to the reference for any grid size.
-// tests/test_tree_model.py executes this schedule on the CPU.
+// tests/test_tree_model.py executes this exact schedule on the CPU.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -191,29 +191,39 @@ struct GroupCache {
 // Exact reference semantics for the rare elements the fast path cannot
 // certify (zeros, inf/NaN, ties, binade edges): IEEE division, quant.hpp
 // :217-228 verbatim. Out of line so it never bloats the hot loop.
-static __device__ __noinline__ void slow_elem(float xv, float uv, double s, double q, double* term,
-                                              float* dx) {
+static __device__ __noinline__ double2 slow_elem(float xv, float uv, double s, double q) {
   const GradTerm gt = grad_term(xv, s, q);
-  *dx = masked_upstream(gt.mask, uv);
-  *term = __dmul_rn(gt.d_ds, (double)uv);
+  return make_double2(__dmul_rn(gt.d_ds, (double)uv), (double)masked_upstream(gt.mask, uv));
+}
+
+// Pin a uniform double in a register (stops the compiler from
+// rematerializing it from the dynamically indexed parameter bank per use).
+__device__ __forceinline__ double pin(double v) {
+  double r;
+  asm volatile("mov.b64 %0, %1;" : "=d"(r) : "d"(v));
+  return r;
 }
 
 // One element: term = d_ds * up (double) and d_input, with z = RN(x/s)
 // from certified_quotient (qfb_device.cuh); uncertified elements take the
-// exact IEEE path in slow_elem.
+// exact IEEE path in slow_elem (returned in registers, never via memory).
 template <typename T, bool kDx>
 __device__ __forceinline__ double elem(T* sx, const T* su, int k, const DivCtx& dc, double q) {
   const float xv = to_f<T>(sx[k]);
   const float uv = to_f<T>(su[k]);
   double z;
-  const bool ok = certified_quotient((double)xv, dc, z);
-  // Branch-free fast path computed speculatively (shorter dependency chain);
-  // an uncertified element is recomputed exactly and overrides it.
+  // one rare-path test: uncertified quotient or a non-finite upstream
+  const bool up_finite = (__float_as_uint(uv) & 0x7f800000u) != 0x7f800000u;
+  const bool ok = certified_quotient((double)xv, dc, z) && up_finite;
   const bool mask = fabs(z) <= q;
   const double d_ds = mask ? __dadd_rn(rint(z), -z) : copysign(q, z);
   double term = __dmul_rn(d_ds, (double)uv);
-  float dx = masked_upstream(mask, uv);
-  if (__builtin_expect(!ok, 0)) slow_elem(xv, uv, dc.s, q, &term, &dx);
+  float dx = mask ? uv : __uint_as_float(__float_as_uint(uv) & 0x80000000u);  // finite up
+  if (__builtin_expect(!ok, 0)) {
+    const double2 r = slow_elem(xv, uv, dc.s, q);
+    term = r.x;
+    dx = (float)r.y;  // exact: r.y is a float widened
+  }
   if (kDx) sx[k] = from_f<T>(dx);
   return term;
 }
@@ -243,108 +253,122 @@ __device__ __forceinline__ double group_sum(T* sx, const T* su, int glen, const 
   return __dadd_rn(acc_l, acc_r);
 }
 
-constexpr int kWarpsPerCta = kBwdThreads / 32;
-
 template <typename T>
 __global__ void __launch_bounds__(kBwdThreads, 3) bwd_kernel(const __grid_constant__ BwdBatch bt) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ __align__(8) uint64_t bars[kWarpsPerCta][kStages];
-  __shared__ TileRef refs[kWarpsPerCta][2];
-  const int lane = threadIdx.x & 31;
-  const int wid = threadIdx.x >> 5;
-  Stage<T>* stages = reinterpret_cast<Stage<T>*>(smem_raw) + wid * kStages;
-  uint64_t* wb = bars[wid];
-  TileRef* wr = refs[wid];
+  Stage<T>* stages = reinterpret_cast<Stage<T>*>(smem_raw);
+  __shared__ __align__(8) uint64_t bars[kStages];
+  __shared__ TileRef sh_tile[2];
+  __shared__ double red[kBwdThreads / 32];
+  const int tid = threadIdx.x;
   const uint32_t total = bt.tile_begin[bt.n];
-  const uint32_t nwarps = gridDim.x * kWarpsPerCta;
-  const uint32_t first = blockIdx.x * kWarpsPerCta + wid;
-  if (first >= total) return;
+  if (blockIdx.x >= total) return;
 
-  // Lane 0 is this warp's producer.
-  if (lane == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&wb[s], 1);
+  // Thread 0 is the producer: it locates tiles and issues their bulk copies
+  // one tile ahead; everyone reads the tile descriptors from smem.
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
-    wr[0] = locate_full<T>(bt, first);
-    if (bt.d[wr[0].di].vec) issue_tile<T>(bt.d[wr[0].di], wr[0], stages[0], &wb[0]);
+    sh_tile[0] = locate_full<T>(bt, blockIdx.x);
+    if (bt.d[sh_tile[0].di].vec) issue_tile<T>(bt.d[sh_tile[0].di], sh_tile[0], stages[0], &bars[0]);
   }
-  __syncwarp();
+  __syncthreads();
 
-  uint32_t phase_bits = 0;
+  uint32_t phase_bits = 0;  // per-stage mbarrier parity
   GroupCache gc;
   int it = 0;
-  for (uint32_t tile_id = first; tile_id < total; tile_id += nwarps, ++it) {
+  for (uint32_t tile_id = blockIdx.x; tile_id < total; tile_id += gridDim.x, ++it) {
     const int sidx = it & (kStages - 1);
     Stage<T>& st = stages[sidx];
-    const TileRef cur = wr[it & 1];
+    const TileRef cur = sh_tile[it & 1];
     const BwdDesc& d = bt.d[cur.di];
 
-    const uint32_t next_id = tile_id + nwarps;
-    if (lane == 0 && next_id < total) {
-      bulk_wait_read_all();  // the other stage's last bulk store has read it
+    // Producer: next tile into the other stage (freed by the barrier that
+    // ended the previous iteration).
+    const uint32_t next_id = tile_id + gridDim.x;
+    if (tid == 0 && next_id < total) {
+      bulk_wait_read_all();  // the stage's last bulk store has read it
       const TileRef nxt = locate_full<T>(bt, next_id);
-      wr[(it + 1) & 1] = nxt;
-      if (bt.d[nxt.di].vec) issue_tile<T>(bt.d[nxt.di], nxt, stages[sidx ^ 1], &wb[sidx ^ 1]);
+      sh_tile[(it + 1) & 1] = nxt;
+      if (bt.d[nxt.di].vec) issue_tile<T>(bt.d[nxt.di], nxt, stages[sidx ^ 1], &bars[sidx ^ 1]);
     }
 
     const uint64_t w0 = cur.w0, w1 = cur.w1;
-    const int off = cur.off;
+    const int off = cur.off;  // tile start in stage
     if (d.vec) {
-      mbar_wait(&wb[sidx], (phase_bits >> sidx) & 1u);
+      mbar_wait(&bars[sidx], (phase_bits >> sidx) & 1u);
       phase_bits ^= 1u << sidx;
+      // elements past the bulk window (only at the very end of a tensor)
       const uint64_t e_end = cur.A + (uint64_t)cur.m;
       const uint64_t e_w1 = w1 / sizeof(T);
-      if (e_w1 < e_end) {  // elements past the bulk window (tensor end)
-        for (uint64_t e = e_w1 + lane; e < e_end; e += 32) {
+      if (e_w1 < e_end) {
+        for (uint64_t e = e_w1 + tid; e < e_end; e += kBwdThreads) {
           st.x[e - w0 / sizeof(T)] = static_cast<const T*>(d.x)[e];
           st.up[e - w0 / sizeof(T)] = static_cast<const T*>(d.up)[e];
         }
-        __syncwarp();
+        __syncthreads();
       }
     } else {
-      for (int e = lane; e < cur.m; e += 32) {
+      for (int e = tid; e < cur.m; e += kBwdThreads) {
         st.x[off + e] = static_cast<const T*>(d.x)[cur.A + e];
         st.up[off + e] = static_cast<const T*>(d.up)[cur.A + e];
       }
-      __syncwarp();
+      __syncthreads();
     }
 
+    // This thread's leaf group: two left folds from 0.0 over its halves (or
+    // one fold if <= 8 elements), in registers, then their sum.
     int glo, glen;
-    gc.get(cur.m, (int)d.g, lane, glo, glen);
+    gc.get(cur.m, (int)d.g, tid, glo, glen);
     DivCtx dc;
-    dc.s = cur.s;
-    dc.y = cur.y;
+    dc.s = pin(cur.s);
+    dc.y = pin(cur.y);
     dc.usable = cur.s >= 0x1p-100 && cur.s <= 0x1p100;
-    const double q = d.q;
+    const double q = pin(d.q);
     const bool want_dx = d.dx != nullptr;
     T* sx = st.x + off + glo;
     const T* su = st.up + off + glo;
-    double v = want_dx ? group_sum<T, true>(sx, su, glen, dc, q)
-                       : group_sum<T, false>(sx, su, glen, dc, q);
-    __syncwarp();  // the warp tile's d_input is complete in the stage
+    const double v = want_dx ? group_sum<T, true>(sx, su, glen, dc, q)
+                             : group_sum<T, false>(sx, su, glen, dc, q);
+    __syncthreads();  // stage.x now holds d_input for the whole tile
 
-    // perfect-tree butterfly over the warp's 2^g groups -> tile partial
+    // Warp-level butterfly now; the cross-warp step after the copy-out.
     const int groups = 1 << d.g;
-    for (int o = 1; o < groups; o <<= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
-    if (lane == 0) d.partials[((uint64_t)cur.seg << d.tps_log) + cur.t] = v;
+    const int wl = groups < 32 ? groups : 32;
+    double wv = v;
+    for (int o = 1; o < wl; o <<= 1) wv = __dadd_rn(wv, __shfl_xor_sync(0xffffffffu, wv, o));
+    if ((tid & 31) == 0) red[tid >> 5] = wv;
 
-    // d_input -> HBM: aligned interior as one bulk store, ragged ends by lanes
+    // d_input -> HBM. The 16-byte-aligned interior of the tile goes out as
+    // ONE bulk store (TMA) issued by thread 0 after the barrier below; the
+    // ragged head/tail elements are stored by threads.
+    const uint64_t b0 = cur.A * sizeof(T), b1 = (cur.A + (uint64_t)cur.m) * sizeof(T);
+    const uint64_t i0 = (b0 + 15) & ~uint64_t(15), i1 = b1 & ~uint64_t(15);
     if (want_dx) {
-      const uint64_t b0 = cur.A * sizeof(T), b1 = (cur.A + (uint64_t)cur.m) * sizeof(T);
-      const uint64_t i0 = (b0 + 15) & ~uint64_t(15), i1 = b1 & ~uint64_t(15);
-      const int head = (int)(((i0 > b1 ? b1 : i0) - b0) / sizeof(T));
+      const int head = (int)((i0 > b1 ? b1 : i0) - b0) / (int)sizeof(T);
       const int tail0 = i1 > i0 ? (int)((i1 - b0) / sizeof(T)) : head;
-      for (int e = lane; e < head; e += 32) static_cast<T*>(d.dx)[cur.A + e] = st.x[off + e];
-      for (int e = tail0 + lane; e < cur.m; e += 32) static_cast<T*>(d.dx)[cur.A + e] = st.x[off + e];
-      if (lane == 0 && i1 > i0) {
-        fence_proxy_async_smem();
-        bulk_s2g(static_cast<char*>(d.dx) + i0, reinterpret_cast<const char*>(st.x) + (i0 - w0),
-                 (uint32_t)(i1 - i0));
-        bulk_commit();
-      }
+      for (int e = tid; e < head; e += kBwdThreads)
+        static_cast<T*>(d.dx)[cur.A + e] = st.x[off + e];
+      for (int e = tail0 + tid; e < cur.m; e += kBwdThreads)
+        static_cast<T*>(d.dx)[cur.A + e] = st.x[off + e];
     }
-    __syncwarp();  // stage and refs reused by the producer
+    __syncthreads();  // d_input complete in the stage; red complete
+    if (tid == 0 && want_dx && i1 > i0) {
+      fence_proxy_async_smem();  // generic-proxy smem writes -> async proxy
+      bulk_s2g(static_cast<char*>(d.dx) + i0, reinterpret_cast<const char*>(st.x) + (i0 - w0),
+               (uint32_t)(i1 - i0));
+      bulk_commit();
+    }
+
+    // Perfect-tree combine of the warp sums (groups > 32) -> tile partial.
+    if (tid < 32) {
+      const int nw = groups > 32 ? groups >> 5 : 1;
+      double r = tid < nw ? red[tid] : 0.0;
+      for (int o = 1; o < nw; o <<= 1) r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, o));
+      if (tid == 0) d.partials[((uint64_t)cur.seg << d.tps_log) + cur.t] = r;
+    }
   }
-  if (lane == 0) bulk_wait_all();  // d_input bulk stores complete before exit
+  if (tid == 0) bulk_wait_all();  // d_input bulk stores complete before exit
 }
 
 // Finisher: one warp per (descriptor, channel). Each row's 2^tps_log tile
@@ -404,7 +428,7 @@ __global__ void __launch_bounds__(32) bwd_finish_kernel(const __grid_constant__ 
 
 template <typename T>
 constexpr size_t stage_bytes() {
-  return sizeof(Stage<T>) * kStages * kWarpsPerCta;
+  return sizeof(Stage<T>) * kStages;
 }
 
 }  // namespace

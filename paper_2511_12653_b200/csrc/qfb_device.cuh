@@ -76,14 +76,25 @@ __device__ __forceinline__ bool fast_div_ok(float s) {
 //  - subnormal/tiny quotients: |z| < 0.5 rounds to +-0 for both paths, and
 //    copysign restores the sign of x that FMA-based correction can lose on
 //    signed zeros. tools/verify_div.cu test 2 checks every 2^32 x.
+// Branch-free: a NaN x runs the arithmetic on garbage (the min/max clip
+// drops NaN) and the final select returns the quieted input, exactly what
+// the host's NaN propagation yields.
 __device__ __forceinline__ float fq_value_fast(float x, float s, float y, float q) {
-  if (isnan(x)) return quiet_nan(x);
   const float q0 = __fmul_rn(x, y);
   float z = __fmaf_rn(__fmaf_rn(-s, q0, x), y, q0);
   z = fabsf(q0) < 0x1p100f ? z : q0;
   z = copysignf(z, x);
-  z = fminf(fmaxf(z, -q), q);  // never NaN here: select clip == min/max
-  return __fmul_rn(s, rintf(z));
+  z = fminf(fmaxf(z, -q), q);  // == the compare-select clip for non-NaN z
+  const float r = __fmul_rn(s, rintf(z));
+  return isnan(x) ? quiet_nan(x) : r;
+}
+
+// Pin a uniform in a register (stops rematerialization from the
+// dynamically indexed parameter bank at every use).
+__device__ __forceinline__ float pin_f(float v) {
+  float r;
+  asm volatile("mov.b32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
 }
 
 // ----------------------------------------------------------- binary16 ---

@@ -232,6 +232,7 @@ __global__ void __launch_bounds__(kEwThreads, 5)
     const EwDesc& d = bt.d[r.di];
     const bool streaming = (d.flags & kEwStreaming) != 0;
     const bool half_out = (d.flags & kEwHalfGrid) != 0;
+    const float qv = pin_f(d.q);
     const uint4* src = ring + s * kEwChunk;
     // Per-thread scale cache: units of a chunk mostly share a channel, so
     // the channel, its scales and reciprocals are recomputed only when the
@@ -262,14 +263,14 @@ __global__ void __launch_bounds__(kEwThreads, 5)
         float o[V];
         if (fast[j]) {
 #pragma unroll
-          for (int i = 0; i < V; ++i) o[i] = fq_value_fast(v[i], sc[j], rc[j], d.q);
+          for (int i = 0; i < V; ++i) o[i] = fq_value_fast(v[i], sc[j], rc[j], qv);
         } else {
 #pragma unroll
-          for (int i = 0; i < V; ++i) o[i] = fq_value(v[i], sc[j], d.q);
+          for (int i = 0; i < V; ++i) o[i] = fq_value(v[i], sc[j], qv);
         }
         // f16 store: FQ outputs of finite inputs are bounded by q*s; when
         // that is within the half range a plain packed conversion is exact
-        const bool plain = sizeof(T) == 2 ? (!special && sc[j] * d.q <= 65504.0f) : !half_out;
+        const bool plain = sizeof(T) == 2 ? (!special && sc[j] * qv <= 65504.0f) : !half_out;
         const uint4 packed = plain ? Elem<T>::pack_in_range(o) : Elem<T>::pack(o, v, half_out, nf);
         st_v4(static_cast<uint4*>(d.y[j]) + u, packed, streaming);
       }

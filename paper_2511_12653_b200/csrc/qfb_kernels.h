@@ -117,10 +117,10 @@ struct ResolveDesc {
 cudaError_t launch_resolve(const ResolveDesc& d, uint32_t* status, cudaStream_t st);
 
 // --------------------------------------------------------- backward ----
-constexpr int kBwdThreads = 256;  // 8 independent warps per CTA
-constexpr int kBwdGroupsLog = 5;  // leaf groups per warp tile (= lanes)
+constexpr int kBwdThreads = 256;
+constexpr int kBwdGroupsLog = 8;  // leaf groups per full tile (= threads)
 constexpr int kLeafMax = 16;      // leaf-group size bound (two <=8 folds)
-constexpr int kBwdTileMax = kLeafMax << kBwdGroupsLog;  // 512 elements per warp tile
+constexpr int kBwdTileMax = kLeafMax << kBwdGroupsLog;  // 4096 elements
 constexpr int kMaxBwdDesc = 64;
 
 struct BwdDesc {

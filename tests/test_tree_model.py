@@ -13,7 +13,7 @@ import numpy as np
 import pytest
 
 LEAF_MAX = 16
-GROUPS_LOG = 5
+GROUPS_LOG = 8
 
 
 def leaf_depth(n):
