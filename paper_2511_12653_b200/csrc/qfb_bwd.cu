@@ -253,71 +253,141 @@ __device__ __forceinline__ double group_sum(T* sx, const T* su, int glen, const 
   return __dadd_rn(acc_l, acc_r);
 }
 
+// ---------------------------------------------------------------------
+// Warp-specialized main pass. 8 consumer warps (256 lanes = 256 leaf
+// groups of a tile) + 1 producer warp. Per stage s of the 2-deep ring:
+//   full[s]  producer -> consumers: TileRef written, x/up landed (TMA tx)
+//   done[s]  consumers -> producer: d_input written into the stage and the
+//            8 warp sums in red[s] (one arrive per consumer warp)
+// The producer finalizes tile j (cross-warp tree step -> partial, ragged
+// d_input ends, one TMA bulk store of the aligned interior), waits for the
+// store to have read the stage, then refills the stage with tile j+2.
+// Consumers never execute a CTA-wide barrier.
+// ---------------------------------------------------------------------
+constexpr int kConsumerWarps = kBwdThreads / 32;      // 8
+constexpr int kBwdCtaThreads = kBwdThreads + 32;     // + producer warp
+
 template <typename T>
-__global__ void __launch_bounds__(kBwdThreads, 3) bwd_kernel(const __grid_constant__ BwdBatch bt) {
+__device__ __forceinline__ void produce(const BwdBatch& bt, uint32_t tile_id, Stage<T>& st,
+                                        TileRef* ref, uint64_t* full, int lane) {
+  TileRef r;
+  if (lane == 0) r = locate_full<T>(bt, tile_id);
+  // broadcast the fields the lanes need for a manual fill
+  const int di = __shfl_sync(0xffffffffu, r.di, 0);
+  const BwdDesc& d = bt.d[di];
+  if (d.vec) {
+    if (lane == 0) {
+      *ref = r;
+      const uint64_t e_end = r.A + (uint64_t)r.m;
+      const uint64_t e_w1 = r.w1 / sizeof(T);
+      // elements past the bulk window (only at the very end of a tensor)
+      for (uint64_t e = e_w1; e < e_end; ++e) {
+        st.x[e - r.w0 / sizeof(T)] = static_cast<const T*>(d.x)[e];
+        st.up[e - r.w0 / sizeof(T)] = static_cast<const T*>(d.up)[e];
+      }
+      issue_tile<T>(d, r, st, full);  // arrive.expect_tx releases the stores above
+    }
+  } else {
+    // unaligned buffers: the producer warp fills the stage itself
+    const uint64_t A = __shfl_sync(0xffffffffu, r.A, 0);
+    const int m = __shfl_sync(0xffffffffu, r.m, 0);
+    const int off = __shfl_sync(0xffffffffu, r.off, 0);
+    for (int e = lane; e < m; e += 32) {
+      st.x[off + e] = static_cast<const T*>(d.x)[A + e];
+      st.up[off + e] = static_cast<const T*>(d.up)[A + e];
+    }
+    __syncwarp();
+    if (lane == 0) {
+      *ref = r;
+      mbar_arrive_expect_tx(full, 0);
+    }
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void finalize(const BwdBatch& bt, const TileRef& cur, Stage<T>& st,
+                                         const double* red, int lane) {
+  const BwdDesc& d = bt.d[cur.di];
+  // cross-warp perfect-tree step over the consumer warps' sums
+  const int groups = 1 << d.g;
+  const int nw = groups > 32 ? groups >> 5 : 1;
+  double r = lane < nw ? red[lane] : 0.0;
+  for (int o = 1; o < nw; o <<= 1) r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, o));
+  if (lane == 0) d.partials[((uint64_t)cur.seg << d.tps_log) + cur.t] = r;
+  if (d.dx == nullptr) return;
+  // d_input: ragged ends by lanes, aligned interior as one bulk store
+  const uint64_t b0 = cur.A * sizeof(T), b1 = (cur.A + (uint64_t)cur.m) * sizeof(T);
+  const uint64_t i0 = (b0 + 15) & ~uint64_t(15), i1 = b1 & ~uint64_t(15);
+  const int head = (int)(((i0 > b1 ? b1 : i0) - b0) / sizeof(T));
+  const int tail0 = i1 > i0 ? (int)((i1 - b0) / sizeof(T)) : head;
+  for (int e = lane; e < head; e += 32) static_cast<T*>(d.dx)[cur.A + e] = st.x[cur.off + e];
+  for (int e = tail0 + lane; e < cur.m; e += 32) static_cast<T*>(d.dx)[cur.A + e] = st.x[cur.off + e];
+  if (lane == 0 && i1 > i0) {
+    fence_proxy_async_smem();
+    bulk_s2g(static_cast<char*>(d.dx) + i0, reinterpret_cast<const char*>(st.x) + (i0 - cur.w0),
+             (uint32_t)(i1 - i0));
+    bulk_commit();
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kBwdCtaThreads, 3) bwd_kernel(const __grid_constant__ BwdBatch bt) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Stage<T>* stages = reinterpret_cast<Stage<T>*>(smem_raw);
-  __shared__ __align__(8) uint64_t bars[kStages];
-  __shared__ TileRef sh_tile[2];
-  __shared__ double red[kBwdThreads / 32];
+  __shared__ __align__(8) uint64_t full[kStages];
+  __shared__ __align__(8) uint64_t done[kStages];
+  __shared__ TileRef refs[kStages];
+  __shared__ double red[kStages][kConsumerWarps];
   const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int lane = tid & 31;
   const uint32_t total = bt.tile_begin[bt.n];
   if (blockIdx.x >= total) return;
 
-  // Thread 0 is the producer: it locates tiles and issues their bulk copies
-  // one tile ahead; everyone reads the tile descriptors from smem.
   if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&done[s], kConsumerWarps);
+    }
     fence_mbar_init();
-    sh_tile[0] = locate_full<T>(bt, blockIdx.x);
-    if (bt.d[sh_tile[0].di].vec) issue_tile<T>(bt.d[sh_tile[0].di], sh_tile[0], stages[0], &bars[0]);
   }
-  __syncthreads();
+  __syncthreads();  // the only CTA barrier: barrier init
 
-  uint32_t phase_bits = 0;  // per-stage mbarrier parity
+  if (warp == kConsumerWarps) {
+    // ----------------------------- producer warp -----------------------
+    uint32_t j_id = blockIdx.x;
+    for (int s = 0; s < kStages; ++s) {
+      const uint32_t id = blockIdx.x + (uint32_t)s * gridDim.x;
+      if (id < total) produce<T>(bt, id, stages[s], &refs[s], &full[s], lane);
+    }
+    uint32_t done_phase = 0;
+    for (int j = 0; j_id < total; ++j, j_id += gridDim.x) {
+      const int s = j & (kStages - 1);
+      mbar_wait(&done[s], (done_phase >> s) & 1u);
+      done_phase ^= 1u << s;
+      const TileRef cur = refs[s];
+      finalize<T>(bt, cur, stages[s], red[s], lane);
+      if (lane == 0) bulk_wait_read_all();  // the store has read the stage
+      __syncwarp();
+      const uint32_t nid = j_id + (uint32_t)kStages * gridDim.x;
+      if (nid < total) produce<T>(bt, nid, stages[s], &refs[s], &full[s], lane);
+    }
+    if (lane == 0) bulk_wait_all();
+    return;
+  }
+
+  // ------------------------------- consumer warps ----------------------
+  uint32_t full_phase = 0;
   GroupCache gc;
   int it = 0;
   for (uint32_t tile_id = blockIdx.x; tile_id < total; tile_id += gridDim.x, ++it) {
-    const int sidx = it & (kStages - 1);
-    Stage<T>& st = stages[sidx];
-    const TileRef cur = sh_tile[it & 1];
+    const int s = it & (kStages - 1);
+    mbar_wait(&full[s], (full_phase >> s) & 1u);
+    full_phase ^= 1u << s;
+    Stage<T>& st = stages[s];
+    const TileRef cur = refs[s];
     const BwdDesc& d = bt.d[cur.di];
 
-    // Producer: next tile into the other stage (freed by the barrier that
-    // ended the previous iteration).
-    const uint32_t next_id = tile_id + gridDim.x;
-    if (tid == 0 && next_id < total) {
-      bulk_wait_read_all();  // the stage's last bulk store has read it
-      const TileRef nxt = locate_full<T>(bt, next_id);
-      sh_tile[(it + 1) & 1] = nxt;
-      if (bt.d[nxt.di].vec) issue_tile<T>(bt.d[nxt.di], nxt, stages[sidx ^ 1], &bars[sidx ^ 1]);
-    }
-
-    const uint64_t w0 = cur.w0, w1 = cur.w1;
-    const int off = cur.off;  // tile start in stage
-    if (d.vec) {
-      mbar_wait(&bars[sidx], (phase_bits >> sidx) & 1u);
-      phase_bits ^= 1u << sidx;
-      // elements past the bulk window (only at the very end of a tensor)
-      const uint64_t e_end = cur.A + (uint64_t)cur.m;
-      const uint64_t e_w1 = w1 / sizeof(T);
-      if (e_w1 < e_end) {
-        for (uint64_t e = e_w1 + tid; e < e_end; e += kBwdThreads) {
-          st.x[e - w0 / sizeof(T)] = static_cast<const T*>(d.x)[e];
-          st.up[e - w0 / sizeof(T)] = static_cast<const T*>(d.up)[e];
-        }
-        __syncthreads();
-      }
-    } else {
-      for (int e = tid; e < cur.m; e += kBwdThreads) {
-        st.x[off + e] = static_cast<const T*>(d.x)[cur.A + e];
-        st.up[off + e] = static_cast<const T*>(d.up)[cur.A + e];
-      }
-      __syncthreads();
-    }
-
-    // This thread's leaf group: two left folds from 0.0 over its halves (or
-    // one fold if <= 8 elements), in registers, then their sum.
     int glo, glen;
     gc.get(cur.m, (int)d.g, tid, glo, glen);
     DivCtx dc;
@@ -325,50 +395,18 @@ __global__ void __launch_bounds__(kBwdThreads, 3) bwd_kernel(const __grid_consta
     dc.y = pin(cur.y);
     dc.usable = cur.s >= 0x1p-100 && cur.s <= 0x1p100;
     const double q = pin(d.q);
-    const bool want_dx = d.dx != nullptr;
-    T* sx = st.x + off + glo;
-    const T* su = st.up + off + glo;
-    const double v = want_dx ? group_sum<T, true>(sx, su, glen, dc, q)
-                             : group_sum<T, false>(sx, su, glen, dc, q);
-    __syncthreads();  // stage.x now holds d_input for the whole tile
-
-    // Warp-level butterfly now; the cross-warp step after the copy-out.
+    T* sx = st.x + cur.off + glo;
+    const T* su = st.up + cur.off + glo;
+    double v = d.dx != nullptr ? group_sum<T, true>(sx, su, glen, dc, q)
+                               : group_sum<T, false>(sx, su, glen, dc, q);
+    // warp-level perfect-tree butterfly
     const int groups = 1 << d.g;
     const int wl = groups < 32 ? groups : 32;
-    double wv = v;
-    for (int o = 1; o < wl; o <<= 1) wv = __dadd_rn(wv, __shfl_xor_sync(0xffffffffu, wv, o));
-    if ((tid & 31) == 0) red[tid >> 5] = wv;
-
-    // d_input -> HBM. The 16-byte-aligned interior of the tile goes out as
-    // ONE bulk store (TMA) issued by thread 0 after the barrier below; the
-    // ragged head/tail elements are stored by threads.
-    const uint64_t b0 = cur.A * sizeof(T), b1 = (cur.A + (uint64_t)cur.m) * sizeof(T);
-    const uint64_t i0 = (b0 + 15) & ~uint64_t(15), i1 = b1 & ~uint64_t(15);
-    if (want_dx) {
-      const int head = (int)((i0 > b1 ? b1 : i0) - b0) / (int)sizeof(T);
-      const int tail0 = i1 > i0 ? (int)((i1 - b0) / sizeof(T)) : head;
-      for (int e = tid; e < head; e += kBwdThreads)
-        static_cast<T*>(d.dx)[cur.A + e] = st.x[off + e];
-      for (int e = tail0 + tid; e < cur.m; e += kBwdThreads)
-        static_cast<T*>(d.dx)[cur.A + e] = st.x[off + e];
-    }
-    __syncthreads();  // d_input complete in the stage; red complete
-    if (tid == 0 && want_dx && i1 > i0) {
-      fence_proxy_async_smem();  // generic-proxy smem writes -> async proxy
-      bulk_s2g(static_cast<char*>(d.dx) + i0, reinterpret_cast<const char*>(st.x) + (i0 - w0),
-               (uint32_t)(i1 - i0));
-      bulk_commit();
-    }
-
-    // Perfect-tree combine of the warp sums (groups > 32) -> tile partial.
-    if (tid < 32) {
-      const int nw = groups > 32 ? groups >> 5 : 1;
-      double r = tid < nw ? red[tid] : 0.0;
-      for (int o = 1; o < nw; o <<= 1) r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, o));
-      if (tid == 0) d.partials[((uint64_t)cur.seg << d.tps_log) + cur.t] = r;
-    }
+    for (int o = 1; o < wl; o <<= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) red[s][warp] = v;
+    __syncwarp();  // the warp's d_input and sum are written
+    if (lane == 0) mbar_arrive(&done[s]);
   }
-  if (tid == 0) bulk_wait_all();  // d_input bulk stores complete before exit
 }
 
 // Finisher: one warp per (descriptor, channel). Each row's 2^tps_log tile
@@ -440,13 +478,13 @@ cudaError_t bwd_occupancy(int dtype, int* blocks_per_sm) {
                              (int)stage_bytes<float>());
     if (e != cudaSuccess) return e;
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, bwd_kernel<float>,
-                                                         kBwdThreads, stage_bytes<float>());
+                                                         kBwdCtaThreads, stage_bytes<float>());
   }
   e = cudaFuncSetAttribute(bwd_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)stage_bytes<__half>());
   if (e != cudaSuccess) return e;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, bwd_kernel<__half>,
-                                                       kBwdThreads, stage_bytes<__half>());
+                                                       kBwdCtaThreads, stage_bytes<__half>());
 }
 
 cudaError_t launch_bwd(int dtype, const BwdBatch& b, int grid, cudaStream_t st) {
@@ -454,9 +492,9 @@ cudaError_t launch_bwd(int dtype, const BwdBatch& b, int grid, cudaStream_t st) 
   if (tiles == 0) return cudaSuccess;
   if ((uint32_t)grid > tiles) grid = (int)tiles;
   if (dtype == 0)
-    bwd_kernel<float><<<grid, kBwdThreads, stage_bytes<float>(), st>>>(b);
+    bwd_kernel<float><<<grid, kBwdCtaThreads, stage_bytes<float>(), st>>>(b);
   else
-    bwd_kernel<__half><<<grid, kBwdThreads, stage_bytes<__half>(), st>>>(b);
+    bwd_kernel<__half><<<grid, kBwdCtaThreads, stage_bytes<__half>(), st>>>(b);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   uint32_t warps = 0;
