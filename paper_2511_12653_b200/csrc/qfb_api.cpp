@@ -713,7 +713,17 @@ qfb_status qfb_fq_bwd_multi(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc* t
     }
     b.n = cnt;
     b.tile_begin[cnt] = (uint32_t)tb;
-    const int grid = ctx->sm_count * ctx->bwd_blocks_per_sm[dtype];
+    // ring sized from the largest tile of the batch (node size bound)
+    uint32_t max_tile = 1;
+    for (int32_t k = 0; k < cnt; ++k) {
+      const uint64_t span = 1ull << b.d[k].tps_log;
+      max_tile = std::max<uint32_t>(max_tile, (uint32_t)((b.d[k].inner + span - 1) / span));
+    }
+    size_t smem = 0;
+    bwd_ring_size(dtype, max_tile, &b.stage_elems, &b.nstages, &smem);
+    int per_sm = 0;
+    if (bwd_occupancy_smem(dtype, smem, &per_sm) != cudaSuccess || per_sm < 1) per_sm = 1;
+    const int grid = ctx->sm_count * per_sm;
     cudaError_t e = launch_bwd(dtype, b, grid, ctx->stream);
     if (e != cudaSuccess) return cuda_fail(e, "bwd_kernel launch");
     ctx->launches += 2;  // main pass + finisher

@@ -40,8 +40,10 @@ namespace qfb {
 
 namespace {
 
-constexpr int kStages = 2;
-constexpr int kWinPad = 32;  // window slack: 16-byte rounding at both ends
+constexpr int kMaxStages = 4;
+constexpr int kWinPad = 32;                       // window slack: 16-byte rounding at both ends
+constexpr size_t kRingBudget = 72 * 1024;         // per CTA: 3 CTAs per SM
+constexpr size_t kRingMax = 2 * 2 * (kBwdTileMax + kWinPad) * 4;  // 2 stages of the largest f32 tile
 
 // Descend `levels` levels of the reference split from node (lo, m) along
 // the bits of `path` (MSB first): bit 0 = left child [lo, lo + m/2),
@@ -59,11 +61,18 @@ __device__ __forceinline__ void descend(I& lo, I& m, uint32_t path, int levels) 
   }
 }
 
+// One ring stage: the x and upstream windows of a tile (runtime stride).
 template <typename T>
 struct Stage {
-  T x[kBwdTileMax + kWinPad];
-  T up[kBwdTileMax + kWinPad];
+  T* x;
+  T* up;
 };
+
+template <typename T>
+__device__ __forceinline__ Stage<T> stage_at(unsigned char* base, uint32_t stage_elems, int s) {
+  T* p = reinterpret_cast<T*>(base) + (size_t)s * 2 * stage_elems;
+  return Stage<T>{p, p + stage_elems};
+}
 
 template <typename T>
 __device__ __forceinline__ float to_f(T v) {
@@ -333,11 +342,12 @@ __device__ __forceinline__ void finalize(const BwdBatch& bt, const TileRef& cur,
 template <typename T>
 __global__ void __launch_bounds__(kBwdCtaThreads, 3) bwd_kernel(const __grid_constant__ BwdBatch bt) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  Stage<T>* stages = reinterpret_cast<Stage<T>*>(smem_raw);
-  __shared__ __align__(8) uint64_t full[kStages];
-  __shared__ __align__(8) uint64_t done[kStages];
-  __shared__ TileRef refs[kStages];
-  __shared__ double red[kStages][kConsumerWarps];
+  __shared__ __align__(8) uint64_t full[kMaxStages];
+  __shared__ __align__(8) uint64_t done[kMaxStages];
+  __shared__ TileRef refs[kMaxStages];
+  __shared__ double red[kMaxStages][kConsumerWarps];
+  const int nst = bt.nstages;
+  const uint32_t se = bt.stage_elems;
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   const int lane = tid & 31;
@@ -345,7 +355,7 @@ __global__ void __launch_bounds__(kBwdCtaThreads, 3) bwd_kernel(const __grid_con
   if (blockIdx.x >= total) return;
 
   if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < nst; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&done[s], kConsumerWarps);
     }
@@ -356,21 +366,24 @@ __global__ void __launch_bounds__(kBwdCtaThreads, 3) bwd_kernel(const __grid_con
   if (warp == kConsumerWarps) {
     // ----------------------------- producer warp -----------------------
     uint32_t j_id = blockIdx.x;
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < nst; ++s) {
       const uint32_t id = blockIdx.x + (uint32_t)s * gridDim.x;
-      if (id < total) produce<T>(bt, id, stages[s], &refs[s], &full[s], lane);
+      Stage<T> st = stage_at<T>(smem_raw, se, s);
+      if (id < total) produce<T>(bt, id, st, &refs[s], &full[s], lane);
     }
     uint32_t done_phase = 0;
-    for (int j = 0; j_id < total; ++j, j_id += gridDim.x) {
-      const int s = j & (kStages - 1);
+    int s = 0;
+    for (; j_id < total; j_id += gridDim.x) {
       mbar_wait(&done[s], (done_phase >> s) & 1u);
       done_phase ^= 1u << s;
+      Stage<T> st = stage_at<T>(smem_raw, se, s);
       const TileRef cur = refs[s];
-      finalize<T>(bt, cur, stages[s], red[s], lane);
+      finalize<T>(bt, cur, st, red[s], lane);
       if (lane == 0) bulk_wait_read_all();  // the store has read the stage
       __syncwarp();
-      const uint32_t nid = j_id + (uint32_t)kStages * gridDim.x;
-      if (nid < total) produce<T>(bt, nid, stages[s], &refs[s], &full[s], lane);
+      const uint32_t nid = j_id + (uint32_t)nst * gridDim.x;
+      if (nid < total) produce<T>(bt, nid, st, &refs[s], &full[s], lane);
+      s = s + 1 == nst ? 0 : s + 1;
     }
     if (lane == 0) bulk_wait_all();
     return;
@@ -379,12 +392,11 @@ __global__ void __launch_bounds__(kBwdCtaThreads, 3) bwd_kernel(const __grid_con
   // ------------------------------- consumer warps ----------------------
   uint32_t full_phase = 0;
   GroupCache gc;
-  int it = 0;
-  for (uint32_t tile_id = blockIdx.x; tile_id < total; tile_id += gridDim.x, ++it) {
-    const int s = it & (kStages - 1);
+  int s = 0;
+  for (uint32_t tile_id = blockIdx.x; tile_id < total; tile_id += gridDim.x) {
     mbar_wait(&full[s], (full_phase >> s) & 1u);
     full_phase ^= 1u << s;
-    Stage<T>& st = stages[s];
+    Stage<T> st = stage_at<T>(smem_raw, se, s);
     const TileRef cur = refs[s];
     const BwdDesc& d = bt.d[cur.di];
 
@@ -406,6 +418,7 @@ __global__ void __launch_bounds__(kBwdCtaThreads, 3) bwd_kernel(const __grid_con
     if (lane == 0) red[s][warp] = v;
     __syncwarp();  // the warp's d_input and sum are written
     if (lane == 0) mbar_arrive(&done[s]);
+    s = s + 1 == nst ? 0 : s + 1;
   }
 }
 
@@ -464,37 +477,52 @@ __global__ void __launch_bounds__(32) bwd_finish_kernel(const __grid_constant__ 
   (void)warp_base_mul;
 }
 
+}  // namespace
+
+void bwd_ring_size(int dtype, uint32_t max_tile, uint32_t* stage_elems, int32_t* nstages,
+                   size_t* smem_bytes) {
+  const size_t es = dtype == 0 ? 4 : 2;
+  uint32_t se = max_tile + kWinPad;
+  se = (se + 7u) & ~7u;  // 16-byte multiple for both element sizes
+  const size_t stage = 2 * (size_t)se * es;
+  int ns = (int)(kRingBudget / stage);
+  if (ns > kMaxStages) ns = kMaxStages;
+  if (ns < 2) ns = 2;
+  *stage_elems = se;
+  *nstages = ns;
+  *smem_bytes = stage * (size_t)ns;
+}
+
+namespace {
+
 template <typename T>
-constexpr size_t stage_bytes() {
-  return sizeof(Stage<T>) * kStages;
+cudaError_t set_smem() {
+  return cudaFuncSetAttribute(bwd_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)(kRingMax > kRingBudget ? kRingMax : kRingBudget));
 }
 
 }  // namespace
 
 cudaError_t bwd_occupancy(int dtype, int* blocks_per_sm) {
-  cudaError_t e;
-  if (dtype == 0) {
-    e = cudaFuncSetAttribute(bwd_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)stage_bytes<float>());
-    if (e != cudaSuccess) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, bwd_kernel<float>,
-                                                         kBwdCtaThreads, stage_bytes<float>());
-  }
-  e = cudaFuncSetAttribute(bwd_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)stage_bytes<__half>());
+  return bwd_occupancy_smem(dtype, kRingBudget, blocks_per_sm);
+}
+
+cudaError_t bwd_occupancy_smem(int dtype, size_t smem, int* blocks_per_sm) {
+  cudaError_t e = dtype == 0 ? set_smem<float>() : set_smem<__half>();
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, bwd_kernel<__half>,
-                                                       kBwdCtaThreads, stage_bytes<__half>());
+  const void* f = dtype == 0 ? (const void*)bwd_kernel<float> : (const void*)bwd_kernel<__half>;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, kBwdCtaThreads, smem);
 }
 
 cudaError_t launch_bwd(int dtype, const BwdBatch& b, int grid, cudaStream_t st) {
   const uint32_t tiles = b.tile_begin[b.n];
   if (tiles == 0) return cudaSuccess;
   if ((uint32_t)grid > tiles) grid = (int)tiles;
+  const size_t smem = (size_t)b.nstages * 2 * b.stage_elems * (dtype == 0 ? 4 : 2);
   if (dtype == 0)
-    bwd_kernel<float><<<grid, kBwdCtaThreads, stage_bytes<float>(), st>>>(b);
+    bwd_kernel<float><<<grid, kBwdCtaThreads, smem, st>>>(b);
   else
-    bwd_kernel<__half><<<grid, kBwdCtaThreads, stage_bytes<__half>(), st>>>(b);
+    bwd_kernel<__half><<<grid, kBwdCtaThreads, smem, st>>>(b);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   uint32_t warps = 0;

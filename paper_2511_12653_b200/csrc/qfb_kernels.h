@@ -146,12 +146,19 @@ struct BwdDesc {
 
 struct BwdBatch {
   int32_t n;
-  int32_t pad;
+  int32_t nstages;       // TMA ring depth (2..4), sized from the max tile
+  uint32_t stage_elems;  // elements per array per stage (16-byte multiple)
+  uint32_t pad2;
   uint32_t tile_begin[kMaxBwdDesc + 1];
   BwdDesc d[kMaxBwdDesc];
 };
 
-cudaError_t bwd_occupancy(int dtype, int* blocks_per_sm);
+cudaError_t bwd_occupancy(int dtype, int* blocks_per_sm);  // at the default ring size
+cudaError_t bwd_occupancy_smem(int dtype, size_t smem, int* blocks_per_sm);
+// Ring sizing: stage_elems / nstages / dynamic smem for a batch whose
+// largest tile has max_tile elements.
+void bwd_ring_size(int dtype, uint32_t max_tile, uint32_t* stage_elems, int32_t* nstages,
+                   size_t* smem_bytes);
 // Main pass (tile partials) + finisher (segment trees, chain, outer fold);
 // stream order replaces fences and tickets.
 cudaError_t launch_bwd(int dtype, const BwdBatch& b, int grid, cudaStream_t st);
