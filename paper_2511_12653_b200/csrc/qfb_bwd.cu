@@ -166,40 +166,33 @@ __device__ __forceinline__ void issue_tile(const BwdDesc& d, const TileRef& r, S
 
 // Group (leaf) of this thread inside a tile of m elements: depends only on
 // (m, g), and a descriptor's tiles take at most two sizes -> 2-slot cache.
-// The two leaf groups (2i, 2i+1) of consumer lane i inside a tile of m
-// elements: depend only on (m, g); a descriptor's tiles take at most two
-// sizes -> 2-slot cache.
-struct Pair {
-  int lo0, len0, lo1, len1;
-};
+struct GroupCache {
+  int k0 = -1, lo0 = 0, len0 = 0;
+  int k1 = -1, lo1 = 0, len1 = 0;
 
-struct PairCache {
-  int k0 = -1, k1 = -1;
-  Pair p0{0, 0, 0, 0}, p1{0, 0, 0, 0};
-
-  __device__ __forceinline__ Pair get(int m, int g, int lane_idx) {
+  __device__ __forceinline__ void get(int m, int g, int tid, int& glo, int& glen) {
     const int k = m | (g << 16);
-    if (k0 == k) return p0;
-    if (k1 == k) return p1;
-    Pair p{0, 0, 0, 0};
-    const int groups = 1 << g;
-    if (2 * lane_idx < groups) {
-      int l = 0, mm = m;
-      descend<int>(l, mm, (uint32_t)(2 * lane_idx), g);
-      p.lo0 = l;
-      p.len0 = mm;
+    if (k0 == k) {
+      glo = lo0;
+      glen = len0;
+      return;
     }
-    if (2 * lane_idx + 1 < groups) {
-      int l = 0, mm = m;
-      descend<int>(l, mm, (uint32_t)(2 * lane_idx + 1), g);
-      p.lo1 = l;
-      p.len1 = mm;
+    if (k1 == k) {
+      glo = lo1;
+      glen = len1;
+      return;
     }
+    int l = 0, mm = m;
+    if (tid < (1 << g)) descend<int>(l, mm, (uint32_t)tid, g);
+    else mm = 0;
     k1 = k0;
-    p1 = p0;
+    lo1 = lo0;
+    len1 = len0;
     k0 = k;
-    p0 = p;
-    return p;
+    lo0 = l;
+    len0 = mm;
+    glo = l;
+    glen = mm;
   }
 };
 
@@ -244,33 +237,29 @@ __device__ __forceinline__ double elem(T* sx, const T* su, int k, const DivCtx& 
   return term;
 }
 
-// Two adjacent leaf groups' sums, each in the reference order: a group of
-// <= 8 elements is one left fold from 0.0, a larger one is fold(left half)
-// + fold(right half). The (up to) four folds are independent chains and are
-// interleaved for ILP. Returns g0 + g1 (the first level of the perfect
-// tree above the leaf groups), or g0 alone when the tile has one group.
+// A leaf group's sum in the reference order: fold(left half) + fold(right
+// half) from 0.0 each (or one fold if <= 8 elements). The two folds are
+// independent chains, so they are interleaved for ILP.
 template <typename T, bool kDx>
-__device__ __forceinline__ double pair_sum(T* sx0, const T* su0, int len0, T* sx1, const T* su1,
-                                           int len1, const DivCtx& dc, double q, bool single) {
-  const int h0 = len0 > 8 ? len0 >> 1 : len0;
-  const int r0 = len0 - h0;
-  const int h1 = len1 > 8 ? len1 >> 1 : len1;
-  const int r1 = len1 - h1;
-  T* x0r = sx0 + h0;
-  const T* u0r = su0 + h0;
-  T* x1r = sx1 + h1;
-  const T* u1r = su1 + h1;
-  double a0 = 0.0, b0 = 0.0, a1 = 0.0, b1 = 0.0;
-  const int kmax = max(max(h0, r0), max(h1, r1));
-  for (int k = 0; k < kmax; ++k) {
-    if (k < h0) a0 = __dadd_rn(a0, elem<T, kDx>(sx0, su0, k, dc, q));
-    if (k < r0) b0 = __dadd_rn(b0, elem<T, kDx>(x0r, u0r, k, dc, q));
-    if (k < h1) a1 = __dadd_rn(a1, elem<T, kDx>(sx1, su1, k, dc, q));
-    if (k < r1) b1 = __dadd_rn(b1, elem<T, kDx>(x1r, u1r, k, dc, q));
+__device__ __forceinline__ double group_sum(T* sx, const T* su, int glen, const DivCtx& dc,
+                                            double q) {
+  if (glen <= 8) {
+    double acc = 0.0;
+    for (int k = 0; k < glen; ++k) acc = __dadd_rn(acc, elem<T, kDx>(sx, su, k, dc, q));
+    return acc;
   }
-  const double g0 = len0 > 8 ? __dadd_rn(a0, b0) : a0;
-  const double g1 = len1 > 8 ? __dadd_rn(a1, b1) : a1;
-  return single ? g0 : __dadd_rn(g0, g1);
+  const int h = glen >> 1;  // left; right has glen - h >= h elements
+  T* rx = sx + h;
+  const T* ru = su + h;
+  double acc_l = 0.0, acc_r = 0.0;
+  for (int k = 0; k < h; ++k) {
+    const double tl = elem<T, kDx>(sx, su, k, dc, q);
+    const double tr = elem<T, kDx>(rx, ru, k, dc, q);
+    acc_l = __dadd_rn(acc_l, tl);
+    acc_r = __dadd_rn(acc_r, tr);
+  }
+  if (glen - h > h) acc_r = __dadd_rn(acc_r, elem<T, kDx>(rx, ru, h, dc, q));
+  return __dadd_rn(acc_l, acc_r);
 }
 
 // ---------------------------------------------------------------------
@@ -284,8 +273,8 @@ __device__ __forceinline__ double pair_sum(T* sx0, const T* su0, int len0, T* sx
 // store to have read the stage, then refills the stage with tile j+2.
 // Consumers never execute a CTA-wide barrier.
 // ---------------------------------------------------------------------
-constexpr int kConsumerWarps = kBwdThreads / 64;      // 4 (two groups per lane)
-constexpr int kBwdCtaThreads = kBwdThreads / 2 + 32; // + producer warp
+constexpr int kConsumerWarps = kBwdThreads / 32;      // 8
+constexpr int kBwdCtaThreads = kBwdThreads + 32;     // + producer warp
 
 template <typename T>
 __device__ __forceinline__ void produce(const BwdBatch& bt, uint32_t tile_id, Stage<T>& st,
@@ -328,11 +317,24 @@ template <typename T>
 __device__ __forceinline__ void finalize(const BwdBatch& bt, const TileRef& cur, Stage<T>& st,
                                          const double* red, int lane) {
   const BwdDesc& d = bt.d[cur.di];
-  // cross-warp perfect-tree step over the consumer warps' sums
+  // perfect tree over the tile's 2^g group sums: each lane folds `per`
+  // consecutive sums as a perfect subtree, then an xor butterfly
   const int groups = 1 << d.g;
-  const int nw = groups > 64 ? groups >> 6 : 1;  // consumer warps holding groups
-  double r = lane < nw ? red[lane] : 0.0;
-  for (int o = 1; o < nw; o <<= 1) r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, o));
+  const int per = groups >= 32 ? groups >> 5 : 1;
+  const int lanes_used = groups >= 32 ? 32 : groups;
+  double r = 0.0;
+  if (lane < lanes_used) {
+    const double* g = red + lane * per;
+    switch (per) {
+      case 1: r = g[0]; break;
+      case 2: r = __dadd_rn(g[0], g[1]); break;
+      case 4: r = __dadd_rn(__dadd_rn(g[0], g[1]), __dadd_rn(g[2], g[3])); break;
+      default:
+        r = __dadd_rn(__dadd_rn(__dadd_rn(g[0], g[1]), __dadd_rn(g[2], g[3])),
+                      __dadd_rn(__dadd_rn(g[4], g[5]), __dadd_rn(g[6], g[7])));
+    }
+  }
+  for (int o = 1; o < lanes_used; o <<= 1) r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, o));
   if (lane == 0) d.partials[((uint64_t)cur.seg << d.tps_log) + cur.t] = r;
   if (d.dx == nullptr) return;
   // d_input: ragged ends by lanes, aligned interior as one bulk store
@@ -356,7 +358,7 @@ __global__ void __launch_bounds__(kBwdCtaThreads, 3) bwd_kernel(const __grid_con
   __shared__ __align__(8) uint64_t full[kMaxStages];
   __shared__ __align__(8) uint64_t done[kMaxStages];
   __shared__ TileRef refs[kMaxStages];
-  __shared__ double red[kMaxStages][kConsumerWarps];
+  __shared__ double red[kMaxStages][kBwdThreads];  // per-group sums of a tile
   const int nst = bt.nstages;
   const uint32_t se = bt.stage_elems;
   const int tid = threadIdx.x;
@@ -402,7 +404,7 @@ __global__ void __launch_bounds__(kBwdCtaThreads, 3) bwd_kernel(const __grid_con
 
   // ------------------------------- consumer warps ----------------------
   uint32_t full_phase = 0;
-  PairCache pc;
+  GroupCache gc;
   int s = 0;
   for (uint32_t tile_id = blockIdx.x; tile_id < total; tile_id += gridDim.x) {
     mbar_wait(&full[s], (full_phase >> s) & 1u);
@@ -411,25 +413,19 @@ __global__ void __launch_bounds__(kBwdCtaThreads, 3) bwd_kernel(const __grid_con
     const TileRef cur = refs[s];
     const BwdDesc& d = bt.d[cur.di];
 
-    const Pair pr = pc.get(cur.m, (int)d.g, tid);
+    int glo, glen;
+    gc.get(cur.m, (int)d.g, tid, glo, glen);
     DivCtx dc;
     dc.s = pin(cur.s);
     dc.y = pin(cur.y);
     dc.usable = cur.s >= 0x1p-100 && cur.s <= 0x1p100;
     const double q = pin(d.q);
-    const int groups = 1 << d.g;
-    T* sx0 = st.x + cur.off + pr.lo0;
-    const T* su0 = st.up + cur.off + pr.lo0;
-    T* sx1 = st.x + cur.off + pr.lo1;
-    const T* su1 = st.up + cur.off + pr.lo1;
-    const bool single = groups == 1;
-    double v = d.dx != nullptr ? pair_sum<T, true>(sx0, su0, pr.len0, sx1, su1, pr.len1, dc, q, single)
-                               : pair_sum<T, false>(sx0, su0, pr.len0, sx1, su1, pr.len1, dc, q, single);
-    // warp-level perfect-tree butterfly over the lanes' pair sums
-    const int lanes_used = groups >= 64 ? 32 : (groups >> 1 ? groups >> 1 : 1);
-    for (int o = 1; o < lanes_used; o <<= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
-    if (lane == 0) red[s][warp] = v;
-    __syncwarp();  // the warp's d_input and sum are written
+    T* sx = st.x + cur.off + glo;
+    const T* su = st.up + cur.off + glo;
+    double v = d.dx != nullptr ? group_sum<T, true>(sx, su, glen, dc, q)
+                               : group_sum<T, false>(sx, su, glen, dc, q);
+    red[s][tid] = v;  // the producer runs the tile's tree reduction
+    __syncwarp();     // the warp's d_input and group sums are written
     if (lane == 0) mbar_arrive(&done[s]);
     s = s + 1 == nst ? 0 : s + 1;
   }
