@@ -252,6 +252,7 @@ __device__ __forceinline__ double group_sum(T* sx, const T* su, int glen, const 
   T* rx = sx + h;
   const T* ru = su + h;
   double acc_l = 0.0, acc_r = 0.0;
+#pragma unroll 2
   for (int k = 0; k < h; ++k) {
     const double tl = elem<T, kDx>(sx, su, k, dc, q);
     const double tr = elem<T, kDx>(rx, ru, k, dc, q);

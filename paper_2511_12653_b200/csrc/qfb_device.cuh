@@ -182,7 +182,10 @@ __device__ __forceinline__ bool certified_quotient(double x, const DivCtx& c, do
   const double r1 = __fma_rn(-c.s, z, x);
   const int hi = __double2hiint(z);
   const int lo = __double2loint(z);
-  const double thr = __dmul_rn(c.s, __hiloint2double((hi & 0x7ff00000) - (53 << 20), 0));
+  // thr = s * 2^(E(z) - 53) built by adding exponents (s and thr normal for
+  // usable s and nonzero finite x; anything else fails the comparison)
+  const int thr_hi = __double2hiint(c.s) + (hi & 0x7ff00000) - (1076 << 20);
+  const double thr = __hiloint2double(thr_hi, __double2loint(c.s));
   return c.usable && ((hi & 0x000fffff) | lo) != 0 && fabs(r1) < thr;
 }
 
