@@ -48,6 +48,7 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=10)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-graph", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0)
     return p.parse_args()
 
@@ -270,6 +271,7 @@ def run_qfb(args):
     from paper_2511_12653_b200.frontend import FrontendQuantPass
 
     ws, rank, local = dist_env()
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     pg = None
@@ -354,6 +356,31 @@ def run_qfb(args):
                                "traffic": (traffic or {}).get(args.dtype, {}).get("fwd_bytes_per_launch")},
                 "step_gbps": gbps / ws, "step_frac": (gbps / ws) / peak}
 
+    # ------------------------------------- the same step as a CUDA graph --
+    graph_ms = None
+    if ws == 1 and not args.no_graph:
+        try:
+            graphs = []
+            for si in range(nsets):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    fp.forward(si)
+                    fp.backward(si)
+                graphs.append(g)
+            for i in range(args.warmup):
+                graphs[i % nsets].replay()
+            torch.cuda.synchronize(dev)
+            g0 = torch.cuda.Event(enable_timing=True)
+            g1 = torch.cuda.Event(enable_timing=True)
+            g0.record(stream)
+            for i in range(args.steps):
+                graphs[i % nsets].replay()
+            g1.record(stream)
+            torch.cuda.synchronize(dev)
+            graph_ms = g0.elapsed_time(g1) / args.steps
+        except Exception as exc:  # pragma: no cover
+            graph_ms = f"capture failed: {exc}"
+
     # ---------------------------------------------------- e2e (host API) --
     e2e = None
     if not args.no_e2e:
@@ -385,6 +412,7 @@ def run_qfb(args):
                 "kernel_ms": {"fwd": fwd_ms, "bwd": bwd_ms},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clocks,
+                "graph_ms_per_step": graph_ms,
                 "wall_ms_per_step": (wall1 - wall0) * 1000.0 / args.steps}
         print(json.dumps(line))
     if pg is not None:

@@ -72,6 +72,7 @@ struct qfb_ctx {
   int ew_blocks_per_sm[2][2] = {{4, 4}, {4, 4}};  // [dtype][chain]
   int bwd_blocks_per_sm[2] = {4, 4};
   int tma_blocks_per_sm[2] = {0, 0};  // 0: TMA forward unavailable
+  std::vector<std::pair<size_t, int>> bwd_occ[2];  // (smem, blocks/SM) cache
   uint32_t* d_status = nullptr;
   uint32_t* h_status = nullptr;  // pinned
   DevBuf ws_f64;                 // partials / segment results
@@ -721,8 +722,14 @@ qfb_status qfb_fq_bwd_multi(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc* t
     }
     size_t smem = 0;
     bwd_ring_size(dtype, max_tile, &b.stage_elems, &b.nstages, &smem);
+    // cached: keeps steady-state launches free of runtime queries (graph capture)
     int per_sm = 0;
-    if (bwd_occupancy_smem(dtype, smem, &per_sm) != cudaSuccess || per_sm < 1) per_sm = 1;
+    for (const auto& kv : ctx->bwd_occ[dtype])
+      if (kv.first == smem) per_sm = kv.second;
+    if (per_sm == 0) {
+      if (bwd_occupancy_smem(dtype, smem, &per_sm) != cudaSuccess || per_sm < 1) per_sm = 1;
+      ctx->bwd_occ[dtype].emplace_back(smem, per_sm);
+    }
     const int grid = ctx->sm_count * per_sm;
     cudaError_t e = launch_bwd(dtype, b, grid, ctx->stream);
     if (e != cudaSuccess) return cuda_fail(e, "bwd_kernel launch");
