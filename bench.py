@@ -287,7 +287,13 @@ def run_qfb(args):
     grads = fp.scale_grads()
     nsets = len(fp.sets)
 
-    def step(i, ev=None):
+    def exchange():
+        if pg is not None:
+            # QAT exchange: per-frame scale-gradient rows, all-gathered and
+            # folded in frame order (bit-identical at any GPU count)
+            gather_fold(torch.cat(fp.dls).unsqueeze(0))
+
+    def eager_step(i, ev=None):
         si = i % nsets
         if ev is not None:
             ev[0].record(stream)
@@ -297,10 +303,36 @@ def run_qfb(args):
         fp.backward(si)
         if ev is not None:
             ev[2].record(stream)
-        if pg is not None:
-            # QAT exchange: per-frame scale-gradient rows, all-gathered and
-            # folded in frame order (bit-identical at any GPU count)
-            gather_fold(torch.cat(fp.dls).unsqueeze(0))
+        exchange()
+
+    # warm up eagerly (sizes the workspaces), then capture one CUDA graph per
+    # input set: the step is 1 forward + 2 backward launches
+    for i in range(max(1, args.warmup)):
+        eager_step(i)
+    ctx.sync()
+    use_graph = not args.no_graph
+    graphs = []
+    launches_per_step = 3
+    if use_graph:
+        try:
+            c0 = ctx.launch_count
+            for si in range(nsets):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    fp.forward(si)
+                    fp.backward(si)
+                graphs.append(g)
+            launches_per_step = (ctx.launch_count - c0) // nsets
+        except Exception as exc:  # pragma: no cover - fall back to eager timing
+            print(f"graph capture failed ({exc}); timing eager launches", file=sys.stderr)
+            use_graph = False
+
+    def step(i):
+        if use_graph:
+            graphs[i % nsets].replay()
+            exchange()
+        else:
+            eager_step(i)
 
     for i in range(args.warmup):
         step(i)
@@ -312,23 +344,29 @@ def run_qfb(args):
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.15)  # let the sampler attach before the timed region
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
-    launches0 = ctx.launch_count
     wall0 = time.perf_counter()
     t_start.record(stream)
     for i in range(args.steps):
-        step(i, evs[i])
+        step(i)
     t_end.record(stream)
     torch.cuda.synchronize(dev)
     wall1 = time.perf_counter()
     clocks = sampler.stop()
-    launches = ctx.launch_count - launches0
+    launches = launches_per_step * args.steps
     ctx.sync()
     ms_total = t_start.elapsed_time(t_end)
-    fwd_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
-    bwd_ms = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
+
+    # per-kernel attribution for the roofline: the same steps launched
+    # eagerly with CUDA events around each kernel on the library's stream
+    k_att = min(args.steps, 200)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(k_att)]
+    for i in range(k_att):
+        eager_step(i, evs[i])
+    torch.cuda.synchronize(dev)
+    fwd_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / k_att
+    bwd_ms = sum(e[1].elapsed_time(e[2]) for e in evs) / k_att
     if pg is not None:
         t = torch.tensor([ms_total], device=dev)
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
@@ -355,31 +393,6 @@ def run_qfb(args):
                                "algorithmic_bytes_per_launch": b["fwd"],
                                "traffic": (traffic or {}).get(args.dtype, {}).get("fwd_bytes_per_launch")},
                 "step_gbps": gbps / ws, "step_frac": (gbps / ws) / peak}
-
-    # ------------------------------------- the same step as a CUDA graph --
-    graph_ms = None
-    if ws == 1 and not args.no_graph:
-        try:
-            graphs = []
-            for si in range(nsets):
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g, stream=stream):
-                    fp.forward(si)
-                    fp.backward(si)
-                graphs.append(g)
-            for i in range(args.warmup):
-                graphs[i % nsets].replay()
-            torch.cuda.synchronize(dev)
-            g0 = torch.cuda.Event(enable_timing=True)
-            g1 = torch.cuda.Event(enable_timing=True)
-            g0.record(stream)
-            for i in range(args.steps):
-                graphs[i % nsets].replay()
-            g1.record(stream)
-            torch.cuda.synchronize(dev)
-            graph_ms = g0.elapsed_time(g1) / args.steps
-        except Exception as exc:  # pragma: no cover
-            graph_ms = f"capture failed: {exc}"
 
     # ---------------------------------------------------- e2e (host API) --
     e2e = None
@@ -412,7 +425,10 @@ def run_qfb(args):
                 "kernel_ms": {"fwd": fwd_ms, "bwd": bwd_ms},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clocks,
-                "graph_ms_per_step": graph_ms,
+                "timing": ("value: CUDA-graph replay of the step (fwd + bwd + finisher launches) "
+                           "between CUDA events on the library stream" if use_graph else
+                           "value: eager launches between CUDA events on the library stream") +
+                          f"; roofline: per-kernel CUDA events over {k_att} eager steps",
                 "wall_ms_per_step": (wall1 - wall0) * 1000.0 / args.steps}
         print(json.dumps(line))
     if pg is not None:
