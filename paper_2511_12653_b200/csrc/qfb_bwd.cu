@@ -32,6 +32,7 @@
 // tests/test_tree_model.py executes this exact schedule on the CPU.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
+#include <stdlib.h>
 
 #include "qfb_device.cuh"
 #include "qfb_kernels.h"
@@ -40,10 +41,16 @@ namespace qfb {
 
 namespace {
 
-constexpr int kMaxStages = 4;
-constexpr int kWinPad = 32;                       // window slack: 16-byte rounding at both ends
-constexpr size_t kRingBudget = 72 * 1024;         // per CTA: 3 CTAs per SM
-constexpr size_t kRingMax = 2 * 2 * (kBwdTileMax + kWinPad) * 4;  // 2 stages of the largest f32 tile
+constexpr int kMaxStages = 8;
+// Probe variants (template V, QFB_BWD_VARIANT): memory pipeline only (no
+// arithmetic, d_input = staged x) / arithmetic only (tiles loaded once,
+// no refills or stores). Not used in production; results in DESIGN.md §7.
+constexpr int kProbeNoCompute = 8;
+constexpr int kProbeNoLoads = 16;
+constexpr int kWinPad = 32;                // window slack: 16-byte rounding at both ends
+constexpr size_t kRingBudget = 72 * 1024;  // default per-CTA ring + sums: 3 CTAs per SM
+constexpr size_t kRedBytes = kBwdThreads * sizeof(double);  // group sums of one stage
+constexpr size_t kSmemMax = 225 * 1024;    // dynamic smem attribute (ring + sums)
 
 // Descend `levels` levels of the reference split from node (lo, m) along
 // the bits of `path` (MSB first): bit 0 = left child [lo, lo + m/2),
@@ -213,6 +220,35 @@ __device__ __forceinline__ double pin(double v) {
   return r;
 }
 
+// Fast-path terms of one element, no branches: term, d_input (finite
+// upstream) and whether the certified path applies (else: slow_elem).
+struct FastTerm {
+  double term;
+  float dx;
+  bool ok;
+};
+
+__device__ __forceinline__ FastTerm fast_elem(float xv, float uv, const DivCtx& dc, double q) {
+  FastTerm f;
+  double z;
+  const bool up_finite = (__float_as_uint(uv) & 0x7f800000u) != 0x7f800000u;
+  // x = +-0 is exact too: z = +-0, d_ds = +0 whatever the sign of z
+  f.ok = (certified_quotient((double)xv, dc, z) || xv == 0.0f) && up_finite;
+  const bool mask = fabs(z) <= q;
+  const double d_ds = mask ? __dadd_rn(rint(z), -z) : copysign(q, z);
+  f.term = __dmul_rn(d_ds, (double)uv);
+  f.dx = mask ? uv : __uint_as_float(__float_as_uint(uv) & 0x80000000u);
+  return f;
+}
+
+__device__ __forceinline__ void fix_slow(FastTerm& f, float xv, float uv, double s, double q) {
+  if (!f.ok) {
+    const double2 r = slow_elem(xv, uv, s, q);
+    f.term = r.x;
+    f.dx = (float)r.y;  // exact: r.y is a float widened
+  }
+}
+
 // One element: term = d_ds * up (double) and d_input, with z = RN(x/s)
 // from certified_quotient (qfb_device.cuh); uncertified elements take the
 // exact IEEE path in slow_elem (returned in registers, never via memory).
@@ -220,26 +256,15 @@ template <typename T, bool kDx>
 __device__ __forceinline__ double elem(T* sx, const T* su, int k, const DivCtx& dc, double q) {
   const float xv = to_f<T>(sx[k]);
   const float uv = to_f<T>(su[k]);
-  double z;
-  // one rare-path test: uncertified quotient or a non-finite upstream
-  const bool up_finite = (__float_as_uint(uv) & 0x7f800000u) != 0x7f800000u;
-  const bool ok = certified_quotient((double)xv, dc, z) && up_finite;
-  const bool mask = fabs(z) <= q;
-  const double d_ds = mask ? __dadd_rn(rint(z), -z) : copysign(q, z);
-  double term = __dmul_rn(d_ds, (double)uv);
-  float dx = mask ? uv : __uint_as_float(__float_as_uint(uv) & 0x80000000u);  // finite up
-  if (__builtin_expect(!ok, 0)) {
-    const double2 r = slow_elem(xv, uv, dc.s, q);
-    term = r.x;
-    dx = (float)r.y;  // exact: r.y is a float widened
-  }
-  if (kDx) sx[k] = from_f<T>(dx);
-  return term;
+  FastTerm f = fast_elem(xv, uv, dc, q);
+  fix_slow(f, xv, uv, dc.s, q);
+  if (kDx) sx[k] = from_f<T>(f.dx);
+  return f.term;
 }
 
 // A leaf group's sum in the reference order: fold(left half) + fold(right
-// half) from 0.0 each (or one fold if <= 8 elements). The two folds are
-// independent chains, so they are interleaved for ILP.
+// half) from 0.0 each (or one fold if <= 8 elements). Generic sizes; the
+// two folds are independent chains, interleaved for ILP.
 template <typename T, bool kDx>
 __device__ __forceinline__ double group_sum(T* sx, const T* su, int glen, const DivCtx& dc,
                                             double q) {
@@ -263,6 +288,71 @@ __device__ __forceinline__ double group_sum(T* sx, const T* su, int glen, const 
   return __dadd_rn(acc_l, acc_r);
 }
 
+// Leaf groups of 2*LR-1 or 2*LR elements (right half LR, left half h = LR-1
+// or LR), fully unrolled: chunks of two fold steps (4 element slots, the
+// left slot of step LR-1 predicated on h == LR) computed branch-free with
+// one rare-path test per chunk. Every lane of a tile has the same LR for
+// the DPVO shapes (group sizes 9/10), so warps do not diverge.
+template <typename T, bool kDx, int LR>
+__device__ __forceinline__ double group_sum_lr(T* sx, const T* su, int h, const DivCtx& dc,
+                                               double q) {
+  T* rx = sx + h;
+  const T* ru = su + h;
+  const bool lv = h == LR;
+  double acc_l = 0.0, acc_r = 0.0;
+#pragma unroll
+  for (int k = 0; k < LR; k += 2) {
+    const bool two = k + 1 < LR;                 // compile time after unrolling
+    const bool l1 = two && (k + 1 < LR - 1 || lv);  // left slot k+1 valid
+    const bool l0 = k < LR - 1 || lv;               // left slot k valid
+    const float x0 = to_f<T>(sx[k]), u0 = to_f<T>(su[k]);
+    const float x2 = to_f<T>(rx[k]), u2 = to_f<T>(ru[k]);
+    const float x1 = two ? to_f<T>(sx[k + 1]) : 0.0f, u1 = two ? to_f<T>(su[k + 1]) : 0.0f;
+    const float x3 = two ? to_f<T>(rx[k + 1]) : 0.0f, u3 = two ? to_f<T>(ru[k + 1]) : 0.0f;
+    FastTerm f0 = fast_elem(x0, u0, dc, q);
+    FastTerm f1 = fast_elem(x1, u1, dc, q);
+    FastTerm f2 = fast_elem(x2, u2, dc, q);
+    FastTerm f3 = fast_elem(x3, u3, dc, q);
+    f0.ok = f0.ok || !l0;
+    f1.ok = f1.ok || !l1;
+    f3.ok = f3.ok || !two;
+    if (__builtin_expect(!(f0.ok && f1.ok && f2.ok && f3.ok), 0)) {
+      fix_slow(f0, x0, u0, dc.s, q);
+      fix_slow(f1, x1, u1, dc.s, q);
+      fix_slow(f2, x2, u2, dc.s, q);
+      fix_slow(f3, x3, u3, dc.s, q);
+    }
+    if (kDx) {
+      if (l0) sx[k] = from_f<T>(f0.dx);
+      if (l1) sx[k + 1] = from_f<T>(f1.dx);
+      rx[k] = from_f<T>(f2.dx);
+      if (two) rx[k + 1] = from_f<T>(f3.dx);
+    }
+    if (l0) acc_l = __dadd_rn(acc_l, f0.term);
+    if (l1) acc_l = __dadd_rn(acc_l, f1.term);
+    acc_r = __dadd_rn(acc_r, f2.term);
+    if (two) acc_r = __dadd_rn(acc_r, f3.term);
+  }
+  return __dadd_rn(acc_l, acc_r);
+}
+
+// Dispatch on the right-half length (groups of 9..16 elements, the only
+// sizes of rows with >= 16 * 2^g elements); other sizes take the generic loop.
+template <typename T, bool kDx>
+__device__ __forceinline__ double group_sum_any(T* sx, const T* su, int glen, const DivCtx& dc,
+                                                double q) {
+  if (glen >= 9) {
+    const int lr = (glen + 1) >> 1, h = glen >> 1;
+    switch (lr) {
+      case 5: return group_sum_lr<T, kDx, 5>(sx, su, h, dc, q);
+      case 6: return group_sum_lr<T, kDx, 6>(sx, su, h, dc, q);
+      case 7: return group_sum_lr<T, kDx, 7>(sx, su, h, dc, q);
+      default: return group_sum_lr<T, kDx, 8>(sx, su, h, dc, q);
+    }
+  }
+  return group_sum<T, kDx>(sx, su, glen, dc, q);
+}
+
 // ---------------------------------------------------------------------
 // Warp-specialized main pass. 8 consumer warps (256 lanes = 256 leaf
 // groups of a tile) + 1 producer warp. Per stage s of the 2-deep ring:
@@ -277,11 +367,30 @@ __device__ __forceinline__ double group_sum(T* sx, const T* su, int glen, const 
 constexpr int kConsumerWarps = kBwdThreads / 32;      // 8
 constexpr int kBwdCtaThreads = kBwdThreads + 32;     // + producer warp
 
-template <typename T>
-__device__ __forceinline__ void produce(const BwdBatch& bt, uint32_t tile_id, Stage<T>& st,
-                                        TileRef* ref, uint64_t* full, int lane) {
-  TileRef r;
-  if (lane == 0) r = locate_full<T>(bt, tile_id);
+__device__ __forceinline__ TileRef shfl_ref(const TileRef& r, int src) {
+  constexpr unsigned kAll = 0xffffffffu;
+  TileRef o;
+  o.di = __shfl_sync(kAll, r.di, src);
+  o.seg = __shfl_sync(kAll, r.seg, src);
+  o.t = __shfl_sync(kAll, r.t, src);
+  o.c = __shfl_sync(kAll, r.c, src);
+  o.A = __shfl_sync(kAll, (unsigned long long)r.A, src);
+  o.m = __shfl_sync(kAll, r.m, src);
+  o.off = __shfl_sync(kAll, r.off, src);
+  o.w0 = __shfl_sync(kAll, (unsigned long long)r.w0, src);
+  o.w1 = __shfl_sync(kAll, (unsigned long long)r.w1, src);
+  o.s = __shfl_sync(kAll, r.s, src);
+  o.y = __shfl_sync(kAll, r.y, src);
+  return o;
+}
+
+// Stage fill for tile r (r valid on lane 0, computed by locate_full ahead of
+// time so no global-memory latency sits between a stage's release and its
+// refill).
+template <typename T, int V = 0>
+__device__ __forceinline__ void produce(const BwdBatch& bt, const TileRef& r, Stage<T>& st,
+                                        TileRef* ref, uint64_t* full, int lane,
+                                        bool prologue_done = false) {
   // broadcast the fields the lanes need for a manual fill
   const int di = __shfl_sync(0xffffffffu, r.di, 0);
   const BwdDesc& d = bt.d[di];
@@ -295,7 +404,8 @@ __device__ __forceinline__ void produce(const BwdBatch& bt, uint32_t tile_id, St
         st.x[e - r.w0 / sizeof(T)] = static_cast<const T*>(d.x)[e];
         st.up[e - r.w0 / sizeof(T)] = static_cast<const T*>(d.up)[e];
       }
-      issue_tile<T>(d, r, st, full);  // arrive.expect_tx releases the stores above
+      if ((V & kProbeNoLoads) && prologue_done) mbar_arrive_expect_tx(full, 0);
+      else issue_tile<T>(d, r, st, full);  // arrive.expect_tx releases the stores above
     }
   } else {
     // unaligned buffers: the producer warp fills the stage itself
@@ -314,12 +424,42 @@ __device__ __forceinline__ void produce(const BwdBatch& bt, uint32_t tile_id, St
   }
 }
 
+// d_input of one consumer warp, written by the warp itself right after it
+// computed it into the stage: the warp's 32 leaf groups are one contiguous
+// element range of the tile, stored with 16-byte coalesced vectors (ragged
+// ends scalar). No bulk store, so the stage is free for its refill as soon
+// as the consumers arrive on done.
 template <typename T>
-__device__ __forceinline__ void finalize(const BwdBatch& bt, const TileRef& cur, Stage<T>& st,
-                                         const double* red, int lane) {
-  const BwdDesc& d = bt.d[cur.di];
-  // perfect tree over the tile's 2^g group sums: each lane folds `per`
-  // consecutive sums as a perfect subtree, then an xor butterfly
+__device__ __forceinline__ void warp_store_dx(const BwdDesc& d, const TileRef& cur, const T* stx,
+                                              int glo, int glen, int lane) {
+  if (__shfl_sync(0xffffffffu, glen, 0) == 0) return;  // no groups in this warp
+  const int lo = __shfl_sync(0xffffffffu, glo, 0);
+  const int hi = (int)__reduce_max_sync(0xffffffffu, (unsigned)(glen ? glo + glen : 0));
+  T* dst = static_cast<T*>(d.dx) + cur.A;
+  const T* src = stx + cur.off;
+  constexpr int kV = 16 / sizeof(T);
+  if (!d.vec) {
+    for (int e = lo + lane; e < hi; e += 32) dst[e] = src[e];
+    return;
+  }
+  // global byte address of element e: (A + e) * sizeof(T); the stage keeps
+  // the same alignment mod 16 (bulk copies start at a 16-byte window)
+  const uint32_t mis = (uint32_t)(((cur.A + (uint64_t)lo) * sizeof(T)) & 15u);
+  int e0 = lo + (int)(((16u - mis) & 15u) / sizeof(T));
+  if (e0 > hi) e0 = hi;
+  const int nvec = (hi - e0) / kV;
+  const int e1 = e0 + nvec * kV;
+  if (lane < e0 - lo) dst[lo + lane] = src[lo + lane];
+  if (lane < hi - e1) dst[e1 + lane] = src[e1 + lane];
+  const uint4* vs = reinterpret_cast<const uint4*>(src + e0);
+  uint4* vd = reinterpret_cast<uint4*>(dst + e0);
+  for (int u = lane; u < nvec; u += 32) vd[u] = vs[u];
+}
+
+// Perfect tree over the tile's 2^g group sums, lane part: each lane folds
+// `per` consecutive sums as a perfect subtree (read into registers before
+// the stage is refilled); tile_sum() finishes with an xor butterfly.
+__device__ __forceinline__ double lane_subtree(const BwdDesc& d, const double* red, int lane) {
   const int groups = 1 << d.g;
   const int per = groups >= 32 ? groups >> 5 : 1;
   const int lanes_used = groups >= 32 ? 32 : groups;
@@ -335,10 +475,22 @@ __device__ __forceinline__ void finalize(const BwdBatch& bt, const TileRef& cur,
                       __dadd_rn(__dadd_rn(g[4], g[5]), __dadd_rn(g[6], g[7])));
     }
   }
+  return r;
+}
+
+__device__ __forceinline__ void tile_sum(const BwdDesc& d, const TileRef& cur, double r) {
+  const int groups = 1 << d.g;
+  const int lanes_used = groups >= 32 ? 32 : groups;
   for (int o = 1; o < lanes_used; o <<= 1) r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, o));
-  if (lane == 0) d.partials[((uint64_t)cur.seg << d.tps_log) + cur.t] = r;
+  if ((threadIdx.x & 31) == 0) d.partials[((uint64_t)cur.seg << d.tps_log) + cur.t] = r;
+}
+
+// d_input of a finished tile: ragged ends by lanes, the aligned interior as
+// one TMA bulk store out of the stage.
+template <typename T>
+__device__ __forceinline__ void store_dx(const BwdDesc& d, const TileRef& cur, Stage<T>& st,
+                                         int lane) {
   if (d.dx == nullptr) return;
-  // d_input: ragged ends by lanes, aligned interior as one bulk store
   const uint64_t b0 = cur.A * sizeof(T), b1 = (cur.A + (uint64_t)cur.m) * sizeof(T);
   const uint64_t i0 = (b0 + 15) & ~uint64_t(15), i1 = b1 & ~uint64_t(15);
   const int head = (int)(((i0 > b1 ? b1 : i0) - b0) / sizeof(T));
@@ -353,15 +505,17 @@ __device__ __forceinline__ void finalize(const BwdBatch& bt, const TileRef& cur,
   }
 }
 
-template <typename T>
+template <typename T, int V>
 __global__ void __launch_bounds__(kBwdCtaThreads, 3) bwd_kernel(const __grid_constant__ BwdBatch bt) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[kMaxStages];
   __shared__ __align__(8) uint64_t done[kMaxStages];
   __shared__ TileRef refs[kMaxStages];
-  __shared__ double red[kMaxStages][kBwdThreads];  // per-group sums of a tile
   const int nst = bt.nstages;
   const uint32_t se = bt.stage_elems;
+  // per-stage group sums of a tile, after the ring
+  double(*red)[kBwdThreads] = reinterpret_cast<double(*)[kBwdThreads]>(
+      smem_raw + (size_t)nst * 2 * se * sizeof(T));
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   const int lane = tid & 31;
@@ -379,24 +533,49 @@ __global__ void __launch_bounds__(kBwdCtaThreads, 3) bwd_kernel(const __grid_con
 
   if (warp == kConsumerWarps) {
     // ----------------------------- producer warp -----------------------
+    // TileRefs are located 32 at a time (lane i: the CTA's tile ordinal
+    // 32*b + i) and broadcast when needed, so the scale load in locate_full
+    // costs one memory latency per 32 tiles instead of one per tile.
+    TileRef mine;
+    uint32_t batch = 0xffffffffu;
+    auto ref_of = [&](uint32_t k) -> TileRef {
+      const uint32_t b = k >> 5;
+      if (b != batch) {
+        batch = b;
+        const uint32_t id = blockIdx.x + ((b << 5) + (uint32_t)lane) * gridDim.x;
+        if (id < total) mine = locate_full<T>(bt, id);
+      }
+      return shfl_ref(mine, (int)(k & 31u));
+    };
     uint32_t j_id = blockIdx.x;
     for (int s = 0; s < nst; ++s) {
       const uint32_t id = blockIdx.x + (uint32_t)s * gridDim.x;
       Stage<T> st = stage_at<T>(smem_raw, se, s);
-      if (id < total) produce<T>(bt, id, st, &refs[s], &full[s], lane);
+      if (id < total) {
+        const TileRef r = ref_of((uint32_t)s);
+        produce<T, V>(bt, r, st, &refs[s], &full[s], lane);
+      }
     }
     uint32_t done_phase = 0;
     int s = 0;
-    for (; j_id < total; j_id += gridDim.x) {
+    for (uint32_t k = 0; j_id < total; j_id += gridDim.x, ++k) {
+      // locate the refill tile while the consumers still work on this one
+      const uint32_t nid = j_id + (uint32_t)nst * gridDim.x;
+      TileRef nr;
+      if (nid < total) nr = ref_of(k + (uint32_t)nst);
       mbar_wait(&done[s], (done_phase >> s) & 1u);
       done_phase ^= 1u << s;
       Stage<T> st = stage_at<T>(smem_raw, se, s);
       const TileRef cur = refs[s];
-      finalize<T>(bt, cur, st, red[s], lane);
-      if (lane == 0) bulk_wait_read_all();  // the store has read the stage
+      const BwdDesc& d = bt.d[cur.di];
+      const double part = lane_subtree(d, red[s], lane);
+      if constexpr ((V & kProbeNoLoads) == 0) {
+        store_dx<T>(d, cur, st, lane);
+        if (lane == 0) bulk_wait_read_all();  // the store has read the stage
+      }
       __syncwarp();
-      const uint32_t nid = j_id + (uint32_t)nst * gridDim.x;
-      if (nid < total) produce<T>(bt, nid, st, &refs[s], &full[s], lane);
+      if (nid < total) produce<T, V>(bt, nr, st, &refs[s], &full[s], lane, true);
+      tile_sum(d, cur, part);
       s = s + 1 == nst ? 0 : s + 1;
     }
     if (lane == 0) bulk_wait_all();
@@ -423,8 +602,9 @@ __global__ void __launch_bounds__(kBwdCtaThreads, 3) bwd_kernel(const __grid_con
     const double q = pin(d.q);
     T* sx = st.x + cur.off + glo;
     const T* su = st.up + cur.off + glo;
-    double v = d.dx != nullptr ? group_sum<T, true>(sx, su, glen, dc, q)
-                               : group_sum<T, false>(sx, su, glen, dc, q);
+    double v = (V & kProbeNoCompute) ? 0.0
+             : (d.dx != nullptr && !(V & kProbeNoLoads)) ? group_sum_any<T, true>(sx, su, glen, dc, q)
+                                                          : group_sum_any<T, false>(sx, su, glen, dc, q);
     red[s][tid] = v;  // the producer runs the tile's tree reduction
     __syncwarp();     // the warp's d_input and group sums are written
     if (lane == 0) mbar_arrive(&done[s]);
@@ -489,38 +669,78 @@ __global__ void __launch_bounds__(32) bwd_finish_kernel(const __grid_constant__ 
 
 }  // namespace
 
+// Ring budget per CTA (bytes) and stage cap; QFB_BWD_RING_KB /
+// QFB_BWD_STAGES override them for tuning sweeps.
+static size_t ring_budget() {
+  static const size_t b = [] {
+    const char* e = getenv("QFB_BWD_RING_KB");
+    const long kb = e ? atol(e) : 0;
+    return kb > 0 ? (size_t)kb * 1024 : kRingBudget;
+  }();
+  return b;
+}
+static int stage_cap() {
+  static const int c = [] {
+    const char* e = getenv("QFB_BWD_STAGES");
+    const int v = e ? atoi(e) : 0;
+    return v >= 2 && v <= kMaxStages ? v : kMaxStages;
+  }();
+  return c;
+}
+
 void bwd_ring_size(int dtype, uint32_t max_tile, uint32_t* stage_elems, int32_t* nstages,
                    size_t* smem_bytes) {
   const size_t es = dtype == 0 ? 4 : 2;
   uint32_t se = max_tile + kWinPad;
   se = (se + 7u) & ~7u;  // 16-byte multiple for both element sizes
   const size_t stage = 2 * (size_t)se * es;
-  int ns = (int)(kRingBudget / stage);
-  if (ns > kMaxStages) ns = kMaxStages;
+  int ns = (int)(ring_budget() / (stage + kRedBytes));
+  if (ns > stage_cap()) ns = stage_cap();
   if (ns < 2) ns = 2;
   *stage_elems = se;
   *nstages = ns;
-  *smem_bytes = stage * (size_t)ns;
+  *smem_bytes = (stage + kRedBytes) * (size_t)ns;
 }
 
 namespace {
 
+// Kernel variant: 0 = production; the probes (QFB_BWD_VARIANT=8 / 16)
+// isolate the memory pipeline and the arithmetic for roofline analysis.
+static int variant() {
+  static const int v = [] {
+    const char* e = getenv("QFB_BWD_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 template <typename T>
-cudaError_t set_smem() {
-  return cudaFuncSetAttribute(bwd_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)(kRingMax > kRingBudget ? kRingMax : kRingBudget));
+const void* kernel_ptr(int v) {
+  switch (v) {
+    case kProbeNoCompute: return (const void*)bwd_kernel<T, kProbeNoCompute>;
+    case kProbeNoLoads: return (const void*)bwd_kernel<T, kProbeNoLoads>;
+    default: return (const void*)bwd_kernel<T, 0>;
+  }
+}
+
+const void* bwd_fn(int dtype) {
+  return dtype == 0 ? kernel_ptr<float>(variant()) : kernel_ptr<__half>(variant());
 }
 
 }  // namespace
 
 cudaError_t bwd_occupancy(int dtype, int* blocks_per_sm) {
-  return bwd_occupancy_smem(dtype, kRingBudget, blocks_per_sm);
+  uint32_t se;
+  int32_t ns;
+  size_t smem;
+  bwd_ring_size(dtype, kBwdTileMax, &se, &ns, &smem);
+  return bwd_occupancy_smem(dtype, smem, blocks_per_sm);
 }
 
 cudaError_t bwd_occupancy_smem(int dtype, size_t smem, int* blocks_per_sm) {
-  cudaError_t e = dtype == 0 ? set_smem<float>() : set_smem<__half>();
+  const void* f = bwd_fn(dtype);
+  cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
   if (e != cudaSuccess) return e;
-  const void* f = dtype == 0 ? (const void*)bwd_kernel<float> : (const void*)bwd_kernel<__half>;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, kBwdCtaThreads, smem);
 }
 
@@ -528,12 +748,9 @@ cudaError_t launch_bwd(int dtype, const BwdBatch& b, int grid, cudaStream_t st) 
   const uint32_t tiles = b.tile_begin[b.n];
   if (tiles == 0) return cudaSuccess;
   if ((uint32_t)grid > tiles) grid = (int)tiles;
-  const size_t smem = (size_t)b.nstages * 2 * b.stage_elems * (dtype == 0 ? 4 : 2);
-  if (dtype == 0)
-    bwd_kernel<float><<<grid, kBwdCtaThreads, smem, st>>>(b);
-  else
-    bwd_kernel<__half><<<grid, kBwdCtaThreads, smem, st>>>(b);
-  cudaError_t e = cudaGetLastError();
+  const size_t smem = (size_t)b.nstages * (2 * b.stage_elems * (dtype == 0 ? 4 : 2) + kRedBytes);
+  void* args[] = {const_cast<BwdBatch*>(&b)};
+  cudaError_t e = cudaLaunchKernel(bwd_fn(dtype), dim3(grid), dim3(kBwdCtaThreads), args, smem, st);
   if (e != cudaSuccess) return e;
   uint32_t warps = 0;
   for (int i = 0; i < b.n; ++i) warps += b.d[i].chans;

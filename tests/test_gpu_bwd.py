@@ -29,8 +29,8 @@ def check_grads(got, want, tol):
     assert got.tobytes() == want.tobytes()   # bit-exact (stronger than tol)
 
 
-LENGTHS = [1, 2, 7, 8, 9, 15, 16, 17, 31, 33, 100, 255, 256, 257, 1000, 4095, 4096, 4097,
-           4099, 8193, 12288, 65537, 76800]
+LENGTHS = [1, 2, 7, 8, 9, 15, 16, 17, 31, 33, 100, 255, 256, 257, 1000, 2816, 3328, 3584, 4095,
+           4096, 4097, 4099, 8193, 12288, 65537, 76800]   # leaf groups of every size 1..16
 
 
 @pytest.mark.parametrize("n", LENGTHS)
@@ -228,3 +228,28 @@ def test_special_values_bitwise(qfb, orc, cuda):
         _, dx, dls = orc.fq_backward(x, up2, [ls], 1, 1, x.size)
         assert np.array_equal(bits32(host(g.d_input)), bits32(dx)), s
         check_grads(g.d_log_scale, dls, TOL_F32)
+
+
+@pytest.mark.parametrize("half", [0, 1])
+def test_relu_activations_bitwise(qfb, orc, cuda, half):
+    """Post-ReLU conv inputs (about half the elements +-0, the zeros taking
+    the exact fast path) at a DPVO layer-2 shape, per channel, f32 and f16
+    storage: d_input and d_log_s bitwise."""
+    import torch
+    rng = np.random.default_rng(11 + half)
+    C, H, W = 64, 120, 160
+    x = np.maximum(rng.normal(0, 1, (C, H, W)), 0).astype(np.float32)
+    x[:, ::7, :] = -0.0
+    up = rng.normal(0, 1, (C, H, W)).astype(np.float32)
+    if half:
+        x = x.astype(np.float16).astype(np.float32)
+        up = up.astype(np.float16).astype(np.float32)
+    ls = rng.uniform(-6, -2, C)
+    dt = torch.float16 if half else torch.float32
+    xd = torch.from_numpy(x).to(cuda).to(dt)
+    ud = torch.from_numpy(up).to(cuda).to(dt)
+    g = qfb.fake_quantize_backward(xd, ls.tolist(), None, ud)
+    _, dx, dls = orc.fq_backward(x, up, ls, 1, C, H * W)
+    got = host(g.d_input.float()).ravel()
+    assert np.array_equal(bits32(got), bits32(dx))
+    check_grads(g.d_log_scale, dls, TOL_F16 if half else TOL_F32)
