@@ -50,6 +50,8 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-graph", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0)
+    p.add_argument("--no-secondary", action="store_true",
+                   help="skip the config-3 chain window and config-5 forward-throughput lines")
     return p.parse_args()
 
 
@@ -148,11 +150,13 @@ class RefCpuWorkload:
     A bounded sample (a fixed subset of blocks, sized to `budget_s`) is
     timed and converted to frames/s = frames-worth of elements / seconds."""
 
-    def __init__(self, consumers, threads, dtype="f32", seed=7):
+    def __init__(self, consumers, threads, dtype="f32", seed=7, do_bwd=True):
         import numpy as np
         import oracle
         self.ref = oracle.Reference()
         self.threads = threads
+        self.do_bwd = 1 if do_bwd else 0
+        self.reps = 1
         self.half = 1 if dtype == "f16" else 0
         rng = np.random.default_rng(seed)
         self.items = []
@@ -173,19 +177,27 @@ class RefCpuWorkload:
         self.order = order
         self.sel = order
 
-    def _run(self, idx):
+    def _run(self, idx, reps=1):
         sel = [self.items[i] for i in idx]
         st, secs, _ = self.ref.bench_points([s[0] for s in sel], [s[1] for s in sel],
                                             [s[2] for s in sel], [s[3] for s in sel],
                                             [s[4] for s in sel], half=self.half,
-                                            threads=self.threads, reps=1)
+                                            do_bwd=self.do_bwd, threads=self.threads, reps=reps)
         assert st == 0, f"reference bench failed: {st}"
-        return secs, sum(s[2] * s[3] for s in sel)
+        return secs, reps * sum(s[2] * s[3] for s in sel)
 
     def size(self, budget_s):
+        """Pick the sample: a subset of one frame's blocks when a frame takes
+        longer than the budget, else whole frames repeated (reps) to fill it."""
         probe = self.order[:max(2 * self.threads, 8)]
         secs, elems = self._run(probe)
         want = elems / max(secs, 1e-9) * budget_s
+        self.reps = 1
+        if want >= self.frame_elems:
+            self.sel = self.order
+            secs, elems = self._run(self.sel)          # one full frame, warm
+            self.reps = max(1, int(round(budget_s / max(secs, 1e-9))))
+            return self
         acc, k = 0, 0
         while k < len(self.order) and acc < want:
             it = self.items[self.order[k]]
@@ -195,20 +207,21 @@ class RefCpuWorkload:
         return self
 
     def run(self):
-        secs, elems = self._run(self.sel)
+        secs, elems = self._run(self.sel, self.reps)
         return secs, elems / self.frame_elems
 
     def describe(self, secs, frames):
+        ops = "fake_quantize + fake_quantize_backward" if self.do_bwd else "fake_quantize"
         return (f"{frames:.3f} frames-worth of quant-point elements ({len(self.sel)} of "
-                f"{len(self.items)} 4-channel blocks) in {secs:.2f} s on {self.threads} threads; "
-                f"reference quant.hpp fake_quantize + fake_quantize_backward, -O3 from its sources")
+                f"{len(self.items)} 4-channel blocks x {self.reps} reps) in {secs:.2f} s on "
+                f"{self.threads} threads; reference quant.hpp {ops}, -O3 from its sources")
 
 
-def cpu_reference_frames_per_s(consumers, budget_s, threads, dtype="f32"):
+def cpu_reference_frames_per_s(consumers, budget_s, threads, dtype="f32", do_bwd=True):
     import oracle
     if not oracle.reference_available():
         return None
-    w = RefCpuWorkload(consumers, threads, dtype).size(budget_s)
+    w = RefCpuWorkload(consumers, threads, dtype, do_bwd=do_bwd).size(budget_s)
     secs, frames = w.run()
     return {"value": frames / secs, "unit": UNIT, "cores": threads, "kind": "reference",
             "sample": w.describe(secs, frames)}
@@ -399,6 +412,10 @@ def run_qfb(args):
     if not args.no_e2e:
         e2e = run_e2e(args, q, ctx, fp, stream, dev, pg, ws)
 
+    secondary = None
+    if not args.no_secondary:
+        secondary = run_secondary(args, ctx, stream, dev, peak, rank, ws)
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         cons = [(p, c) for p in fp.points for c in p.consumers]
@@ -424,7 +441,7 @@ def run_qfb(args):
                 "gbps": gbps, "hbm_frac": (gbps / ws) / peak,
                 "kernel_ms": {"fwd": fwd_ms, "bwd": bwd_ms},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": launches, "clocks": clocks,
+                "gpu_launches": launches, "clocks": clocks, "secondary": secondary,
                 "timing": ("value: CUDA-graph replay of the step (fwd + bwd + finisher launches) "
                            "between CUDA events on the library stream" if use_graph else
                            "value: eager launches between CUDA events on the library stream") +
@@ -436,6 +453,70 @@ def run_qfb(args):
         pg.destroy_process_group()
     ctx.close()
     return 0
+
+
+def time_device(fn, stream, reps, warmup=2):
+    """ms per call of fn() on `stream` (CUDA events, synchronized)."""
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(reps):
+        fn()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    return t0.elapsed_time(t1) / reps
+
+
+def run_secondary(args, ctx, stream, dev, peak, rank, ws):
+    """BASELINE configs 3 and 5 on this GPU (reported beside the headline):
+    c3 = fused quant->act->quant chains over every quant point of a 15-frame
+    window + its patch/update-operator inputs (ReLU and GELU variants);
+    c5 = the fused multi-point forward alone (inference front-end), 8 frames
+    per launch, frames/s, with the reference's forward timed on the host."""
+    import torch
+    from paper_2511_12653_b200.frontend import FrontendQuantPass, WindowChainPass
+    out = {}
+    for gelu in (False, True):
+        wp = WindowChainPass(ctx, frames=15, patches=96, gelu=gelu, dtype=args.dtype, device=dev)
+        ms = time_device(wp.run, stream, reps=10)
+        gb = wp.bytes_per_run() / (ms / 1e3) / 1e9
+        out["c3_chain_window_" + ("gelu" if gelu else "relu")] = {
+            "ms_per_window": ms, "gbps": gb, "hbm_frac": gb / peak,
+            "bytes_per_window": wp.bytes_per_run(), "quant_points": len(wp.points),
+            "launches_per_window": 1,
+            "workload": "15-frame window: 22 encoder quant points x 15 frames + gmap/imap (96 patches x "
+                        "15) + corr/net/inp (21,600 edges), relu(a [+ b]) or gelu -> K fake-quant outputs"}
+        del wp
+        torch.cuda.empty_cache()
+    fp = FrontendQuantPass(ctx, frames=8, dtype=args.dtype, sets=2, seed=11 + rank, device=dev)
+    k = [0]
+
+    def fwd():
+        fp.forward(k[0] % 2)
+        k[0] += 1
+    ms = time_device(fwd, stream, reps=50)
+    fps = fp.frames / (ms / 1e3)
+    gb = fp.bytes_per_step()["fwd"] / (ms / 1e3) / 1e9
+    c5 = {"value": ws * fps, "unit": "frames/s", "per_gpu_frames_per_s": fps, "gbps": gb,
+          "hbm_frac": gb / peak, "frames_per_launch": fp.frames,
+          "seconds_for_32x1000_frames": 32000.0 / (ws * fps),
+          "workload": "BASELINE config 5: fused multi-point fake-quant forward of the 22 DPVO "
+                      "activation quant points (inference front-end), 8 frames per launch"}
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        cons = [(p, c) for p in fp.points for c in p.consumers]
+        try:
+            c5["cpu_baseline"] = cpu_reference_frames_per_s(cons, 5.0, host_threads(), args.dtype,
+                                                            do_bwd=False)
+        except Exception as exc:  # pragma: no cover
+            c5["cpu_baseline"] = {"value": None, "sample": f"failed: {exc}"}
+    out["c5_forward_throughput"] = c5
+    del fp
+    torch.cuda.empty_cache()
+    return out
 
 
 def run_e2e(args, q, ctx, fp, stream, dev, pg, ws):

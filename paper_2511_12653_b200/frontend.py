@@ -24,7 +24,8 @@ from typing import List
 
 import numpy as np
 
-from . import (CBwdDesc, CFqDesc, F16, F32, Context, check, lib, scale_grad_factors)
+from . import (ACT_GELU, ACT_NONE, ACT_RELU, CBwdDesc, CChainDesc, CFqDesc, F16, F32, Context, check,
+               lib, scale_grad_factors)
 
 H, W = 480, 640
 
@@ -164,3 +165,109 @@ class FrontendQuantPass:
     def bytes_per_step(self) -> dict:
         b = frame_bytes(self.points, self.esize)
         return {k: v * self.frames for k, v in b.items()}
+
+
+# ------------------------------------------------------------------------
+# BASELINE config 3: fused quant -> act -> quant chains over a sliding
+# window (exec.hpp:431-451 residual joins maybe_half(relu(add(a, b))) and
+# multi-consumer points).
+# ------------------------------------------------------------------------
+
+@dataclass
+class ChainPoint:
+    name: str
+    outer: int
+    channels: int
+    inner: int
+    consumers: int     # K fake-quant outputs from one read
+    act: int           # ACT_NONE / ACT_RELU / ACT_GELU (GELU variant)
+    residual: bool     # a + b join before the activation
+
+    @property
+    def numel(self) -> int:
+        return self.outer * self.channels * self.inner
+
+
+# Encoder points whose input is a residual join relu(x + y) (BasicEncoder4:
+# the outputs of layer1.0, layer1.1, layer2.0, layer2.1).
+_RESIDUAL = ("layer1.1.conv1.in", "layer2.0.in", "layer2.1.conv1.in", "conv2.in")
+
+
+def window_chain_points(frames: int = 15, patches: int = 96, gelu: bool = False,
+                        h: int = H, w: int = W) -> List[ChainPoint]:
+    """Every activation quant point of a `frames`-frame window: the 19
+    per-frame encoder tensors (outer = frames, per-channel scales) and the
+    patch / update-operator inputs of the window (gmap, imap, and
+    per-edge corr / net / inp for E = patches * frames * frames edges,
+    per-tensor scales)."""
+    act = ACT_GELU if gelu else ACT_RELU
+    pts = []
+    for p in dpvo_quant_points(h, w):
+        first = p.name == "image"
+        res = any(p.name.endswith(r) for r in _RESIDUAL)
+        pts.append(ChainPoint(p.name, frames, p.channels, p.inner, len(p.consumers),
+                              ACT_NONE if first else act, res))
+    n_patch = patches * frames
+    edges = patches * frames * frames
+    # per-tensor scales: one [1, 1, n] row (same arithmetic, 16-byte units)
+    pts += [ChainPoint("patch.gmap", 1, 1, n_patch * 128 * 9, 1, ACT_NONE, False),
+            ChainPoint("patch.imap", 1, 1, n_patch * 384, 1, ACT_NONE, False),
+            ChainPoint("update.corr", 1, 1, edges * 2 * 49 * 9, 1, ACT_NONE, False),
+            ChainPoint("update.net", 1, 1, edges * 384, 1, act, True),
+            ChainPoint("update.inp", 1, 1, edges * 384, 1, act, False)]
+    return pts
+
+
+class WindowChainPass:
+    """Device buffers + one qfb_fq_chain_multi table for a window of chain
+    points: per point a (the producing op's output), b (the skip tensor of a
+    residual join), K fake-quant outputs."""
+
+    def __init__(self, ctx: Context, frames: int = 15, patches: int = 96, gelu: bool = False,
+                 dtype: str = "f32", seed: int = 3, device=None, h: int = H, w: int = W):
+        import torch
+        self.ctx = ctx
+        self.points = window_chain_points(frames, patches, gelu, h, w)
+        self.frames = frames
+        self.dtype_code = F32 if dtype == "f32" else F16
+        tdt = torch.float32 if dtype == "f32" else torch.float16
+        self.esize = 4 if dtype == "f32" else 2
+        dev = device if device is not None else torch.device("cuda", ctx.device)
+        rng = np.random.default_rng(seed)
+        L = lib()
+        self.keep = []
+        descs = []
+        for pi, p in enumerate(self.points):
+            a = torch.empty(p.numel, dtype=tdt, device=dev)
+            check(L.qfb_fill_rng(ctx.handle, self.dtype_code, a.data_ptr(), a.numel(), seed, 2 * pi, 0,
+                                 1, 1.0, 0.0))
+            b = None
+            if p.residual:
+                b = torch.empty(p.numel, dtype=tdt, device=dev)
+                check(L.qfb_fill_rng(ctx.handle, self.dtype_code, b.data_ptr(), b.numel(), seed,
+                                     2 * pi + 1, 0, 1, 1.0, 0.0))
+            d = CChainDesc()
+            d.a = a.data_ptr()
+            d.b = b.data_ptr() if b is not None else 0
+            d.preact = 0
+            d.outer, d.channels, d.inner = p.outer, p.channels, p.inner
+            d.n_out, d.act, d.dtype, d.q_max, d.flags = p.consumers, p.act, self.dtype_code, 127, 0
+            for k in range(p.consumers):
+                s = np.exp(rng.uniform(np.log(1e-3), np.log(0.1), p.channels)).astype(np.float32)
+                st = torch.from_numpy(s).to(dev)
+                y = torch.empty(p.numel, dtype=tdt, device=dev)
+                d.y[k], d.scale[k] = y.data_ptr(), st.data_ptr()
+                self.keep += [st, y]
+            self.keep += [a] + ([b] if b is not None else [])
+            descs.append(d)
+        self.table = (CChainDesc * len(descs))(*descs)
+        self.n = len(descs)
+        ctx.sync()
+
+    def run(self) -> None:
+        check(lib().qfb_fq_chain_multi(self.ctx.handle, self.table, self.n))
+
+    def bytes_per_run(self) -> int:
+        """Algorithmic bytes: read a (+ b), write K outputs."""
+        return sum(p.numel * (1 + (1 if p.residual else 0) + p.consumers) * self.esize
+                   for p in self.points)
