@@ -71,7 +71,8 @@ struct qfb_ctx {
   int sm_count = 148;
   int ew_blocks_per_sm[2][2] = {{4, 4}, {4, 4}};  // [dtype][chain]
   int bwd_blocks_per_sm[2] = {4, 4};
-  int tma_blocks_per_sm[2] = {0, 0};  // 0: TMA forward unavailable
+  int tma_blocks_per_sm[2][2][kTmaStagesMax + 1] = {};  // [dtype][chain][stages]; 0: unavailable
+  int tma_stages_env = 0;  // QFB_FWD_STAGES: fixed ring depth (tuning sweeps)
   std::vector<std::pair<size_t, int>> bwd_occ[2];  // (smem, blocks/SM) cache
   uint32_t* d_status = nullptr;
   uint32_t* h_status = nullptr;  // pinned
@@ -207,6 +208,20 @@ qfb_status plan_ew(int dtype, const EwJob& j, std::vector<EwDesc>& out) {
   return QFB_OK;
 }
 
+// TMA ring depth for one launch (measured on B200). Bytes in
+// flight per SM with 16 KB chunks: 2 stages x 5 CTAs -> 80 KB, 3 x 4 ->
+// 128 KB, 4 x 3 -> 144 KB. Deeper rings fill and drain slower and leave a
+// longer one-chunk tail, so short launches (one frame) take 3 stages and
+// long ones (>= 64 chunks per CTA, e.g. 8 frames) 4. Chains stage two
+// arrays per chunk and keep 2 stages; f16 is element-rate bound and wants
+// the most CTAs (2 stages).
+int tma_stages(const qfb_ctx* ctx, int dtype, bool chain, uint64_t chunks) {
+  if (ctx->tma_stages_env) return ctx->tma_stages_env;
+  if (chain || dtype != 0) return 2;
+  const uint64_t ctas4 = (uint64_t)ctx->sm_count * (uint64_t)std::max(1, ctx->tma_blocks_per_sm[dtype][0][4]);
+  return chunks >= 64 * ctas4 ? 4 : 3;
+}
+
 qfb_status run_ew(qfb_ctx* ctx, int dtype, const std::vector<EwDesc>& descs, bool chain) {
   size_t i = 0;
   while (i < descs.size()) {
@@ -222,12 +237,14 @@ qfb_status run_ew(qfb_ctx* ctx, int dtype, const std::vector<EwDesc>& descs, boo
     b.n = n;
     b.chunk_begin[n] = chunks;
     if (chunks == 0) continue;
-    bool all_vec = !chain && ctx->tma_blocks_per_sm[dtype] > 0;
+    const int stages = tma_stages(ctx, dtype, chain, chunks);
+    const int tma_per_sm = ctx->tma_blocks_per_sm[dtype][chain ? 1 : 0][stages];
+    bool all_vec = tma_per_sm > 0;
     for (int k = 0; k < n && all_vec; ++k) all_vec = b.d[k].vec > 1;
     cudaError_t e;
     if (all_vec) {
-      const int grid = (int)std::min<uint64_t>(chunks, (uint64_t)ctx->sm_count * ctx->tma_blocks_per_sm[dtype]);
-      e = launch_ew_tma(dtype, b, ctx->d_status, grid, ctx->stream);
+      const int grid = (int)std::min<uint64_t>(chunks, (uint64_t)ctx->sm_count * tma_per_sm);
+      e = launch_ew_tma(dtype, chain, stages, b, ctx->d_status, grid, ctx->stream);
     } else {
       const int grid = (int)std::min<uint64_t>(
           chunks, (uint64_t)ctx->sm_count * ctx->ew_blocks_per_sm[dtype][chain ? 1 : 0]);
@@ -381,11 +398,19 @@ qfb_status qfb_ctx_create(int32_t device, void* stream, qfb_ctx** out) {
     for (int dt = 0; dt < 2; ++dt) {
       int per = 0;
       if (bwd_occupancy(dt, &per) == cudaSuccess && per > 0) c->bwd_blocks_per_sm[dt] = per;
-      per = 0;
-      if (ew_tma_occupancy(dt, &per) == cudaSuccess && per > 0) c->tma_blocks_per_sm[dt] = per;
+      for (int ch = 0; ch < 2; ++ch)
+        for (int ns = kTmaStagesMin; ns <= kTmaStagesMax; ++ns) {
+          per = 0;
+          if (ew_tma_occupancy(dt, ch != 0, ns, &per) == cudaSuccess && per > 0)
+            c->tma_blocks_per_sm[dt][ch][ns] = per;
+        }
     }
     if (const char* env = getenv("QFB_DISABLE_TMA_FWD"))
-      if (env[0] == '1') c->tma_blocks_per_sm[0] = c->tma_blocks_per_sm[1] = 0;
+      if (env[0] == '1') std::memset(c->tma_blocks_per_sm, 0, sizeof c->tma_blocks_per_sm);
+    if (const char* env = getenv("QFB_FWD_STAGES")) {
+      const int v = atoi(env);
+      if (v >= kTmaStagesMin && v <= kTmaStagesMax) c->tma_stages_env = v;
+    }
   }
   if (e == cudaSuccess) e = cudaMalloc(&c->d_status, sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMallocHost(&c->h_status, sizeof(uint32_t));

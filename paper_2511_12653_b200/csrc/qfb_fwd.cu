@@ -9,6 +9,7 @@
 // (SM count x resident CTAs) persistent CTAs striding over 1024-unit chunks.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
+#include <stdlib.h>
 
 #include "../../include/qfb_portable.h"
 #include "qfb_device.cuh"
@@ -161,7 +162,6 @@ __global__ void __launch_bounds__(kEwThreads, kChain ? 3 : 4) ew_kernel(const __
 // chunks ahead, so the bytes in flight no longer depend on registers or
 // occupancy; threads read conflict-free 16-byte vectors from smem and write
 // outputs with 16-byte stores.
-constexpr int kFwdStages = 2;
 constexpr int kFwdChunkBytes = kEwChunk * 16;  // 16 KB
 
 struct ChunkRef {
@@ -185,25 +185,34 @@ __device__ __forceinline__ ChunkRef locate_chunk(const EwBatch& bt, uint32_t chu
   return r;
 }
 
-template <typename T>
-__global__ void __launch_bounds__(kEwThreads, 5)
+// kChain: quant -> act -> quant chains (a [+ b] staged, K outputs, optional
+// demotion / pre-activation output); 2 arrays per stage, 3 CTAs per SM.
+template <typename T, bool kChain, int kFwdStages>
+__global__ void __launch_bounds__(kEwThreads, (kChain ? 6 : 10) / kFwdStages)
     ew_tma_kernel(const __grid_constant__ EwBatch bt, uint32_t* __restrict__ status) {
   constexpr int V = Elem<T>::kPerVec;
+  constexpr int kArrays = kChain ? 2 : 1;  // a [, b] per stage
   extern __shared__ __align__(128) unsigned char fsmem[];
   uint4* ring = reinterpret_cast<uint4*>(fsmem);
   __shared__ __align__(8) uint64_t bars[kFwdStages];
   __shared__ ChunkRef refs[kFwdStages];
   const int tid = threadIdx.x;
+
   const uint32_t total = bt.chunk_begin[bt.n];
   if (blockIdx.x >= total) return;
 
+  // chunks go round robin over the CTAs (consecutive chunks in flight
+  // across the grid at any time: a compact, channel-interleaved window)
   auto issue = [&](uint32_t chunk, int s) {
     const ChunkRef r = locate_chunk(bt, chunk);
+    const EwDesc& d = bt.d[r.di];
+    const bool has_b = kChain && d.b != nullptr;
     refs[s] = r;
     fence_proxy_async_smem();
-    mbar_arrive_expect_tx(&bars[s], r.units * 16u);
-    bulk_g2s(ring + s * kEwChunk, static_cast<const uint4*>(bt.d[r.di].a) + r.u0, r.units * 16u,
-             &bars[s]);
+    mbar_arrive_expect_tx(&bars[s], r.units * 16u * (has_b ? 2u : 1u));
+    uint4* st = ring + s * kArrays * kEwChunk;
+    bulk_g2s(st, static_cast<const uint4*>(d.a) + r.u0, r.units * 16u, &bars[s]);
+    if (has_b) bulk_g2s(st + kEwChunk, static_cast<const uint4*>(d.b) + r.u0, r.units * 16u, &bars[s]);
   };
   if (tid == 0) {
     for (int s = 0; s < kFwdStages; ++s) mbar_init(&bars[s], 1);
@@ -233,7 +242,7 @@ __global__ void __launch_bounds__(kEwThreads, 5)
     const bool streaming = (d.flags & kEwStreaming) != 0;
     const bool half_out = (d.flags & kEwHalfGrid) != 0;
     const float qv = pin_f(d.q);
-    const uint4* src = ring + s * kEwChunk;
+    const uint4* src = ring + s * kArrays * kEwChunk;
     // Per-thread scale cache: units of a chunk mostly share a channel, so
     // the channel, its scales and reciprocals are recomputed only when the
     // row changes.
@@ -256,7 +265,28 @@ __global__ void __launch_bounds__(kEwThreads, 5)
         }
       }
       float v[V];
-      const bool special = Elem<T>::unpack_flag(src[k], v);
+      bool special = Elem<T>::unpack_flag(src[k], v);
+      if constexpr (kChain) {
+        if (d.b != nullptr) {
+          float w[V];
+          special |= Elem<T>::unpack_flag(src[kEwChunk + k], w);
+#pragma unroll
+          for (int i = 0; i < V; ++i) v[i] = x86_add(v[i], w[i]);  // tensor.hpp:126-134
+        }
+        if (d.act != 0) {
+#pragma unroll
+          for (int i = 0; i < V; ++i) v[i] = apply_act(v[i], d.act);
+        }
+        if (d.flags & kEwDemoteIn) {
+#pragma unroll
+          for (int i = 0; i < V; ++i) v[i] = half_grid(v[i], v[i], nf);  // tensor.hpp:159-170
+        }
+        if (d.preact != nullptr) {
+          st_v4(static_cast<uint4*>(d.preact) + u, Elem<T>::pack(v, v, false, nf), streaming);
+        }
+        // act/add may create inf/NaN from finite inputs: take the checked pack
+        special = true;
+      }
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         if (j >= d.n_out) break;
@@ -411,19 +441,35 @@ __global__ void resolve_kernel(const __grid_constant__ ResolveDesc d, uint32_t* 
 
 }  // namespace
 
-size_t ew_tma_smem() { return (size_t)kFwdStages * kFwdChunkBytes; }
+size_t ew_tma_smem(bool chain, int stages) { return (size_t)stages * kFwdChunkBytes * (chain ? 2 : 1); }
 
-cudaError_t ew_tma_occupancy(int dtype, int* blocks_per_sm) {
-  const void* f = dtype == 0 ? (const void*)ew_tma_kernel<float> : (const void*)ew_tma_kernel<__half>;
-  cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ew_tma_smem());
-  if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, kEwThreads, ew_tma_smem());
+template <typename T, bool kChain>
+static const void* tma_fn_c(int stages) {
+  switch (stages) {
+    case 3: return (const void*)ew_tma_kernel<T, kChain, 3>;
+    case 4: return (const void*)ew_tma_kernel<T, kChain, 4>;
+    default: return (const void*)ew_tma_kernel<T, kChain, 2>;
+  }
 }
 
-cudaError_t launch_ew_tma(int dtype, const EwBatch& b, uint32_t* status, int grid, cudaStream_t st) {
-  if (dtype == 0) ew_tma_kernel<float><<<grid, kEwThreads, ew_tma_smem(), st>>>(b, status);
-  else ew_tma_kernel<__half><<<grid, kEwThreads, ew_tma_smem(), st>>>(b, status);
-  return cudaGetLastError();
+static const void* tma_fn(int dtype, bool chain, int stages) {
+  if (dtype == 0) return chain ? tma_fn_c<float, true>(stages) : tma_fn_c<float, false>(stages);
+  return chain ? tma_fn_c<__half, true>(stages) : tma_fn_c<__half, false>(stages);
+}
+
+cudaError_t ew_tma_occupancy(int dtype, bool chain, int stages, int* blocks_per_sm) {
+  const void* f = tma_fn(dtype, chain, stages);
+  const int smem = (int)ew_tma_smem(chain, stages);
+  cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, kEwThreads, smem);
+}
+
+cudaError_t launch_ew_tma(int dtype, bool chain, int stages, const EwBatch& b, uint32_t* status,
+                          int grid, cudaStream_t st) {
+  void* args[] = {const_cast<EwBatch*>(&b), &status};
+  return cudaLaunchKernel(tma_fn(dtype, chain, stages), dim3(grid), dim3(kEwThreads), args,
+                          ew_tma_smem(chain, stages), st);
 }
 
 cudaError_t launch_ew(int dtype, bool chain, const EwBatch& b, uint32_t* status, int grid,

@@ -69,8 +69,12 @@ cudaError_t ew_occupancy(int dtype, bool chain, int* blocks_per_sm);
 cudaError_t launch_ew(int dtype, bool chain, const EwBatch& b, uint32_t* status, int grid,
                       cudaStream_t st);
 // TMA-staged plain forward: every descriptor must be on the vector path.
-cudaError_t ew_tma_occupancy(int dtype, int* blocks_per_sm);
-cudaError_t launch_ew_tma(int dtype, const EwBatch& b, uint32_t* status, int grid, cudaStream_t st);
+// chain = true: quant->act->quant descriptors (a and b staged); stages =
+// TMA ring depth 2..4 (16 KB chunks per array).
+constexpr int kTmaStagesMin = 2, kTmaStagesMax = 4;
+cudaError_t ew_tma_occupancy(int dtype, bool chain, int stages, int* blocks_per_sm);
+cudaError_t launch_ew_tma(int dtype, bool chain, int stages, const EwBatch& b, uint32_t* status,
+                          int grid, cudaStream_t st);
 
 // int8 codes (vec path when aligned).
 struct CodesDesc {
