@@ -391,6 +391,48 @@ qfb_status qfb_quant_pass_host(qfb_ctx* ctx, qfb_precision prec,
                                const qfb_host_point* points, int32_t n,
                                const qfb_quant_config* cfg);
 
+
+/* ---------------------------------------------------------------------- */
+/* On-disk formats (host only, no GPU needed) — SURVEY.md §8 f4.           */
+/* QSIM tensors: tensor_io.hpp:1-125 (magic "QSIM", u32 version 1, u32     */
+/* rank, u64 dims, u8 precision tag, little-endian float32). Several       */
+/* tensors may be concatenated in one blob; qfb_qsim_parse advances        */
+/* *offset past one tensor like qf::parse_tensor (tensor_io.hpp:68-99).   */
+/* Errors are QFB_ERR_IO with the reference's IoError messages.            */
+/* ---------------------------------------------------------------------- */
+typedef struct qfb_tensor_file qfb_tensor_file;
+qfb_status qfb_qsim_parse(const void* buf, size_t size, size_t* offset,
+                          qfb_tensor_file** out);          /* parse_tensor :68  */
+qfb_status qfb_qsim_load(const char* path, qfb_tensor_file** out);  /* load_tensor :119 */
+qfb_status qfb_qsim_info(const qfb_tensor_file* t, int32_t* rank, const int64_t** shape,
+                         int32_t* precision, int64_t* numel, const float** data);
+void qfb_qsim_free(qfb_tensor_file* t);
+/* Byte-identical to serialize_tensor (tensor_io.hpp:55-66); out == NULL  */
+/* queries the size.                                                      */
+qfb_status qfb_qsim_serialize(const float* data, int32_t rank, const int64_t* shape,
+                              int32_t precision, char* out, size_t cap, size_t* size);
+qfb_status qfb_qsim_save(const char* path, const float* data, int32_t rank,
+                         const int64_t* shape, int32_t precision);  /* save_tensor :115 */
+
+/* QSCL scale checkpoints: distill.hpp:287-362 (magic "QSCL", u32 version */
+/* 1, u64 manifest length, JSON manifest, float32 log-scale payload).     */
+/* Layers are exposed in name order (qf::ScaleSet is a std::map).         */
+typedef struct qfb_scales qfb_scales;
+qfb_status qfb_qscl_parse(const void* buf, size_t size, qfb_scales** out); /* parse_scales :324 */
+qfb_status qfb_qscl_load(const char* path, qfb_scales** out);               /* load_scales :360 */
+int32_t qfb_qscl_count(const qfb_scales* s);
+qfb_status qfb_qscl_layer(const qfb_scales* s, int32_t i, const char** name,
+                          const double** log_w, int64_t* count, double* log_a);
+void qfb_qscl_free(qfb_scales* s);
+/* Byte-identical to serialize_scales (distill.hpp:296-318): layers in   */
+/* name order, log scales stored as float32.                              */
+qfb_status qfb_qscl_serialize(int32_t n, const char* const* names,
+                              const double* const* log_w, const int64_t* counts,
+                              const double* log_a, char* out, size_t cap, size_t* size);
+qfb_status qfb_qscl_save(const char* path, int32_t n, const char* const* names,
+                         const double* const* log_w, const int64_t* counts,
+                         const double* log_a);                      /* save_scales :320 */
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

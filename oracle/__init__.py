@@ -242,6 +242,108 @@ class Reference:
                                        ctypes.POINTER(_vp), _i32, _i32, _i32, _i32, _i32,
                                        ctypes.POINTER(_dbl), ctypes.POINTER(_dbl)]
 
+        _sz = ctypes.c_size_t
+        L.ref_serialize_tensor.restype = _i32
+        L.ref_serialize_tensor.argtypes = [_vp, _vp, _i32, _i32, _vp, _sz, ctypes.POINTER(_sz)]
+        L.ref_parse_tensor.restype = _i32
+        L.ref_parse_tensor.argtypes = [ctypes.c_char_p, _sz, ctypes.POINTER(_sz), _i64p,
+                                       ctypes.POINTER(_i32), ctypes.POINTER(_i32), _vp, _i64,
+                                       ctypes.POINTER(_i64)]
+        L.ref_serialize_scales.restype = _i32
+        L.ref_serialize_scales.argtypes = [_i32, _vp, _vp, _vp, _vp, _vp, _sz, ctypes.POINTER(_sz)]
+        L.ref_scales_roundtrip.restype = _i32
+        L.ref_scales_roundtrip.argtypes = [ctypes.c_char_p, _sz, _vp, _sz, ctypes.POINTER(_sz)]
+        L.ref_scales_layer.restype = _i32
+        L.ref_scales_layer.argtypes = [ctypes.c_char_p, _sz, _i32, ctypes.c_char_p, _sz, _f64p, _i64,
+                                       ctypes.POINTER(_i64), ctypes.POINTER(_dbl), ctypes.POINTER(_i32)]
+        L.ref_distill_loss.restype = _i32
+        L.ref_distill_loss.argtypes = [_f32p, _f32p, _i64p, _f32p, _f32p, _i64p, _dbl, _f64p, _f32p,
+                                       _f32p]
+
+    # ---- formats (tensor_io.hpp, distill.hpp:287-362) ----
+    def serialize_tensor(self, data, precision=0):
+        a = np.require(np.asarray(data, dtype=np.float32), requirements='C')
+        sh = np.array(a.shape if a.ndim else [], dtype=np.int64)
+        size = ctypes.c_size_t()
+        shp = sh.ctypes.data if sh.size else None
+        st = self.L.ref_serialize_tensor(a.ctypes.data, shp, a.ndim, precision, None, 0, ctypes.byref(size))
+        if st:
+            return st, None
+        out = ctypes.create_string_buffer(size.value)
+        st = self.L.ref_serialize_tensor(a.ctypes.data, shp, a.ndim, precision, out, size.value,
+                                         ctypes.byref(size))
+        return st, out.raw[:size.value]
+
+    def parse_tensor(self, buf, offset=0):
+        """-> (status, data, shape, precision, new_offset)"""
+        off = ctypes.c_size_t(offset)
+        shape = np.zeros(8, dtype=np.int64)
+        rank, prec, n = _i32(), _i32(), _i64()
+        st = self.L.ref_parse_tensor(buf, len(buf), ctypes.byref(off), shape, ctypes.byref(rank),
+                                     ctypes.byref(prec), None, 0, ctypes.byref(n))
+        if st:
+            return st, None, None, None, offset
+        data = np.zeros(max(1, n.value), dtype=np.float32)
+        off = ctypes.c_size_t(offset)
+        st = self.L.ref_parse_tensor(buf, len(buf), ctypes.byref(off), shape, ctypes.byref(rank),
+                                     ctypes.byref(prec), data.ctypes.data, n.value, ctypes.byref(n))
+        return st, data[:n.value], tuple(int(v) for v in shape[:rank.value]), prec.value, off.value
+
+    def serialize_scales(self, scales):
+        names = list(scales.keys())
+        n = len(names)
+        enc = [nm.encode("utf-8", "surrogateescape") for nm in names]
+        c_names = (ctypes.c_char_p * max(1, n))(*enc)
+        ws = [np.ascontiguousarray(np.asarray(scales[nm][0], dtype=np.float64)) for nm in names]
+        c_w = (_vp * max(1, n))(*[w.ctypes.data if w.size else None for w in ws])
+        c_cnt = (_i64 * max(1, n))(*[w.size for w in ws])
+        c_a = (_dbl * max(1, n))(*[float(scales[nm][1]) for nm in names])
+        size = ctypes.c_size_t()
+        st = self.L.ref_serialize_scales(n, c_names, c_w, c_cnt, c_a, None, 0, ctypes.byref(size))
+        if st:
+            return st, None
+        out = ctypes.create_string_buffer(size.value)
+        st = self.L.ref_serialize_scales(n, c_names, c_w, c_cnt, c_a, out, size.value, ctypes.byref(size))
+        return st, out.raw[:size.value]
+
+    def scales_roundtrip(self, buf):
+        size = ctypes.c_size_t()
+        st = self.L.ref_scales_roundtrip(buf, len(buf), None, 0, ctypes.byref(size))
+        if st:
+            return st, None
+        out = ctypes.create_string_buffer(size.value)
+        st = self.L.ref_scales_roundtrip(buf, len(buf), out, size.value, ctypes.byref(size))
+        return st, out.raw[:size.value]
+
+    def parse_scales(self, buf):
+        """-> (status, {name: (log_w list, log_a)})"""
+        out = {}
+        nl = _i32(0)
+        i = 0
+        while True:
+            name = ctypes.create_string_buffer(4096)
+            w = np.zeros(1 << 16, dtype=np.float64)
+            cnt, a = _i64(), _dbl()
+            st = self.L.ref_scales_layer(buf, len(buf), i, name, 4096, w, w.size, ctypes.byref(cnt),
+                                         ctypes.byref(a), ctypes.byref(nl))
+            if st:
+                return st, None
+            if i >= nl.value:
+                return 0, out
+            out[name.value.decode("utf-8", "surrogateescape")] = (w[:cnt.value].tolist(), a.value)
+            i += 1
+
+    def distill_loss(self, fs, ft, is_, it, lam):
+        """distill.hpp:126-141 -> (status, [total, mse_f, mse_i, cos_f, cos_i], d_f, d_i)"""
+        fs, ft, is_, it = [np.ascontiguousarray(a, dtype=np.float32) for a in (fs, ft, is_, it)]
+        fsh = np.array(fs.shape, dtype=np.int64)
+        ish = np.array(is_.shape, dtype=np.int64)
+        o6 = np.zeros(6, dtype=np.float64)
+        df = np.zeros_like(fs)
+        di = np.zeros_like(is_)
+        st = self.L.ref_distill_loss(fs, ft, fsh, is_, it, ish, lam, o6, df, di)
+        return st, o6[:5], df, di
+
     @staticmethod
     def _d4(cfg=None):
         c = cfg or default_cfg()

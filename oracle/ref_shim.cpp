@@ -13,16 +13,19 @@
 #include <atomic>
 #include <chrono>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <span>
 #include <thread>
 #include <vector>
 
+#include "quantfuse/distill.hpp"
 #include "quantfuse/exec.hpp"
 #include "quantfuse/half.hpp"
 #include "quantfuse/quant.hpp"
 #include "quantfuse/rng.hpp"
 #include "quantfuse/tensor.hpp"
+#include "quantfuse/tensor_io.hpp"
 
 namespace {
 
@@ -247,6 +250,117 @@ int ref_bench_points(int32_t npoints, const float* const* x,
     double cs = 0.0;
     for (double v : sums) cs += v;
     if (checksum) *checksum = cs;
+  });
+}
+
+// ---------------------------------------------------------------------
+// Formats (tensor_io.hpp, distill.hpp:287-362) and the distillation loss
+// (distill.hpp:66-141), for the f3/f4 parity tests and golden fixtures.
+// ---------------------------------------------------------------------
+static int copy_out(const std::string& b, char* out, size_t cap, size_t* size) {
+  *size = b.size();
+  if (out) {
+    if (cap < b.size()) return 2;
+    std::memcpy(out, b.data(), b.size());
+  }
+  return 0;
+}
+
+int ref_serialize_tensor(const float* data, const int64_t* shape, int rank, int prec, char* out,
+                         size_t cap, size_t* size) {
+  int rc = 0;
+  const int st = guarded([&] {
+    std::vector<int64_t> sh(shape, shape + rank);
+    int64_t n = 1;
+    for (int64_t d : sh) n *= d;
+    qf::Tensor t(sh, std::vector<float>(data, data + n), prec_of(prec));
+    rc = copy_out(qf::serialize_tensor(t), out, cap, size);
+  });
+  return st ? st : rc;
+}
+
+// Parses one tensor at *offset; shape_out holds up to 8 dims, data_out up
+// to cap_n floats (*numel is always set).
+int ref_parse_tensor(const char* buf, size_t size, size_t* offset, int64_t* shape_out, int* rank,
+                     int* prec, float* data_out, int64_t cap_n, int64_t* numel) {
+  return guarded([&] {
+    const std::string b(buf, size);
+    size_t off = *offset;
+    qf::Tensor t = qf::parse_tensor(b, off);
+    *offset = off;
+    *rank = (int)t.shape.size();
+    for (size_t i = 0; i < t.shape.size() && i < 8; ++i) shape_out[i] = t.shape[i];
+    *prec = (int)t.precision;
+    *numel = (int64_t)t.data.size();
+    if (data_out && (int64_t)t.data.size() <= cap_n)
+      std::memcpy(data_out, t.data.data(), t.data.size() * 4);
+  });
+}
+
+int ref_serialize_scales(int n, const char* const* names, const double* const* log_w,
+                         const int64_t* counts, const double* log_a, char* out, size_t cap,
+                         size_t* size) {
+  int rc = 0;
+  const int st = guarded([&] {
+    qf::ScaleSet set;
+    for (int i = 0; i < n; ++i) {
+      qf::ScaleParams p;
+      p.log_w_scale.assign(log_w[i], log_w[i] + counts[i]);
+      p.log_a_scale = log_a[i];
+      set.by_layer[names[i]] = p;
+    }
+    rc = copy_out(qf::serialize_scales(set), out, cap, size);
+  });
+  return st ? st : rc;
+}
+
+// parse_scales then serialize_scales (the reference's round trip).
+int ref_scales_roundtrip(const char* buf, size_t size, char* out, size_t cap, size_t* osize) {
+  int rc = 0;
+  const int st = guarded([&] {
+    const qf::ScaleSet set = qf::parse_scales(std::string(buf, size));
+    rc = copy_out(qf::serialize_scales(set), out, cap, osize);
+  });
+  return st ? st : rc;
+}
+
+// Layer i (name order) of a parsed QSCL blob.
+int ref_scales_layer(const char* buf, size_t size, int i, char* name, size_t name_cap,
+                     double* log_w, int64_t cap_w, int64_t* count, double* log_a, int* n_layers) {
+  return guarded([&] {
+    const qf::ScaleSet set = qf::parse_scales(std::string(buf, size));
+    *n_layers = (int)set.by_layer.size();
+    int k = 0;
+    for (const auto& [nm, p] : set.by_layer) {
+      if (k++ != i) continue;
+      std::snprintf(name, name_cap, "%s", nm.c_str());
+      *count = (int64_t)p.log_w_scale.size();
+      for (int64_t j = 0; j < *count && j < cap_w; ++j) log_w[j] = p.log_w_scale[(size_t)j];
+      *log_a = p.log_a_scale;
+    }
+  });
+}
+
+// distill_loss over [C, H, W] feature/descriptor pairs (distill.hpp:126-141):
+// out6 = {total, mse_f, mse_i, cos_f, cos_i, 0}; d_f / d_i gradients.
+int ref_distill_loss(const float* fs, const float* ft, const int64_t* fshape, const float* is,
+                     const float* it, const int64_t* ishape, double lambda, double* out6, float* d_f,
+                     float* d_i) {
+  return guarded([&] {
+    auto mk = [](const float* p, const int64_t* sh) {
+      std::vector<int64_t> v(sh, sh + 3);
+      return qf::Tensor(v, std::vector<float>(p, p + v[0] * v[1] * v[2]));
+    };
+    const qf::DistillLoss dl = qf::distill_loss(mk(fs, fshape), mk(ft, fshape), mk(is, ishape),
+                                                mk(it, ishape), lambda);
+    out6[0] = dl.total;
+    out6[1] = dl.mse_f;
+    out6[2] = dl.mse_i;
+    out6[3] = dl.cos_f;
+    out6[4] = dl.cos_i;
+    out6[5] = 0.0;
+    std::memcpy(d_f, dl.d_features.data.data(), dl.d_features.data.size() * 4);
+    std::memcpy(d_i, dl.d_descriptors.data.data(), dl.d_descriptors.data.size() * 4);
   });
 }
 

@@ -33,6 +33,16 @@ qfb_status fail(qfb_status st, const char* fmt, ...) {
   return st;
 }
 
+}  // namespace
+
+// Shared with the other host TUs (qfb_formats.cpp, qfb_train.cpp).
+qfb_status qfb::set_error(qfb_status st, const char* msg) {
+  g_last_error = msg;
+  return st;
+}
+
+namespace {
+
 qfb_status cuda_fail(cudaError_t e, const char* where) {
   return fail(QFB_ERR_CUDA, "%s: %s (%s)", where, cudaGetErrorName(e), cudaGetErrorString(e));
 }

@@ -8,7 +8,12 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "../../include/qfb.h"
+
 namespace qfb {
+
+// Sets the thread-local qfb_last_error() message (qfb_api.cpp).
+qfb_status set_error(qfb_status st, const char* msg);
 
 struct FastDivHost {
   uint32_t d, m, s, pad;
