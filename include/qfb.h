@@ -393,6 +393,36 @@ qfb_status qfb_quant_pass_host(qfb_ctx* ctx, qfb_precision prec,
 
 
 /* ---------------------------------------------------------------------- */
+/* Scale-only QAT step pieces on the device — SURVEY.md §8 f3.            */
+/* ---------------------------------------------------------------------- */
+/* One tensor pair of qf::distill_loss (pair_loss, distill.hpp:66-124):     */
+/* student/teacher are DEVICE float32 [channels, hw]; writes d_student      */
+/* (= the reference's d_s, then scaled float(d * grad_scale) like the      */
+/* trainer's 1/chunk_len scaling, distill.hpp:243-246; 1.0 = none) and     */
+/* out2 (DEVICE double[2]) = {mse, mean per-location cosine}. Bit-exact:    */
+/* the MSE and the cosine mean use the reference's pairwise tree.          */
+qfb_status qfb_distill_pair(qfb_ctx* ctx, const float* student, const float* teacher,
+                            int64_t channels, int64_t hw, double lambda_cos,
+                            double grad_scale, float* d_student, double* out2);
+/* qf::distill_loss (distill.hpp:126-141) on HOST buffers: out5 = {total,   */
+/* mse_f, mse_i, cos_f, cos_i}; d_features / d_descriptors host float32.   */
+qfb_status qfb_distill_loss_host(qfb_ctx* ctx, const float* f_s, const float* f_t,
+                                 int64_t f_channels, int64_t f_hw, const float* i_s,
+                                 const float* i_t, int64_t i_channels, int64_t i_hw,
+                                 double lambda_cos, double grad_scale, double* out5,
+                                 float* d_features, float* d_descriptors);
+/* Adam over the flattened scale vector (distill.hpp:264-279), all DEVICE  */
+/* double arrays. bc1/bc2 = 1 - beta^t from qfb_adam_bias_corrections (the */
+/* host libm pow, like the reference). A non-finite gradient skips the     */
+/* whole update (grads.all_finite(), distill.hpp:254-258): *skipped        */
+/* (DEVICE u32) = number of non-finite gradients, 0 when applied.          */
+qfb_status qfb_adam_bias_corrections(double beta1, double beta2, int64_t t,
+                                     double* bc1, double* bc2);
+qfb_status qfb_adam_step(qfb_ctx* ctx, double* params, double* m, double* v,
+                         const double* grads, int64_t n, double beta1, double beta2,
+                         double lr, double eps, double bc1, double bc2, uint32_t* skipped);
+
+/* ---------------------------------------------------------------------- */
 /* On-disk formats (host only, no GPU needed) — SURVEY.md §8 f4.           */
 /* QSIM tensors: tensor_io.hpp:1-125 (magic "QSIM", u32 version 1, u32     */
 /* rank, u64 dims, u8 precision tag, little-endian float32). Several       */

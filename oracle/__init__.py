@@ -105,6 +105,10 @@ class Oracle:
         L.orc_rng_normal.argtypes = [_u64, _u64, _u64]
         L.orc_fill_rng.restype = None
         L.orc_fill_rng.argtypes = [_f32p, _i64, _u64, _u64, _u64, _i32, _dbl, _dbl, _i32]
+        L.orc_distill_pair.restype = _i32
+        L.orc_distill_pair.argtypes = [_f32p, _f32p, _i64, _i64, _dbl, _dbl, _f32p, _f64p]
+        L.orc_adam.restype = _i32
+        L.orc_adam.argtypes = [_f64p, _f64p, _f64p, _f64p, _i64, _dbl, _dbl, _dbl, _dbl, _i64]
 
     # scalar math
     def softplus(self, x): return self.L.orc_softplus(x)
@@ -188,6 +192,29 @@ class Oracle:
         out = np.empty(n, dtype=np.float32)
         self.L.orc_fill_rng(out, n, seed, stream, offset, kind, lo, hi, half)
         return out
+
+    def distill_pair(self, s, t, lam, grad_scale=1.0):
+        """pair_loss (distill.hpp:66-124) over [C, ...]: (status, [mse, cos], d_s)"""
+        s = np.ascontiguousarray(s, dtype=np.float32)
+        t = np.ascontiguousarray(t, dtype=np.float32)
+        c = s.shape[0]
+        hw = s.size // c
+        ds = np.zeros_like(s)
+        o2 = np.zeros(2, dtype=np.float64)
+        st = self.L.orc_distill_pair(s, t, c, hw, lam, grad_scale, ds, o2)
+        return st, o2, ds
+
+    def distill_loss(self, fs, ft, is_, it, lam, grad_scale=1.0):
+        """distill.hpp:126-141: (status, [total, mse_f, mse_i, cos_f, cos_i], d_f, d_i)"""
+        s1, f2, df = self.distill_pair(fs, ft, lam, grad_scale)
+        s2, i2, di = self.distill_pair(is_, it, lam, grad_scale)
+        total = f2[0] + i2[0] + lam * (1.0 - f2[1]) + lam * (1.0 - i2[1])
+        return s1 or s2, np.array([total, f2[0], i2[0], f2[1], i2[1]]), df, di
+
+    def adam(self, p, m, v, g, b1, b2, lr, eps, t):
+        """distill.hpp:264-279 in place; returns 1 (skipped) on a non-finite gradient"""
+        return self.L.orc_adam(p, m, v, np.ascontiguousarray(g, dtype=np.float64), p.size, b1, b2,
+                               lr, eps, t)
 
 
 class Reference:

@@ -402,3 +402,71 @@ void orc_fill_rng(float* out, int64_t n, uint64_t seed, uint64_t stream,
     out[i] = f;
   }
 }
+
+/* ------------------------------------------- distillation loss (f3) */
+/* pair_loss, distill.hpp:66-124, for one [c, hw] pair: out2 = {mse, mean
+ * cosine}; d_s as the reference builds it (0.0f + float(2d/n), then += the
+ * cosine term per location), finally scaled float(d * grad_scale) like the
+ * trainer (distill.hpp:243-246). Returns 0, or 1 (ShapeError) for c < 1. */
+int orc_distill_pair(const float* s, const float* t, int64_t c, int64_t hw, double lambda,
+                     double grad_scale, float* d_s, double* out2) {
+  if (c < 1 || hw < 1) return 1;
+  const int64_t n = c * hw;
+  double* sq = (double*)malloc(sizeof(double) * (size_t)n);
+  double* cl = (double*)malloc(sizeof(double) * (size_t)hw);
+  if (!sq || !cl) {
+    free(sq);
+    free(cl);
+    return 2;
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    const double d = (double)s[i] - (double)t[i];
+    sq[i] = d * d;
+    d_s[i] = 0.0f + (float)(2.0 * d / (double)n);
+  }
+  out2[0] = orc_pairwise_sum(sq, n) / (double)n;
+  const double w = lambda / (double)hw;
+  for (int64_t p = 0; p < hw; ++p) {
+    double dot = 0.0, na2 = 0.0, nb2 = 0.0;
+    for (int64_t ch = 0; ch < c; ++ch) {
+      const double a = s[ch * hw + p], b = t[ch * hw + p];
+      dot += a * b;
+      na2 += a * a;
+      nb2 += b * b;
+    }
+    if (na2 == 0.0 || nb2 == 0.0) {
+      cl[p] = 0.0;
+      continue;
+    }
+    const double nrm = sqrt(na2 * nb2);
+    const double cosv = dot / nrm;
+    cl[p] = cosv;
+    for (int64_t ch = 0; ch < c; ++ch) {
+      const double a = s[ch * hw + p], b = t[ch * hw + p];
+      d_s[ch * hw + p] += (float)(-w * (b / nrm - cosv * a / na2));
+    }
+  }
+  out2[1] = orc_pairwise_sum(cl, hw) / (double)hw;
+  for (int64_t i = 0; i < n; ++i) d_s[i] = (float)((double)d_s[i] * grad_scale);
+  free(sq);
+  free(cl);
+  return 0;
+}
+
+/* Adam over the flattened scales, distill.hpp:264-279; returns 1 and leaves
+ * everything unchanged when a gradient is non-finite (distill.hpp:254-258). */
+int orc_adam(double* p, double* m, double* v, const double* g, int64_t n, double b1, double b2,
+             double lr, double eps, int64_t t) {
+  for (int64_t i = 0; i < n; ++i)
+    if (!isfinite(g[i])) return 1;
+  const double bc1 = 1.0 - pow(b1, (double)t);
+  const double bc2 = 1.0 - pow(b2, (double)t);
+  for (int64_t k = 0; k < n; ++k) {
+    m[k] = b1 * m[k] + (1.0 - b1) * g[k];
+    v[k] = b2 * v[k] + (1.0 - b2) * g[k] * g[k];
+    const double mhat = m[k] / bc1;
+    const double vhat = v[k] / bc2;
+    p[k] -= lr * mhat / (sqrt(vhat) + eps);
+  }
+  return 0;
+}

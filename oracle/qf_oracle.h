@@ -94,6 +94,12 @@ double orc_rng_normal(uint64_t seed, uint64_t stream, uint64_t index);
 void orc_fill_rng(float* out, int64_t n, uint64_t seed, uint64_t stream,
                   uint64_t offset, int kind, double lo, double hi, int half);
 
+/* distill.hpp:66-124 (one pair) and :264-279 (Adam) */
+int orc_distill_pair(const float* s, const float* t, int64_t c, int64_t hw, double lambda,
+                     double grad_scale, float* d_s, double* out2);
+int orc_adam(double* p, double* m, double* v, const double* g, int64_t n, double b1, double b2,
+             double lr, double eps, int64_t t);
+
 #ifdef __cplusplus
 }
 #endif

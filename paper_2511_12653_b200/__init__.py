@@ -629,3 +629,71 @@ def model_layer_counts(plan: ExecutionPlan, n_act: int, c_out: int, per: int, we
     check(_lib.qfb_exec_model_layer(ctypes.byref(c), n_act, c_out, per, int(weights_cached),
                                     int(fused_fails), ctypes.byref(t)))
     return t
+
+
+# ------------------------------------------------- QAT step --
+
+_sig("qfb_distill_pair", _i32, [_vp, _vp, _vp, _i64, _i64, ctypes.c_double, ctypes.c_double, _vp, _vp])
+_sig("qfb_adam_bias_corrections", _i32, [ctypes.c_double, ctypes.c_double, _i64,
+                                         ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)])
+_sig("qfb_adam_step", _i32, [_vp, _vp, _vp, _vp, _vp, _i64, ctypes.c_double, ctypes.c_double,
+                             ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double, _vp])
+
+
+def distill_pair(student, teacher, lambda_cos: float, grad_scale: float = 1.0,
+                 ctx: Optional[Context] = None):
+    """One tensor pair of qf::distill_loss (distill.hpp:66-124) on the GPU:
+    student/teacher float32 CUDA tensors [C, ...]. Returns (d_student,
+    out2) with out2 a float64 CUDA tensor {mse, mean cosine}; d_student is
+    scaled float(d * grad_scale) like the trainer's 1/chunk_len scaling."""
+    import torch
+    if tuple(student.shape) != tuple(teacher.shape):
+        raise ShapeError(f"distill_loss: student {list(student.shape)} vs teacher {list(teacher.shape)}")
+    if student.dim() < 1 or student.shape[0] < 1:
+        raise ShapeError("distill_loss: channel dim must be >= 1")
+    if student.dtype != torch.float32 or teacher.dtype != torch.float32:
+        raise ValueError("distill_loss: float32 tensors expected (promote_full first)")
+    s = student.contiguous()
+    t = teacher.contiguous()
+    c = s.shape[0]
+    hw = s.numel() // c
+    d = torch.empty_like(s)
+    out2 = torch.empty(2, dtype=torch.float64, device=s.device)
+    ctx = ctx or default_context(s.device.index)
+    check(_lib.qfb_distill_pair(ctx.handle, _vp(s.data_ptr()), _vp(t.data_ptr()), c, hw, lambda_cos,
+                                grad_scale, _vp(d.data_ptr()), _vp(out2.data_ptr())))
+    return d, out2
+
+
+def distill_loss(f_s, f_t, i_s, i_t, lambda_cos: float, grad_scale: float = 1.0,
+                 ctx: Optional[Context] = None):
+    """qf::distill_loss (distill.hpp:126-141): returns (dict of total, mse_f,
+    mse_i, cos_f, cos_i as Python floats, d_features, d_descriptors)."""
+    df, f2 = distill_pair(f_s, f_t, lambda_cos, grad_scale, ctx)
+    di, i2 = distill_pair(i_s, i_t, lambda_cos, grad_scale, ctx)
+    mf, cf = f2.tolist()
+    mi, ci = i2.tolist()
+    total = mf + mi + lambda_cos * (1.0 - cf) + lambda_cos * (1.0 - ci)
+    return {"total": total, "mse_f": mf, "mse_i": mi, "cos_f": cf, "cos_i": ci}, df, di
+
+
+def adam_bias_corrections(beta1: float, beta2: float, t: int):
+    b1, b2 = ctypes.c_double(), ctypes.c_double()
+    check(_lib.qfb_adam_bias_corrections(beta1, beta2, t, ctypes.byref(b1), ctypes.byref(b2)))
+    return b1.value, b2.value
+
+
+def adam_step(params, m, v, grads, t: int, lr: float, beta1: float = 0.9, beta2: float = 0.999,
+              eps: float = 1e-8, skipped=None, ctx: Optional[Context] = None):
+    """Adam over the flattened scale vector (distill.hpp:264-279), in place
+    on float64 CUDA tensors; the update is skipped when any gradient is
+    non-finite. Returns the device u32 counter of non-finite gradients."""
+    import torch
+    bc1, bc2 = adam_bias_corrections(beta1, beta2, t)
+    if skipped is None:
+        skipped = torch.zeros(1, dtype=torch.int32, device=params.device)
+    ctx = ctx or default_context(params.device.index)
+    check(_lib.qfb_adam_step(ctx.handle, _vp(params.data_ptr()), _vp(m.data_ptr()), _vp(v.data_ptr()),
+                             _vp(grads.data_ptr()), params.numel(), beta1, beta2, lr, eps, bc1, bc2,
+                             _vp(skipped.data_ptr())))
+    return skipped

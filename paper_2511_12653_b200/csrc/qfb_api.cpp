@@ -97,6 +97,7 @@ struct qfb_ctx {
   DevBuf pass_params;
   void* pinned = nullptr;  // pinned staging for params and scale gradients
   size_t pinned_bytes = 0;
+  DevBuf train_ws[4];      // scratch of the trainer ops (qfb_train.cu)
 };
 
 namespace {
@@ -117,6 +118,23 @@ qfb_status grow(qfb_ctx* ctx, DevBuf& b, size_t bytes, bool zero) {
   b.bytes = nb;
   return QFB_OK;
 }
+
+}  // namespace
+
+// ---- internal accessors for the other TUs (qfb_kernels.h) ----
+qfb_status qfb::ctx_scratch(qfb_ctx* ctx, int slot, size_t bytes, void** p) {
+  if (!ctx) return fail(QFB_ERR_VALUE, "null qfb_ctx");
+  if (slot < 0 || slot >= 4) return fail(QFB_ERR_VALUE, "scratch slot out of range");
+  if (qfb_status st = grow(ctx, ctx->train_ws[slot], std::max<size_t>(bytes, 8), false)) return st;
+  *p = ctx->train_ws[slot].p;
+  return QFB_OK;
+}
+cudaStream_t qfb::ctx_stream(const qfb_ctx* ctx) { return ctx->stream; }
+int qfb::ctx_device(const qfb_ctx* ctx) { return ctx->device; }
+void qfb::ctx_count_launches(qfb_ctx* ctx, int n) { ctx->launches += n; }
+qfb_status qfb::cuda_error(cudaError_t e, const char* where) { return cuda_fail(e, where); }
+
+namespace {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 

@@ -14,6 +14,13 @@ namespace qfb {
 
 // Sets the thread-local qfb_last_error() message (qfb_api.cpp).
 qfb_status set_error(qfb_status st, const char* msg);
+// Context internals for the other TUs: a grow-only device scratch buffer
+// per slot (0..3), the stream/device, launch accounting, CUDA error mapping.
+qfb_status ctx_scratch(qfb_ctx* ctx, int slot, size_t bytes, void** p);
+cudaStream_t ctx_stream(const qfb_ctx* ctx);
+int ctx_device(const qfb_ctx* ctx);
+void ctx_count_launches(qfb_ctx* ctx, int n);
+qfb_status cuda_error(cudaError_t e, const char* where);
 
 struct FastDivHost {
   uint32_t d, m, s, pad;

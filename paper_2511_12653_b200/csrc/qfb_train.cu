@@ -1,0 +1,339 @@
+// qfb_train.cu — the on-device pieces of the scale-only QAT step around the
+// fake-quant path, bit-exact with the reference:
+//
+//  - distillation loss per tensor pair (distill.hpp:66-124 pair_loss): MSE
+//    over all elements with the fixed pairwise tree (tensor.hpp:100-109),
+//    per-location cosine over the channel axis (sequential channel folds in
+//    double, zero-norm locations guarded), and the student gradient
+//    d_s = float(2d/n) (+)= float(-w (b/nrm - cos a/na2)) in float32, then the
+//    trainer's chunk scaling float(d * inv) (distill.hpp:243-246);
+//  - Adam over the flattened scale vector (distill.hpp:264-279) with the
+//    trainer's skip rule (a non-finite gradient skips the whole update,
+//    distill.hpp:254-258), decided on the device so the step stays
+//    capturable in a CUDA graph.
+//
+// The exact pairwise sum of n terms runs as: one thread per leaf group of
+// the reference tree (depth D = least with ceil(n/2^D) <= 16; a group is
+// fold(first half) + fold(second half) from 0.0, or one fold if <= 8), then
+// perfect-tree halving of the 2^D group sums in shared memory, 2048 per CTA
+// per pass (the tree above depth D is perfect). All HBM
+// traffic is one read of s and t, one write of d_s: the loss is HBM-bound.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <string>
+
+#include "../../include/qfb.h"
+#include "qfb_kernels.h"
+
+namespace qfb {
+namespace {
+
+constexpr int kLeaf = 16;
+constexpr int kRedThreads = 1024;  // halving kernel: 2048 values per CTA
+
+__host__ __device__ __forceinline__ uint32_t tree_depth(uint64_t n) {
+  uint32_t d = 0;
+  while (((n + (1ull << d) - 1) >> d) > (uint64_t)kLeaf) ++d;
+  return d;
+}
+
+// Node `g` at depth `levels` of the reference split of [0, n).
+__device__ __forceinline__ void node_of(uint64_t n, uint32_t g, uint32_t levels, uint64_t& lo,
+                                        uint64_t& m) {
+  lo = 0;
+  m = n;
+  for (int l = (int)levels - 1; l >= 0; --l) {
+    const uint64_t h = m >> 1;
+    if ((g >> l) & 1u) {
+      lo += h;
+      m -= h;
+    } else {
+      m = h;
+    }
+  }
+}
+
+// MSE terms of pair_loss (distill.hpp:84-91): d = double(s) - double(t),
+// term d*d; the student gradient starts as 0.0f + float(2d/n).
+struct MseTerm {
+  const float* s;
+  const float* t;
+  float* ds;
+  double inv_n2;  // unused (kept for layout); 2.0 * d / n is evaluated literally
+  double n;
+  __device__ __forceinline__ double operator()(uint64_t i) const {
+    const double d = __dadd_rn((double)__ldg(s + i), -(double)__ldg(t + i));
+    ds[i] = __fadd_rn(0.0f, __double2float_rn(__ddiv_rn(__dmul_rn(2.0, d), n)));
+    return __dmul_rn(d, d);
+  }
+};
+
+// Stored terms (cosines per location).
+struct LoadTerm {
+  const double* v;
+  __device__ __forceinline__ double operator()(uint64_t i) const { return v[i]; }
+};
+
+template <typename Term>
+__device__ __forceinline__ double fold(const Term& f, uint64_t lo, uint64_t m) {
+  double acc = 0.0;
+  for (uint64_t k = 0; k < m; ++k) acc = __dadd_rn(acc, f(lo + k));
+  return acc;
+}
+
+// One thread per leaf group: its sum in the reference order.
+template <typename Term>
+__global__ void leaf_sums_kernel(Term f, uint64_t n, uint32_t depth, double* out) {
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= (1u << depth)) return;
+  uint64_t lo, m;
+  node_of(n, g, depth, lo, m);
+  double r;
+  if (m <= 8) {
+    r = fold(f, lo, m);
+  } else {
+    const uint64_t h = m >> 1;
+    r = __dadd_rn(fold(f, lo, h), fold(f, lo + h, m - h));
+  }
+  out[g] = r;
+}
+
+// Perfect-tree halving: CTA b reduces in[2048 b .. 2048 b + 2048) (a power
+// of two count `cnt` <= 2048 when fewer remain) to out[b]. With `final`,
+// the single result is divided by `div` into res.
+__global__ void __launch_bounds__(kRedThreads) halve_kernel(const double* in, uint32_t cnt,
+                                                            double* out, double div, double* res) {
+  __shared__ double sm[2 * kRedThreads];
+  const uint32_t per = cnt < 2u * kRedThreads ? cnt : 2u * kRedThreads;
+  const uint64_t base = (uint64_t)blockIdx.x * per;
+  for (uint32_t i = threadIdx.x; i < per; i += kRedThreads) sm[i] = in[base + i];
+  __syncthreads();
+  for (uint32_t w = per >> 1; w >= 1; w >>= 1) {
+    double v = 0.0;
+    if (threadIdx.x < w) v = __dadd_rn(sm[2 * threadIdx.x], sm[2 * threadIdx.x + 1]);
+    __syncthreads();
+    if (threadIdx.x < w) sm[threadIdx.x] = v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (res) *res = __ddiv_rn(sm[0], div);
+    else out[blockIdx.x] = sm[0];
+  }
+}
+
+// pairwise_sum(terms, n) / div -> *res (device), via scratch `ws` (>= 2^D
+// + 2^D/2048 doubles).
+template <typename Term>
+cudaError_t pairwise_sum_dev(const Term& f, uint64_t n, double div, double* res, double* ws,
+                             cudaStream_t st, int* launches) {
+  const uint32_t depth = tree_depth(n);
+  const uint32_t groups = 1u << depth;
+  leaf_sums_kernel<Term><<<(groups + 255) / 256, 256, 0, st>>>(f, n, depth, ws);
+  ++*launches;
+  double* in = ws;
+  double* out = ws + groups;
+  uint32_t cnt = groups;
+  for (;;) {
+    const uint32_t per = cnt < 2u * kRedThreads ? cnt : 2u * kRedThreads;
+    const uint32_t blocks = cnt / per;
+    halve_kernel<<<blocks, kRedThreads, 0, st>>>(in, cnt, out, div, blocks == 1 ? res : nullptr);
+    ++*launches;
+    if (blocks == 1) break;
+    double* t = in;
+    in = out;
+    out = t;
+    cnt = blocks;
+  }
+  return cudaGetLastError();
+}
+
+// Per-location cosine + its gradient (distill.hpp:94-121), then the
+// trainer's chunk scaling of the whole gradient column (distill.hpp:245).
+__global__ void cosine_kernel(const float* __restrict__ s, const float* __restrict__ t,
+                              float* __restrict__ ds, uint64_t c, uint64_t hw, double w,
+                              double gscale, double* __restrict__ cos_loc) {
+  const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= hw) return;
+  double dot = 0.0, na2 = 0.0, nb2 = 0.0;
+  for (uint64_t ch = 0; ch < c; ++ch) {
+    const double a = (double)__ldg(s + ch * hw + p);
+    const double b = (double)__ldg(t + ch * hw + p);
+    dot = __dadd_rn(dot, __dmul_rn(a, b));
+    na2 = __dadd_rn(na2, __dmul_rn(a, a));
+    nb2 = __dadd_rn(nb2, __dmul_rn(b, b));
+  }
+  const bool zero = na2 == 0.0 || nb2 == 0.0;  // guarded: cos 0, no gradient
+  double cosv = 0.0, nrm = 1.0;
+  if (!zero) {
+    nrm = __dsqrt_rn(__dmul_rn(na2, nb2));
+    cosv = __ddiv_rn(dot, nrm);
+  }
+  cos_loc[p] = cosv;
+  for (uint64_t ch = 0; ch < c; ++ch) {
+    const uint64_t i = ch * hw + p;
+    float g = ds[i];
+    if (!zero) {
+      const double a = (double)__ldg(s + i);
+      const double b = (double)__ldg(t + i);
+      const double q = __dadd_rn(__ddiv_rn(b, nrm), -__ddiv_rn(__dmul_rn(cosv, a), na2));
+      g = __fadd_rn(g, __double2float_rn(__dmul_rn(-w, q)));
+    }
+    ds[i] = __double2float_rn(__dmul_rn((double)g, gscale));
+  }
+}
+
+// Adam (distill.hpp:264-279); the update is skipped when any gradient is
+// non-finite (all_finite, distill.hpp:254-258): flag[0] counts them.
+__global__ void nonfinite_kernel(const double* __restrict__ g, int64_t n, uint32_t* flag) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (!isfinite(g[i])) atomicAdd(flag, 1u);
+}
+
+__global__ void adam_kernel(double* __restrict__ p, double* __restrict__ m, double* __restrict__ v,
+                            const double* __restrict__ g, int64_t n, double b1, double b2, double lr,
+                            double eps, double bc1, double bc2, const uint32_t* flag) {
+  if (*flag != 0) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double gi = g[i];
+    const double mk = __dadd_rn(__dmul_rn(b1, m[i]), __dmul_rn(__dadd_rn(1.0, -b1), gi));
+    const double vk = __dadd_rn(__dmul_rn(b2, v[i]), __dmul_rn(__dmul_rn(__dadd_rn(1.0, -b2), gi), gi));
+    m[i] = mk;
+    v[i] = vk;
+    const double mhat = __ddiv_rn(mk, bc1);
+    const double vhat = __ddiv_rn(vk, bc2);
+    p[i] = __dadd_rn(p[i], -__ddiv_rn(__dmul_rn(lr, mhat), __dadd_rn(__dsqrt_rn(vhat), eps)));
+  }
+}
+
+}  // namespace
+}  // namespace qfb
+
+using namespace qfb;
+
+namespace {
+
+struct Guard {
+  int prev = -1;
+  explicit Guard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~Guard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+qfb_status err(qfb_status st, const std::string& m) { return set_error(st, m.c_str()); }
+
+}  // namespace
+
+extern "C" {
+
+qfb_status qfb_distill_pair(qfb_ctx* ctx, const float* student, const float* teacher,
+                            int64_t channels, int64_t hw, double lambda_cos, double grad_scale,
+                            float* d_student, double* out2) {
+  if (!ctx) return err(QFB_ERR_VALUE, "null qfb_ctx");
+  if (channels < 1) return err(QFB_ERR_SHAPE, "distill_loss: channel dim must be >= 1");
+  if (hw < 1) return err(QFB_ERR_SHAPE, "distill_loss: non-positive spatial size");
+  if (!student || !teacher || !d_student || !out2) return err(QFB_ERR_VALUE, "distill_pair: null pointer");
+  Guard g(ctx_device(ctx));
+  const cudaStream_t st = ctx_stream(ctx);
+  const uint64_t n = (uint64_t)channels * (uint64_t)hw;
+  const uint64_t groups_n = 1ull << tree_depth(n), groups_hw = 1ull << tree_depth((uint64_t)hw);
+  if (groups_n >= (1ull << 31)) return err(QFB_ERR_UNSUPPORTED, "distill_pair: tensor too large");
+  void *ws = nullptr, *cl = nullptr;
+  const uint64_t gmax = groups_n > groups_hw ? groups_n : groups_hw;
+  if (qfb_status s = ctx_scratch(ctx, 0, (gmax + gmax / 2048 + 2) * sizeof(double), &ws)) return s;
+  if (qfb_status s = ctx_scratch(ctx, 1, (uint64_t)hw * sizeof(double), &cl)) return s;
+  int launches = 0;
+  // MSE (+ d_s = float(2d/n)) then per-location cosine (+ its gradient and
+  // the chunk scaling), then the mean cosine over locations
+  MseTerm mt{student, teacher, d_student, 0.0, (double)n};
+  cudaError_t e = pairwise_sum_dev(mt, n, (double)n, out2, static_cast<double*>(ws), st, &launches);
+  if (e == cudaSuccess) {
+    const double w = lambda_cos / (double)hw;
+    cosine_kernel<<<(unsigned)(((uint64_t)hw + 255) / 256), 256, 0, st>>>(
+        student, teacher, d_student, (uint64_t)channels, (uint64_t)hw, w, grad_scale,
+        static_cast<double*>(cl));
+    ++launches;
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess)
+    e = pairwise_sum_dev(LoadTerm{static_cast<const double*>(cl)}, (uint64_t)hw, (double)hw, out2 + 1,
+                         static_cast<double*>(ws), st, &launches);
+  ctx_count_launches(ctx, launches);
+  if (e != cudaSuccess) return cuda_error(e, "distill_pair");
+  return QFB_OK;
+}
+
+qfb_status qfb_distill_loss_host(qfb_ctx* ctx, const float* f_s, const float* f_t, int64_t f_channels,
+                                 int64_t f_hw, const float* i_s, const float* i_t, int64_t i_channels,
+                                 int64_t i_hw, double lambda_cos, double grad_scale, double* out5,
+                                 float* d_features, float* d_descriptors) {
+  if (!ctx) return err(QFB_ERR_VALUE, "null qfb_ctx");
+  if (!f_s || !f_t || !i_s || !i_t || !out5 || !d_features || !d_descriptors)
+    return err(QFB_ERR_VALUE, "distill_loss_host: null pointer");
+  if (f_channels < 1 || i_channels < 1) return err(QFB_ERR_SHAPE, "distill_loss: channel dim must be >= 1");
+  if (f_hw < 1 || i_hw < 1) return err(QFB_ERR_SHAPE, "distill_loss: non-positive spatial size");
+  Guard g(ctx_device(ctx));
+  const cudaStream_t st = ctx_stream(ctx);
+  const size_t nf = (size_t)f_channels * (size_t)f_hw, ni = (size_t)i_channels * (size_t)i_hw;
+  void* buf = nullptr;
+  if (qfb_status s = ctx_scratch(ctx, 2, (3 * nf + 3 * ni) * sizeof(float) + 4 * sizeof(double), &buf)) return s;
+  float* b = static_cast<float*>(buf);
+  float *dfs = b, *dft = b + nf, *ddf = b + 2 * nf, *dis = b + 3 * nf, *dit = dis + ni, *ddi = dis + 2 * ni;
+  double* dout = reinterpret_cast<double*>(dis + 3 * ni);
+  cudaError_t e = cudaMemcpyAsync(dfs, f_s, nf * 4, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dft, f_t, nf * 4, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dis, i_s, ni * 4, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dit, i_t, ni * 4, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return cuda_error(e, "distill_loss_host H2D");
+  if (qfb_status s = qfb_distill_pair(ctx, dfs, dft, f_channels, f_hw, lambda_cos, grad_scale, ddf, dout)) return s;
+  if (qfb_status s = qfb_distill_pair(ctx, dis, dit, i_channels, i_hw, lambda_cos, grad_scale, ddi, dout + 2)) return s;
+  double h[4];
+  e = cudaMemcpyAsync(h, dout, sizeof h, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_features, ddf, nf * 4, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_descriptors, ddi, ni * 4, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_error(e, "distill_loss_host D2H");
+  // distill.hpp:136-139: total, in the reference's evaluation order
+  out5[1] = h[0];
+  out5[2] = h[2];
+  out5[3] = h[1];
+  out5[4] = h[3];
+  out5[0] = h[0] + h[2] + lambda_cos * (1.0 - h[1]) + lambda_cos * (1.0 - h[3]);
+  return QFB_OK;
+}
+
+qfb_status qfb_adam_bias_corrections(double beta1, double beta2, int64_t t, double* bc1, double* bc2) {
+  if (!bc1 || !bc2) return err(QFB_ERR_VALUE, "adam_bias_corrections: null pointer");
+  if (t < 1) return err(QFB_ERR_VALUE, "adam_bias_corrections: step must be >= 1");
+  *bc1 = 1.0 - std::pow(beta1, (double)t);  // distill.hpp:265-266 (host libm pow)
+  *bc2 = 1.0 - std::pow(beta2, (double)t);
+  return QFB_OK;
+}
+
+qfb_status qfb_adam_step(qfb_ctx* ctx, double* params, double* m, double* v, const double* grads,
+                         int64_t n, double beta1, double beta2, double lr, double eps, double bc1,
+                         double bc2, uint32_t* skipped) {
+  if (!ctx) return err(QFB_ERR_VALUE, "null qfb_ctx");
+  if (n < 0 || (n > 0 && (!params || !m || !v || !grads)) || !skipped)
+    return err(QFB_ERR_VALUE, "adam_step: bad arguments");
+  Guard g(ctx_device(ctx));
+  const cudaStream_t st = ctx_stream(ctx);
+  cudaError_t e = cudaMemsetAsync(skipped, 0, sizeof(uint32_t), st);
+  const int blocks = (int)((n + 255) / 256 > 1024 ? 1024 : (n + 255) / 256);
+  if (e == cudaSuccess && n > 0) {
+    nonfinite_kernel<<<blocks, 256, 0, st>>>(grads, n, skipped);
+    adam_kernel<<<blocks, 256, 0, st>>>(params, m, v, grads, n, beta1, beta2, lr, eps, bc1, bc2, skipped);
+    ctx_count_launches(ctx, 2);
+    e = cudaGetLastError();
+  }
+  if (e != cudaSuccess) return cuda_error(e, "adam_step");
+  return QFB_OK;
+}
+
+}  // extern "C"
