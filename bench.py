@@ -516,6 +516,24 @@ def run_secondary(args, ctx, stream, dev, peak, rank, ws):
     out["c5_forward_throughput"] = c5
     del fp
     torch.cuda.empty_cache()
+    # f2: the same forward emitting int8 codes (1 byte per quant-point element)
+    fq = FrontendQuantPass(ctx, frames=8, dtype=args.dtype, sets=2, seed=11 + rank, device=dev,
+                           int8_out=True)
+    k[0] = 0
+
+    def fwd8():
+        fq.forward(k[0] % 2)
+        k[0] += 1
+    ms = time_device(fwd8, stream, reps=50)
+    fps = fq.frames / (ms / 1e3)
+    gb = fq.bytes_per_step()["fwd_int8"] / (ms / 1e3) / 1e9
+    out["c5_forward_int8_codes"] = {
+        "value": ws * fps, "unit": "frames/s", "per_gpu_frames_per_s": fps, "gbps": gb,
+        "hbm_frac": gb / peak, "frames_per_launch": fq.frames,
+        "workload": "config 5 forward emitting int8 codes (QFB_FLAG_INT8_OUT, SURVEY §8 f2): "
+                    "input read once, 1 byte written per quant-point element"}
+    del fq
+    torch.cuda.empty_cache()
     return out
 
 

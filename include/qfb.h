@@ -85,6 +85,10 @@ typedef enum qfb_precision {
 #define QFB_FLAG_HALF_GRID 0x1u /* f32 storage: round outputs to binary16 */
                                 /* grid (round_to_half, half.hpp:72-82)   */
 #define QFB_FLAG_STREAMING 0x2u /* evict-first loads/stores (data >> L2)  */
+#define QFB_FLAG_INT8_OUT  0x4u /* qfb_fq_fwd_multi: every output y[k] of */
+                                /* the entry receives the int8 codes      */
+                                /* (int8_codes, quant.hpp:174-207; 1 byte */
+                                /* per element) instead of FQ values      */
 
 /* ---------------------------------------------------------------------- */
 /* Quantization config: qf::QuantConfig (quant.hpp:35-61).                */

@@ -205,7 +205,9 @@ qfb_status plan_ew(int dtype, const EwJob& j, std::vector<EwDesc>& out) {
     d.b = j.b ? static_cast<const char*>(j.b) + elem_off * es : nullptr;
     d.preact = j.preact ? static_cast<char*>(j.preact) + elem_off * es : nullptr;
     for (int k = 0; k < 2; ++k) {
-      d.y[k] = k < j.n_out ? static_cast<char*>(j.y[k]) + elem_off * es : nullptr;
+      // int8-code outputs are 1 byte per element
+      const int oes = (j.flags & kEwInt8Out) ? 1 : es;
+      d.y[k] = k < j.n_out ? static_cast<char*>(j.y[k]) + elem_off * oes : nullptr;
       d.s[k] = k < j.n_out ? j.s[k] : nullptr;
     }
     d.nunits = (uint32_t)(elems / unit);
@@ -241,11 +243,11 @@ qfb_status plan_ew(int dtype, const EwJob& j, std::vector<EwDesc>& out) {
 // 128 KB, 4 x 3 -> 144 KB. Deeper rings fill and drain slower and leave a
 // longer one-chunk tail, so short launches (one frame) take 3 stages and
 // long ones (>= 64 chunks per CTA, e.g. 8 frames) 4. Chains stage two
-// arrays per chunk and keep 2 stages; f16 is element-rate bound and wants
-// the most CTAs (2 stages).
-int tma_stages(const qfb_ctx* ctx, int dtype, bool chain, uint64_t chunks) {
+// arrays per chunk and keep 2 stages; f16 and int8-code emission are
+// element-rate bound and want the most CTAs (2 stages).
+int tma_stages(const qfb_ctx* ctx, int dtype, bool chain, bool int8_out, uint64_t chunks) {
   if (ctx->tma_stages_env) return ctx->tma_stages_env;
-  if (chain || dtype != 0) return 2;
+  if (chain || dtype != 0 || int8_out) return 2;
   const uint64_t ctas4 = (uint64_t)ctx->sm_count * (uint64_t)std::max(1, ctx->tma_blocks_per_sm[dtype][0][4]);
   return chunks >= 64 * ctas4 ? 4 : 3;
 }
@@ -265,7 +267,9 @@ qfb_status run_ew(qfb_ctx* ctx, int dtype, const std::vector<EwDesc>& descs, boo
     b.n = n;
     b.chunk_begin[n] = chunks;
     if (chunks == 0) continue;
-    const int stages = tma_stages(ctx, dtype, chain, chunks);
+    bool int8_out = false;
+    for (int k = 0; k < n; ++k) int8_out = int8_out || (b.d[k].flags & kEwInt8Out) != 0;
+    const int stages = tma_stages(ctx, dtype, chain, int8_out, chunks);
     const int tma_per_sm = ctx->tma_blocks_per_sm[dtype][chain ? 1 : 0][stages];
     bool all_vec = tma_per_sm > 0;
     for (int k = 0; k < n && all_vec; ++k) all_vec = b.d[k].vec > 1;
@@ -530,7 +534,8 @@ qfb_status qfb_fq_fwd_multi(qfb_ctx* ctx, qfb_dtype dtype, const qfb_fq_desc* ta
     float q;
     if (qfb_status st = q_of(t.q_max, &q)) return st;
     EwJob j{t.x, nullptr, nullptr, {t.y[0], t.y[1]}, {t.scale[0], t.scale[1]}, t.outer,
-            t.channels, t.inner, t.n_out, QFB_ACT_NONE, t.flags & (kEwHalfGrid | kEwStreaming), q};
+            t.channels, t.inner, t.n_out, QFB_ACT_NONE,
+            t.flags & (kEwHalfGrid | kEwStreaming | kEwInt8Out), q};
     if (qfb_status st = plan_ew(dtype, j, d)) return st;
   }
   DeviceGuard g(ctx->device);

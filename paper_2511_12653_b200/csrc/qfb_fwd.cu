@@ -46,6 +46,40 @@ __device__ __forceinline__ void fq_unit(const float* v, float s, float q, float*
   }
 }
 
+// int8 codes of one unit (quant.hpp:174-207: (int8)nearbyintf(clip(x/s)),
+// NaN -> 0), with the same proven division shortcut as the FQ value: the
+// clipped, rounded quotient is identical to rint(clip(IEEE x/s)).
+template <int V>
+__device__ __forceinline__ void code_unit(const float* v, float s, float y, bool fast, float q,
+                                          uint32_t* c) {
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    if (fast) {
+      const float q0 = __fmul_rn(v[i], y);
+      float z = __fmaf_rn(__fmaf_rn(-s, q0, v[i]), y, q0);
+      z = fabsf(q0) < 0x1p100f ? z : q0;
+      z = fminf(fmaxf(copysignf(z, v[i]), -q), q);
+      // round-to-nearest-even into the low byte: 1.5*2^23 + z, |z| <= q
+      const uint32_t b = __float_as_uint(__fadd_rn(z, 12582912.0f));
+      c[i] = isnan(v[i]) ? 0u : b;
+    } else {
+      c[i] = (uint32_t)(uint8_t)fq_code(v[i], s, q);
+    }
+  }
+}
+
+// Store V codes (low bytes of c) at unit u of an int8 output (V bytes).
+template <int V>
+__device__ __forceinline__ void store_codes(void* y, uint32_t u, const uint32_t* c) {
+  uint32_t w[V / 4];
+#pragma unroll
+  for (int k = 0; k < V / 4; ++k)
+    w[k] = __byte_perm(__byte_perm(c[4 * k], c[4 * k + 1], 0x0040), __byte_perm(c[4 * k + 2], c[4 * k + 3], 0x0040),
+                       0x5410);
+  if constexpr (V == 4) reinterpret_cast<uint32_t*>(y)[u] = w[0];
+  else reinterpret_cast<uint2*>(y)[u] = make_uint2(w[0], w[1]);
+}
+
 // Vector path: every unit is one 16-byte vector, all its elements share a
 // channel (host guarantees inner % kPerVec == 0 and 16-byte alignment).
 // kChain = false is the plain multi-output fake-quant forward (no b, no
@@ -95,8 +129,15 @@ __device__ __forceinline__ void ew_vec(const EwDesc& d, uint32_t ubase, bool& nf
       }
     }
     for (int j = 0; j < d.n_out; ++j) {
+      const float s = __ldg(d.s[j] + ch);
+      if (d.flags & kEwInt8Out) {
+        uint32_t c[V];
+        code_unit<V>(v, s, fast_div_ok(s) ? __frcp_rn(s) : 1.0f, fast_div_ok(s), d.q, c);
+        store_codes<V>(d.y[j], u, c);
+        continue;
+      }
       float o[V];
-      fq_unit<V>(v, __ldg(d.s[j] + ch), d.q, o);
+      fq_unit<V>(v, s, d.q, o);
       st_v4(static_cast<uint4*>(d.y[j]) + u, Elem<T>::pack(o, v, half_out, nf), streaming);
     }
   }
@@ -128,6 +169,10 @@ __device__ __forceinline__ void ew_scalar(const EwDesc& d, uint32_t ubase, bool&
     if (demote_in) v = half_grid(v, v, nf);
     if (d.preact != nullptr) Elem<T>::store1(d.preact, u, v, v, false, nf);
     for (int j = 0; j < d.n_out; ++j) {
+      if (d.flags & kEwInt8Out) {
+        static_cast<int8_t*>(d.y[j])[u] = fq_code(v, __ldg(d.s[j] + ch), d.q);
+        continue;
+      }
       float o;
       fq_unit<1>(&v, __ldg(d.s[j] + ch), d.q, &o);
       Elem<T>::store1(d.y[j], u, o, v, half_out, nf);
@@ -286,6 +331,16 @@ __global__ void __launch_bounds__(kEwThreads, (kChain ? 6 : 10) / kFwdStages)
         }
         // act/add may create inf/NaN from finite inputs: take the checked pack
         special = true;
+      }
+      if (!kChain && (d.flags & kEwInt8Out)) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          if (j >= d.n_out) break;
+          uint32_t c[V];
+          code_unit<V>(v, sc[j], rc[j], fast[j], qv, c);
+          store_codes<V>(d.y[j], u, c);
+        }
+        continue;
       }
 #pragma unroll
       for (int j = 0; j < 2; ++j) {

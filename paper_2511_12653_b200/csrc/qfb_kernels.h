@@ -48,6 +48,7 @@ constexpr int kMaxEwDesc = 96;
 
 constexpr uint32_t kEwHalfGrid = 0x1u;   // == QFB_FLAG_HALF_GRID
 constexpr uint32_t kEwStreaming = 0x2u;  // == QFB_FLAG_STREAMING
+constexpr uint32_t kEwInt8Out = 0x4u;    // == QFB_FLAG_INT8_OUT: outputs are int8 codes
 constexpr uint32_t kEwDemoteIn = 0x100u; // chain: demote v before FQ
 
 // One fused elementwise job: v = act(a (+ b)) [demote]; preact = v;

@@ -71,7 +71,7 @@ def frame_bytes(points: List[QuantPoint], esize: int) -> dict:
     uniq = sum(p.numel for p in points)
     qp = sum(p.numel * len(p.consumers) for p in points)
     return {"fwd": (uniq + qp) * esize, "bwd": 3 * qp * esize, "unique_elems": uniq,
-            "quant_point_elems": qp}
+            "quant_point_elems": qp, "fwd_int8": uniq * esize + qp}
 
 
 class FrontendQuantPass:
@@ -81,10 +81,14 @@ class FrontendQuantPass:
     steps never hit L2-resident inputs."""
 
     def __init__(self, ctx: Context, frames: int = 1, dtype: str = "f32", sets: int = 1,
-                 seed: int = 1, device=None, h: int = H, w: int = W):
+                 seed: int = 1, device=None, h: int = H, w: int = W, int8_out: bool = False):
+        """int8_out: the forward emits the int8 codes of every quant point
+        (QFB_FLAG_INT8_OUT, 1 byte per element) instead of the
+        fake-quant values; the backward is unchanged."""
         import torch
         self.ctx = ctx
         self.frames = frames
+        self.int8_out = int8_out
         self.dtype_code = F32 if dtype == "f32" else F16
         tdt = torch.float32 if dtype == "f32" else torch.float16
         self.esize = 4 if dtype == "f32" else 2
@@ -104,9 +108,11 @@ class FrontendQuantPass:
             self.fac.append(torch.tensor(s64 + chain, dtype=torch.float64, device=dev))
             self.dls.append(torch.zeros(p.channels, dtype=torch.float64, device=dev))
         # outputs shared across sets (written every step)
-        self.y = [torch.empty((frames, p.channels, p.height, p.width), dtype=tdt, device=dev)
+        ydt = torch.int8 if int8_out else tdt
+        self.y = [torch.empty((frames, p.channels, p.height, p.width), dtype=ydt, device=dev)
                   for p, _ in self.consumers]
-        self.dx = [torch.empty_like(t) for t in self.y]
+        self.dx = [torch.empty((frames, p.channels, p.height, p.width), dtype=tdt, device=dev)
+                   for p, _ in self.consumers]
         self.sets = []
         for si in range(sets):
             xs = []
@@ -131,7 +137,7 @@ class FrontendQuantPass:
             d = CFqDesc()
             d.x = xs[pi].data_ptr()
             d.outer, d.channels, d.inner = self.frames, p.channels, p.inner
-            d.n_out, d.q_max, d.flags = len(p.consumers), 127, 0
+            d.n_out, d.q_max, d.flags = len(p.consumers), 127, (0x4 if self.int8_out else 0)
             for k in range(len(p.consumers)):
                 d.y[k] = self.y[ci + k].data_ptr()
                 d.scale[k] = self.s32[ci + k].data_ptr()
