@@ -424,38 +424,6 @@ __device__ __forceinline__ void produce(const BwdBatch& bt, const TileRef& r, St
   }
 }
 
-// d_input of one consumer warp, written by the warp itself right after it
-// computed it into the stage: the warp's 32 leaf groups are one contiguous
-// element range of the tile, stored with 16-byte coalesced vectors (ragged
-// ends scalar). No bulk store, so the stage is free for its refill as soon
-// as the consumers arrive on done.
-template <typename T>
-__device__ __forceinline__ void warp_store_dx(const BwdDesc& d, const TileRef& cur, const T* stx,
-                                              int glo, int glen, int lane) {
-  if (__shfl_sync(0xffffffffu, glen, 0) == 0) return;  // no groups in this warp
-  const int lo = __shfl_sync(0xffffffffu, glo, 0);
-  const int hi = (int)__reduce_max_sync(0xffffffffu, (unsigned)(glen ? glo + glen : 0));
-  T* dst = static_cast<T*>(d.dx) + cur.A;
-  const T* src = stx + cur.off;
-  constexpr int kV = 16 / sizeof(T);
-  if (!d.vec) {
-    for (int e = lo + lane; e < hi; e += 32) dst[e] = src[e];
-    return;
-  }
-  // global byte address of element e: (A + e) * sizeof(T); the stage keeps
-  // the same alignment mod 16 (bulk copies start at a 16-byte window)
-  const uint32_t mis = (uint32_t)(((cur.A + (uint64_t)lo) * sizeof(T)) & 15u);
-  int e0 = lo + (int)(((16u - mis) & 15u) / sizeof(T));
-  if (e0 > hi) e0 = hi;
-  const int nvec = (hi - e0) / kV;
-  const int e1 = e0 + nvec * kV;
-  if (lane < e0 - lo) dst[lo + lane] = src[lo + lane];
-  if (lane < hi - e1) dst[e1 + lane] = src[e1 + lane];
-  const uint4* vs = reinterpret_cast<const uint4*>(src + e0);
-  uint4* vd = reinterpret_cast<uint4*>(dst + e0);
-  for (int u = lane; u < nvec; u += 32) vd[u] = vs[u];
-}
-
 // Perfect tree over the tile's 2^g group sums, lane part: each lane folds
 // `per` consecutive sums as a perfect subtree (read into registers before
 // the stage is refilled); tile_sum() finishes with an xor butterfly.
