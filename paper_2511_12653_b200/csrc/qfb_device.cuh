@@ -89,6 +89,17 @@ __device__ __forceinline__ float fq_value_fast(float x, float s, float y, float 
   return isnan(x) ? quiet_nan(x) : r;
 }
 
+// fq_value_fast for a finite, non-NaN x with |x * y| < 2^100 (binary16
+// inputs, |x| <= 65504, with s >= 2^-80): the overflow guard and the NaN
+// select of fq_value_fast are identities there and are dropped.
+__device__ __forceinline__ float fq_value_fast_finite(float x, float s, float y, float q) {
+  const float q0 = __fmul_rn(x, y);
+  float z = __fmaf_rn(__fmaf_rn(-s, q0, x), y, q0);
+  z = copysignf(z, x);
+  z = fminf(fmaxf(z, -q), q);
+  return __fmul_rn(s, rintf(z));
+}
+
 // Pin a uniform in a register (stops rematerialization from the
 // dynamically indexed parameter bank at every use).
 __device__ __forceinline__ float pin_f(float v) {

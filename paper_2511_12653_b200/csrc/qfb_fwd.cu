@@ -329,8 +329,10 @@ __global__ void __launch_bounds__(kEwThreads, (kChain ? 6 : 10) / kFwdStages)
         if (d.preact != nullptr) {
           st_v4(static_cast<uint4*>(d.preact) + u, Elem<T>::pack(v, v, false, nf), streaming);
         }
-        // act/add may create inf/NaN from finite inputs: take the checked pack
-        special = true;
+        // f16 units: finite a, b stay finite through add (|a + b| <= 131008
+        // in float), ReLU and the portable GELU, so `special` (inf/NaN in a
+        // or b) still selects the guarded FQ and the checked pack; f32 units
+        // are always treated as special (no screening)
       }
       if (!kChain && (d.flags & kEwInt8Out)) {
 #pragma unroll
@@ -346,7 +348,11 @@ __global__ void __launch_bounds__(kEwThreads, (kChain ? 6 : 10) / kFwdStages)
       for (int j = 0; j < 2; ++j) {
         if (j >= d.n_out) break;
         float o[V];
-        if (fast[j]) {
+        if (sizeof(T) == 2 && !special && fast[j] && sc[j] >= 0x1p-80f) {
+          // binary16 unit without inf/NaN: |x / s| < 2^96, no guards needed
+#pragma unroll
+          for (int i = 0; i < V; ++i) o[i] = fq_value_fast_finite(v[i], sc[j], rc[j], qv);
+        } else if (fast[j]) {
 #pragma unroll
           for (int i = 0; i < V; ++i) o[i] = fq_value_fast(v[i], sc[j], rc[j], qv);
         } else {

@@ -309,3 +309,32 @@ def test_resolve_scales_device_close(qfb, cuda):
     assert np.array_equal(s32.cpu().numpy(), np.array(hs, dtype=np.float64).astype(np.float32)) or \
         np.sum(s32.cpu().numpy() != np.array(hs).astype(np.float32)) <= 2
     assert np.max(np.abs(ch.cpu().numpy() - hc)) < 1e-15
+
+
+@pytest.mark.parametrize("act", [0, 1, 2])
+def test_chain_f16_extremes(qfb, orc, cuda, act):
+    """binary16 chains through the screened fast path and its exits:
+    a + b beyond 65504 (saturating demotion), inf/NaN operands (guarded FQ,
+    checked pack, non-finite latch), scales below 2^-80 (guarded FQ), and
+    plain FQ of f16 inputs with the same mix."""
+    import torch
+    rng = np.random.default_rng(31 + act)
+    C, H, W = 8, 16, 64
+    a = rng.normal(0, 2, (C, H, W)).astype(np.float16).astype(np.float32)
+    b = rng.normal(0, 2, (C, H, W)).astype(np.float16).astype(np.float32)
+    a[1, :, :8] = 60000.0
+    b[1, :, :8] = 60000.0
+    a[2, 0, :4] = [65504.0, -65504.0, 0.0, -0.0]
+    b[3, 0, :4] = [-0.0, 1.0, -65504.0, 2.0]
+    s = np.exp(rng.uniform(-6, -2, C))
+    s[4] = 1e-30
+    s[5] = 30.0
+    st, ys, _ = orc.fq_chain(a, b, [s], 1, C, H * W, act=act, half=1)
+    outs, _ = qfb.fq_chain(to_dev(a, cuda, torch.float16), to_dev(b, cuda, torch.float16), scales=(s.tolist(),),
+                           act=act, half=True, channel_axis=0)
+    assert np.array_equal(bits32(host(outs[0]).ravel()), bits32(ys[0]))
+    # plain forward on the same f16 tensor, with infinities (FQ(+-inf) = +-q*s)
+    a[2, 0, :2] = [np.inf, -np.inf]
+    y = qfb.fake_quantize(to_dev(a, cuda, torch.float16), s.tolist())
+    _, want = orc.fake_quantize(a, s, 1, C, H * W, half=1)
+    assert np.array_equal(bits32(host(y).ravel()), bits32(want))
