@@ -10,7 +10,8 @@
  *
  * GELU: the reference has no GELU (parity unpinned). This
  * header DEFINES the GELU of the fused chain (tanh form,
- * 0.5*x*(1+tanh(sqrt(2/pi)*(x+0.044715*x^3)))) with a portable expf, and the
+ * 0.5*x*(1+tanh(sqrt(2/pi)*(x+0.044715*x^3))), evaluated as x/(1+e^{-2u}))
+ * with a portable expf, and the
  * CPU oracle includes this same header, so oracle and kernel agree bitwise
  * by construction. It is the only code shared by oracle and product.
  */
@@ -76,18 +77,16 @@ QFB_HD float qfb_p_expf(float x) {
   return QFB_P_MUL(QFB_P_MUL(p, qfb_p_exp2i(k1)), qfb_p_exp2i(k2));
 }
 
-/* tanh-form GELU. +-inf map to +inf / -0. */
+/* tanh-form GELU, 0.5 x (1 + tanh(u)) with u = sqrt(2/pi) (x + 0.044715 x^3),
+ * evaluated as the identical x * sigmoid(2u) = x / (1 + e^{-2u}): one
+ * portable exp and one IEEE division. +inf -> +inf, -inf -> -0 (the
+ * limits; -inf / inf would be NaN). */
 QFB_HD float qfb_p_gelu(float x) {
+  if (x < -3.0e38f) return -0.0f;
   const float x3 = QFB_P_MUL(QFB_P_MUL(x, x), x);
   const float u = QFB_P_MUL(0.7978845834732055664f, QFB_P_FMA(0.044715f, x3, x));
-  const float au = u < 0.0f ? -u : u;
-  const float e = qfb_p_expf(QFB_P_MUL(2.0f, au));
-  /* tanh(|u|) = 1 - 2/(e^{2|u|}+1) */
-  float t = QFB_P_ADD(1.0f, -QFB_P_DIV(2.0f, QFB_P_ADD(e, 1.0f)));
-  if (u < 0.0f) t = -t;
-  const float hx = QFB_P_MUL(0.5f, x);
-  if (x < -3.0e38f) return -0.0f; /* 0.5*(-inf)*0 would be NaN */
-  return QFB_P_MUL(hx, QFB_P_ADD(1.0f, t));
+  const float e = qfb_p_expf(QFB_P_MUL(-2.0f, u));
+  return QFB_P_DIV(x, QFB_P_ADD(1.0f, e));
 }
 
 #endif /* QFB_PORTABLE_H_ */
