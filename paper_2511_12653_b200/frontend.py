@@ -242,6 +242,7 @@ class WindowChainPass:
         rng = np.random.default_rng(seed)
         L = lib()
         self.keep = []
+        self.buffers = []   # per point: (a, b or None, [y], [scale]) for checks
         descs = []
         for pi, p in enumerate(self.points):
             a = torch.empty(p.numel, dtype=tdt, device=dev)
@@ -258,12 +259,16 @@ class WindowChainPass:
             d.preact = 0
             d.outer, d.channels, d.inner = p.outer, p.channels, p.inner
             d.n_out, d.act, d.dtype, d.q_max, d.flags = p.consumers, p.act, self.dtype_code, 127, 0
+            ys, ss = [], []
             for k in range(p.consumers):
                 s = np.exp(rng.uniform(np.log(1e-3), np.log(0.1), p.channels)).astype(np.float32)
                 st = torch.from_numpy(s).to(dev)
                 y = torch.empty(p.numel, dtype=tdt, device=dev)
                 d.y[k], d.scale[k] = y.data_ptr(), st.data_ptr()
                 self.keep += [st, y]
+                ys.append(y)
+                ss.append(s)
+            self.buffers.append((a, b, ys, ss))
             self.keep += [a] + ([b] if b is not None else [])
             descs.append(d)
         self.table = (CChainDesc * len(descs))(*descs)
