@@ -304,7 +304,7 @@ def run_qfb(args):
         if pg is not None:
             # QAT exchange: per-frame scale-gradient rows, all-gathered and
             # folded in frame order (bit-identical at any GPU count)
-            gather_fold(torch.cat(fp.dls).unsqueeze(0))
+            gather_fold(fp.dls_flat.unsqueeze(0))
 
     def eager_step(i, ev=None):
         si = i % nsets
@@ -516,6 +516,8 @@ def run_secondary(args, ctx, stream, dev, peak, rank, ws):
     out["c5_forward_throughput"] = c5
     del fp
     torch.cuda.empty_cache()
+    out["c4_qat_step"] = run_qat_step(args, ctx, stream, dev, peak, rank, ws)
+    out["c1_per_tensor_fwd"] = run_c1(args, ctx, stream, dev, peak, rank, ws)
     # f2: the same forward emitting int8 codes (1 byte per quant-point element)
     fq = FrontendQuantPass(ctx, frames=8, dtype=args.dtype, sets=2, seed=11 + rank, device=dev,
                            int8_out=True)
@@ -535,6 +537,97 @@ def run_secondary(args, ctx, stream, dev, peak, rank, ws):
     del fq
     torch.cuda.empty_cache()
     return out
+
+
+def run_c1(args, ctx, stream, dev, peak, rank, ws):
+    """BASELINE config 1: per-tensor fake-quant forward of the fnet output
+    map [1, 128, 120, 160]: the latency of one call (inputs
+    resident) and GB/s over 128 rotating distinct maps (2.5 GB >> L2); the
+    reference's fake_quantize on one host thread beside it."""
+    import torch
+    import paper_2511_12653_b200 as q
+    n = 128 * 120 * 160
+    tdt = torch.float32 if args.dtype == "f32" else torch.float16
+    esize = 4 if args.dtype == "f32" else 2
+    L = q.lib()
+    xs = torch.empty((128, n), dtype=tdt, device=dev)
+    q.check(L.qfb_fill_rng(ctx.handle, 0 if args.dtype == "f32" else 1, xs.data_ptr(), xs.numel(), 1, 0, 0, 1,
+                           1.0, 0.0))
+    ys = torch.empty_like(xs)
+    s = torch.tensor([q.resolve_scale([q.softplus_inv(4.0 / 127)])[0]], dtype=torch.float32, device=dev)
+    dt = 0 if args.dtype == "f32" else 1
+    k = [0]
+
+    def one():
+        i = k[0] % 128
+        k[0] += 1
+        q.check(L.qfb_fq_fwd(ctx.handle, dt, xs[i].data_ptr(), ys[i].data_ptr(), 1, 1, n, s.data_ptr(), 127, 0))
+    lat = time_device(one, stream, reps=1, warmup=3)
+    ms = time_device(one, stream, reps=256, warmup=8)
+    gb = 2 * n * esize / (ms / 1e3) / 1e9
+    res = {"us_single_call": lat * 1e3, "us_per_call_rotating": ms * 1e3, "gbps": gb, "hbm_frac": gb / peak,
+           "workload": "BASELINE config 1: per-tensor fake-quant fwd of [1,128,120,160], 128 rotating maps"}
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        try:
+            import numpy as np
+            import oracle
+            if oracle.reference_available():
+                ref = oracle.Reference()
+                x = xs[0].float().cpu().numpy().reshape(1, 128, 120, 160)
+                sv = float(s.item())
+                ref.fake_quantize(x, x.shape, [sv])            # warm
+                t0 = time.perf_counter()
+                reps = 5
+                for _ in range(reps):
+                    ref.fake_quantize(x, x.shape, [sv])
+                cpu_ms = (time.perf_counter() - t0) * 1e3 / reps
+                res["cpu_baseline"] = {"ms_per_call": cpu_ms, "cores": 1, "kind": "reference",
+                                       "sample": f"{reps} calls of qf::fake_quantize per-tensor on the "
+                                                 f"same map, one host thread"}
+        except Exception as exc:  # pragma: no cover
+            res["cpu_baseline"] = {"value": None, "sample": f"failed: {exc}"}
+    del xs, ys
+    torch.cuda.empty_cache()
+    return res
+
+
+def run_qat_step(args, ctx, stream, dev, peak, rank, ws):
+    """BASELINE config 4: one scale-only QAT step over 64 frames (64 / N per
+    rank): fused fake-quant forward, per-frame distillation loss (fnet and
+    inet pairs), scale-only backward (frame rows accumulated in order), Adam
+    on the 1,494 scales (+ at N > 1 the gather-fold of the scale gradients).
+    Convolutions excluded (cuDNN); features and upstream are synthetic. The
+    step's ~260 launches replay as one CUDA graph."""
+    import torch
+    from paper_2511_12653_b200.dist import gather_fold
+    from paper_2511_12653_b200.frontend import QatStep
+    frames = max(1, 64 // ws)
+    qs = QatStep(ctx, frames=frames, dtype=args.dtype, seed=21 + rank, device=dev)
+    for _ in range(2):
+        qs.run()
+    torch.cuda.synchronize(dev)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        qs.run()
+
+    def step():
+        g.replay()
+        if ws > 1:
+            gather_fold(qs.grads.unsqueeze(0))
+    ms = time_device(step, stream, reps=5, warmup=1)
+    if ws > 1:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = t.item()
+    gb = qs.bytes_per_step() / (ms / 1e3) / 1e9
+    res = {"ms_per_step": ms, "frames_per_step": 64, "frames_per_s": 64 / (ms / 1e3),
+           "gbps_per_gpu": gb, "hbm_frac": gb / peak, "scaling": "strong (64 frames over N GPUs)",
+           "workload": "BASELINE config 4: scale-only QAT step over 64 frames (fwd FQ 22 points, "
+                       "distill loss fnet+inet per frame, bwd FQ with frame-ordered accumulation, "
+                       "Adam on 1,494 scales); convolutions excluded"}
+    del qs, g
+    torch.cuda.empty_cache()
+    return res
 
 
 def run_e2e(args, q, ctx, fp, stream, dev, pg, ws):

@@ -408,6 +408,12 @@ qfb_status qfb_quant_pass_host(qfb_ctx* ctx, qfb_precision prec,
 qfb_status qfb_distill_pair(qfb_ctx* ctx, const float* student, const float* teacher,
                             int64_t channels, int64_t hw, double lambda_cos,
                             double grad_scale, float* d_student, double* out2);
+/* The same for `pairs` independent pairs of one shape stored back to back */
+/* ([pairs, channels, hw], e.g. the frames of a chunk), in one set of     */
+/* launches; out (DEVICE double[pairs][2]).                               */
+qfb_status qfb_distill_batch(qfb_ctx* ctx, const float* student, const float* teacher,
+                             int64_t pairs, int64_t channels, int64_t hw, double lambda_cos,
+                             double grad_scale, float* d_student, double* out);
 /* qf::distill_loss (distill.hpp:126-141) on HOST buffers: out5 = {total,   */
 /* mse_f, mse_i, cos_f, cos_i}; d_features / d_descriptors host float32.   */
 qfb_status qfb_distill_loss_host(qfb_ctx* ctx, const float* f_s, const float* f_t,

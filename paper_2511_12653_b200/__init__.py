@@ -634,6 +634,7 @@ def model_layer_counts(plan: ExecutionPlan, n_act: int, c_out: int, per: int, we
 # ------------------------------------------------- QAT step --
 
 _sig("qfb_distill_pair", _i32, [_vp, _vp, _vp, _i64, _i64, ctypes.c_double, ctypes.c_double, _vp, _vp])
+_sig("qfb_distill_batch", _i32, [_vp, _vp, _vp, _i64, _i64, _i64, ctypes.c_double, ctypes.c_double, _vp, _vp])
 _sig("qfb_adam_bias_corrections", _i32, [ctypes.c_double, ctypes.c_double, _i64,
                                          ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)])
 _sig("qfb_adam_step", _i32, [_vp, _vp, _vp, _vp, _vp, _i64, ctypes.c_double, ctypes.c_double,

@@ -60,11 +60,12 @@ struct MseTerm {
   const float* s;
   const float* t;
   float* ds;
-  double inv_n2;  // unused (kept for layout); 2.0 * d / n is evaluated literally
   double n;
-  __device__ __forceinline__ double operator()(uint64_t i) const {
-    const double d = __dadd_rn((double)__ldg(s + i), -(double)__ldg(t + i));
-    ds[i] = __fadd_rn(0.0f, __double2float_rn(__ddiv_rn(__dmul_rn(2.0, d), n)));
+  uint64_t stride;  // elements per pair (batch b starts at b * stride)
+  __device__ __forceinline__ double operator()(uint32_t b, uint64_t i) const {
+    const uint64_t j = (uint64_t)b * stride + i;
+    const double d = __dadd_rn((double)__ldg(s + j), -(double)__ldg(t + j));
+    ds[j] = __fadd_rn(0.0f, __double2float_rn(__ddiv_rn(__dmul_rn(2.0, d), n)));
     return __dmul_rn(d, d);
   }
 };
@@ -72,40 +73,49 @@ struct MseTerm {
 // Stored terms (cosines per location).
 struct LoadTerm {
   const double* v;
-  __device__ __forceinline__ double operator()(uint64_t i) const { return v[i]; }
+  uint64_t stride;
+  __device__ __forceinline__ double operator()(uint32_t b, uint64_t i) const {
+    return v[(uint64_t)b * stride + i];
+  }
 };
 
 template <typename Term>
-__device__ __forceinline__ double fold(const Term& f, uint64_t lo, uint64_t m) {
+__device__ __forceinline__ double fold(const Term& f, uint32_t b, uint64_t lo, uint64_t m) {
   double acc = 0.0;
-  for (uint64_t k = 0; k < m; ++k) acc = __dadd_rn(acc, f(lo + k));
+  for (uint64_t k = 0; k < m; ++k) acc = __dadd_rn(acc, f(b, lo + k));
   return acc;
 }
 
-// One thread per leaf group: its sum in the reference order.
+// One thread per leaf group of pair b = blockIdx.y: its sum in the
+// reference order.
 template <typename Term>
 __global__ void leaf_sums_kernel(Term f, uint64_t n, uint32_t depth, double* out) {
   const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t b = blockIdx.y;
   if (g >= (1u << depth)) return;
   uint64_t lo, m;
   node_of(n, g, depth, lo, m);
   double r;
   if (m <= 8) {
-    r = fold(f, lo, m);
+    r = fold(f, b, lo, m);
   } else {
     const uint64_t h = m >> 1;
-    r = __dadd_rn(fold(f, lo, h), fold(f, lo + h, m - h));
+    r = __dadd_rn(fold(f, b, lo, h), fold(f, b, lo + h, m - h));
   }
-  out[g] = r;
+  out[((uint64_t)b << depth) + g] = r;
 }
 
-// Perfect-tree halving: CTA b reduces in[2048 b .. 2048 b + 2048) (a power
-// of two count `cnt` <= 2048 when fewer remain) to out[b]. With `final`,
-// the single result is divided by `div` into res.
+// Perfect-tree halving: per pair y = blockIdx.y (cnt values each), CTA x
+// reduces in[2048 x .. 2048 x + 2048) (a power of two count `cnt` <= 2048
+// when fewer remain) to out[x]. On the last pass the single result per pair
+// is divided by `div` into res[y * res_stride].
 __global__ void __launch_bounds__(kRedThreads) halve_kernel(const double* in, uint32_t cnt,
-                                                            double* out, double div, double* res) {
+                                                            double* out, double div, double* res,
+                                                            uint32_t res_stride) {
   __shared__ double sm[2 * kRedThreads];
   const uint32_t per = cnt < 2u * kRedThreads ? cnt : 2u * kRedThreads;
+  in += (uint64_t)blockIdx.y * cnt;
+  out += (uint64_t)blockIdx.y * (cnt / per);
   const uint64_t base = (uint64_t)blockIdx.x * per;
   for (uint32_t i = threadIdx.x; i < per; i += kRedThreads) sm[i] = in[base + i];
   __syncthreads();
@@ -117,27 +127,28 @@ __global__ void __launch_bounds__(kRedThreads) halve_kernel(const double* in, ui
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    if (res) *res = __ddiv_rn(sm[0], div);
+    if (res) res[(uint64_t)blockIdx.y * res_stride] = __ddiv_rn(sm[0], div);
     else out[blockIdx.x] = sm[0];
   }
 }
 
-// pairwise_sum(terms, n) / div -> *res (device), via scratch `ws` (>= 2^D
-// + 2^D/2048 doubles).
+// pairwise_sum(terms of pair b, n) / div -> res[b * res_stride] for the nb
+// pairs, via scratch `ws` (>= nb * (2^D + 2^D/2048) doubles).
 template <typename Term>
-cudaError_t pairwise_sum_dev(const Term& f, uint64_t n, double div, double* res, double* ws,
-                             cudaStream_t st, int* launches) {
+cudaError_t pairwise_sum_dev(const Term& f, uint64_t n, uint32_t nb, double div, double* res,
+                             uint32_t res_stride, double* ws, cudaStream_t st, int* launches) {
   const uint32_t depth = tree_depth(n);
   const uint32_t groups = 1u << depth;
-  leaf_sums_kernel<Term><<<(groups + 255) / 256, 256, 0, st>>>(f, n, depth, ws);
+  leaf_sums_kernel<Term><<<dim3((groups + 255) / 256, nb), 256, 0, st>>>(f, n, depth, ws);
   ++*launches;
   double* in = ws;
-  double* out = ws + groups;
+  double* out = ws + (uint64_t)nb * groups;
   uint32_t cnt = groups;
   for (;;) {
     const uint32_t per = cnt < 2u * kRedThreads ? cnt : 2u * kRedThreads;
     const uint32_t blocks = cnt / per;
-    halve_kernel<<<blocks, kRedThreads, 0, st>>>(in, cnt, out, div, blocks == 1 ? res : nullptr);
+    halve_kernel<<<dim3(blocks, nb), kRedThreads, 0, st>>>(in, cnt, out, div, blocks == 1 ? res : nullptr,
+                                                          res_stride);
     ++*launches;
     if (blocks == 1) break;
     double* t = in;
@@ -150,12 +161,21 @@ cudaError_t pairwise_sum_dev(const Term& f, uint64_t n, double div, double* res,
 
 // Per-location cosine + its gradient (distill.hpp:94-121), then the
 // trainer's chunk scaling of the whole gradient column (distill.hpp:245).
+// One thread per (pair, location): the channel loops are sequential in the
+// reference order; the loads of a channel step are independent of the
+// accumulations, so unrolling keeps several in flight.
 __global__ void cosine_kernel(const float* __restrict__ s, const float* __restrict__ t,
                               float* __restrict__ ds, uint64_t c, uint64_t hw, double w,
                               double gscale, double* __restrict__ cos_loc) {
   const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= hw) return;
+  const uint64_t pair = blockIdx.y;
+  s += pair * c * hw;
+  t += pair * c * hw;
+  ds += pair * c * hw;
+  cos_loc += pair * hw;
   double dot = 0.0, na2 = 0.0, nb2 = 0.0;
+#pragma unroll 8
   for (uint64_t ch = 0; ch < c; ++ch) {
     const double a = (double)__ldg(s + ch * hw + p);
     const double b = (double)__ldg(t + ch * hw + p);
@@ -170,6 +190,7 @@ __global__ void cosine_kernel(const float* __restrict__ s, const float* __restri
     cosv = __ddiv_rn(dot, nrm);
   }
   cos_loc[p] = cosv;
+#pragma unroll 4
   for (uint64_t ch = 0; ch < c; ++ch) {
     const uint64_t i = ch * hw + p;
     float g = ds[i];
@@ -232,41 +253,49 @@ qfb_status err(qfb_status st, const std::string& m) { return set_error(st, m.c_s
 
 extern "C" {
 
-qfb_status qfb_distill_pair(qfb_ctx* ctx, const float* student, const float* teacher,
-                            int64_t channels, int64_t hw, double lambda_cos, double grad_scale,
-                            float* d_student, double* out2) {
+qfb_status qfb_distill_batch(qfb_ctx* ctx, const float* student, const float* teacher, int64_t pairs,
+                             int64_t channels, int64_t hw, double lambda_cos, double grad_scale,
+                             float* d_student, double* out) {
   if (!ctx) return err(QFB_ERR_VALUE, "null qfb_ctx");
   if (channels < 1) return err(QFB_ERR_SHAPE, "distill_loss: channel dim must be >= 1");
-  if (hw < 1) return err(QFB_ERR_SHAPE, "distill_loss: non-positive spatial size");
-  if (!student || !teacher || !d_student || !out2) return err(QFB_ERR_VALUE, "distill_pair: null pointer");
+  if (hw < 1 || pairs < 1) return err(QFB_ERR_SHAPE, "distill_loss: non-positive size");
+  if (pairs > 65535) return err(QFB_ERR_UNSUPPORTED, "distill_batch: at most 65535 pairs per call");
+  if (!student || !teacher || !d_student || !out) return err(QFB_ERR_VALUE, "distill_pair: null pointer");
   Guard g(ctx_device(ctx));
   const cudaStream_t st = ctx_stream(ctx);
   const uint64_t n = (uint64_t)channels * (uint64_t)hw;
+  const uint32_t nb = (uint32_t)pairs;
   const uint64_t groups_n = 1ull << tree_depth(n), groups_hw = 1ull << tree_depth((uint64_t)hw);
   if (groups_n >= (1ull << 31)) return err(QFB_ERR_UNSUPPORTED, "distill_pair: tensor too large");
   void *ws = nullptr, *cl = nullptr;
   const uint64_t gmax = groups_n > groups_hw ? groups_n : groups_hw;
-  if (qfb_status s = ctx_scratch(ctx, 0, (gmax + gmax / 2048 + 2) * sizeof(double), &ws)) return s;
-  if (qfb_status s = ctx_scratch(ctx, 1, (uint64_t)hw * sizeof(double), &cl)) return s;
+  if (qfb_status s = ctx_scratch(ctx, 0, nb * (gmax + gmax / 2048 + 2) * sizeof(double), &ws)) return s;
+  if (qfb_status s = ctx_scratch(ctx, 1, nb * (uint64_t)hw * sizeof(double), &cl)) return s;
   int launches = 0;
   // MSE (+ d_s = float(2d/n)) then per-location cosine (+ its gradient and
   // the chunk scaling), then the mean cosine over locations
-  MseTerm mt{student, teacher, d_student, 0.0, (double)n};
-  cudaError_t e = pairwise_sum_dev(mt, n, (double)n, out2, static_cast<double*>(ws), st, &launches);
+  MseTerm mt{student, teacher, d_student, (double)n, n};
+  cudaError_t e = pairwise_sum_dev(mt, n, nb, (double)n, out, 2, static_cast<double*>(ws), st, &launches);
   if (e == cudaSuccess) {
     const double w = lambda_cos / (double)hw;
-    cosine_kernel<<<(unsigned)(((uint64_t)hw + 255) / 256), 256, 0, st>>>(
+    cosine_kernel<<<dim3((unsigned)(((uint64_t)hw + 255) / 256), nb), 256, 0, st>>>(
         student, teacher, d_student, (uint64_t)channels, (uint64_t)hw, w, grad_scale,
         static_cast<double*>(cl));
     ++launches;
     e = cudaGetLastError();
   }
   if (e == cudaSuccess)
-    e = pairwise_sum_dev(LoadTerm{static_cast<const double*>(cl)}, (uint64_t)hw, (double)hw, out2 + 1,
-                         static_cast<double*>(ws), st, &launches);
+    e = pairwise_sum_dev(LoadTerm{static_cast<const double*>(cl), (uint64_t)hw}, (uint64_t)hw, nb, (double)hw,
+                         out + 1, 2, static_cast<double*>(ws), st, &launches);
   ctx_count_launches(ctx, launches);
-  if (e != cudaSuccess) return cuda_error(e, "distill_pair");
+  if (e != cudaSuccess) return cuda_error(e, "distill_batch");
   return QFB_OK;
+}
+
+qfb_status qfb_distill_pair(qfb_ctx* ctx, const float* student, const float* teacher,
+                            int64_t channels, int64_t hw, double lambda_cos, double grad_scale,
+                            float* d_student, double* out2) {
+  return qfb_distill_batch(ctx, student, teacher, 1, channels, hw, lambda_cos, grad_scale, d_student, out2);
 }
 
 qfb_status qfb_distill_loss_host(qfb_ctx* ctx, const float* f_s, const float* f_t, int64_t f_channels,

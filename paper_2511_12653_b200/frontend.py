@@ -81,7 +81,8 @@ class FrontendQuantPass:
     steps never hit L2-resident inputs."""
 
     def __init__(self, ctx: Context, frames: int = 1, dtype: str = "f32", sets: int = 1,
-                 seed: int = 1, device=None, h: int = H, w: int = W, int8_out: bool = False):
+                 seed: int = 1, device=None, h: int = H, w: int = W, int8_out: bool = False,
+                 grads_out=None):
         """int8_out: the forward emits the int8 codes of every quant point
         (QFB_FLAG_INT8_OUT, 1 byte per element) instead of the
         fake-quant values; the backward is unchanged."""
@@ -99,6 +100,11 @@ class FrontendQuantPass:
         L = lib()
         # scales: per consumer, per channel
         self.log_s, self.s32, self.fac, self.dls = [], [], [], []
+        n_grad = sum(p.channels for p, _ in self.consumers)
+        self.dls_flat = (grads_out if grads_out is not None
+                         else torch.zeros(n_grad, dtype=torch.float64, device=dev))
+        assert self.dls_flat.numel() == n_grad and self.dls_flat.dtype == torch.float64
+        goff = 0
         for p, _ in self.consumers:
             s = np.exp(rng.uniform(np.log(1e-3), np.log(0.1), p.channels))
             ls = np.log(np.expm1(s))
@@ -106,7 +112,8 @@ class FrontendQuantPass:
             self.log_s.append(ls)
             self.s32.append(torch.tensor(np.array(s64, dtype=np.float64).astype(np.float32), device=dev))
             self.fac.append(torch.tensor(s64 + chain, dtype=torch.float64, device=dev))
-            self.dls.append(torch.zeros(p.channels, dtype=torch.float64, device=dev))
+            self.dls.append(self.dls_flat[goff:goff + p.channels])
+            goff += p.channels
         # outputs shared across sets (written every step)
         ydt = torch.int8 if int8_out else tdt
         self.y = [torch.empty((frames, p.channels, p.height, p.width), dtype=ydt, device=dev)
@@ -165,8 +172,7 @@ class FrontendQuantPass:
         check(lib().qfb_fq_bwd_multi(self.ctx.handle, self.dtype_code, s["bwd"], s["nb"]))
 
     def scale_grads(self):
-        import torch
-        return torch.cat(self.dls)
+        return self.dls_flat
 
     def bytes_per_step(self) -> dict:
         b = frame_bytes(self.points, self.esize)
@@ -282,3 +288,87 @@ class WindowChainPass:
         """Algorithmic bytes: read a (+ b), write K outputs."""
         return sum(p.numel * (1 + (1 if p.residual else 0) + p.consumers) * self.esize
                    for p in self.points)
+
+
+# ------------------------------------------------------------------------
+# BASELINE config 4: the scale-only QAT step of a batch of frames
+# (distill.hpp:227-279) minus the convolutions (cuDNN territory): the fused
+# fake-quant forward of every activation quant point, the distillation loss
+# of every frame's fnet/inet outputs, the scale-only backward of every quant
+# point (frame rows accumulate in frame order, the trainer's g += grad), and
+# Adam on the scale vector. Features and upstream gradients are synthetic.
+# ------------------------------------------------------------------------
+
+class QatStep:
+    """One scale-only QAT step over `frames` frames on one GPU (or this
+    rank's shard); every piece is a qfb launch, capturable as one graph."""
+
+    def __init__(self, ctx: Context, frames: int = 64, dtype: str = "f32", seed: int = 21, device=None,
+                 h: int = H, w: int = W, lambda_cos: float = 1.0, lr: float = 5e-3,
+                 n_weight_scales: int = 592):
+        import torch
+        from . import adam_bias_corrections
+        self.ctx = ctx
+        self.frames = frames
+        self.lam = lambda_cos
+        self.lr = lr
+        dev = device if device is not None else torch.device("cuda", ctx.device)
+        n_act = sum(p.channels * len(p.consumers) for p in dpvo_quant_points(h, w))
+        self.n_act = n_act
+        self.n_params = n_act + n_weight_scales
+        # the backward writes its scale gradients straight into the optimizer's vector
+        self.grads = torch.zeros(self.n_params, dtype=torch.float64, device=dev)
+        self.fp = FrontendQuantPass(ctx, frames=frames, dtype=dtype, sets=1, seed=seed, device=dev, h=h, w=w,
+                                    grads_out=self.grads[:n_act])
+        h4, w4 = h // 4, w // 4
+        L = lib()
+        # synthetic student / teacher encoder outputs per frame (fnet 128, inet 384 channels)
+        self.feat = []
+        for k, c in enumerate((128, 384)):
+            t = [torch.empty((frames, c, h4, w4), dtype=torch.float32, device=dev) for _ in range(2)]
+            for j, tt in enumerate(t):
+                check(L.qfb_fill_rng(ctx.handle, F32, tt.data_ptr(), tt.numel(), seed + 17, 10 * k + j, 0, 1,
+                                     1.0, 0.0))
+            self.feat.append((c, t[0], t[1], torch.empty_like(t[0])))
+        # per pair (fnet, inet): [frames][mse, cos]; self.loss[f, k] views them
+        self.loss_k = [torch.zeros((frames, 2), dtype=torch.float64, device=dev) for _ in range(2)]
+        self.loss = torch.stack(self.loss_k, dim=1)  # refreshed by losses()
+        # flattened trainable scales: the activation scales of the pass + weight scales
+        self.params = torch.empty(self.n_params, dtype=torch.float64, device=dev)
+        self.params[:n_act] = torch.from_numpy(np.concatenate(self.fp.log_s)).to(dev)
+        self.params[n_act:] = -4.0
+        self.m = torch.zeros_like(self.params)
+        self.v = torch.zeros_like(self.params)
+        self.skipped = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.t = 1
+        self.bc = adam_bias_corrections(0.9, 0.999, self.t)
+        ctx.sync()
+        torch.cuda.synchronize(dev)
+
+    def run(self) -> None:
+        """fwd (1 launch) -> per-frame distill loss (2 pairs) -> bwd (1
+        launch + finisher, gradients land in the optimizer vector) -> Adam
+        (2 launches). All on the context's stream."""
+        from . import _lib, _vp
+        self.fp.forward(0)
+        inv = 1.0 / self.frames
+        for k, (c, s, t, d) in enumerate(self.feat):
+            # every frame's pair_loss in one batched call (per-frame trees)
+            hw = s.shape[2] * s.shape[3]
+            check(_lib.qfb_distill_batch(self.ctx.handle, _vp(s.data_ptr()), _vp(t.data_ptr()), self.frames, c,
+                                         hw, self.lam, inv, _vp(d.data_ptr()), _vp(self.loss_k[k].data_ptr())))
+        self.fp.backward(0)
+        b1, b2 = self.bc
+        check(_lib.qfb_adam_step(self.ctx.handle, _vp(self.params.data_ptr()), _vp(self.m.data_ptr()),
+                                 _vp(self.v.data_ptr()), _vp(self.grads.data_ptr()), self.n_params, 0.9, 0.999,
+                                 self.lr, 1e-8, b1, b2, _vp(self.skipped.data_ptr())))
+
+    def losses(self):
+        """[frames, 2 pairs, (mse, cos)] of the last run."""
+        import torch
+        return torch.stack(self.loss_k, dim=1)
+
+    def bytes_per_step(self) -> int:
+        b = self.fp.bytes_per_step()
+        feat = sum(2 * s.numel() * 4 + s.numel() * 4 for (_c, s, _t, _d) in self.feat)
+        return b["fwd"] + b["bwd"] + feat
