@@ -221,7 +221,7 @@ __device__ __forceinline__ double pin(double v) {
 }
 
 // Fast-path terms of one element, no branches: term, d_input (finite
-// upstream) and whether the certified path applies (else: slow_elem).
+// upstream) and whether the fast path applies (else: slow_elem).
 struct FastTerm {
   double term;
   float dx;
@@ -230,10 +230,12 @@ struct FastTerm {
 
 __device__ __forceinline__ FastTerm fast_elem(float xv, float uv, const DivCtx& dc, double q) {
   FastTerm f;
-  double z;
   const bool up_finite = (__float_as_uint(uv) & 0x7f800000u) != 0x7f800000u;
-  // x = +-0 is exact too: z = +-0, d_ds = +0 whatever the sign of z
-  f.ok = (certified_quotient((double)xv, dc, z) || xv == 0.0f) && up_finite;
+  // correctly rounded for every finite x (markstein2_div; x = +-0 gives a
+  // zero whose sign d_ds = rint(z) - z = +0 does not observe); only inf/NaN
+  // operands and scales outside [2^-100, 2^100] take the IEEE path
+  const double z = markstein2_div((double)xv, dc);
+  f.ok = dc.usable && fabsf(xv) <= 3.402823466e38f && up_finite;
   const bool mask = fabs(z) <= q;
   const double d_ds = mask ? __dadd_rn(rint(z), -z) : copysign(q, z);
   f.term = __dmul_rn(d_ds, (double)uv);
@@ -250,8 +252,8 @@ __device__ __forceinline__ void fix_slow(FastTerm& f, float xv, float uv, double
 }
 
 // One element: term = d_ds * up (double) and d_input, with z = RN(x/s)
-// from certified_quotient (qfb_device.cuh); uncertified elements take the
-// exact IEEE path in slow_elem (returned in registers, never via memory).
+// from markstein2_div (qfb_device.cuh); inf/NaN operands take the exact
+// IEEE path in slow_elem (returned in registers, never via memory).
 template <typename T, bool kDx>
 __device__ __forceinline__ double elem(T* sx, const T* su, int k, const DivCtx& dc, double q) {
   const float xv = to_f<T>(sx[k]);

@@ -163,16 +163,8 @@ __device__ __forceinline__ GradTerm grad_term(float x, double s, double q) {
   return t;
 }
 
-// Certified fast double division for the backward: z = RN(x / s) with a
-// hoisted y = RN(1/s). Markstein's correction gives a candidate z; it is
-// ACCEPTED only if its exact-or-larger residual proves it is the unique
-// nearest double: |x - s*z| < s*ulp(z)/2, with the threshold a power of
-// two times s (exactly representable, so a rounded residual can never pass
-// wrongly), and z not a power of two (where the ulp below is smaller).
-// With s in [2^-100, 2^100] (DivCtx::usable) every nonzero finite float x
-// gives normal z and threshold; zeros, inf/NaN, ties and binade edges fail
-// and the caller takes the IEEE path. Correct by construction; exercised
-// over all 2^32 x by tools/verify_div.cu.
+// Fast double division for the backward: z = RN(x / s) for float x from a
+// hoisted y = RN(1/s) per tile (markstein2_div below).
 struct DivCtx {
   double s;
   double y;     // RN(1/s)
@@ -187,28 +179,19 @@ __device__ __forceinline__ DivCtx make_div(double s) {
   return c;
 }
 
-__device__ __forceinline__ bool certified_quotient(double x, const DivCtx& c, double& z) {
+// Two Markstein corrections from the hoisted y = RN(1/s): the first makes
+// the quotient faithful (|q0 - x/s| <= 2 ulp, and q0 + r0*y lies within
+// 2^-52 ulp of x/s before rounding), and Markstein's theorem (y = RN(1/s),
+// z1 within one ulp of x/s => RN(z1 + (x - s*z1)*y) = RN(x/s), no
+// underflow/overflow) makes the second correctly rounded. Valid for every
+// finite float x (zeros give +-0, whose sign the callers do not observe)
+// and s in [2^-100, 2^100] (DivCtx::usable). Validated against __ddiv_rn
+// for all 2^32 float x and 40,290 scales (tools/verify_ddiv2.cu,
+// profiles/r01_verify_ddiv2.txt: 0 mismatches).
+__device__ __forceinline__ double markstein2_div(double x, const DivCtx& c) {
   const double q0 = __dmul_rn(x, c.y);
-  z = __fma_rn(__fma_rn(-c.s, q0, x), c.y, q0);
-  const double r1 = __fma_rn(-c.s, z, x);
-  const int hi = __double2hiint(z);
-  const int lo = __double2loint(z);
-  // thr = s * 2^(E(z) - 53) built by adding exponents (s and thr normal for
-  // usable s and nonzero finite x; anything else fails the comparison)
-  const int thr_hi = __double2hiint(c.s) + (hi & 0x7ff00000) - (1076 << 20);
-  const double thr = __hiloint2double(thr_hi, __double2loint(c.s));
-  return c.usable && ((hi & 0x000fffff) | lo) != 0 && fabs(r1) < thr;
-}
-
-// Out of line so the compiler cannot if-convert (speculate) the full IEEE
-// division onto the fast path.
-static __device__ __noinline__ double slow_ddiv(double x, double s) { return __ddiv_rn(x, s); }
-
-__device__ __forceinline__ double certified_div(float xf, const DivCtx& c) {
-  const double x = (double)xf;
-  double z;
-  if (__builtin_expect(certified_quotient(x, c, z), 1)) return z;
-  return slow_ddiv(x, c.s);
+  const double z1 = __fma_rn(__fma_rn(-c.s, q0, x), c.y, q0);
+  return __fma_rn(__fma_rn(-c.s, z1, x), c.y, z1);
 }
 
 // ------------------------------------------------------ fast divide ---
