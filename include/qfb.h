@@ -426,6 +426,12 @@ qfb_status qfb_distill_loss_host(qfb_ctx* ctx, const float* f_s, const float* f_
 /* host libm pow, like the reference). A non-finite gradient skips the     */
 /* whole update (grads.all_finite(), distill.hpp:254-258): *skipped        */
 /* (DEVICE u32) = number of non-finite gradients, 0 when applied.          */
+/* Row-order fold of nrows gradient rows [nrows, n] (DEVICE doubles):     */
+/* out = ((into + r0) + r1) + ... (into nullable: r0 + r1 + ...) — the    */
+/* combine step of the multi-GPU scale-gradient exchange, bit-identical   */
+/* to the trainer's frame-order accumulation (frontend.hpp:222-228).      */
+qfb_status qfb_fold_rows(qfb_ctx* ctx, const double* rows, int64_t nrows, int64_t n,
+                         const double* into, double* out);
 qfb_status qfb_adam_bias_corrections(double beta1, double beta2, int64_t t,
                                      double* bc1, double* bc2);
 qfb_status qfb_adam_step(qfb_ctx* ctx, double* params, double* m, double* v,

@@ -635,6 +635,7 @@ def model_layer_counts(plan: ExecutionPlan, n_act: int, c_out: int, per: int, we
 
 _sig("qfb_distill_pair", _i32, [_vp, _vp, _vp, _i64, _i64, ctypes.c_double, ctypes.c_double, _vp, _vp])
 _sig("qfb_distill_batch", _i32, [_vp, _vp, _vp, _i64, _i64, _i64, ctypes.c_double, ctypes.c_double, _vp, _vp])
+_sig("qfb_fold_rows", _i32, [_vp, _vp, _i64, _i64, _vp, _vp])
 _sig("qfb_adam_bias_corrections", _i32, [ctypes.c_double, ctypes.c_double, _i64,
                                          ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)])
 _sig("qfb_adam_step", _i32, [_vp, _vp, _vp, _vp, _vp, _i64, ctypes.c_double, ctypes.c_double,
@@ -698,3 +699,15 @@ def adam_step(params, m, v, grads, t: int, lr: float, beta1: float = 0.9, beta2:
                              _vp(grads.data_ptr()), params.numel(), beta1, beta2, lr, eps, bc1, bc2,
                              _vp(skipped.data_ptr())))
     return skipped
+
+
+def fold_rows_device(rows, into=None, ctx: Optional[Context] = None):
+    """((into + r0) + r1) + ... over the rows of a [R, n] float64 CUDA tensor
+    in one launch (qfb_fold_rows)."""
+    import torch
+    rows = rows.contiguous()
+    out = torch.empty(rows.shape[1:], dtype=torch.float64, device=rows.device)
+    ctx = ctx or default_context(rows.device.index)
+    check(_lib.qfb_fold_rows(ctx.handle, _vp(rows.data_ptr()), rows.shape[0], out.numel(),
+                             _vp(into.contiguous().data_ptr() if into is not None else None), _vp(out.data_ptr())))
+    return out

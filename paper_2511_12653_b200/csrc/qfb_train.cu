@@ -227,6 +227,18 @@ __global__ void adam_kernel(double* __restrict__ p, double* __restrict__ m, doub
   }
 }
 
+// Row-order fold of per-frame gradient rows (the multi-GPU exchange's
+// combine step): out[j] = ((into[j] + r0[j]) + r1[j]) + ..., one thread per
+// column, so the bits equal the single-process frame-order accumulation.
+__global__ void fold_rows_kernel(const double* __restrict__ rows, int64_t nrows, int64_t n,
+                                 const double* __restrict__ into, double* __restrict__ out) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double acc = into ? __dadd_rn(into[j], rows[j]) : rows[j];
+  for (int64_t r = 1; r < nrows; ++r) acc = __dadd_rn(acc, rows[r * n + j]);
+  out[j] = acc;
+}
+
 }  // namespace
 }  // namespace qfb
 
@@ -335,6 +347,18 @@ qfb_status qfb_distill_loss_host(qfb_ctx* ctx, const float* f_s, const float* f_
   out5[4] = h[3];
   out5[0] = h[0] + h[2] + lambda_cos * (1.0 - h[1]) + lambda_cos * (1.0 - h[3]);
   return QFB_OK;
+}
+
+qfb_status qfb_fold_rows(qfb_ctx* ctx, const double* rows, int64_t nrows, int64_t n, const double* into,
+                         double* out) {
+  if (!ctx) return err(QFB_ERR_VALUE, "null qfb_ctx");
+  if (nrows < 1 || n < 0 || (n > 0 && (!rows || !out))) return err(QFB_ERR_VALUE, "fold_rows: bad arguments");
+  if (n == 0) return QFB_OK;
+  Guard g(ctx_device(ctx));
+  fold_rows_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx_stream(ctx)>>>(rows, nrows, n, into, out);
+  ctx_count_launches(ctx, 1);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? QFB_OK : cuda_error(e, "fold_rows");
 }
 
 qfb_status qfb_adam_bias_corrections(double beta1, double beta2, int64_t t, double* bc1, double* bc2) {

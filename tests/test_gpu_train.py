@@ -67,3 +67,24 @@ def test_adam_vs_oracle_and_skip(qfb, orc, cuda):
     sk = qfb.adam_step(P, M, V, dev(g, cuda), 6, 5e-3)
     torch.cuda.synchronize()
     assert int(sk.item()) == 1 and torch.equal(P, before)
+
+
+def test_fold_rows_device_is_frame_order(qfb, cuda):
+    """qfb_fold_rows == ((into + r0) + r1) + ... bit for bit (the exchange's
+    combine step, dist.fold_rows on CUDA tensors)."""
+    import torch
+    from paper_2511_12653_b200.dist import fold_rows
+    rng = np.random.default_rng(3)
+    rows = rng.normal(0, 1, (8, 1494)) * np.exp(rng.uniform(-30, 30, (8, 1494)))
+    into = rng.normal(0, 1, 1494)
+    want = rows[0].copy()
+    for r in rows[1:]:
+        want = want + r
+    want2 = into + rows[0]
+    for r in rows[1:]:
+        want2 = want2 + r
+    got = fold_rows(dev(rows, cuda))
+    got2 = fold_rows(dev(rows, cuda), into=dev(into, cuda))
+    torch.cuda.synchronize()
+    assert got.cpu().numpy().tobytes() == want.tobytes()
+    assert got2.cpu().numpy().tobytes() == want2.tobytes()
