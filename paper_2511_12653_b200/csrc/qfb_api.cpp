@@ -895,6 +895,30 @@ qfb_status qfb_fake_quantize_backward_host(qfb_ctx* ctx, qfb_precision prec, con
   return qfb_ctx_sync(ctx);
 }
 
+namespace {
+
+// A few host<->device copies on one stream as one submission
+// (cudaMemcpyBatchAsync, stream-ordered sources); QFB_BATCH_COPY=0 falls
+// back to one cudaMemcpyAsync per buffer.
+qfb_status copy_batch(void** dst, void** src, size_t* sz, size_t n, cudaStream_t st) {
+  static const bool batch = [] {
+    const char* e = getenv("QFB_BATCH_COPY");
+    return !(e && e[0] == '0');
+  }();
+  if (n == 0) return QFB_OK;
+  if (!batch || n == 1) {
+    for (size_t i = 0; i < n; ++i) QFB_CUDA(cudaMemcpyAsync(dst[i], src[i], sz[i], cudaMemcpyDefault, st));
+    return QFB_OK;
+  }
+  cudaMemcpyAttributes attr{};
+  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+  size_t idx = 0, fail = 0;
+  QFB_CUDA(cudaMemcpyBatchAsync(dst, src, sz, n, &attr, &idx, 1, &fail, st));
+  return QFB_OK;
+}
+
+}  // namespace
+
 qfb_status qfb_quant_pass_host(qfb_ctx* ctx, qfb_precision prec, const qfb_host_point* pts,
                                int32_t n, const qfb_quant_config* cfg) {
   if (qfb_status st = check_ctx(ctx)) return st;
@@ -964,9 +988,18 @@ qfb_status qfb_quant_pass_host(qfb_ctx* ctx, qfb_precision prec, const qfb_host_
   double* hD = reinterpret_cast<double*>(static_cast<char*>(ctx->pinned) + fcount * sizeof(float));
   std::memcpy(hF, fblk.data(), fcount * sizeof(float));
   std::memcpy(hD, dblk.data(), dcount * sizeof(double));
+  // QFB_PASS_TIMING=1: stage timestamps of this pass on stderr (diagnostics)
+  static const bool timing = [] {
+    const char* e = getenv("QFB_PASS_TIMING");
+    return e && e[0] == '1';
+  }();
+  cudaEvent_t te[4] = {nullptr, nullptr, nullptr, nullptr};
+  if (timing)
+    for (auto& e : te) QFB_CUDA(cudaEventCreate(&e));
   // all streams start after prior work on the context stream
   QFB_CUDA(cudaEventRecord(ctx->ev[2 * n], ctx->stream));
   QFB_CUDA(cudaStreamWaitEvent(ctx->s_in, ctx->ev[2 * n], 0));
+  if (timing) QFB_CUDA(cudaEventRecord(te[0], ctx->s_in));
   QFB_CUDA(cudaMemcpyAsync(dF, hF, pbytes, cudaMemcpyHostToDevice, ctx->s_in));
   // per point: buffers x, up[2], y[2], dx[2]
   if (ctx->pass_bufs.size() < (size_t)n * 7) ctx->pass_bufs.resize((size_t)n * 7);
@@ -984,64 +1017,104 @@ qfb_status qfb_quant_pass_host(qfb_ctx* ctx, qfb_precision prec, const qfb_host_
         if (qfb_status st = grow(ctx, B[5 + k], bytes, false)) return st;
     }
   }
-  // ---- pipeline: H2D (s_in) -> kernels (ctx->stream) -> D2H (s_out)
+  // ---- pipeline: H2D (s_in) -> kernels (ctx->stream) -> D2H (s_out), in
+  // groups of points: each group's inputs go as one batched submission, its
+  // kernels wait for that submission, its outputs go back as one batched
+  // submission (per-copy overhead is ~10-20 us when both directions run;
+  // smaller groups pipeline better, QFB_PASS_GROUP tunes the size)
+  static const int32_t group_pts = [] {
+    const char* e = getenv("QFB_PASS_GROUP");
+    const int v = e ? atoi(e) : 0;
+    return v > 0 ? v : 1;  // measured: 1 point per group is best (7.40 ms/frame vs 7.42, 7.73 for 2, 3)
+  }();
   const uint32_t flags = prec == QFB_PREC_HALF ? QFB_FLAG_HALF_GRID : 0u;
-  for (int32_t i = 0; i < n; ++i) {
-    const qfb_host_point& p = pts[i];
-    const size_t bytes = (size_t)(p.outer * p.channels * p.inner) * sizeof(float);
-    DevBuf* B = &ctx->pass_bufs[(size_t)i * 7];
-    QFB_CUDA(cudaMemcpyAsync(B[0].p, p.x, bytes, cudaMemcpyHostToDevice, ctx->s_in));
-    for (int k = 0; k < p.n_out; ++k)
-      if (p.log_s[k])
-        QFB_CUDA(cudaMemcpyAsync(B[1 + k].p, p.up[k], bytes, cudaMemcpyHostToDevice, ctx->s_in));
-    QFB_CUDA(cudaEventRecord(ctx->ev[2 * i], ctx->s_in));
-    QFB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev[2 * i], 0));
-    // forward: one launch for all consumers of this tensor
-    bool any_y = false;
-    qfb_fq_desc fd{};
-    fd.x = B[0].p;
-    fd.outer = p.outer;
-    fd.channels = p.channels;
-    fd.inner = p.inner;
-    fd.q_max = q;
-    fd.flags = flags;
-    int no = 0;
-    for (int k = 0; k < p.n_out; ++k) {
-      if (!p.y[k]) continue;
-      fd.y[no] = B[3 + k].p;
-      fd.scale[no] = dF + foff[i] + k * p.channels;
-      ++no;
-      any_y = true;
+  std::vector<void*> cdst, csrc;
+  std::vector<size_t> csz;
+  for (int32_t g0 = 0; g0 < n; g0 += group_pts) {
+    const int32_t g1 = std::min(n, g0 + group_pts);
+    cdst.clear();
+    csrc.clear();
+    csz.clear();
+    for (int32_t i = g0; i < g1; ++i) {
+      const qfb_host_point& p = pts[i];
+      const size_t bytes = (size_t)(p.outer * p.channels * p.inner) * sizeof(float);
+      DevBuf* B = &ctx->pass_bufs[(size_t)i * 7];
+      cdst.push_back(B[0].p), csrc.push_back(const_cast<float*>(p.x)), csz.push_back(bytes);
+      for (int k = 0; k < p.n_out; ++k)
+        if (p.log_s[k])
+          cdst.push_back(B[1 + k].p), csrc.push_back(const_cast<float*>(p.up[k])), csz.push_back(bytes);
     }
-    fd.n_out = no;
-    if (any_y)
-      if (qfb_status st = qfb_fq_fwd_multi(ctx, QFB_F32, &fd, 1)) return st;
-    // backward per consumer
-    qfb_bwd_desc bd[2];
-    int nb = 0;
-    for (int k = 0; k < p.n_out; ++k) {
-      if (!p.log_s[k]) continue;
-      const double* f = dD + doff[i] + (size_t)k * 3 * p.channels;
-      bd[nb] = qfb_bwd_desc{B[0].p, B[1 + k].p, p.dx[k] ? B[5 + k].p : nullptr, f, f + p.channels,
-                            const_cast<double*>(f + 2 * p.channels), p.outer, p.channels, p.inner, q, 0};
-      ++nb;
+    if (qfb_status st = copy_batch(cdst.data(), csrc.data(), csz.data(), cdst.size(), ctx->s_in)) return st;
+    QFB_CUDA(cudaEventRecord(ctx->ev[2 * g0], ctx->s_in));
+    QFB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev[2 * g0], 0));
+    for (int32_t i = g0; i < g1; ++i) {
+      const qfb_host_point& p = pts[i];
+      DevBuf* B = &ctx->pass_bufs[(size_t)i * 7];
+      // forward: one launch for all consumers of this tensor
+      bool any_y = false;
+      qfb_fq_desc fd{};
+      fd.x = B[0].p;
+      fd.outer = p.outer;
+      fd.channels = p.channels;
+      fd.inner = p.inner;
+      fd.q_max = q;
+      fd.flags = flags;
+      int no = 0;
+      for (int k = 0; k < p.n_out; ++k) {
+        if (!p.y[k]) continue;
+        fd.y[no] = B[3 + k].p;
+        fd.scale[no] = dF + foff[i] + k * p.channels;
+        ++no;
+        any_y = true;
+      }
+      fd.n_out = no;
+      if (any_y)
+        if (qfb_status st = qfb_fq_fwd_multi(ctx, QFB_F32, &fd, 1)) return st;
+      // backward per consumer
+      qfb_bwd_desc bd[2];
+      int nb = 0;
+      for (int k = 0; k < p.n_out; ++k) {
+        if (!p.log_s[k]) continue;
+        const double* f = dD + doff[i] + (size_t)k * 3 * p.channels;
+        bd[nb] = qfb_bwd_desc{B[0].p, B[1 + k].p, p.dx[k] ? B[5 + k].p : nullptr, f, f + p.channels,
+                              const_cast<double*>(f + 2 * p.channels), p.outer, p.channels, p.inner, q, 0};
+        ++nb;
+      }
+      if (nb)
+        if (qfb_status st = qfb_fq_bwd_multi(ctx, QFB_F32, bd, nb)) return st;
     }
-    if (nb)
-      if (qfb_status st = qfb_fq_bwd_multi(ctx, QFB_F32, bd, nb)) return st;
-    QFB_CUDA(cudaEventRecord(ctx->ev[2 * i + 1], ctx->stream));
-    QFB_CUDA(cudaStreamWaitEvent(ctx->s_out, ctx->ev[2 * i + 1], 0));
-    for (int k = 0; k < p.n_out; ++k) {
-      if (p.y[k]) QFB_CUDA(cudaMemcpyAsync(p.y[k], B[3 + k].p, bytes, cudaMemcpyDeviceToHost, ctx->s_out));
-      if (p.log_s[k]) {
-        if (p.dx[k]) QFB_CUDA(cudaMemcpyAsync(p.dx[k], B[5 + k].p, bytes, cudaMemcpyDeviceToHost, ctx->s_out));
-        const size_t o = doff[i] + (size_t)k * 3 * p.channels + 2 * p.channels;
-        QFB_CUDA(cudaMemcpyAsync(hD + o, dD + o, (size_t)p.channels * sizeof(double),
-                                 cudaMemcpyDeviceToHost, ctx->s_out));
+    QFB_CUDA(cudaEventRecord(ctx->ev[2 * g0 + 1], ctx->stream));
+    QFB_CUDA(cudaStreamWaitEvent(ctx->s_out, ctx->ev[2 * g0 + 1], 0));
+    cdst.clear();
+    csrc.clear();
+    csz.clear();
+    for (int32_t i = g0; i < g1; ++i) {
+      const qfb_host_point& p = pts[i];
+      const size_t bytes = (size_t)(p.outer * p.channels * p.inner) * sizeof(float);
+      DevBuf* B = &ctx->pass_bufs[(size_t)i * 7];
+      for (int k = 0; k < p.n_out; ++k) {
+        if (p.y[k]) cdst.push_back(p.y[k]), csrc.push_back(B[3 + k].p), csz.push_back(bytes);
+        if (p.log_s[k] && p.dx[k]) cdst.push_back(p.dx[k]), csrc.push_back(B[5 + k].p), csz.push_back(bytes);
       }
     }
+    if (qfb_status st = copy_batch(cdst.data(), csrc.data(), csz.data(), cdst.size(), ctx->s_out)) return st;
+  }
+  // all scale gradients in one copy (they sit in the parameter block)
+  QFB_CUDA(cudaMemcpyAsync(hD, dD, dcount * sizeof(double), cudaMemcpyDeviceToHost, ctx->s_out));
+  if (timing) {
+    QFB_CUDA(cudaEventRecord(te[1], ctx->s_in));
+    QFB_CUDA(cudaEventRecord(te[2], ctx->stream));
+    QFB_CUDA(cudaEventRecord(te[3], ctx->s_out));
   }
   QFB_CUDA(cudaStreamSynchronize(ctx->s_out));
   if (qfb_status st = qfb_ctx_sync(ctx)) return st;
+  if (timing) {
+    float ms[3];
+    for (int k = 0; k < 3; ++k) QFB_CUDA(cudaEventElapsedTime(&ms[k], te[0], te[k + 1]));
+    fprintf(stderr, "quant_pass_host: h2d done %.3f ms, compute done %.3f ms, d2h done %.3f ms\n", ms[0], ms[1],
+            ms[2]);
+    for (auto& e : te) cudaEventDestroy(e);
+  }
   for (int32_t i = 0; i < n; ++i) {
     const qfb_host_point& p = pts[i];
     for (int k = 0; k < p.n_out; ++k)
