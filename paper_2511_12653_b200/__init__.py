@@ -24,7 +24,7 @@ import os
 from typing import Optional, Sequence, Union
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libqfb.so")
+LIB_PATH = os.environ.get("QFB_LIB_PATH") or os.path.join(_HERE, "libqfb.so")  # override: tuning builds
 
 # ---------------------------------------------------------------- errors --
 

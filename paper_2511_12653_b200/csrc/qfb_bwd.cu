@@ -50,7 +50,7 @@ constexpr int kProbeNoLoads = 16;
 constexpr int kWinPad = 32;                // window slack: 16-byte rounding at both ends
 constexpr size_t kRingBudget = 72 * 1024;  // default per-CTA ring + sums: 3 CTAs per SM
 constexpr size_t kRedBytes = kBwdThreads * sizeof(double);  // group sums of one stage
-constexpr size_t kSmemMax = 225 * 1024;    // dynamic smem attribute (ring + sums)
+constexpr size_t kSmemMax = 220 * 1024;    // dynamic smem attribute (ring + sums; + static <= 227 KB)
 
 // Descend `levels` levels of the reference split from node (lo, m) along
 // the bits of `path` (MSB first): bit 0 = left child [lo, lo + m/2),
