@@ -394,6 +394,16 @@ typedef struct qfb_host_point {
 qfb_status qfb_quant_pass_host(qfb_ctx* ctx, qfb_precision prec,
                                const qfb_host_point* points, int32_t n,
                                const qfb_quant_config* cfg);
+/* The same pass split in two so consecutive frames overlap (frame k+1's   */
+/* uploads run under frame k's downloads): submit enqueues everything on  */
+/* in-flight slot 0 or 1 and returns; wait blocks until that slot's       */
+/* outputs are in the host buffers, copies its scale gradients out and    */
+/* reports errors. Host buffers of a slot must stay valid and untouched   */
+/* until its wait. qfb_quant_pass_host == submit(slot 0) + wait(slot 0).  */
+qfb_status qfb_quant_pass_host_submit(qfb_ctx* ctx, qfb_precision prec,
+                                      const qfb_host_point* points, int32_t n,
+                                      const qfb_quant_config* cfg, int32_t slot);
+qfb_status qfb_quant_pass_host_wait(qfb_ctx* ctx, int32_t slot);
 
 
 /* ---------------------------------------------------------------------- */

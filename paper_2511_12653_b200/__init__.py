@@ -197,6 +197,9 @@ _sig("qfb_exec_trace_reset", _i32, [_vp])
 _sig("qfb_exec_model_layer", _i32, [ctypes.POINTER(CExecPlan), _i64, _i64, _i64, _i32, _i32,
                                     ctypes.POINTER(CExecTrace)])
 _sig("qfb_quant_pass_host", _i32, [_vp, _i32, ctypes.POINTER(CHostPoint), _i32, ctypes.POINTER(CQuantConfig)])
+_sig("qfb_quant_pass_host_submit", _i32, [_vp, _i32, ctypes.POINTER(CHostPoint), _i32,
+                                          ctypes.POINTER(CQuantConfig), _i32])
+_sig("qfb_quant_pass_host_wait", _i32, [_vp, _i32])
 _sig("qfb_fake_quantize_backward_host", _i32, [_vp, _i32, _vp, _vp, _vp, _i64, _i64, _i64, _pd,
                                                 ctypes.POINTER(CQuantConfig), _pd, _i32])
 

@@ -90,13 +90,23 @@ struct qfb_ctx {
   DevBuf ws_u32;                 // tickets (kept zero between launches)
   DevBuf host_io[6];             // scratch for the *_host entry points
   int64_t launches = 0;
-  // qfb_quant_pass_host: copy streams, events and per-point device buffers
+  // qfb_quant_pass_host: copy streams and, per in-flight slot, events,
+  // per-point device buffers and pinned staging
   cudaStream_t s_in = nullptr, s_out = nullptr;
-  std::vector<cudaEvent_t> ev;
-  std::vector<DevBuf> pass_bufs;
-  DevBuf pass_params;
-  void* pinned = nullptr;  // pinned staging for params and scale gradients
-  size_t pinned_bytes = 0;
+  struct PassSlot {
+    std::vector<cudaEvent_t> ev;
+    std::vector<DevBuf> bufs;
+    DevBuf params;
+    void* pinned = nullptr;  // params up, scale gradients and the status word down
+    size_t pinned_bytes = 0;
+    cudaEvent_t done = nullptr;  // after the slot's last download
+    bool busy = false;
+    // what wait() hands back: d_log_s destinations and their offsets in pinned
+    std::vector<std::pair<double*, size_t>> grads;
+    std::vector<int64_t> grad_len;
+    uint32_t* h_status = nullptr;  // inside pinned
+    const double* grad_base = nullptr;  // the pinned double block
+  } slots[2];
   DevBuf train_ws[4];      // scratch of the trainer ops (qfb_train.cu)
 };
 
@@ -466,11 +476,14 @@ qfb_status qfb_ctx_destroy(qfb_ctx* ctx) {
   if (ctx->ws_u32.p) cudaFree(ctx->ws_u32.p);
   for (auto& b : ctx->host_io)
     if (b.p) cudaFree(b.p);
-  for (auto& b : ctx->pass_bufs)
-    if (b.p) cudaFree(b.p);
-  if (ctx->pass_params.p) cudaFree(ctx->pass_params.p);
-  if (ctx->pinned) cudaFreeHost(ctx->pinned);
-  for (auto e : ctx->ev) cudaEventDestroy(e);
+  for (auto& sl : ctx->slots) {
+    for (auto& b : sl.bufs)
+      if (b.p) cudaFree(b.p);
+    if (sl.params.p) cudaFree(sl.params.p);
+    if (sl.pinned) cudaFreeHost(sl.pinned);
+    for (auto e : sl.ev) cudaEventDestroy(e);
+    if (sl.done) cudaEventDestroy(sl.done);
+  }
   if (ctx->s_in) cudaStreamDestroy(ctx->s_in);
   if (ctx->s_out) cudaStreamDestroy(ctx->s_out);
   delete ctx;
@@ -919,11 +932,16 @@ qfb_status copy_batch(void** dst, void** src, size_t* sz, size_t n, cudaStream_t
 
 }  // namespace
 
-qfb_status qfb_quant_pass_host(qfb_ctx* ctx, qfb_precision prec, const qfb_host_point* pts,
-                               int32_t n, const qfb_quant_config* cfg) {
+qfb_status qfb_quant_pass_host_submit(qfb_ctx* ctx, qfb_precision prec, const qfb_host_point* pts,
+                                      int32_t n, const qfb_quant_config* cfg, int32_t slot) {
   if (qfb_status st = check_ctx(ctx)) return st;
   if (qfb_status st = qfb_quant_config_validate(cfg)) return st;
   if (n < 0 || (n > 0 && !pts)) return fail(QFB_ERR_VALUE, "quant_pass_host: bad table");
+  if (slot < 0 || slot > 1) return fail(QFB_ERR_VALUE, "quant_pass_host: slot must be 0 or 1");
+  auto& sl = ctx->slots[slot];
+  if (sl.busy) return fail(QFB_ERR_VALUE, "quant_pass_host: slot %d still in flight (wait first)", slot);
+  sl.grads.clear();
+  sl.grad_len.clear();
   if (n == 0) return QFB_OK;
   const int32_t q = qfb_q_max(cfg);
   // ---- validate everything and build the parameter block on the host
@@ -966,26 +984,30 @@ qfb_status qfb_quant_pass_host(qfb_ctx* ctx, qfb_precision prec, const qfb_host_
     QFB_CUDA(cudaStreamCreateWithFlags(&ctx->s_in, cudaStreamNonBlocking));
     QFB_CUDA(cudaStreamCreateWithFlags(&ctx->s_out, cudaStreamNonBlocking));
   }
-  while ((int32_t)ctx->ev.size() < 2 * n + 1) {
+  if (!sl.done) QFB_CUDA(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
+  while ((int32_t)sl.ev.size() < 2 * n + 1) {
     cudaEvent_t e;
     QFB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    ctx->ev.push_back(e);
+    sl.ev.push_back(e);
   }
   const size_t pbytes = fcount * sizeof(float) + dcount * sizeof(double);
-  if (qfb_status st = grow(ctx, ctx->pass_params, pbytes, false)) return st;
-  float* dF = static_cast<float*>(ctx->pass_params.p);
-  double* dD = reinterpret_cast<double*>(static_cast<char*>(ctx->pass_params.p) + fcount * sizeof(float));
+  if (qfb_status st = grow(ctx, sl.params, pbytes, false)) return st;
+  float* dF = static_cast<float*>(sl.params.p);
+  double* dD = reinterpret_cast<double*>(static_cast<char*>(sl.params.p) + fcount * sizeof(float));
   // Pinned staging: a copy from/to pageable memory is synchronous for the
-  // issuing thread and would serialize the pipeline.
-  if (ctx->pinned_bytes < pbytes) {
-    if (ctx->pinned) QFB_CUDA(cudaFreeHost(ctx->pinned));
-    ctx->pinned = nullptr;
-    ctx->pinned_bytes = 0;
-    QFB_CUDA(cudaMallocHost(&ctx->pinned, pbytes));
-    ctx->pinned_bytes = pbytes;
+  // issuing thread and would serialize the pipeline. One extra slot at the
+  // end receives the status word.
+  if (sl.pinned_bytes < pbytes + 16) {
+    if (sl.pinned) QFB_CUDA(cudaFreeHost(sl.pinned));
+    sl.pinned = nullptr;
+    sl.pinned_bytes = 0;
+    QFB_CUDA(cudaMallocHost(&sl.pinned, pbytes + 16));
+    sl.pinned_bytes = pbytes + 16;
   }
-  float* hF = static_cast<float*>(ctx->pinned);
-  double* hD = reinterpret_cast<double*>(static_cast<char*>(ctx->pinned) + fcount * sizeof(float));
+  float* hF = static_cast<float*>(sl.pinned);
+  double* hD = reinterpret_cast<double*>(static_cast<char*>(sl.pinned) + fcount * sizeof(float));
+  sl.h_status = reinterpret_cast<uint32_t*>(static_cast<char*>(sl.pinned) + pbytes);
+  sl.grad_base = hD;
   std::memcpy(hF, fblk.data(), fcount * sizeof(float));
   std::memcpy(hD, dblk.data(), dcount * sizeof(double));
   // QFB_PASS_TIMING=1: stage timestamps of this pass on stderr (diagnostics)
@@ -997,16 +1019,16 @@ qfb_status qfb_quant_pass_host(qfb_ctx* ctx, qfb_precision prec, const qfb_host_
   if (timing)
     for (auto& e : te) QFB_CUDA(cudaEventCreate(&e));
   // all streams start after prior work on the context stream
-  QFB_CUDA(cudaEventRecord(ctx->ev[2 * n], ctx->stream));
-  QFB_CUDA(cudaStreamWaitEvent(ctx->s_in, ctx->ev[2 * n], 0));
+  QFB_CUDA(cudaEventRecord(sl.ev[2 * n], ctx->stream));
+  QFB_CUDA(cudaStreamWaitEvent(ctx->s_in, sl.ev[2 * n], 0));
   if (timing) QFB_CUDA(cudaEventRecord(te[0], ctx->s_in));
   QFB_CUDA(cudaMemcpyAsync(dF, hF, pbytes, cudaMemcpyHostToDevice, ctx->s_in));
   // per point: buffers x, up[2], y[2], dx[2]
-  if (ctx->pass_bufs.size() < (size_t)n * 7) ctx->pass_bufs.resize((size_t)n * 7);
+  if (sl.bufs.size() < (size_t)n * 7) sl.bufs.resize((size_t)n * 7);
   for (int32_t i = 0; i < n; ++i) {
     const qfb_host_point& p = pts[i];
     const size_t bytes = (size_t)(p.outer * p.channels * p.inner) * sizeof(float);
-    DevBuf* B = &ctx->pass_bufs[(size_t)i * 7];
+    DevBuf* B = &sl.bufs[(size_t)i * 7];
     if (qfb_status st = grow(ctx, B[0], bytes, false)) return st;
     for (int k = 0; k < p.n_out; ++k) {
       if (p.log_s[k])
@@ -1038,18 +1060,18 @@ qfb_status qfb_quant_pass_host(qfb_ctx* ctx, qfb_precision prec, const qfb_host_
     for (int32_t i = g0; i < g1; ++i) {
       const qfb_host_point& p = pts[i];
       const size_t bytes = (size_t)(p.outer * p.channels * p.inner) * sizeof(float);
-      DevBuf* B = &ctx->pass_bufs[(size_t)i * 7];
+      DevBuf* B = &sl.bufs[(size_t)i * 7];
       cdst.push_back(B[0].p), csrc.push_back(const_cast<float*>(p.x)), csz.push_back(bytes);
       for (int k = 0; k < p.n_out; ++k)
         if (p.log_s[k])
           cdst.push_back(B[1 + k].p), csrc.push_back(const_cast<float*>(p.up[k])), csz.push_back(bytes);
     }
     if (qfb_status st = copy_batch(cdst.data(), csrc.data(), csz.data(), cdst.size(), ctx->s_in)) return st;
-    QFB_CUDA(cudaEventRecord(ctx->ev[2 * g0], ctx->s_in));
-    QFB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev[2 * g0], 0));
+    QFB_CUDA(cudaEventRecord(sl.ev[2 * g0], ctx->s_in));
+    QFB_CUDA(cudaStreamWaitEvent(ctx->stream, sl.ev[2 * g0], 0));
     for (int32_t i = g0; i < g1; ++i) {
       const qfb_host_point& p = pts[i];
-      DevBuf* B = &ctx->pass_bufs[(size_t)i * 7];
+      DevBuf* B = &sl.bufs[(size_t)i * 7];
       // forward: one launch for all consumers of this tensor
       bool any_y = false;
       qfb_fq_desc fd{};
@@ -1083,15 +1105,15 @@ qfb_status qfb_quant_pass_host(qfb_ctx* ctx, qfb_precision prec, const qfb_host_
       if (nb)
         if (qfb_status st = qfb_fq_bwd_multi(ctx, QFB_F32, bd, nb)) return st;
     }
-    QFB_CUDA(cudaEventRecord(ctx->ev[2 * g0 + 1], ctx->stream));
-    QFB_CUDA(cudaStreamWaitEvent(ctx->s_out, ctx->ev[2 * g0 + 1], 0));
+    QFB_CUDA(cudaEventRecord(sl.ev[2 * g0 + 1], ctx->stream));
+    QFB_CUDA(cudaStreamWaitEvent(ctx->s_out, sl.ev[2 * g0 + 1], 0));
     cdst.clear();
     csrc.clear();
     csz.clear();
     for (int32_t i = g0; i < g1; ++i) {
       const qfb_host_point& p = pts[i];
       const size_t bytes = (size_t)(p.outer * p.channels * p.inner) * sizeof(float);
-      DevBuf* B = &ctx->pass_bufs[(size_t)i * 7];
+      DevBuf* B = &sl.bufs[(size_t)i * 7];
       for (int k = 0; k < p.n_out; ++k) {
         if (p.y[k]) cdst.push_back(p.y[k]), csrc.push_back(B[3 + k].p), csz.push_back(bytes);
         if (p.log_s[k] && p.dx[k]) cdst.push_back(p.dx[k]), csrc.push_back(B[5 + k].p), csz.push_back(bytes);
@@ -1106,23 +1128,54 @@ qfb_status qfb_quant_pass_host(qfb_ctx* ctx, qfb_precision prec, const qfb_host_
     QFB_CUDA(cudaEventRecord(te[2], ctx->stream));
     QFB_CUDA(cudaEventRecord(te[3], ctx->s_out));
   }
-  QFB_CUDA(cudaStreamSynchronize(ctx->s_out));
-  if (qfb_status st = qfb_ctx_sync(ctx)) return st;
+  // the status word of this pass's kernels rides down with the gradients
+  QFB_CUDA(cudaEventRecord(sl.ev[2 * n], ctx->stream));
+  QFB_CUDA(cudaStreamWaitEvent(ctx->s_out, sl.ev[2 * n], 0));
+  QFB_CUDA(cudaMemcpyAsync(sl.h_status, ctx->d_status, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->s_out));
+  QFB_CUDA(cudaEventRecord(sl.done, ctx->s_out));
+  for (int32_t i = 0; i < n; ++i) {
+    const qfb_host_point& p = pts[i];
+    for (int k = 0; k < p.n_out; ++k)
+      if (p.log_s[k]) {
+        sl.grads.emplace_back(p.d_log_s[k], doff[i] + (size_t)k * 3 * p.channels + 2 * p.channels);
+        sl.grad_len.push_back(p.channels);
+      }
+  }
+  sl.busy = true;
   if (timing) {
+    QFB_CUDA(cudaEventSynchronize(te[3]));
     float ms[3];
     for (int k = 0; k < 3; ++k) QFB_CUDA(cudaEventElapsedTime(&ms[k], te[0], te[k + 1]));
     fprintf(stderr, "quant_pass_host: h2d done %.3f ms, compute done %.3f ms, d2h done %.3f ms\n", ms[0], ms[1],
             ms[2]);
     for (auto& e : te) cudaEventDestroy(e);
   }
-  for (int32_t i = 0; i < n; ++i) {
-    const qfb_host_point& p = pts[i];
-    for (int k = 0; k < p.n_out; ++k)
-      if (p.log_s[k])
-        std::memcpy(p.d_log_s[k], hD + doff[i] + (size_t)k * 3 * p.channels + 2 * p.channels,
-                    (size_t)p.channels * sizeof(double));
+  return QFB_OK;
+}
+
+qfb_status qfb_quant_pass_host_wait(qfb_ctx* ctx, int32_t slot) {
+  if (qfb_status st = check_ctx(ctx)) return st;
+  if (slot < 0 || slot > 1) return fail(QFB_ERR_VALUE, "quant_pass_host: slot must be 0 or 1");
+  auto& sl = ctx->slots[slot];
+  if (!sl.busy) return QFB_OK;
+  DeviceGuard g(ctx->device);
+  sl.busy = false;
+  QFB_CUDA(cudaEventSynchronize(sl.done));
+  for (size_t i = 0; i < sl.grads.size(); ++i)
+    std::memcpy(sl.grads[i].first, sl.grad_base + sl.grads[i].second, (size_t)sl.grad_len[i] * sizeof(double));
+  if (*sl.h_status != 0) {
+    QFB_CUDA(cudaMemsetAsync(ctx->d_status, 0, sizeof(uint32_t), ctx->stream));
+    QFB_CUDA(cudaStreamSynchronize(ctx->stream));
+    return fail(QFB_ERR_NONFINITE, "demote_half: non-finite value on the binary16 path");
   }
   return QFB_OK;
+}
+
+qfb_status qfb_quant_pass_host(qfb_ctx* ctx, qfb_precision prec, const qfb_host_point* pts, int32_t n,
+                               const qfb_quant_config* cfg) {
+  if (qfb_status st = qfb_quant_pass_host_wait(ctx, 0)) return st;
+  if (qfb_status st = qfb_quant_pass_host_submit(ctx, prec, pts, n, cfg, 0)) return st;
+  return qfb_quant_pass_host_wait(ctx, 0);
 }
 
 }  // extern "C"

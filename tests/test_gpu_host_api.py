@@ -101,3 +101,53 @@ def test_quant_pass_host_matches_reference(qfb, orc, ref, cuda):
             assert np.array_equal(bits32(dx.numpy()), bits32(wdx))
             assert dls.tobytes() == wdls.tobytes()
     ctx.close()
+
+
+def _pass_table(qfb, rng, shapes):
+    import torch
+    keep, pts, checks = [], [], []
+    for C, H, W, n_out in shapes:
+        x = torch.from_numpy(rng.normal(0, 1, C * H * W).astype(np.float32)).pin_memory()
+        p = qfb.CHostPoint()
+        p.x = x.data_ptr()
+        p.outer, p.channels, p.inner, p.n_out = 1, C, H * W, n_out
+        keep.append(x)
+        for k in range(n_out):
+            s = np.exp(rng.uniform(np.log(1e-3), np.log(0.1), C))
+            ls = np.log(np.expm1(s))
+            up = torch.from_numpy(rng.normal(0, 1, C * H * W).astype(np.float32)).pin_memory()
+            y = torch.empty(C * H * W).pin_memory()
+            dx = torch.empty(C * H * W).pin_memory()
+            dls = np.zeros(C)
+            keep += [s, ls, up, y, dx, dls]
+            p.s[k], p.y[k], p.log_s[k] = s.ctypes.data, y.data_ptr(), ls.ctypes.data
+            p.up[k], p.dx[k], p.d_log_s[k] = up.data_ptr(), dx.data_ptr(), dls.ctypes.data
+            checks.append((x.numpy(), s, ls, up.numpy(), y, dx, dls, C, H * W))
+        pts.append(p)
+    return (qfb.CHostPoint * len(pts))(*pts), len(pts), checks, keep
+
+
+def test_quant_pass_two_slots_in_flight(qfb, ref, cuda):
+    """submit(slot 0), submit(slot 1), wait both: each slot's outputs equal
+    the reference's per-point calls; a busy slot refuses a second submit."""
+    rng = np.random.default_rng(21)
+    shapes = [(3, 48, 64, 2), (32, 24, 32, 1), (64, 12, 16, 2)]
+    t0 = _pass_table(qfb, rng, shapes)
+    t1 = _pass_table(qfb, rng, shapes)
+    ctx = qfb.Context(0)
+    cfg = qfb.QuantConfig().to_c()
+    L = qfb.lib()
+    for _ in range(2):
+        qfb.check(L.qfb_quant_pass_host_submit(ctx.handle, 0, t0[0], t0[1], ctypes.byref(cfg), 0))
+        qfb.check(L.qfb_quant_pass_host_submit(ctx.handle, 0, t1[0], t1[1], ctypes.byref(cfg), 1))
+        assert L.qfb_quant_pass_host_submit(ctx.handle, 0, t0[0], t0[1], ctypes.byref(cfg), 0) == 2
+        qfb.check(L.qfb_quant_pass_host_wait(ctx.handle, 0))
+        qfb.check(L.qfb_quant_pass_host_wait(ctx.handle, 1))
+        for checks in (t0[2], t1[2]):
+            for x, s, ls, up, y, dx, dls, C, HW in checks:
+                _, wy = ref.fake_quantize(x, [C, HW], s, per_channel=True)
+                assert np.array_equal(bits32(y.numpy()), bits32(wy))
+                _, wdx, wdls = ref.fq_backward(x, up, [C, HW], ls, per_channel=True)
+                assert np.array_equal(bits32(dx.numpy()), bits32(wdx))
+                assert dls.tobytes() == wdls.tobytes()
+    ctx.close()
