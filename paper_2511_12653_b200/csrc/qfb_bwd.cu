@@ -16,11 +16,12 @@
 // butterfly computes (IEEE addition is commutative), so:
 //   tile    = 2^g consecutive leaf groups (g = min(D, 8)), <= 4096 elements,
 //             staged into shared memory by the TMA engine (cp.async.bulk +
-//             mbarrier, double-buffered: tile i+1 lands while tile i
-//             computes); each thread owns one leaf group, computes its
-//             elements' terms in registers and folds them in reference order,
-//             writing d_input back into the stage; a coalesced 16-byte copy
-//             moves d_input to HBM; warp/CTA butterfly = the subtree's sum;
+//             mbarrier ring, 2..8 stages); each consumer thread owns one leaf
+//             group, computes its elements' terms in registers and folds them
+//             in reference order, writing d_input back into the stage; the
+//             producer warp reduces the 2^g group sums as a perfect tree
+//             (lane subtrees + xor butterfly = the tile's subtree sum) and
+//             sends d_input out with one TMA bulk store;
 //   segment = one row: its 2^(D-g) tile partials are reduced in tree order
 //             by a small stream-ordered finisher kernel (one warp per
 //             channel: per-lane perfect subtrees + xor butterfly), which also
@@ -204,9 +205,9 @@ struct GroupCache {
 };
 
 // Terms of one element: d_ds * up (double) and d_input (x86 NaN rules).
-// Exact reference semantics for the rare elements the fast path cannot
-// certify (zeros, inf/NaN, ties, binade edges): IEEE division, quant.hpp
-// :217-228 verbatim. Out of line so it never bloats the hot loop.
+// Exact reference semantics for the rare elements the fast path does not
+// cover (inf/NaN operands, scales outside [2^-100, 2^100]): IEEE division,
+// quant.hpp:217-228 verbatim. Out of line so it never bloats the hot loop.
 static __device__ __noinline__ double2 slow_elem(float xv, float uv, double s, double q) {
   const GradTerm gt = grad_term(xv, s, q);
   return make_double2(__dmul_rn(gt.d_ds, (double)uv), (double)masked_upstream(gt.mask, uv));

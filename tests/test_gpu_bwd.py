@@ -206,7 +206,7 @@ def test_bwd_multi_table_and_determinism(qfb, orc, cuda):
 
 def test_special_values_bitwise(qfb, orc, cuda):
     """inf / NaN / +-0 / subnormal / huge x and +-inf / NaN upstream through
-    the certified division and the x86 NaN rules of d_input."""
+    the fast two-correction quotient, its IEEE exits and the x86 NaN rules of d_input."""
     rng = np.random.default_rng(77)
     sp = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 1e-45, -1e-45, 1.17e-38, 3.4e38, -3.4e38,
                    0.5, -0.5, 1.5, 127.0, 127.5, -127.5, 126.5, 1e-8], dtype=np.float32)
