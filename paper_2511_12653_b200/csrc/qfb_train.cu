@@ -24,6 +24,7 @@
 #include <string>
 
 #include "../../include/qfb.h"
+#include "qfb_device.cuh"
 #include "qfb_kernels.h"
 
 namespace qfb {
@@ -55,20 +56,12 @@ __device__ __forceinline__ void node_of(uint64_t n, uint32_t g, uint32_t levels,
 }
 
 // MSE terms of pair_loss (distill.hpp:84-91): d = double(s) - double(t),
-// term d*d; the student gradient starts as 0.0f + float(2d/n).
-struct MseTerm {
-  const float* s;
-  const float* t;
-  float* ds;
-  double n;
-  uint64_t stride;  // elements per pair (batch b starts at b * stride)
-  __device__ __forceinline__ double operator()(uint32_t b, uint64_t i) const {
-    const uint64_t j = (uint64_t)b * stride + i;
-    const double d = __dadd_rn((double)__ldg(s + j), -(double)__ldg(t + j));
-    ds[j] = __fadd_rn(0.0f, __double2float_rn(__ddiv_rn(__dmul_rn(2.0, d), n)));
-    return __dmul_rn(d, d);
-  }
-};
+// term d*d (the matching gradient 0.0f + float(2d/n) is produced by the
+// cosine kernel, which reads s and t anyway).
+__device__ __forceinline__ double mse_term(float sv, float tv) {
+  const double d = __dadd_rn((double)sv, -(double)tv);
+  return __dmul_rn(d, d);
+}
 
 // Stored terms (cosines per location).
 struct LoadTerm {
@@ -105,6 +98,52 @@ __global__ void leaf_sums_kernel(Term f, uint64_t n, uint32_t depth, double* out
   out[((uint64_t)b << depth) + g] = r;
 }
 
+// MSE leaf sums with coalesced loads: warp w of a CTA owns 32 consecutive
+// leaf groups (<= 512 contiguous elements), stages their s and t through
+// shared memory with coalesced loads, then each lane folds its group in
+// the reference order. Pair b = blockIdx.y.
+constexpr int kMseWarps = 8;
+__global__ void __launch_bounds__(kMseWarps * 32) mse_leaf_kernel(const float* __restrict__ s,
+                                                                 const float* __restrict__ t, uint64_t n,
+                                                                 uint32_t depth, double* out) {
+  __shared__ float ss[kMseWarps][2][32 * kLeaf];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t b = blockIdx.y;
+  const uint32_t groups = 1u << depth;
+  const uint32_t g = (blockIdx.x * kMseWarps + warp) * 32u + (uint32_t)lane;
+  uint64_t lo = 0, m = 0;
+  if (g < groups) node_of(n, g, depth, lo, m);
+  // the warp's element range [w0, w1)
+  const uint64_t w0 = __shfl_sync(0xffffffffu, lo, 0);
+  const uint32_t last = min(31u, groups > (g - lane) ? groups - (g - lane) - 1u : 0u);
+  const uint64_t w1 = __shfl_sync(0xffffffffu, lo + m, (int)last);
+  if (g - (uint32_t)lane >= groups) return;  // warp past the end
+  const float* sp = s + (uint64_t)b * n + w0;
+  const float* tp = t + (uint64_t)b * n + w0;
+  const int cnt = (int)(w1 - w0);
+  for (int i = lane; i < cnt; i += 32) {
+    ss[warp][0][i] = __ldg(sp + i);
+    ss[warp][1][i] = __ldg(tp + i);
+  }
+  __syncwarp();
+  if (g >= groups) return;
+  const float* a = ss[warp][0] + (lo - w0);
+  const float* c = ss[warp][1] + (lo - w0);
+  auto fold = [&](int k0, int k1) {
+    double acc = 0.0;
+    for (int k = k0; k < k1; ++k) acc = __dadd_rn(acc, mse_term(a[k], c[k]));
+    return acc;
+  };
+  double r;
+  if (m <= 8) {
+    r = fold(0, (int)m);
+  } else {
+    const int h = (int)(m >> 1);
+    r = __dadd_rn(fold(0, h), fold(h, (int)m));
+  }
+  out[((uint64_t)b << depth) + g] = r;
+}
+
 // Perfect-tree halving: per pair y = blockIdx.y (cnt values each), CTA x
 // reduces in[2048 x .. 2048 x + 2048) (a power of two count `cnt` <= 2048
 // when fewer remain) to out[x]. On the last pass the single result per pair
@@ -134,6 +173,10 @@ __global__ void __launch_bounds__(kRedThreads) halve_kernel(const double* in, ui
 
 // pairwise_sum(terms of pair b, n) / div -> res[b * res_stride] for the nb
 // pairs, via scratch `ws` (>= nb * (2^D + 2^D/2048) doubles).
+// Halving passes over nb x 2^depth leaf sums already in ws.
+cudaError_t halve_all(uint32_t depth, uint32_t nb, double div, double* res, uint32_t res_stride, double* ws,
+                      cudaStream_t st, int* launches);
+
 template <typename Term>
 cudaError_t pairwise_sum_dev(const Term& f, uint64_t n, uint32_t nb, double div, double* res,
                              uint32_t res_stride, double* ws, cudaStream_t st, int* launches) {
@@ -141,6 +184,12 @@ cudaError_t pairwise_sum_dev(const Term& f, uint64_t n, uint32_t nb, double div,
   const uint32_t groups = 1u << depth;
   leaf_sums_kernel<Term><<<dim3((groups + 255) / 256, nb), 256, 0, st>>>(f, n, depth, ws);
   ++*launches;
+  return halve_all(depth, nb, div, res, res_stride, ws, st, launches);
+}
+
+cudaError_t halve_all(uint32_t depth, uint32_t nb, double div, double* res, uint32_t res_stride, double* ws,
+                      cudaStream_t st, int* launches) {
+  const uint32_t groups = 1u << depth;
   double* in = ws;
   double* out = ws + (uint64_t)nb * groups;
   uint32_t cnt = groups;
@@ -166,7 +215,7 @@ cudaError_t pairwise_sum_dev(const Term& f, uint64_t n, uint32_t nb, double div,
 // accumulations, so unrolling keeps several in flight.
 __global__ void cosine_kernel(const float* __restrict__ s, const float* __restrict__ t,
                               float* __restrict__ ds, uint64_t c, uint64_t hw, double w,
-                              double gscale, double* __restrict__ cos_loc) {
+                              double gscale, double n, double* __restrict__ cos_loc) {
   const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= hw) return;
   const uint64_t pair = blockIdx.y;
@@ -189,15 +238,27 @@ __global__ void cosine_kernel(const float* __restrict__ s, const float* __restri
     nrm = __dsqrt_rn(__dmul_rn(na2, nb2));
     cosv = __ddiv_rn(dot, nrm);
   }
+  // the per-element divisions by n, nrm and na2 use hoisted reciprocals and
+  // two Markstein corrections (correctly rounded, qfb_device.cuh
+  // markstein2_div; a zero numerator may come out +0 instead of -0, which
+  // the following float additions to a non-negative-zero g cannot observe)
+  DivCtx dn, dr, da;
+  dn.s = n;
+  dn.y = __drcp_rn(n);
+  dr.s = nrm;
+  dr.y = __drcp_rn(nrm);
+  da.s = zero ? 1.0 : na2;
+  da.y = __drcp_rn(da.s);
   cos_loc[p] = cosv;
 #pragma unroll 4
   for (uint64_t ch = 0; ch < c; ++ch) {
     const uint64_t i = ch * hw + p;
-    float g = ds[i];
+    const double a = (double)__ldg(s + i);
+    const double b = (double)__ldg(t + i);
+    // MSE part (distill.hpp:89-90): 0.0f + float(2d/n)
+    float g = __fadd_rn(0.0f, __double2float_rn(markstein2_div(__dmul_rn(2.0, __dadd_rn(a, -b)), dn)));
     if (!zero) {
-      const double a = (double)__ldg(s + i);
-      const double b = (double)__ldg(t + i);
-      const double q = __dadd_rn(__ddiv_rn(b, nrm), -__ddiv_rn(__dmul_rn(cosv, a), na2));
+      const double q = __dadd_rn(markstein2_div(b, dr), -markstein2_div(__dmul_rn(cosv, a), da));
       g = __fadd_rn(g, __double2float_rn(__dmul_rn(-w, q)));
     }
     ds[i] = __double2float_rn(__dmul_rn((double)g, gscale));
@@ -286,12 +347,18 @@ qfb_status qfb_distill_batch(qfb_ctx* ctx, const float* student, const float* te
   int launches = 0;
   // MSE (+ d_s = float(2d/n)) then per-location cosine (+ its gradient and
   // the chunk scaling), then the mean cosine over locations
-  MseTerm mt{student, teacher, d_student, (double)n, n};
-  cudaError_t e = pairwise_sum_dev(mt, n, nb, (double)n, out, 2, static_cast<double*>(ws), st, &launches);
+  const uint32_t depth_n = tree_depth(n);
+  const uint32_t per_cta = 32u * kMseWarps;
+  mse_leaf_kernel<<<dim3(((1u << depth_n) + per_cta - 1) / per_cta, nb), per_cta, 0, st>>>(
+      student, teacher, n, depth_n, static_cast<double*>(ws));
+  ++launches;
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess)
+    e = halve_all(depth_n, nb, (double)n, out, 2, static_cast<double*>(ws), st, &launches);
   if (e == cudaSuccess) {
     const double w = lambda_cos / (double)hw;
     cosine_kernel<<<dim3((unsigned)(((uint64_t)hw + 255) / 256), nb), 256, 0, st>>>(
-        student, teacher, d_student, (uint64_t)channels, (uint64_t)hw, w, grad_scale,
+        student, teacher, d_student, (uint64_t)channels, (uint64_t)hw, w, grad_scale, (double)n,
         static_cast<double*>(cl));
     ++launches;
     e = cudaGetLastError();

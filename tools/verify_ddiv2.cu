@@ -58,6 +58,36 @@ __global__ void all_x_kernel(const double* scales, int ns) {
   }
 }
 
+// Random double numerators (53-bit significands, exponents within +-60 of
+// the divisor's) against the same divisors: the distillation loss divides
+// doubles (2d/n, b/nrm, cos*a/na2) with hoisted reciprocals too.
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+
+__global__ void random_num_kernel(const double* scales, int ns, uint32_t per_thread) {
+  const int si = blockIdx.y;
+  if (si >= ns) return;
+  const double s = scales[si];
+  const double y = __drcp_rn(s);
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int es = (int)((__double_as_longlong(s) >> 52) & 0x7ff);
+  for (uint32_t k = 0; k < per_thread; ++k) {
+    const uint64_t r = mix64((t << 20) ^ ((uint64_t)si << 44) ^ k);
+    int e = es + (int)((r >> 52) % 121) - 60;
+    if (e < 200) e = 200;  // keep quotients and residuals normal (well inside the range)
+    if (e > 1800) e = 1800;
+    const double x = __longlong_as_double((long long)((r & 0x800fffffffffffffull) | ((uint64_t)e << 52)));
+    if (__double_as_longlong(__ddiv_rn(x, s)) != __double_as_longlong(ddiv2(x, s, y))) {
+      const unsigned long long i = atomicAdd(&g_bad, 1ull);
+      if (i < 8) g_first[i] = ((unsigned long long)si << 32) | k;
+    }
+  }
+}
+
 int main(int argc, char** argv) {
   const int n_random = argc > 1 ? atoi(argv[1]) : 2048;
   const int single = argc > 2 ? atoi(argv[2]) : 0;
@@ -96,6 +126,22 @@ int main(int argc, char** argv) {
   cudaError_t err = cudaDeviceSynchronize();
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
+  // double numerators: 2^30 random per scale
+  unsigned long long bad_f = 0;
+  cudaMemcpyFromSymbol(&bad_f, g_bad, sizeof bad_f);
+  cudaEventRecord(e0);
+  for (int b = 0; b < ns; b += chunk) {
+    const int n = ns - b < chunk ? ns - b : chunk;
+    random_num_kernel<<<dim3((1u << 20) / 256, n), 256>>>(d_sc + b, n, 1024);
+  }
+  cudaEventRecord(e1);
+  cudaDeviceSynchronize();
+  float ms2 = 0;
+  cudaEventElapsedTime(&ms2, e0, e1);
+  unsigned long long bad_all = 0;
+  cudaMemcpyFromSymbol(&bad_all, g_bad, sizeof bad_all);
+  printf("verify_ddiv2 double numerators: %d scales x 2^30 random doubles: %llu mismatches (%.1f s)\n", ns,
+         bad_all - bad_f, ms2 / 1e3);
   unsigned long long bad = 0, first[8];
   cudaMemcpyFromSymbol(&bad, g_bad, sizeof bad);
   cudaMemcpyFromSymbol(first, g_first, sizeof first);
