@@ -14,9 +14,11 @@
 #pragma once
 
 #include <cstdint>
+#include <map>
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "qfb.h"
@@ -226,6 +228,96 @@ inline void fake_quantize_backward(Context& ctx, const DeviceView& x, const void
                                    double* d_log_s, bool accumulate = false, int q_max = 127) {
   check(qfb_fq_bwd(ctx.get(), x.dtype, x.data, up, dx, x.outer, x.channels, x.inner, d_scale64,
                    d_chain, q_max, d_log_s, accumulate ? 1 : 0));
+}
+
+// ------------------------------------------- QAT step pieces (f3) --
+// qf::DistillLoss (distill.hpp:48-55) shape.
+template <class Tensor>
+struct DistillLoss {
+  double total = 0.0, mse_f = 0.0, mse_i = 0.0, cos_f = 0.0, cos_i = 0.0;
+  Tensor d_features;
+  Tensor d_descriptors;
+};
+
+// qf::distill_loss (distill.hpp:126-141) on host tensors [C, ...]; computed
+// on the GPU, bit-identical.
+template <class Tensor>
+inline DistillLoss<Tensor> distill_loss(Context& ctx, const Tensor& f_s, const Tensor& f_t, const Tensor& i_s,
+                                        const Tensor& i_t, double lambda_cos) {
+  if (f_s.shape != f_t.shape || i_s.shape != i_t.shape) throw ShapeError("distill_loss: student/teacher shape");
+  if (f_s.shape.empty() || f_s.shape[0] < 1) throw ShapeError("distill_loss: channel dim must be >= 1");
+  const int64_t fc = f_s.shape[0], ic = i_s.shape[0];
+  DistillLoss<Tensor> out{0, 0, 0, 0, 0, f_s, i_s};
+  out.d_features.precision = decltype(f_s.precision)(0);
+  out.d_descriptors.precision = decltype(i_s.precision)(0);
+  double o5[5];
+  check(qfb_distill_loss_host(ctx.get(), f_s.data.data(), f_t.data.data(), fc, (int64_t)f_s.data.size() / fc,
+                              i_s.data.data(), i_t.data.data(), ic, (int64_t)i_s.data.size() / ic, lambda_cos,
+                              1.0, o5, out.d_features.data.data(), out.d_descriptors.data.data()));
+  out.total = o5[0];
+  out.mse_f = o5[1];
+  out.mse_i = o5[2];
+  out.cos_f = o5[3];
+  out.cos_i = o5[4];
+  return out;
+}
+
+// ------------------------------------------------------ formats (f4) --
+// qf::load_tensor / save_tensor (tensor_io.hpp:115-125).
+template <class Tensor>
+inline Tensor load_tensor(const std::string& path) {
+  qfb_tensor_file* t = nullptr;
+  check(qfb_qsim_load(path.c_str(), &t));
+  int32_t rank = 0, prec = 0;
+  const int64_t* shape = nullptr;
+  int64_t n = 0;
+  const float* data = nullptr;
+  check(qfb_qsim_info(t, &rank, &shape, &prec, &n, &data));
+  Tensor out(std::vector<int64_t>(shape, shape + rank), std::vector<float>(data, data + n),
+             static_cast<decltype(Tensor{}.precision)>(prec));
+  qfb_qsim_free(t);
+  return out;
+}
+
+template <class Tensor>
+inline void save_tensor(const std::string& path, const Tensor& t) {
+  check(qfb_qsim_save(path.c_str(), t.data.data(), (int32_t)t.shape.size(), t.shape.data(),
+                      (int32_t)t.precision));
+}
+
+// qf::load_scales / save_scales (distill.hpp:320-362): name -> (log_w, log_a).
+using ScaleMap = std::map<std::string, std::pair<std::vector<double>, double>>;
+
+inline ScaleMap load_scales(const std::string& path) {
+  qfb_scales* sc = nullptr;
+  check(qfb_qscl_load(path.c_str(), &sc));
+  ScaleMap out;
+  for (int32_t i = 0; i < qfb_qscl_count(sc); ++i) {
+    const char* name = nullptr;
+    const double* w = nullptr;
+    int64_t cnt = 0;
+    double a = 0.0;
+    check(qfb_qscl_layer(sc, i, &name, &w, &cnt, &a));
+    out[name] = {std::vector<double>(w, w + cnt), a};
+  }
+  qfb_qscl_free(sc);
+  return out;
+}
+
+// Any qf::ScaleSet-shaped value (by_layer: name -> {log_w_scale, log_a_scale}).
+template <class SetT>
+inline void save_scales(const std::string& path, const SetT& set) {
+  std::vector<const char*> names;
+  std::vector<const double*> w;
+  std::vector<int64_t> counts;
+  std::vector<double> a;
+  for (const auto& [name, p] : set.by_layer) {
+    names.push_back(name.c_str());
+    w.push_back(p.log_w_scale.data());
+    counts.push_back((int64_t)p.log_w_scale.size());
+    a.push_back(p.log_a_scale);
+  }
+  check(qfb_qscl_save(path.c_str(), (int32_t)names.size(), names.data(), w.data(), counts.data(), a.data()));
 }
 
 }  // namespace qfb

@@ -110,10 +110,29 @@ def test_cpp_mirror_compiles_against_reference_types(tmp_path):
     src.write_text(r'''
 #include <cstdio>
 #include <span>
+#include "quantfuse/distill.hpp"
 #include "quantfuse/quant.hpp"
+#include "quantfuse/tensor_io.hpp"
 #include "qfb.hpp"
 int main() {
   qf::QuantConfig cfg;
+  // formats (host only): our writers/readers round-trip the reference's
+  {
+    qf::Tensor t({2, 3}, {1, -2, 3, 4.5f, -0.0f, 6}, qf::Precision::EmulatedHalf);
+    qf::save_tensor("t_ref.qsim", t);
+    qf::Tensor u = qfb::load_tensor<qf::Tensor>("t_ref.qsim");
+    if (u.shape != t.shape || u.data != t.data || u.precision != t.precision) return 4;
+    qfb::save_tensor("t_qfb.qsim", u);
+    if (qf::read_file("t_qfb.qsim") != qf::read_file("t_ref.qsim")) return 5;
+    qf::ScaleSet set;
+    set.by_layer["conv1"] = qf::ScaleParams{{-3.0, -2.5}, -1.25};
+    set.by_layer["fnet_out"] = qf::ScaleParams{{-4.0}, -2.0};
+    qf::save_scales("s_ref.qscl", set);
+    qfb::ScaleMap m = qfb::load_scales("s_ref.qscl");
+    if (m.size() != 2 || m["conv1"].first.size() != 2 || m["fnet_out"].second != -2.0) return 6;
+    qfb::save_scales("s_qfb.qscl", set);
+    if (qf::read_file("s_qfb.qscl") != qf::read_file("s_ref.qscl")) return 7;
+  }
   // host scale math: bit-identical to the reference
   for (double ls : {-30.0, -3.0, 0.0, 2.5}) {
     if (qfb::resolve_scale(ls, cfg) != qf::resolve_scale(ls, cfg)) return 1;
@@ -125,7 +144,8 @@ int main() {
     qf::Tensor y = qfb::fake_quantize(ctx, x, std::span<const double>(s), cfg);
     qf::Tensor y_ref = qf::fake_quantize(x, std::span<const double>(s), cfg);
     auto g = qfb::fake_quantize_backward(ctx, x, std::span<const double>(s), cfg, x, qf::Precision::Full);
-    return y.data == y_ref.data && g.d_log_scale.size() == 2 ? 0 : 3;
+    auto dl = qfb::distill_loss(ctx, x, x, x, x, 1.0);
+    return y.data == y_ref.data && g.d_log_scale.size() == 2 && dl.total == 0.0 ? 0 : 3;
   } catch (const qfb::CudaError&) {
     std::puts("no-gpu");
     return 0;
@@ -136,7 +156,8 @@ int main() {
 }
 ''')
     exe = tmp_path / "dropin"
-    subprocess.run(["g++", "-std=c++20", "-O1", f"-I{ref_inc}", f"-I{ROOT}/include", str(src),
+    json_inc = "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann"
+    subprocess.run(["g++", "-std=c++20", "-O1", f"-I{ref_inc}", f"-I{json_inc}", f"-I{ROOT}/include", str(src),
                     "-o", str(exe), LIB, f"-Wl,-rpath,{os.path.dirname(LIB)}"], check=True)
-    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, cwd=str(tmp_path))
     assert r.returncode == 0, r.stdout + r.stderr
