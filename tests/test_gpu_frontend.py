@@ -50,12 +50,18 @@ def test_frontend_pass_matches_oracle(qfb, orc, cuda, dtype, int8_out):
                 ci += 1
 
 
+@pytest.mark.parametrize("full", [False, True])
 @pytest.mark.parametrize("gelu", [False, True])
-def test_window_chain_pass_matches_oracle(qfb, orc, cuda, gelu):
+def test_window_chain_pass_matches_oracle(qfb, orc, cuda, gelu, full):
+    """full=True is BASELINE config 3 as benched (15-frame window, 96 patches,
+    480x640)."""
     import torch
     from paper_2511_12653_b200.frontend import WindowChainPass
     ctx = qfb.default_context(0)
-    wp = WindowChainPass(ctx, frames=2, patches=4, gelu=gelu, dtype="f32", device=cuda, h=48, w=64)
+    if full:
+        wp = WindowChainPass(ctx, gelu=gelu, dtype="f32", device=cuda)
+    else:
+        wp = WindowChainPass(ctx, frames=2, patches=4, gelu=gelu, dtype="f32", device=cuda, h=48, w=64)
     wp.run()
     torch.cuda.synchronize()
     ctx.sync()
@@ -67,3 +73,37 @@ def test_window_chain_pass_matches_oracle(qfb, orc, cuda, gelu):
         assert st == 0
         for y, w in zip(ys, want):
             assert np.array_equal(b32(y.cpu().numpy()), b32(w)), p.name
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f16"])
+def test_full_size_frame_matches_oracle(qfb, orc, cuda, dtype):
+    """BASELINE config 2 at full size (one 480x640 frame, 41.2 M quant-point
+    elements): every forward output, d_input and scale gradient of the
+    benchmarked pass equals the oracle, plus a size-independent property
+    (FQ values sit on their channel's grid s*q, |q| <= 128)."""
+    import torch
+    from paper_2511_12653_b200.frontend import FrontendQuantPass
+    ctx = qfb.default_context(0)
+    fp = FrontendQuantPass(ctx, frames=1, dtype=dtype, sets=1, seed=77, device=cuda)
+    half = 1 if dtype == "f16" else 0
+    fp.forward(0)
+    fp.backward(0)
+    torch.cuda.synchronize()
+    ctx.sync()
+    ci = 0
+    for pi, p in enumerate(fp.points):
+        x = orc.fill_rng(p.numel, 77, pi, kind=1, lo=1.0, half=half)
+        for _k in p.consumers:
+            s64 = np.array(qfb.scale_grad_factors(fp.log_s[ci].tolist())[0])
+            _, want = orc.fake_quantize(x, s64, 1, p.channels, p.inner, half=half)
+            got = fp.y[ci].float().cpu().numpy().ravel()
+            assert np.array_equal(b32(got), b32(want)), p.name
+            codes = got.astype(np.float64).reshape(p.channels, -1) / s64[:, None]
+            tol = 1e-3 if half else 1e-6
+            assert np.all(np.abs(codes - np.rint(codes)) <= tol * np.maximum(1.0, np.abs(codes)))
+            assert np.all(np.abs(np.rint(codes)) <= 128)
+            up = orc.fill_rng(p.numel, 77 + 500, ci, kind=1, lo=1.0, half=half)
+            _, dx, dls = orc.fq_backward(x, up, fp.log_s[ci], 1, p.channels, p.inner)
+            assert np.array_equal(b32(fp.dx[ci].float().cpu().numpy().ravel()), b32(dx)), p.name
+            assert fp.dls[ci].cpu().numpy().tobytes() == dls.tobytes(), p.name
+            ci += 1
