@@ -48,6 +48,11 @@ constexpr int kMaxStages = 8;
 // no refills or stores). Not used in production; results in DESIGN.md §7.
 constexpr int kProbeNoCompute = 8;
 constexpr int kProbeNoLoads = 16;
+#ifdef QFB_BWD_CHECKED
+constexpr bool kBwdChecked = true;   // A/B build: per-element inf/NaN tests everywhere
+#else
+constexpr bool kBwdChecked = false;
+#endif
 constexpr int kWinPad = 32;                // window slack: 16-byte rounding at both ends
 constexpr size_t kRingBudget = 72 * 1024;  // default per-CTA ring + sums: 3 CTAs per SM
 constexpr size_t kRedBytes = kBwdThreads * sizeof(double);  // group sums of one stage
@@ -339,11 +344,83 @@ __device__ __forceinline__ double group_sum_lr(T* sx, const T* su, int h, const 
   return __dadd_rn(acc_l, acc_r);
 }
 
+// Unchecked fast path for tiles with a usable scale (s in [2^-100, 2^100]):
+// no per-element inf/NaN test. It is exact for every operand:
+//  - non-finite x: markstein2_div gives NaN, so mask = false as for the IEEE
+//    quotient (inf or NaN), and the saturated term takes its sign from x
+//    (x > 0 ? q : -q), which is the reference's (z > 0 ? q : -q) for
+//    z = x/s = +-inf or NaN;
+//  - non-finite upstream: the term d_ds * up is the reference's product
+//    (d_ds is finite here); only d_input differs (masked NaN / inf rules),
+//    and such an element makes the group sum non-finite (term = inf or
+//    NaN; a finite term is < 2^136), so one test per group finds it and
+//    fix_nonfinite_up rewrites those d_input values.
+__device__ __forceinline__ double fast_term(float xv, float uv, const DivCtx& dc, double q,
+                                            float& dx) {
+  const double z = markstein2_div((double)xv, dc);
+  const bool mask = fabs(z) <= q;
+  const double sat = xv > 0.0f ? q : -q;
+  const double d_ds = mask ? __dadd_rn(rint(z), -z) : sat;
+  dx = mask ? uv : __uint_as_float(__float_as_uint(uv) & 0x80000000u);
+  return __dmul_rn(d_ds, (double)uv);
+}
+
+// d_input of the group's non-finite upstream values (rare): the fast path
+// stored up (mask) or +-0 (masked out); masked_upstream gives the
+// reference's value from that mask.
+template <typename T>
+static __device__ __noinline__ void fix_nonfinite_up(T* sx, const T* su, int glen) {
+  for (int k = 0; k < glen; ++k) {
+    const float uv = to_f<T>(su[k]);
+    if ((__float_as_uint(uv) & 0x7f800000u) == 0x7f800000u) {
+      const bool mask = isinf(to_f<T>(sx[k]));
+      sx[k] = from_f<T>(masked_upstream(mask, uv));
+    }
+  }
+}
+
+template <typename T, bool kDx, int LR>
+__device__ __forceinline__ double group_sum_lr_u(T* sx, const T* su, int h, const DivCtx& dc,
+                                                 double q) {
+  T* rx = sx + h;
+  const T* ru = su + h;
+  const bool lv = h == LR;
+  double acc_l = 0.0, acc_r = 0.0;
+#pragma unroll
+  for (int k = 0; k < LR; ++k) {
+    const bool l0 = k < LR - 1 || lv;  // left slot k valid
+    const float x0 = l0 ? to_f<T>(sx[k]) : 0.0f, u0 = l0 ? to_f<T>(su[k]) : 0.0f;
+    const float x2 = to_f<T>(rx[k]), u2 = to_f<T>(ru[k]);
+    float d0, d2;
+    const double t0 = fast_term(x0, u0, dc, q, d0);
+    const double t2 = fast_term(x2, u2, dc, q, d2);
+    if (kDx) {
+      if (l0) sx[k] = from_f<T>(d0);
+      rx[k] = from_f<T>(d2);
+    }
+    if (l0) acc_l = __dadd_rn(acc_l, t0);
+    acc_r = __dadd_rn(acc_r, t2);
+  }
+  const double v = __dadd_rn(acc_l, acc_r);
+  if (kDx && __builtin_expect((__double2hiint(v) & 0x7ff00000) == 0x7ff00000, 0))
+    fix_nonfinite_up<T>(sx, su, h + LR);
+  return v;
+}
+
 // Dispatch on the right-half length (groups of 9..16 elements, the only
 // sizes of rows with >= 16 * 2^g elements); other sizes take the generic loop.
 template <typename T, bool kDx>
 __device__ __forceinline__ double group_sum_any(T* sx, const T* su, int glen, const DivCtx& dc,
                                                 double q) {
+  if (glen >= 9 && dc.usable && !(kBwdChecked)) {
+    const int lr = (glen + 1) >> 1, h = glen >> 1;
+    switch (lr) {
+      case 5: return group_sum_lr_u<T, kDx, 5>(sx, su, h, dc, q);
+      case 6: return group_sum_lr_u<T, kDx, 6>(sx, su, h, dc, q);
+      case 7: return group_sum_lr_u<T, kDx, 7>(sx, su, h, dc, q);
+      default: return group_sum_lr_u<T, kDx, 8>(sx, su, h, dc, q);
+    }
+  }
   if (glen >= 9) {
     const int lr = (glen + 1) >> 1, h = glen >> 1;
     switch (lr) {
@@ -499,6 +576,10 @@ __global__ void __launch_bounds__(kBwdCtaThreads, 3) bwd_kernel(const __grid_con
       mbar_init(&done[s], kConsumerWarps);
     }
     fence_mbar_init();
+    // the finisher (launched as a programmatic dependent) may be scheduled
+    // into SM slots as CTAs retire; it waits for this grid's completion
+    // (griddepcontrol.wait) before it reads any partial
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   }
   __syncthreads();  // the only CTA barrier: barrier init
 
@@ -606,6 +687,7 @@ __global__ void __launch_bounds__(32) bwd_finish_kernel(const __grid_constant__ 
   const uint32_t tps = 1u << d.tps_log;
   const uint32_t lanes = tps < 32u ? tps : 32u;
   const uint32_t per = tps / lanes;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // see bwd_finish_reg_kernel
   const double chain = d.chain[c];
   double acc = 0.0;
   for (uint32_t o = 0; o < d.outer; ++o) {
@@ -636,6 +718,77 @@ __global__ void __launch_bounds__(32) bwd_finish_kernel(const __grid_constant__ 
   }
   if (lane == 0) d.d_log_s[c] = acc;
   (void)warp_base_mul;
+}
+
+// Register finisher for rows of <= 256 tiles (every DPVO shape): no shared
+// memory (so 32 warps per SM hide the partials' load latency), each lane's
+// `per` consecutive partials folded as a perfect subtree in registers, and
+// four rows (frames) of a channel loaded before they are folded in row order.
+// Same tree and fold order as bwd_finish_kernel.
+template <int PER>
+__device__ __forceinline__ double lane_slice(const double* p, int lane) {
+  double a[PER];
+#pragma unroll
+  for (int k = 0; k < PER; ++k) a[k] = p[lane * PER + k];
+#pragma unroll
+  for (int w = PER; w > 1; w >>= 1)
+#pragma unroll
+    for (int k = 0; k < w / 2; ++k) a[k] = __dadd_rn(a[2 * k], a[2 * k + 1]);
+  return a[0];
+}
+
+__device__ __forceinline__ double lane_slice_any(const double* p, int lane, uint32_t per) {
+  switch (per) {
+    case 1: return p[lane];
+    case 2: return lane_slice<2>(p, lane);
+    case 4: return lane_slice<4>(p, lane);
+    default: return lane_slice<8>(p, lane);
+  }
+}
+
+constexpr uint32_t kFinRegMaxTiles = 256;  // per <= 8
+constexpr int kFinRows = 4;
+
+__global__ void __launch_bounds__(32) bwd_finish_reg_kernel(const __grid_constant__ BwdBatch bt) {
+  uint32_t w = blockIdx.x;
+  int di = 0;
+  while (di < bt.n && w >= bt.d[di].chans) {
+    w -= bt.d[di].chans;
+    ++di;
+  }
+  if (di >= bt.n) return;
+  const BwdDesc& d = bt.d[di];
+  const uint32_t c = w;
+  const int lane = threadIdx.x;
+  const uint32_t tps = 1u << d.tps_log;
+  const uint32_t lanes = tps < 32u ? tps : 32u;
+  const uint32_t per = tps / lanes;
+  const bool on = (uint32_t)lane < lanes;
+  // prologue above overlaps the main pass's tail; d_log_s and the partials
+  // are read only after it has completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const double chain = d.chain[c];
+  double acc = d.accumulate ? d.d_log_s[c] : 0.0;
+  for (uint32_t o = 0; o < d.outer; o += kFinRows) {
+    double v[kFinRows];
+#pragma unroll
+    for (int j = 0; j < kFinRows; ++j) {
+      v[j] = 0.0;
+      if (on && o + j < d.outer)
+        v[j] = lane_slice_any(d.partials + (((uint64_t)(o + j) * d.chans + c) << d.tps_log), lane, per);
+    }
+#pragma unroll
+    for (int j = 0; j < kFinRows; ++j) {
+      for (uint32_t off = 1; off < lanes; off <<= 1)
+        v[j] = __dadd_rn(v[j], __shfl_xor_sync(0xffffffffu, v[j], off));
+      if (o + j < d.outer) {
+        const double r = __dmul_rn(v[j], chain);
+        // accumulate == 0: ((r0 + r1) + ...); else ((d_log_s + r0) + r1) + ...
+        acc = (o + j == 0 && !d.accumulate) ? r : __dadd_rn(acc, r);
+      }
+    }
+  }
+  if (lane == 0) d.d_log_s[c] = acc;
 }
 
 }  // namespace
@@ -723,9 +876,33 @@ cudaError_t launch_bwd(int dtype, const BwdBatch& b, int grid, cudaStream_t st) 
   void* args[] = {const_cast<BwdBatch*>(&b)};
   cudaError_t e = cudaLaunchKernel(bwd_fn(dtype), dim3(grid), dim3(kBwdCtaThreads), args, smem, st);
   if (e != cudaSuccess) return e;
-  uint32_t warps = 0;
-  for (int i = 0; i < b.n; ++i) warps += b.d[i].chans;
-  bwd_finish_kernel<<<warps, 32, 0, st>>>(b, 0u);
+  uint32_t warps = 0, max_tps = 0;
+  for (int i = 0; i < b.n; ++i) {
+    warps += b.d[i].chans;
+    max_tps = std::max(max_tps, 1u << b.d[i].tps_log);
+  }
+  static const bool pdl = [] {
+    const char* e = getenv("QFB_FIN_PDL");
+    return !(e && e[0] == '0');
+  }();
+  static const bool force_smem = [] {
+    const char* e = getenv("QFB_FIN_SMEM");
+    return e && e[0] == '1';
+  }();
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(warps);
+    cfg.blockDim = dim3(32);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    if (max_tps <= kFinRegMaxTiles && !force_smem) e = cudaLaunchKernelEx(&cfg, bwd_finish_reg_kernel, b);
+    else e = cudaLaunchKernelEx(&cfg, bwd_finish_kernel, b, 0u);
+    if (e != cudaSuccess) return e;
+  }
   return cudaGetLastError();
 }
 

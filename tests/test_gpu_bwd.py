@@ -230,6 +230,41 @@ def test_special_values_bitwise(qfb, orc, cuda):
         check_grads(g.d_log_scale, dls, TOL_F32)
 
 
+def test_special_values_half_storage(qfb, orc, cuda):
+    """The same specials on binary16 storage: +-inf / NaN x and upstream in
+    rows long enough for the unrolled leaf groups (9/10 elements), per
+    channel; d_input equal (NaN where the reference has NaN), finite-upstream
+    scale gradients bitwise."""
+    import torch
+    rng = np.random.default_rng(78)
+    C, n = 4, 6000
+    x = rng.normal(0, 2, (C, n)).astype(np.float16).astype(np.float32)
+    x[:, ::101] = np.inf
+    x[:, 1::101] = -np.inf
+    x[:, 2::101] = np.nan
+    x[:, 3::101] = -0.0
+    up = rng.normal(0, 1, (C, n)).astype(np.float16).astype(np.float32)
+    ls = rng.uniform(-4, -1, C)
+    for nonfinite_up in (True, False):
+        u = up.copy()
+        if nonfinite_up:
+            u[:, 5::89] = np.inf
+            u[:, 6::89] = -np.inf
+            u[:, 7::89] = np.nan
+        xd = torch.from_numpy(x).to(cuda).half()
+        ud = torch.from_numpy(u).to(cuda).half()
+        g = qfb.fake_quantize_backward(xd, ls.tolist(), None, ud)
+        _, dx, dls = orc.fq_backward(x, u, ls, 1, C, n)
+        got = host(g.d_input.float()).ravel()
+        nan_w = np.isnan(dx)
+        assert np.array_equal(np.isnan(got), nan_w)
+        assert np.array_equal(bits32(got[~nan_w]), bits32(dx[~nan_w]))
+        if nonfinite_up:
+            assert np.array_equal(np.isnan(np.asarray(g.d_log_scale)), np.isnan(dls))
+        else:
+            check_grads(g.d_log_scale, dls, TOL_F16)
+
+
 @pytest.mark.parametrize("half", [0, 1])
 def test_relu_activations_bitwise(qfb, orc, cuda, half):
     """Post-ReLU conv inputs (about half the elements +-0, the zeros taking
