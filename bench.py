@@ -49,6 +49,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-graph", action="store_true")
+    p.add_argument("--graph-steps", type=int, default=8,
+                   help="consecutive steps captured in one CUDA graph (N=1)")
     p.add_argument("--cpu-seconds", type=float, default=15.0)
     p.add_argument("--no-secondary", action="store_true",
                    help="skip the config-3 chain window and config-5 forward-throughput lines")
@@ -326,6 +328,12 @@ def run_qfb(args):
     use_graph = not args.no_graph
     graphs = []
     launches_per_step = 3
+    # steps per graph replay: G consecutive steps (sets alternating) in one
+    # graph, so the per-replay launch gap is paid once per G steps; at N > 1
+    # every step ends in the NCCL exchange, launched outside the graph (G = 1)
+    G = max(1, args.graph_steps) if ws == 1 else 1
+    G = G - G % nsets if G >= nsets else G
+    big = None
     if use_graph:
         try:
             c0 = ctx.launch_count
@@ -336,9 +344,16 @@ def run_qfb(args):
                     fp.backward(si)
                 graphs.append(g)
             launches_per_step = (ctx.launch_count - c0) // nsets
+            if G > 1:
+                big = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(big, stream=stream):
+                    for k in range(G):
+                        fp.forward(k % nsets)
+                        fp.backward(k % nsets)
         except Exception as exc:  # pragma: no cover - fall back to eager timing
             print(f"graph capture failed ({exc}); timing eager launches", file=sys.stderr)
             use_graph = False
+            big = None
 
     def step(i):
         if use_graph:
@@ -347,8 +362,21 @@ def run_qfb(args):
         else:
             eager_step(i)
 
+    def run_steps(k):
+        """k consecutive steps from step 0 (set order preserved)."""
+        i = 0
+        if big is not None:
+            for _ in range(k // G):
+                big.replay()
+            i = (k // G) * G
+        while i < k:
+            step(i)
+            i += 1
+
     for i in range(args.warmup):
         step(i)
+    if big is not None:
+        big.replay()
     ctx.sync()
     if pg is not None:
         pg.barrier()
@@ -361,8 +389,7 @@ def run_qfb(args):
     t_end = torch.cuda.Event(enable_timing=True)
     wall0 = time.perf_counter()
     t_start.record(stream)
-    for i in range(args.steps):
-        step(i)
+    run_steps(args.steps)
     t_end.record(stream)
     torch.cuda.synchronize(dev)
     wall1 = time.perf_counter()
@@ -442,8 +469,9 @@ def run_qfb(args):
                 "kernel_ms": {"fwd": fwd_ms, "bwd": bwd_ms},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clocks, "secondary": secondary,
-                "timing": ("value: CUDA-graph replay of the step (fwd + bwd + finisher launches) "
-                           "between CUDA events on the library stream" if use_graph else
+                "timing": (f"value: CUDA-graph replays of {G} consecutive steps each (fwd + bwd + finisher "
+                           "launches per step, serial on the library stream) between CUDA events"
+                           if use_graph else
                            "value: eager launches between CUDA events on the library stream") +
                           f"; roofline: per-kernel CUDA events over {k_att} eager steps",
                 "wall_ms_per_step": (wall1 - wall0) * 1000.0 / args.steps}

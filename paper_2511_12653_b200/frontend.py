@@ -163,13 +163,18 @@ class FrontendQuantPass:
         bt = (CBwdDesc * len(bwd))(*bwd)
         return {"x": xs, "up": ups, "fwd": ft, "nf": len(fwd), "bwd": bt, "nb": len(bwd)}
 
-    def forward(self, set_index: int = 0) -> None:
+    def forward(self, set_index: int = 0, ctx: Context = None) -> None:
+        """All quant points' forward of one input set, on `ctx`'s stream
+        (default: the pass's context)."""
         s = self.sets[set_index]
-        check(lib().qfb_fq_fwd_multi(self.ctx.handle, self.dtype_code, s["fwd"], s["nf"]))
+        check(lib().qfb_fq_fwd_multi((ctx or self.ctx).handle, self.dtype_code, s["fwd"], s["nf"]))
 
-    def backward(self, set_index: int = 0) -> None:
+    def backward(self, set_index: int = 0, ctx: Context = None) -> None:
+        """All quant points' backward (+ finisher) of one input set. A second
+        context (own stream and scratch) lets the backward of frame k run
+        beside the forward of frame k+1."""
         s = self.sets[set_index]
-        check(lib().qfb_fq_bwd_multi(self.ctx.handle, self.dtype_code, s["bwd"], s["nb"]))
+        check(lib().qfb_fq_bwd_multi((ctx or self.ctx).handle, self.dtype_code, s["bwd"], s["nb"]))
 
     def scale_grads(self):
         return self.dls_flat
