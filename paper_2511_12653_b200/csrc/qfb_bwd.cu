@@ -539,6 +539,10 @@ template <typename T>
 __device__ __forceinline__ void store_dx(const BwdDesc& d, const TileRef& cur, Stage<T>& st,
                                          int lane) {
   if (d.dx == nullptr) return;
+  if (!d.vec) {  // a buffer off a 16-byte boundary: element stores
+    for (int e = lane; e < cur.m; e += 32) static_cast<T*>(d.dx)[cur.A + e] = st.x[cur.off + e];
+    return;
+  }
   const uint64_t b0 = cur.A * sizeof(T), b1 = (cur.A + (uint64_t)cur.m) * sizeof(T);
   const uint64_t i0 = (b0 + 15) & ~uint64_t(15), i1 = b1 & ~uint64_t(15);
   const int head = (int)(((i0 > b1 ? b1 : i0) - b0) / sizeof(T));

@@ -288,3 +288,47 @@ def test_relu_activations_bitwise(qfb, orc, cuda, half):
     got = host(g.d_input.float()).ravel()
     assert np.array_equal(bits32(got), bits32(dx))
     check_grads(g.d_log_scale, dls, TOL_F16 if half else TOL_F32)
+
+
+@pytest.mark.parametrize("half", [0, 1])
+@pytest.mark.parametrize("which", ["x", "up", "dx"])
+def test_unaligned_buffers(qfb, orc, cuda, half, which):
+    """x, upstream or d_input starting off a 16-byte boundary (one element
+    past an aligned allocation): the producer fills the stage itself and
+    d_input is stored element-wise; results bitwise as on aligned buffers."""
+    import torch
+    rng = np.random.default_rng(31 + half)
+    C, HW = 6, 4099
+    n = C * HW
+    x = rng.normal(0, 2, n).astype(np.float32)
+    up = rng.normal(0, 1, n).astype(np.float32)
+    if half:
+        x = x.astype(np.float16).astype(np.float32)
+        up = up.astype(np.float16).astype(np.float32)
+    dt = torch.float16 if half else torch.float32
+    ls = rng.uniform(-4, -1, C)
+
+    def buf(a, off):
+        base = torch.zeros(a.size + 8, dtype=dt, device=cuda)
+        v = base[off:off + a.size]
+        v.copy_(torch.from_numpy(a).to(dt))
+        return base, v
+    bx, xd = buf(x, 1 if which == "x" else 0)
+    bu, ud = buf(up, 1 if which == "up" else 0)
+    bd = torch.full((n + 8,), 7.0, dtype=dt, device=cuda)
+    dxd = bd[1:1 + n] if which == "dx" else bd[:n]
+    s64, chain = qfb.scale_grad_factors(ls.tolist())
+    fac = torch.tensor(s64 + chain, dtype=torch.float64, device=cuda)
+    dls = torch.zeros(C, dtype=torch.float64, device=cuda)
+    ctx = qfb.default_context(0)
+    code = qfb.F16 if half else qfb.F32
+    qfb.check(qfb.lib().qfb_fq_bwd(ctx.handle, code, xd.data_ptr(), ud.data_ptr(), dxd.data_ptr(), 1, C, HW,
+                                   fac.data_ptr(), fac.data_ptr() + 8 * C, 127, dls.data_ptr(), 0))
+    ctx.sync()
+    _, dx, want = orc.fq_backward(x, up, ls, 1, C, HW)
+    assert np.array_equal(bits32(host(dxd.float())), bits32(dx))
+    # the guard elements around d_input are untouched
+    g = host(bd.float())
+    lo = 1 if which == "dx" else 0
+    assert np.all(g[:lo] == 7.0) and np.all(g[lo + n:] == 7.0)
+    check_grads(dls.cpu().numpy(), want, TOL_F16 if half else TOL_F32)
