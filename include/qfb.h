@@ -442,6 +442,28 @@ qfb_status qfb_distill_loss_host(qfb_ctx* ctx, const float* f_s, const float* f_
 /* to the trainer's frame-order accumulation (frontend.hpp:222-228).      */
 qfb_status qfb_fold_rows(qfb_ctx* ctx, const double* rows, int64_t nrows, int64_t n,
                          const double* into, double* out);
+/* ---- multi-GPU scale-gradient exchange ----------------- */
+/* NCCL is loaded at run time (dlopen: the copy already in the process,    */
+/* else libnccl.so.2 / $QFB_NCCL_LIB); without it these return            */
+/* QFB_ERR_NCCL. `comm` is an ncclComm_t (void* here: no NCCL types in    */
+/* the ABI). The step's one exchange replaces the trainer's in-process    */
+/* `g += grad` over a chunk's frames (distill.hpp:249-250,                */
+/* frontend.hpp:222-228) when the frames are sharded over GPUs.           */
+qfb_status qfb_nccl_available(void);
+/* ncclCommInitAll: one communicator per device, single process, one      */
+/* stream per GPU (the process model of SURVEY §8e; no launcher needed).  */
+qfb_status qfb_nccl_comm_init_all(int ndev, const int* devices, void** comms);
+qfb_status qfb_nccl_comm_destroy(void* comm);
+/* In-place ncclAllReduce(sum) of n DEVICE doubles on the context stream  */
+/* (the cheap exchange; its bits depend on the GPU count).                */
+qfb_status qfb_allreduce_scale_grads(qfb_ctx* ctx, void* comm, double* grads, int64_t n);
+/* Bit-stable exchange: ncclAllGather of each rank's rows [rows_per_rank, */
+/* n] into gathered [nranks * rows_per_rank, n] (rank-major = frame order */
+/* when rank k holds frames k*rows_per_rank ...), then qfb_fold_rows      */
+/* (into nullable): identical bits at every GPU count.                     */
+qfb_status qfb_gather_fold_scale_grads(qfb_ctx* ctx, void* comm, const double* rows,
+                                       int64_t rows_per_rank, int64_t n, double* gathered,
+                                       const double* into, double* out);
 qfb_status qfb_adam_bias_corrections(double beta1, double beta2, int64_t t,
                                      double* bc1, double* bc2);
 qfb_status qfb_adam_step(qfb_ctx* ctx, double* params, double* m, double* v,

@@ -714,3 +714,63 @@ def fold_rows_device(rows, into=None, ctx: Optional[Context] = None):
     check(_lib.qfb_fold_rows(ctx.handle, _vp(rows.data_ptr()), rows.shape[0], out.numel(),
                              _vp(into.contiguous().data_ptr() if into is not None else None), _vp(out.data_ptr())))
     return out
+
+
+# ---- multi-GPU exchange through the C-ABI (qfb_nccl.cpp) -------------------
+_sig("qfb_nccl_available", _i32, [])
+_sig("qfb_nccl_comm_init_all", _i32, [ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(_vp)])
+_sig("qfb_nccl_comm_destroy", _i32, [_vp])
+_sig("qfb_allreduce_scale_grads", _i32, [_vp, _vp, _vp, _i64])
+_sig("qfb_gather_fold_scale_grads", _i32, [_vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp])
+
+
+def nccl_available() -> bool:
+    """True when libqfb found an NCCL library to dlopen."""
+    return _lib.qfb_nccl_available() == 0
+
+
+class NcclComms:
+    """Single-process communicators, one per device (ncclCommInitAll), for
+    the C-ABI exchange: the process model of SURVEY §8e. With torchrun
+    (one process per GPU) use dist.gather_fold instead."""
+
+    def __init__(self, devices):
+        self.devices = list(devices)
+        n = len(self.devices)
+        arr = (ctypes.c_int * n)(*self.devices)
+        self._comms = (_vp * n)()
+        check(_lib.qfb_nccl_comm_init_all(n, arr, self._comms))
+
+    def __getitem__(self, i):
+        return self._comms[i]
+
+    def close(self):
+        for i in range(len(self.devices)):
+            if self._comms[i]:
+                _lib.qfb_nccl_comm_destroy(self._comms[i])
+                self._comms[i] = None
+
+
+def gather_fold_scale_grads(comm, rows, nranks: int, into=None, ctx: Optional[Context] = None):
+    """qfb_gather_fold_scale_grads: all-gather this rank's gradient rows
+    [R, n] (float64 CUDA) over `comm` (nranks ranks) and fold all ranks'
+    rows in rank-major (= frame) order; returns the folded [n] vector."""
+    import torch
+    rows = rows.contiguous()
+    ctx = ctx or default_context(rows.device.index)
+    R, n = rows.shape[0], rows[0].numel()
+    gathered = torch.empty((R * nranks, n), dtype=torch.float64, device=rows.device)
+    out = torch.empty(n, dtype=torch.float64, device=rows.device)
+    check(_lib.qfb_gather_fold_scale_grads(ctx.handle, _vp(comm), _vp(rows.data_ptr()), R, n,
+                                           _vp(gathered.data_ptr()),
+                                           _vp(into.contiguous().data_ptr() if into is not None else None),
+                                           _vp(out.data_ptr())))
+    return out
+
+
+def allreduce_scale_grads(comm, grads, ctx: Optional[Context] = None):
+    """qfb_allreduce_scale_grads: in-place ncclAllReduce(sum) of a float64
+    CUDA vector (bits depend on the GPU count; see gather_fold)."""
+    ctx = ctx or default_context(grads.device.index)
+    check(_lib.qfb_allreduce_scale_grads(ctx.handle, _vp(comm), _vp(grads.data_ptr()), grads.numel()))
+    return grads

@@ -161,3 +161,13 @@ int main() {
                     "-o", str(exe), LIB, f"-Wl,-rpath,{os.path.dirname(LIB)}"], check=True)
     r = subprocess.run([str(exe)], capture_output=True, text=True, cwd=str(tmp_path))
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_nccl_loads_at_run_time():
+    """libqfb has no link-time NCCL dependency (dlopen at the call); in this
+    image the system libnccl.so.2 is found, so the exchange is available."""
+    import subprocess
+    from paper_2511_12653_b200 import LIB_PATH, nccl_available
+    deps = subprocess.run(["readelf", "-d", LIB_PATH], capture_output=True, text=True).stdout
+    assert "nccl" not in deps.lower()
+    assert nccl_available()
