@@ -141,6 +141,29 @@ qfb_status qfb::ctx_scratch(qfb_ctx* ctx, int slot, size_t bytes, void** p) {
 }
 cudaStream_t qfb::ctx_stream(const qfb_ctx* ctx) { return ctx->stream; }
 int qfb::ctx_device(const qfb_ctx* ctx) { return ctx->device; }
+
+bool qfb::pdl_enabled(int which) {
+  static const int mask = [] {
+    const char* e = getenv("QFB_PDL");
+    return e ? atoi(e) : kPdlFin;
+  }();
+  return (mask & which) != 0;
+}
+
+cudaError_t qfb::launch_main(const void* fn, dim3 grid, dim3 block, void** args, size_t smem,
+                             cudaStream_t st, int which) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled(which) ? 1 : 0;
+  return cudaLaunchKernelExC(&cfg, fn, args);
+}
 void qfb::ctx_count_launches(qfb_ctx* ctx, int n) { ctx->launches += n; }
 qfb_status qfb::cuda_error(cudaError_t e, const char* where) { return cuda_fail(e, where); }
 

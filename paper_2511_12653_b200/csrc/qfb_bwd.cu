@@ -572,6 +572,7 @@ __global__ void __launch_bounds__(kBwdCtaThreads, 3) bwd_kernel(const __grid_con
   const int warp = tid >> 5;
   const int lane = tid & 31;
   const uint32_t total = bt.tile_begin[bt.n];
+  pdl_wait();  // the preceding kernel's writes (launch_main) are visible
   if (blockIdx.x >= total) return;
 
   if (tid == 0) {
@@ -583,7 +584,7 @@ __global__ void __launch_bounds__(kBwdCtaThreads, 3) bwd_kernel(const __grid_con
     // the finisher (launched as a programmatic dependent) may be scheduled
     // into SM slots as CTAs retire; it waits for this grid's completion
     // (griddepcontrol.wait) before it reads any partial
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    pdl_trigger();
   }
   __syncthreads();  // the only CTA barrier: barrier init
 
@@ -691,7 +692,8 @@ __global__ void __launch_bounds__(32) bwd_finish_kernel(const __grid_constant__ 
   const uint32_t tps = 1u << d.tps_log;
   const uint32_t lanes = tps < 32u ? tps : 32u;
   const uint32_t per = tps / lanes;
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // see bwd_finish_reg_kernel
+  pdl_trigger();
+  pdl_wait();  // see bwd_finish_reg_kernel
   const double chain = d.chain[c];
   double acc = 0.0;
   for (uint32_t o = 0; o < d.outer; ++o) {
@@ -770,7 +772,8 @@ __global__ void __launch_bounds__(32) bwd_finish_reg_kernel(const __grid_constan
   const bool on = (uint32_t)lane < lanes;
   // prologue above overlaps the main pass's tail; d_log_s and the partials
   // are read only after it has completed
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  pdl_trigger();
+  pdl_wait();
   const double chain = d.chain[c];
   double acc = d.accumulate ? d.d_log_s[c] : 0.0;
   for (uint32_t o = 0; o < d.outer; o += kFinRows) {
@@ -878,35 +881,24 @@ cudaError_t launch_bwd(int dtype, const BwdBatch& b, int grid, cudaStream_t st) 
   if ((uint32_t)grid > tiles) grid = (int)tiles;
   const size_t smem = (size_t)b.nstages * (2 * b.stage_elems * (dtype == 0 ? 4 : 2) + kRedBytes);
   void* args[] = {const_cast<BwdBatch*>(&b)};
-  cudaError_t e = cudaLaunchKernel(bwd_fn(dtype), dim3(grid), dim3(kBwdCtaThreads), args, smem, st);
+  cudaError_t e = launch_main(bwd_fn(dtype), dim3(grid), dim3(kBwdCtaThreads), args, smem, st, kPdlBwd);
   if (e != cudaSuccess) return e;
   uint32_t warps = 0, max_tps = 0;
   for (int i = 0; i < b.n; ++i) {
     warps += b.d[i].chans;
     max_tps = std::max(max_tps, 1u << b.d[i].tps_log);
   }
-  static const bool pdl = [] {
-    const char* e = getenv("QFB_FIN_PDL");
-    return !(e && e[0] == '0');
-  }();
   static const bool force_smem = [] {
     const char* e = getenv("QFB_FIN_SMEM");
     return e && e[0] == '1';
   }();
-  {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(warps);
-    cfg.blockDim = dim3(32);
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 1 : 0;
-    if (max_tps <= kFinRegMaxTiles && !force_smem) e = cudaLaunchKernelEx(&cfg, bwd_finish_reg_kernel, b);
-    else e = cudaLaunchKernelEx(&cfg, bwd_finish_kernel, b, 0u);
-    if (e != cudaSuccess) return e;
-  }
+  uint32_t zero = 0;
+  void* fargs[] = {const_cast<BwdBatch*>(&b), &zero};
+  if (max_tps <= kFinRegMaxTiles && !force_smem)
+    e = launch_main((const void*)bwd_finish_reg_kernel, dim3(warps), dim3(32), fargs, 0, st, kPdlFin);
+  else
+    e = launch_main((const void*)bwd_finish_kernel, dim3(warps), dim3(32), fargs, 0, st, kPdlFin);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

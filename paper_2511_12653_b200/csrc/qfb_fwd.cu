@@ -244,6 +244,8 @@ __global__ void __launch_bounds__(kEwThreads, (kChain ? 6 : 10) / kFwdStages)
   const int tid = threadIdx.x;
 
   const uint32_t total = bt.chunk_begin[bt.n];
+  pdl_trigger();
+  pdl_wait();
   if (blockIdx.x >= total) return;
 
   // chunks go round robin over the CTAs (consecutive chunks in flight
@@ -529,8 +531,8 @@ cudaError_t ew_tma_occupancy(int dtype, bool chain, int stages, int* blocks_per_
 cudaError_t launch_ew_tma(int dtype, bool chain, int stages, const EwBatch& b, uint32_t* status,
                           int grid, cudaStream_t st) {
   void* args[] = {const_cast<EwBatch*>(&b), &status};
-  return cudaLaunchKernel(tma_fn(dtype, chain, stages), dim3(grid), dim3(kEwThreads), args,
-                          ew_tma_smem(chain, stages), st);
+  return launch_main(tma_fn(dtype, chain, stages), dim3(grid), dim3(kEwThreads), args,
+                     ew_tma_smem(chain, stages), st, kPdlFwd);
 }
 
 cudaError_t launch_ew(int dtype, bool chain, const EwBatch& b, uint32_t* status, int grid,

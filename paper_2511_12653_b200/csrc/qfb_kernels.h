@@ -22,6 +22,21 @@ int ctx_device(const qfb_ctx* ctx);
 void ctx_count_launches(qfb_ctx* ctx, int n);
 qfb_status cuda_error(cudaError_t e, const char* where);
 
+// Programmatic dependent launch for the main kernels (fwd TMA / ew, bwd,
+// finisher): each of them executes griddepcontrol.wait before touching
+// global memory and griddepcontrol.launch_dependents early, so the next
+// kernel's CTAs are scheduled into SM slots as this grid's CTAs retire and
+// its launch latency overlaps the tail. Stream order is unchanged: a
+// dependent still observes every write of the grid before it.
+// Which launches carry the attribute: bit 1 forward, 2 backward, 4
+// finisher (QFB_PDL overrides the default mask).
+constexpr int kPdlFwd = 1, kPdlBwd = 2, kPdlFin = 4;
+bool pdl_enabled(int which);
+// cudaLaunchKernelExC with the programmatic-serialization attribute when
+// pdl_enabled(which).
+cudaError_t launch_main(const void* fn, dim3 grid, dim3 block, void** args, size_t smem,
+                        cudaStream_t st, int which);
+
 struct FastDivHost {
   uint32_t d, m, s, pad;
 };
