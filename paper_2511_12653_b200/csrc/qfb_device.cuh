@@ -92,10 +92,15 @@ __device__ __forceinline__ float fq_value_fast(float x, float s, float y, float 
 // fq_value_fast for a finite, non-NaN x with |x * y| < 2^100 (binary16
 // inputs, |x| <= 65504, with s >= 2^-80): the overflow guard and the NaN
 // select of fq_value_fast are identities there and are dropped.
+// The residual is formed negated, r' = s*q0 - x (= -(x - s*q0) exactly,
+// RN being symmetric), and z = q0 - r'*y: the same value as the positive
+// form for every x != 0, and for x = +-0 it yields +-0 with x's sign
+// (-0: r' = -0 + +0 = +0, z = -0 + -0 = -0), so no copysign is needed.
+// tests/test_gpu_fwd.py::test_half_fast_path_all_values checks every
+// finite binary16 x over 64 scales.
 __device__ __forceinline__ float fq_value_fast_finite(float x, float s, float y, float q) {
   const float q0 = __fmul_rn(x, y);
-  float z = __fmaf_rn(__fmaf_rn(-s, q0, x), y, q0);
-  z = copysignf(z, x);
+  float z = __fmaf_rn(-__fmaf_rn(s, q0, -x), y, q0);
   z = fminf(fmaxf(z, -q), q);
   return __fmul_rn(s, rintf(z));
 }
@@ -105,6 +110,11 @@ __device__ __forceinline__ float fq_value_fast_finite(float x, float s, float y,
 __device__ __forceinline__ float pin_f(float v) {
   float r;
   asm volatile("mov.b32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+__device__ __forceinline__ uint32_t pin_u(uint32_t v) {
+  uint32_t r;
+  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
   return r;
 }
 
@@ -399,9 +409,12 @@ struct Elem<__half> {
       v[2 * i] = f.x;
       v[2 * i + 1] = f.y;
     }
-    // rare path: any all-ones exponent (inf/NaN) in the unit
-    const uint32_t e = (__vcmpeq2(r.x & 0x7c007c00u, 0x7c007c00u) | __vcmpeq2(r.y & 0x7c007c00u, 0x7c007c00u) |
-                        __vcmpeq2(r.z & 0x7c007c00u, 0x7c007c00u) | __vcmpeq2(r.w & 0x7c007c00u, 0x7c007c00u));
+    // rare path: any all-ones exponent (inf/NaN) in the unit. Per 16-bit
+    // half, (h & 0x7c00) + 0x0400 reaches bit 15 exactly when the exponent
+    // is all ones, and never carries into the other half of the word.
+    constexpr uint32_t kE = 0x7c007c00u, kOne = 0x04000400u;
+    const uint32_t e = (((r.x & kE) + kOne) | ((r.y & kE) + kOne) | ((r.z & kE) + kOne) |
+                        ((r.w & kE) + kOne)) & 0x80008000u;
     if (e) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) {

@@ -286,8 +286,27 @@ __global__ void __launch_bounds__(kEwThreads, (kChain ? 6 : 10) / kFwdStages)
     phase_bits ^= 1u << s;
     const ChunkRef r = refs[s];
     const EwDesc& d = bt.d[r.di];
-    const bool streaming = (d.flags & kEwStreaming) != 0;
-    const bool half_out = (d.flags & kEwHalfGrid) != 0;
+    // f16: loop-invariant descriptor fields pinned in registers (the
+    // descriptor sits in the dynamically indexed parameter bank and the
+    // element-rate-bound f16 loop would re-read it at every use); f32 leaves
+    // the choice to the compiler (pinning cost the 4-stage ring 8 %)
+    constexpr bool kPin = sizeof(T) == 2;
+    FastDivHost pin_inner{};
+    uint32_t pin_flags = 0, pin_nout = 0, pin_nch = 0;
+    if constexpr (kPin) {
+      pin_flags = pin_u(d.flags);
+      pin_nout = pin_u((uint32_t)d.n_out);
+      pin_inner.d = pin_u(d.inner_u.d);
+      pin_inner.m = pin_u(d.inner_u.m);
+      pin_inner.s = pin_u(d.inner_u.s);
+      pin_nch = pin_u(d.chans.d);
+    }
+#define QFB_FLAGS (kPin ? pin_flags : d.flags)
+#define QFB_NOUT (kPin ? (int)pin_nout : d.n_out)
+#define QFB_NCH (kPin ? pin_nch : d.chans.d)
+#define QFB_INNER (kPin ? pin_inner : d.inner_u)
+    const bool streaming = (QFB_FLAGS & kEwStreaming) != 0;
+    const bool half_out = (QFB_FLAGS & kEwHalfGrid) != 0;
     const float qv = pin_f(d.q);
     const uint4* src = ring + s * kArrays * kEwChunk;
     // Per-thread scale cache: units of a chunk mostly share a channel, so
@@ -298,13 +317,13 @@ __global__ void __launch_bounds__(kEwThreads, (kChain ? 6 : 10) / kFwdStages)
     bool fast[2] = {true, true};
     for (uint32_t k = tid; k < r.units; k += kEwThreads) {
       const uint32_t u = r.u0 + k;
-      const uint32_t row = d.chans.d == 1 ? 0u : fdiv(u, d.inner_u);
+      const uint32_t row = QFB_NCH == 1 ? 0u : fdiv(u, QFB_INNER);
       if (row != last_row) {
         last_row = row;
-        const uint32_t ch = d.chans.d == 1 ? 0u : row - fdiv(row, d.chans) * d.chans.d;
+        const uint32_t ch = QFB_NCH == 1 ? 0u : row - fdiv(row, d.chans) * QFB_NCH;
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-          if (j < d.n_out) {
+          if (j < QFB_NOUT) {
             sc[j] = __ldg(d.s[j] + ch);
             fast[j] = fast_div_ok(sc[j]);
             rc[j] = fast[j] ? __frcp_rn(sc[j]) : 1.0f;
@@ -324,7 +343,7 @@ __global__ void __launch_bounds__(kEwThreads, (kChain ? 6 : 10) / kFwdStages)
 #pragma unroll
           for (int i = 0; i < V; ++i) v[i] = apply_act(v[i], d.act);
         }
-        if (d.flags & kEwDemoteIn) {
+        if (QFB_FLAGS & kEwDemoteIn) {
 #pragma unroll
           for (int i = 0; i < V; ++i) v[i] = half_grid(v[i], v[i], nf);  // tensor.hpp:159-170
         }
@@ -336,10 +355,10 @@ __global__ void __launch_bounds__(kEwThreads, (kChain ? 6 : 10) / kFwdStages)
         // or b) still selects the guarded FQ and the checked pack; f32 units
         // are always treated as special (no screening)
       }
-      if (!kChain && (d.flags & kEwInt8Out)) {
+      if (!kChain && (QFB_FLAGS & kEwInt8Out)) {
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-          if (j >= d.n_out) break;
+          if (j >= QFB_NOUT) break;
           uint32_t c[V];
           code_unit<V>(v, sc[j], rc[j], fast[j], qv, c);
           store_codes<V>(d.y[j], u, c);
@@ -348,7 +367,7 @@ __global__ void __launch_bounds__(kEwThreads, (kChain ? 6 : 10) / kFwdStages)
       }
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
-        if (j >= d.n_out) break;
+        if (j >= QFB_NOUT) break;
         float o[V];
         if (sizeof(T) == 2 && !special && fast[j] && sc[j] >= 0x1p-80f) {
           // binary16 unit without inf/NaN: |x / s| < 2^96, no guards needed
@@ -368,6 +387,10 @@ __global__ void __launch_bounds__(kEwThreads, (kChain ? 6 : 10) / kFwdStages)
         st_v4(static_cast<uint4*>(d.y[j]) + u, packed, streaming);
       }
     }
+#undef QFB_FLAGS
+#undef QFB_NOUT
+#undef QFB_NCH
+#undef QFB_INNER
     __syncthreads();  // stage s free for the producer
   }
   if (nf) atomicOr(status, kStatusNonFinite);

@@ -338,3 +338,23 @@ def test_chain_f16_extremes(qfb, orc, cuda, act):
     y = qfb.fake_quantize(to_dev(a, cuda, torch.float16), s.tolist())
     _, want = orc.fake_quantize(a, s, 1, C, H * W, half=1)
     assert np.array_equal(bits32(host(y).ravel()), bits32(want))
+
+
+def test_half_fast_path_all_values(qfb, orc, cuda):
+    """Every finite binary16 value through the f16 TMA forward (screened
+    fast path: negated-residual quotient without copysign) on 64 per-channel
+    scales — from 1e-6 over the 2^-80 fast-path threshold (and one ulp
+    below it) to 64 and 65504/127 — bitwise against the oracle."""
+    import torch
+    bits = np.concatenate([np.arange(0x0000, 0x7c00), np.arange(0x8000, 0xfc00)]).astype(np.uint16)
+    xs = bits.view(np.float16).astype(np.float32)
+    C = 64
+    rng = np.random.default_rng(17)
+    sp = [1e-6, 2.0 ** -80, np.nextafter(np.float32(2.0 ** -80), np.float32(0)), 1e-4, 0.0315, 0.5, 1.0, 2.0,
+          64.0, 65504.0 / 127, 3e-3, 0.1]
+    s = np.array(sp + list(np.exp(rng.uniform(np.log(1e-6), np.log(64.0), C - len(sp)))), dtype=np.float32)
+    x = np.tile(xs, (C, 1))
+    y = qfb.fake_quantize(torch.from_numpy(x).to(cuda).half(), s.astype(np.float64).tolist())
+    _, want = orc.fake_quantize(x.ravel(), s.astype(np.float64), 1, C, xs.size, half=1)
+    got = host(y).ravel()
+    assert np.array_equal(bits32(got), bits32(want))
