@@ -45,7 +45,7 @@ def parse():
     p.add_argument("--impl", default="qfb", choices=["qfb", "reference"])
     p.add_argument("--dtype", default="f32", choices=["f32", "f16"])
     p.add_argument("--sets", type=int, default=2, help="rotating input sets (L2 defeat)")
-    p.add_argument("--e2e-steps", type=int, default=20)
+    p.add_argument("--e2e-steps", type=int, default=60)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-graph", action="store_true")
