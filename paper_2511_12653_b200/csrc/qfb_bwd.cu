@@ -48,11 +48,7 @@ constexpr int kMaxStages = 8;
 // no refills or stores). Not used in production; results in DESIGN.md §7.
 constexpr int kProbeNoCompute = 8;
 constexpr int kProbeNoLoads = 16;
-#ifdef QFB_BWD_CHECKED
-constexpr bool kBwdChecked = true;   // A/B build: per-element inf/NaN tests everywhere
-#else
-constexpr bool kBwdChecked = false;
-#endif
+
 constexpr int kWinPad = 32;                // window slack: 16-byte rounding at both ends
 constexpr size_t kRingBudget = 72 * 1024;  // default per-CTA ring + sums: 3 CTAs per SM
 constexpr size_t kRedBytes = kBwdThreads * sizeof(double);  // group sums of one stage
@@ -296,54 +292,6 @@ __device__ __forceinline__ double group_sum(T* sx, const T* su, int glen, const 
   return __dadd_rn(acc_l, acc_r);
 }
 
-// Leaf groups of 2*LR-1 or 2*LR elements (right half LR, left half h = LR-1
-// or LR), fully unrolled: chunks of two fold steps (4 element slots, the
-// left slot of step LR-1 predicated on h == LR) computed branch-free with
-// one rare-path test per chunk. Every lane of a tile has the same LR for
-// the DPVO shapes (group sizes 9/10), so warps do not diverge.
-template <typename T, bool kDx, int LR>
-__device__ __forceinline__ double group_sum_lr(T* sx, const T* su, int h, const DivCtx& dc,
-                                               double q) {
-  T* rx = sx + h;
-  const T* ru = su + h;
-  const bool lv = h == LR;
-  double acc_l = 0.0, acc_r = 0.0;
-#pragma unroll
-  for (int k = 0; k < LR; k += 2) {
-    const bool two = k + 1 < LR;                 // compile time after unrolling
-    const bool l1 = two && (k + 1 < LR - 1 || lv);  // left slot k+1 valid
-    const bool l0 = k < LR - 1 || lv;               // left slot k valid
-    const float x0 = to_f<T>(sx[k]), u0 = to_f<T>(su[k]);
-    const float x2 = to_f<T>(rx[k]), u2 = to_f<T>(ru[k]);
-    const float x1 = two ? to_f<T>(sx[k + 1]) : 0.0f, u1 = two ? to_f<T>(su[k + 1]) : 0.0f;
-    const float x3 = two ? to_f<T>(rx[k + 1]) : 0.0f, u3 = two ? to_f<T>(ru[k + 1]) : 0.0f;
-    FastTerm f0 = fast_elem(x0, u0, dc, q);
-    FastTerm f1 = fast_elem(x1, u1, dc, q);
-    FastTerm f2 = fast_elem(x2, u2, dc, q);
-    FastTerm f3 = fast_elem(x3, u3, dc, q);
-    f0.ok = f0.ok || !l0;
-    f1.ok = f1.ok || !l1;
-    f3.ok = f3.ok || !two;
-    if (__builtin_expect(!(f0.ok && f1.ok && f2.ok && f3.ok), 0)) {
-      fix_slow(f0, x0, u0, dc.s, q);
-      fix_slow(f1, x1, u1, dc.s, q);
-      fix_slow(f2, x2, u2, dc.s, q);
-      fix_slow(f3, x3, u3, dc.s, q);
-    }
-    if (kDx) {
-      if (l0) sx[k] = from_f<T>(f0.dx);
-      if (l1) sx[k + 1] = from_f<T>(f1.dx);
-      rx[k] = from_f<T>(f2.dx);
-      if (two) rx[k + 1] = from_f<T>(f3.dx);
-    }
-    if (l0) acc_l = __dadd_rn(acc_l, f0.term);
-    if (l1) acc_l = __dadd_rn(acc_l, f1.term);
-    acc_r = __dadd_rn(acc_r, f2.term);
-    if (two) acc_r = __dadd_rn(acc_r, f3.term);
-  }
-  return __dadd_rn(acc_l, acc_r);
-}
-
 // Unchecked fast path for tiles with a usable scale (s in [2^-100, 2^100]):
 // no per-element inf/NaN test. It is exact for every operand:
 //  - non-finite x: markstein2_div gives NaN, so mask = false as for the IEEE
@@ -412,7 +360,7 @@ __device__ __forceinline__ double group_sum_lr_u(T* sx, const T* su, int h, cons
 template <typename T, bool kDx>
 __device__ __forceinline__ double group_sum_any(T* sx, const T* su, int glen, const DivCtx& dc,
                                                 double q) {
-  if (glen >= 9 && dc.usable && !(kBwdChecked)) {
+  if (glen >= 9 && dc.usable) {
     const int lr = (glen + 1) >> 1, h = glen >> 1;
     switch (lr) {
       case 5: return group_sum_lr_u<T, kDx, 5>(sx, su, h, dc, q);
@@ -421,16 +369,7 @@ __device__ __forceinline__ double group_sum_any(T* sx, const T* su, int glen, co
       default: return group_sum_lr_u<T, kDx, 8>(sx, su, h, dc, q);
     }
   }
-  if (glen >= 9) {
-    const int lr = (glen + 1) >> 1, h = glen >> 1;
-    switch (lr) {
-      case 5: return group_sum_lr<T, kDx, 5>(sx, su, h, dc, q);
-      case 6: return group_sum_lr<T, kDx, 6>(sx, su, h, dc, q);
-      case 7: return group_sum_lr<T, kDx, 7>(sx, su, h, dc, q);
-      default: return group_sum_lr<T, kDx, 8>(sx, su, h, dc, q);
-    }
-  }
-  return group_sum<T, kDx>(sx, su, glen, dc, q);
+  return group_sum<T, kDx>(sx, su, glen, dc, q);  // short groups / unusable scales: checked
 }
 
 // ---------------------------------------------------------------------

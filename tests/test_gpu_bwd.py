@@ -332,3 +332,25 @@ def test_unaligned_buffers(qfb, orc, cuda, half, which):
     lo = 1 if which == "dx" else 0
     assert np.all(g[:lo] == 7.0) and np.all(g[lo + n:] == 7.0)
     check_grads(dls.cpu().numpy(), want, TOL_F16 if half else TOL_F32)
+
+
+def test_scales_outside_fast_range(qfb, orc, cuda):
+    """Scales below 2^-100 or above 2^100 (reachable with a permissive
+    QuantConfig: eps 0, s_min 1e-300, s_max 1e300) take the checked path
+    with the exact IEEE quotient; per channel, every row long enough for
+    9/10-element leaf groups. d_input and d_log_s bitwise."""
+    import oracle as O
+    rng = np.random.default_rng(41)
+    C, HW = 4, 5000
+    cfg = qfb.QuantConfig(eps=0.0, s_min=1e-300, s_max=1e300)
+    ocfg = O.OrcCfg(8, 0, 1e-300, 1e-4, 1e300, 0.0)
+    ls = np.array([-300.0, -240.0, 1e31, 1.5])   # s ~ 5e-131, 6e-105, 1e31, 1.7
+    x = rng.normal(0, 1, (C, HW)).astype(np.float32)
+    x[0, ::7] = 0.0
+    x[1, ::5] = np.float32(1e-40)                # subnormal
+    x[3] *= 2.0
+    up = rng.normal(0, 1, (C, HW)).astype(np.float32)
+    g = qfb.fake_quantize_backward(to_dev(x, cuda), ls.tolist(), cfg, to_dev(up, cuda))
+    _, dx, dls = orc.fq_backward(x, up, ls, 1, C, HW, cfg=ocfg)
+    assert np.array_equal(bits32(host(g.d_input).ravel()), bits32(dx))
+    assert np.asarray(g.d_log_scale).tobytes() == dls.tobytes()
