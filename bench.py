@@ -225,8 +225,25 @@ def cpu_reference_frames_per_s(consumers, budget_s, threads, dtype="f32", do_bwd
         return None
     w = RefCpuWorkload(consumers, threads, dtype, do_bwd=do_bwd).size(budget_s)
     secs, frames = w.run()
-    return {"value": frames / secs, "unit": UNIT, "cores": threads, "kind": "reference",
-            "sample": w.describe(secs, frames)}
+    out = {"value": frames / secs, "unit": UNIT, "cores": threads, "kind": "reference",
+           "sample": w.describe(secs, frames), "host": host_cpu_info()}
+    if threads > 1:
+        # the reference at threads = 0 (sequential) as well
+        w1 = RefCpuWorkload(consumers, 1, dtype, do_bwd=do_bwd).size(min(5.0, budget_s / 3))
+        s1, f1 = w1.run()
+        out["single_thread"] = {"value": f1 / s1, "unit": UNIT, "cores": 1, "sample": w1.describe(s1, f1)}
+    return out
+
+
+def host_cpu_info():
+    """hardware_concurrency, the affinity mask and the cgroup CPU quota."""
+    info = {"hardware_concurrency": os.cpu_count(), "affinity": host_threads()}
+    try:
+        q = open("/sys/fs/cgroup/cpu.max").read().split()
+        info["cgroup_cpu_max"] = None if q[0] == "max" else int(q[0]) / int(q[1])
+    except Exception:
+        info["cgroup_cpu_max"] = None
+    return info
 
 
 def host_threads():
