@@ -336,16 +336,35 @@ __global__ void __launch_bounds__(kEwThreads, (kChain ? 6 : 10) / kFwdStages)
         if (d.b != nullptr) {
           float w[V];
           special |= Elem<T>::unpack_flag(src[kEwChunk + k], w);
+          if (sizeof(T) == 2 && !special) {
+            // finite binary16 operands: the plain sum (no NaN to propagate)
 #pragma unroll
-          for (int i = 0; i < V; ++i) v[i] = x86_add(v[i], w[i]);  // tensor.hpp:126-134
+            for (int i = 0; i < V; ++i) v[i] = __fadd_rn(v[i], w[i]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < V; ++i) v[i] = x86_add(v[i], w[i]);  // tensor.hpp:126-134
+          }
         }
         if (d.act != 0) {
 #pragma unroll
           for (int i = 0; i < V; ++i) v[i] = apply_act(v[i], d.act);
         }
         if (QFB_FLAGS & kEwDemoteIn) {
+          if (sizeof(T) == 2 && !special) {
+            // finite values (|a + b| <= 131008; ReLU and the portable GELU
+            // keep them finite): round_to_half is the clamped RNE conversion
+            // (half.hpp:17-39), two elements per conversion
 #pragma unroll
-          for (int i = 0; i < V; ++i) v[i] = half_grid(v[i], v[i], nf);  // tensor.hpp:159-170
+            for (int i = 0; i < V; i += 2) {
+              const float2 f = __half22float2(__floats2half2_rn(fminf(fmaxf(v[i], -65504.0f), 65504.0f),
+                                                                fminf(fmaxf(v[i + 1], -65504.0f), 65504.0f)));
+              v[i] = f.x;
+              v[i + 1] = f.y;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < V; ++i) v[i] = half_grid(v[i], v[i], nf);  // tensor.hpp:159-170
+          }
         }
         if (d.preact != nullptr) {
           st_v4(static_cast<uint4*>(d.preact) + u, Elem<T>::pack(v, v, false, nf), streaming);

@@ -50,29 +50,31 @@ def test_frontend_pass_matches_oracle(qfb, orc, cuda, dtype, int8_out):
                 ci += 1
 
 
-@pytest.mark.parametrize("full", [False, True])
+@pytest.mark.parametrize("dtype,full", [("f32", False), ("f32", True), ("f16", False), ("f16", True)])
 @pytest.mark.parametrize("gelu", [False, True])
-def test_window_chain_pass_matches_oracle(qfb, orc, cuda, gelu, full):
+def test_window_chain_pass_matches_oracle(qfb, orc, cuda, gelu, dtype, full):
     """full=True is BASELINE config 3 as benched (15-frame window, 96 patches,
-    480x640)."""
+    480x640); f16 stores a, b and the outputs in binary16 (the oracle gets
+    the same half-grid values as float, half=1)."""
     import torch
     from paper_2511_12653_b200.frontend import WindowChainPass
     ctx = qfb.default_context(0)
     if full:
-        wp = WindowChainPass(ctx, gelu=gelu, dtype="f32", device=cuda)
+        wp = WindowChainPass(ctx, gelu=gelu, dtype=dtype, device=cuda)
     else:
-        wp = WindowChainPass(ctx, frames=2, patches=4, gelu=gelu, dtype="f32", device=cuda, h=48, w=64)
+        wp = WindowChainPass(ctx, frames=2, patches=4, gelu=gelu, dtype=dtype, device=cuda, h=48, w=64)
     wp.run()
     torch.cuda.synchronize()
     ctx.sync()
+    half = 1 if dtype == "f16" else 0
     for p, (a, b, ys, ss) in zip(wp.points, wp.buffers):
-        ah = a.cpu().numpy()
-        bh = b.cpu().numpy() if b is not None else None
+        ah = a.float().cpu().numpy()
+        bh = b.float().cpu().numpy() if b is not None else None
         scales = [np.asarray(s, dtype=np.float64) for s in ss]
-        st, want, _ = orc.fq_chain(ah, bh, scales, p.outer, p.channels, p.inner, act=p.act)
+        st, want, _ = orc.fq_chain(ah, bh, scales, p.outer, p.channels, p.inner, act=p.act, half=half)
         assert st == 0
         for y, w in zip(ys, want):
-            assert np.array_equal(b32(y.cpu().numpy()), b32(w)), p.name
+            assert np.array_equal(b32(y.float().cpu().numpy()), b32(w)), p.name
 
 
 @pytest.mark.parametrize("dtype", ["f32", "f16"])
