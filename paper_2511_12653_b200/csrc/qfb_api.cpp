@@ -281,6 +281,12 @@ qfb_status plan_ew(int dtype, const EwJob& j, std::vector<EwDesc>& out) {
 int tma_stages(const qfb_ctx* ctx, int dtype, bool chain, bool int8_out, uint64_t chunks) {
   if (ctx->tma_stages_env) return ctx->tma_stages_env;
   if (chain || dtype != 0 || int8_out) return 2;
+  // short launches (about one chunk per CTA, e.g. one 128x120x160 map): the
+  // 2-stage ring's extra CTAs beat depth (6.5 -> 6.0 us per call; with PDL
+  // on these launches the early-scheduled dependents take those CTA slots
+  // and it is 6.6, so kPdlFwdSmall stays off by default)
+  const uint64_t ctas2 = (uint64_t)ctx->sm_count * (uint64_t)std::max(1, ctx->tma_blocks_per_sm[dtype][0][2]);
+  if (chunks < 2 * ctas2) return 2;
   const uint64_t ctas4 = (uint64_t)ctx->sm_count * (uint64_t)std::max(1, ctx->tma_blocks_per_sm[dtype][0][4]);
   return chunks >= 64 * ctas4 ? 4 : 3;
 }
@@ -309,7 +315,8 @@ qfb_status run_ew(qfb_ctx* ctx, int dtype, const std::vector<EwDesc>& descs, boo
     cudaError_t e;
     if (all_vec) {
       const int grid = (int)std::min<uint64_t>(chunks, (uint64_t)ctx->sm_count * tma_per_sm);
-      e = launch_ew_tma(dtype, chain, stages, b, ctx->d_status, grid, ctx->stream);
+      e = launch_ew_tma(dtype, chain, stages, b, ctx->d_status, grid, ctx->stream,
+                        chunks < 4ull * (uint64_t)grid);
     } else {
       const int grid = (int)std::min<uint64_t>(
           chunks, (uint64_t)ctx->sm_count * ctx->ew_blocks_per_sm[dtype][chain ? 1 : 0]);

@@ -571,10 +571,10 @@ cudaError_t ew_tma_occupancy(int dtype, bool chain, int stages, int* blocks_per_
 }
 
 cudaError_t launch_ew_tma(int dtype, bool chain, int stages, const EwBatch& b, uint32_t* status,
-                          int grid, cudaStream_t st) {
+                          int grid, cudaStream_t st, bool small) {
   void* args[] = {const_cast<EwBatch*>(&b), &status};
   return launch_main(tma_fn(dtype, chain, stages), dim3(grid), dim3(kEwThreads), args,
-                     ew_tma_smem(chain, stages), st, kPdlFwd);
+                     ew_tma_smem(chain, stages), st, small ? (kPdlFwd | kPdlFwdSmall) : kPdlFwd);
 }
 
 cudaError_t launch_ew(int dtype, bool chain, const EwBatch& b, uint32_t* status, int grid,

@@ -29,8 +29,9 @@ qfb_status cuda_error(cudaError_t e, const char* where);
 // its launch latency overlaps the tail. Stream order is unchanged: a
 // dependent still observes every write of the grid before it.
 // Which launches carry the attribute: bit 1 forward, 2 backward, 4
-// finisher (QFB_PDL overrides the default mask).
-constexpr int kPdlFwd = 1, kPdlBwd = 2, kPdlFin = 4;
+// finisher, 8 small forward launches (fewer than 4 chunks per CTA);
+// QFB_PDL overrides the default mask (4).
+constexpr int kPdlFwd = 1, kPdlBwd = 2, kPdlFin = 4, kPdlFwdSmall = 8;
 bool pdl_enabled(int which);
 // cudaLaunchKernelExC with the programmatic-serialization attribute when
 // pdl_enabled(which).
@@ -102,7 +103,8 @@ cudaError_t launch_ew(int dtype, bool chain, const EwBatch& b, uint32_t* status,
 constexpr int kTmaStagesMin = 2, kTmaStagesMax = 4;
 cudaError_t ew_tma_occupancy(int dtype, bool chain, int stages, int* blocks_per_sm);
 cudaError_t launch_ew_tma(int dtype, bool chain, int stages, const EwBatch& b, uint32_t* status,
-                          int grid, cudaStream_t st);
+                          int grid, cudaStream_t st,
+                          bool small = false);
 
 // int8 codes (vec path when aligned).
 struct CodesDesc {
