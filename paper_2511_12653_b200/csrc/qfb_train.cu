@@ -100,13 +100,20 @@ __global__ void leaf_sums_kernel(Term f, uint64_t n, uint32_t depth, double* out
 
 // MSE leaf sums with coalesced loads: warp w of a CTA owns 32 consecutive
 // leaf groups (<= 512 contiguous elements), stages their s and t through
-// shared memory with coalesced loads, then each lane folds its group in
-// the reference order. Pair b = blockIdx.y.
+// shared memory with 16-byte loads (scalar when the pointers are not
+// 16-byte aligned), then each lane folds its group in the reference order.
+// With kSub, the CTA's 256 groups — an aligned perfect subtree — are
+// reduced to one value (warp xor butterfly, then the 8 warp sums as a
+// perfect tree) so only 2^(depth-8) values per pair go to the halving
+// passes. Pair b = blockIdx.y.
 constexpr int kMseWarps = 8;
+constexpr int kMseSubLog = 8;  // log2(32 * kMseWarps)
+template <bool kSub>
 __global__ void __launch_bounds__(kMseWarps * 32) mse_leaf_kernel(const float* __restrict__ s,
                                                                  const float* __restrict__ t, uint64_t n,
                                                                  uint32_t depth, double* out) {
-  __shared__ float ss[kMseWarps][2][32 * kLeaf];
+  __shared__ __align__(16) float ss[kMseWarps][2][32 * kLeaf + 8];
+  __shared__ double wsum[kMseWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t b = blockIdx.y;
   const uint32_t groups = 1u << depth;
@@ -117,31 +124,58 @@ __global__ void __launch_bounds__(kMseWarps * 32) mse_leaf_kernel(const float* _
   const uint64_t w0 = __shfl_sync(0xffffffffu, lo, 0);
   const uint32_t last = min(31u, groups > (g - lane) ? groups - (g - lane) - 1u : 0u);
   const uint64_t w1 = __shfl_sync(0xffffffffu, lo + m, (int)last);
-  if (g - (uint32_t)lane >= groups) return;  // warp past the end
-  const float* sp = s + (uint64_t)b * n + w0;
-  const float* tp = t + (uint64_t)b * n + w0;
-  const int cnt = (int)(w1 - w0);
-  for (int i = lane; i < cnt; i += 32) {
-    ss[warp][0][i] = __ldg(sp + i);
-    ss[warp][1][i] = __ldg(tp + i);
+  if (g - (uint32_t)lane >= groups) return;  // warp past the end (never with kSub)
+  const uint64_t e0 = (uint64_t)b * n + w0, e1 = (uint64_t)b * n + w1;
+  uint64_t a0 = e0;  // smem index 0 holds element a0
+  if ((((uintptr_t)s | (uintptr_t)t) & 15u) == 0) {
+    a0 = e0 & ~uint64_t(3);
+    const uint64_t v1 = e1 & ~uint64_t(3);  // [a0, v1) by float4, [v1, e1) scalar
+    const int nv = (int)((v1 - a0) >> 2);
+    for (int i = lane; i < nv; i += 32) {
+      reinterpret_cast<float4*>(ss[warp][0])[i] = __ldg(reinterpret_cast<const float4*>(s + a0) + i);
+      reinterpret_cast<float4*>(ss[warp][1])[i] = __ldg(reinterpret_cast<const float4*>(t + a0) + i);
+    }
+    const int tail = (int)(e1 - v1);
+    if (lane < tail) {
+      ss[warp][0][(v1 - a0) + lane] = __ldg(s + v1 + lane);
+      ss[warp][1][(v1 - a0) + lane] = __ldg(t + v1 + lane);
+    }
+  } else {
+    const int cnt = (int)(e1 - e0);
+    for (int i = lane; i < cnt; i += 32) {
+      ss[warp][0][i] = __ldg(s + e0 + i);
+      ss[warp][1][i] = __ldg(t + e0 + i);
+    }
   }
   __syncwarp();
-  if (g >= groups) return;
-  const float* a = ss[warp][0] + (lo - w0);
-  const float* c = ss[warp][1] + (lo - w0);
-  auto fold = [&](int k0, int k1) {
-    double acc = 0.0;
-    for (int k = k0; k < k1; ++k) acc = __dadd_rn(acc, mse_term(a[k], c[k]));
-    return acc;
-  };
-  double r;
-  if (m <= 8) {
-    r = fold(0, (int)m);
-  } else {
-    const int h = (int)(m >> 1);
-    r = __dadd_rn(fold(0, h), fold(h, (int)m));
+  double r = 0.0;
+  if (g < groups) {
+    const float* a = ss[warp][0] + ((uint64_t)b * n + lo - a0);
+    const float* c = ss[warp][1] + ((uint64_t)b * n + lo - a0);
+    auto fold = [&](int k0, int k1) {
+      double acc = 0.0;
+      for (int k = k0; k < k1; ++k) acc = __dadd_rn(acc, mse_term(a[k], c[k]));
+      return acc;
+    };
+    if (m <= 8) {
+      r = fold(0, (int)m);
+    } else {
+      const int h = (int)(m >> 1);
+      r = __dadd_rn(fold(0, h), fold(h, (int)m));
+    }
   }
-  out[((uint64_t)b << depth) + g] = r;
+  if constexpr (!kSub) {
+    if (g < groups) out[((uint64_t)b << depth) + g] = r;
+  } else {
+    for (int o = 1; o < 32; o <<= 1) r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, o));
+    if (lane == 0) wsum[warp] = r;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const double v = __dadd_rn(__dadd_rn(__dadd_rn(wsum[0], wsum[1]), __dadd_rn(wsum[2], wsum[3])),
+                                 __dadd_rn(__dadd_rn(wsum[4], wsum[5]), __dadd_rn(wsum[6], wsum[7])));
+      out[((uint64_t)b << (depth - kMseSubLog)) + blockIdx.x] = v;
+    }
+  }
 }
 
 // Perfect-tree halving: per pair y = blockIdx.y (cnt values each), CTA x
@@ -349,12 +383,17 @@ qfb_status qfb_distill_batch(qfb_ctx* ctx, const float* student, const float* te
   // the chunk scaling), then the mean cosine over locations
   const uint32_t depth_n = tree_depth(n);
   const uint32_t per_cta = 32u * kMseWarps;
-  mse_leaf_kernel<<<dim3(((1u << depth_n) + per_cta - 1) / per_cta, nb), per_cta, 0, st>>>(
-      student, teacher, n, depth_n, static_cast<double*>(ws));
+  const dim3 mse_grid(((1u << depth_n) + per_cta - 1) / per_cta, nb);
+  const bool sub = depth_n >= (uint32_t)kMseSubLog;  // CTAs reduce whole subtrees
+  if (sub)
+    mse_leaf_kernel<true><<<mse_grid, per_cta, 0, st>>>(student, teacher, n, depth_n, static_cast<double*>(ws));
+  else
+    mse_leaf_kernel<false><<<mse_grid, per_cta, 0, st>>>(student, teacher, n, depth_n, static_cast<double*>(ws));
   ++launches;
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess)
-    e = halve_all(depth_n, nb, (double)n, out, 2, static_cast<double*>(ws), st, &launches);
+    e = halve_all(sub ? depth_n - kMseSubLog : depth_n, nb, (double)n, out, 2, static_cast<double*>(ws), st,
+                  &launches);
   if (e == cudaSuccess) {
     const double w = lambda_cos / (double)hw;
     cosine_kernel<<<dim3((unsigned)(((uint64_t)hw + 255) / 256), nb), 256, 0, st>>>(
