@@ -49,6 +49,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-graph", action="store_true")
+    p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                   help="gloo: exercise the N>1 path with ranks sharing one GPU (tests only)")
     p.add_argument("--graph-steps", type=int, default=8,
                    help="consecutive steps captured in one CUDA graph (N=1)")
     p.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -304,12 +306,18 @@ def run_qfb(args):
 
     ws, rank, local = dist_env()
     local = local % max(1, torch.cuda.device_count())
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # --dist-backend gloo (test only): ranks may share a GPU, so the device is
+    # local % device_count; with NCCL (the default) every rank owns a GPU
+    gpu = local % max(1, torch.cuda.device_count()) if args.dist_backend == "gloo" else local
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     pg = None
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
         pg = dist
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
@@ -399,7 +407,7 @@ def run_qfb(args):
         pg.barrier()
     torch.cuda.synchronize(dev)
 
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(gpu)
     sampler.start()
     time.sleep(0.15)  # let the sampler attach before the timed region
     t_start = torch.cuda.Event(enable_timing=True)
