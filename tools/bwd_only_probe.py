@@ -1,0 +1,34 @@
+"""The backward alone, launched back to back (no forward between): the
+steady-state time of the backward kernel (+ finisher) on one frame of
+BASELINE config 2, for comparison with tools/bwd_traffic_probe.py (the same
+traffic through the forward chain kernel). QFB_BWD_VARIANT selects the
+probes (8: memory pipeline only, 16: arithmetic only)."""
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2511_12653_b200 as q  # noqa: E402
+from paper_2511_12653_b200.frontend import FrontendQuantPass  # noqa: E402
+
+dt = sys.argv[1] if len(sys.argv) > 1 else "f32"
+dev = torch.device("cuda:0")
+stream = torch.cuda.Stream(device=dev)
+torch.cuda.set_stream(stream)
+ctx = q.Context(0, stream.cuda_stream)
+fp = FrontendQuantPass(ctx, frames=1, dtype=dt, sets=2, seed=3, device=dev)
+for i in range(5):
+    fp.backward(i % 2)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record(stream)
+for i in range(200):
+    fp.backward(i % 2)
+e1.record(stream)
+torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / 200
+b = fp.bytes_per_step()["bwd"]
+print(json.dumps({"dtype": dt, "variant": os.environ.get("QFB_BWD_VARIANT", "0"), "us": ms * 1e3,
+                  "gbps": b / (ms / 1e3) / 1e9, "frac": b / (ms / 1e3) / 1e9 / 6551.0}))
