@@ -499,12 +499,17 @@ qfb_status qfb_ctx_create(int32_t device, void* stream, qfb_ctx** out) {
 qfb_status qfb_ctx_destroy(qfb_ctx* ctx) {
   if (!ctx) return QFB_OK;
   DeviceGuard g(ctx->device);
+  // the host pass's copy streams may still move a slot's buffers
   cudaStreamSynchronize(ctx->stream);
+  if (ctx->s_in) cudaStreamSynchronize(ctx->s_in);
+  if (ctx->s_out) cudaStreamSynchronize(ctx->s_out);
   if (ctx->d_status) cudaFree(ctx->d_status);
   if (ctx->h_status) cudaFreeHost(ctx->h_status);
   if (ctx->ws_f64.p) cudaFree(ctx->ws_f64.p);
   if (ctx->ws_u32.p) cudaFree(ctx->ws_u32.p);
   for (auto& b : ctx->host_io)
+    if (b.p) cudaFree(b.p);
+  for (auto& b : ctx->train_ws)
     if (b.p) cudaFree(b.p);
   for (auto& sl : ctx->slots) {
     for (auto& b : sl.bufs)

@@ -88,3 +88,30 @@ def test_fold_rows_device_is_frame_order(qfb, cuda):
     torch.cuda.synchronize()
     assert got.cpu().numpy().tobytes() == want.tobytes()
     assert got2.cpu().numpy().tobytes() == want2.tobytes()
+
+
+def test_context_teardown_frees_device_memory(qfb, cuda):
+    """Contexts that ran the trainer ops (their scratch) and the backward are
+    destroyed without leaking device memory (qfb_ctx_destroy frees every
+    workspace after synchronizing its streams)."""
+    import torch
+    s = torch.randn((128, 120, 160), device=cuda)
+    t = torch.randn_like(s)
+    x = torch.randn((64, 120, 160), device=cuda)
+    up = torch.randn_like(x)
+
+    def cycle():
+        ctx = qfb.Context(0)
+        qfb.distill_pair(s, t, 1.0, ctx=ctx)
+        qfb.fake_quantize_backward(x, [-3.0] * 64, None, up, ctx=ctx)
+        ctx.sync()
+        ctx.close()
+
+    cycle()
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    for _ in range(10):
+        cycle()
+    torch.cuda.synchronize()
+    free1 = torch.cuda.mem_get_info()[0]
+    assert free0 - free1 < 8 << 20, (free0, free1)
