@@ -558,7 +558,8 @@ def run_secondary(args, ctx, stream, dev, peak, rank, ws):
           "hbm_frac": gb / peak, "frames_per_launch": fp.frames,
           "seconds_for_32x1000_frames": 32000.0 / (ws * fps),
           "workload": "BASELINE config 5: fused multi-point fake-quant forward of the 22 DPVO "
-                      "activation quant points (inference front-end), 8 frames per launch"}
+                      "activation quant points (inference front-end), 8 frames per launch; weights "
+                      "are fake-quantized once (cache_weights, exec.hpp:59-60), not per frame"}
     if rank == 0 and ws == 1 and not args.no_cpu:
         cons = [(p, c) for p in fp.points for c in p.consumers]
         try:

@@ -59,16 +59,22 @@ def test_host_fwd_codes_bwd(qfb, orc, ref, cuda):
     ctx.close()
 
 
-def test_quant_pass_host_matches_reference(qfb, orc, ref, cuda):
+@pytest.mark.parametrize("half", [0, 1])
+def test_quant_pass_host_matches_reference(qfb, orc, ref, cuda, half):
     """Frame-level pipelined host pass == per-point reference calls, bitwise
-    (forward outputs, d_input and scale gradients)."""
+    (forward outputs, d_input and scale gradients); half=1 is the
+    reference's EmulatedHalf activations (inputs on the binary16 grid,
+    outputs re-rounded, the half-mode scale floor in the backward)."""
     import torch
-    rng = np.random.default_rng(11)
+    rng = np.random.default_rng(11 + half)
+
+    def grid(a):
+        return a.astype(np.float16).astype(np.float32) if half else a
     shapes = [(3, 48, 64, 2), (32, 24, 32, 1), (32, 24, 32, 2), (64, 12, 16, 1), (7, 5, 9, 1)]
     keep, pts, checks = [], [], []
     D = ctypes.POINTER(ctypes.c_double)
     for C, H, W, n_out in shapes:
-        x = torch.from_numpy(rng.normal(0, 1, C * H * W).astype(np.float32)).pin_memory()
+        x = torch.from_numpy(grid(rng.normal(0, 1, C * H * W).astype(np.float32))).pin_memory()
         p = qfb.CHostPoint()
         p.x = x.data_ptr()
         p.outer, p.channels, p.inner, p.n_out = 1, C, H * W, n_out
@@ -76,7 +82,7 @@ def test_quant_pass_host_matches_reference(qfb, orc, ref, cuda):
         for k in range(n_out):
             s = np.exp(rng.uniform(np.log(1e-3), np.log(0.1), C))
             ls = np.log(np.expm1(s))
-            up = torch.from_numpy(rng.normal(0, 1, C * H * W).astype(np.float32)).pin_memory()
+            up = torch.from_numpy(grid(rng.normal(0, 1, C * H * W).astype(np.float32))).pin_memory()
             y = torch.empty(C * H * W).pin_memory()
             dx = torch.empty(C * H * W).pin_memory()
             dls = np.zeros(C)
@@ -93,11 +99,11 @@ def test_quant_pass_host_matches_reference(qfb, orc, ref, cuda):
     cfg = qfb.QuantConfig().to_c()
     table = (qfb.CHostPoint * len(pts))(*pts)
     for _ in range(2):
-        qfb.check(qfb.lib().qfb_quant_pass_host(ctx.handle, 0, table, len(pts), ctypes.byref(cfg)))
+        qfb.check(qfb.lib().qfb_quant_pass_host(ctx.handle, half, table, len(pts), ctypes.byref(cfg)))
         for x, s, ls, up, y, dx, dls, C, HW in checks:
-            _, wy = ref.fake_quantize(x, [C, HW], s, per_channel=True)
+            _, wy = ref.fake_quantize(x, [C, HW], s, half=half, per_channel=True)
             assert np.array_equal(bits32(y.numpy()), bits32(wy))
-            _, wdx, wdls = ref.fq_backward(x, up, [C, HW], ls, per_channel=True)
+            _, wdx, wdls = ref.fq_backward(x, up, [C, HW], ls, per_channel=True, half=half)
             assert np.array_equal(bits32(dx.numpy()), bits32(wdx))
             assert dls.tobytes() == wdls.tobytes()
     ctx.close()
