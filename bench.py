@@ -625,11 +625,19 @@ def run_c1(args, ctx, stream, dev, peak, rank, ws):
         for _ in range(128):
             one()
     ms = time_device(g.replay, stream, reps=4, warmup=2) / 128
+    # one call as a one-node graph: its device latency without the host launch path
+    g1 = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g1, stream=stream):
+        one()
+    lat_dev = time_device(g1.replay, stream, reps=1, warmup=3)
     gb = 2 * n * esize / (ms / 1e3) / 1e9
-    res = {"us_single_call": lat * 1e3, "us_per_call_rotating_eager": ms_eager * 1e3,
+    res = {"us_single_call": lat * 1e3, "us_single_call_device": lat_dev * 1e3,
+           "us_per_call_rotating_eager": ms_eager * 1e3,
            "us_per_call_rotating": ms * 1e3, "gbps": gb, "hbm_frac": gb / peak,
            "workload": "BASELINE config 1: per-tensor fake-quant fwd of [1,128,120,160], 128 rotating maps",
-           "timing": "us_single_call: one eager call after warm-up; us_per_call_rotating / gbps: 128 calls "
+           "timing": "us_single_call: one eager call after warm-up (host launch path included); "
+                     "us_single_call_device: the same call replayed as a one-node graph; "
+                     "us_per_call_rotating / gbps: 128 calls "
                      "over distinct maps (2.5 GB) replayed as one CUDA graph; _eager: the same calls "
                      "launched one by one from Python"}
     if rank == 0 and ws == 1 and not args.no_cpu:
@@ -651,7 +659,7 @@ def run_c1(args, ctx, stream, dev, peak, rank, ws):
                                                  f"same map, one host thread"}
         except Exception as exc:  # pragma: no cover
             res["cpu_baseline"] = {"value": None, "sample": f"failed: {exc}"}
-    del xs, ys, g
+    del xs, ys, g, g1
     torch.cuda.empty_cache()
     return res
 
