@@ -97,12 +97,24 @@ __device__ __forceinline__ float fq_value_fast(float x, float s, float y, float 
 // form for every x != 0, and for x = +-0 it yields +-0 with x's sign
 // (-0: r' = -0 + +0 = +0, z = -0 + -0 = -0), so no copysign is needed.
 // tests/test_gpu_fwd.py::test_half_fast_path_all_values checks every
-// finite binary16 x over 64 scales.
+// finite binary16 x over 64 scales; tools/verify_div.cu test 2b every f32
+// x with |x| < s * 2^100 (the f32 screen) over 192 scales.
 __device__ __forceinline__ float fq_value_fast_finite(float x, float s, float y, float q) {
   const float q0 = __fmul_rn(x, y);
   float z = __fmaf_rn(-__fmaf_rn(s, q0, -x), y, q0);
   z = fminf(fmaxf(z, -q), q);
   return __fmul_rn(s, rintf(z));
+}
+
+// int8 code bits (low byte) of a screened finite x (|x| < s * 2^100, no
+// NaN): negated-residual quotient, clip, and round-to-nearest-even into the
+// low byte by adding 1.5 * 2^23 (|z| <= q). Equals fq_code
+// (tools/verify_div.cu test 2b, all 2^32 x).
+__device__ __forceinline__ uint32_t fq_code_bits_fast_finite(float x, float s, float y, float q) {
+  const float q0 = __fmul_rn(x, y);
+  float z = __fmaf_rn(-__fmaf_rn(s, q0, -x), y, q0);
+  z = fminf(fmaxf(z, -q), q);
+  return __float_as_uint(__fadd_rn(z, 12582912.0f));
 }
 
 // Pin a uniform in a register (stops rematerialization from the

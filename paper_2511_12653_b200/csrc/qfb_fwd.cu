@@ -51,7 +51,12 @@ __device__ __forceinline__ void fq_unit(const float* v, float s, float q, float*
 // clipped, rounded quotient is identical to rint(clip(IEEE x/s)).
 template <int V>
 __device__ __forceinline__ void code_unit(const float* v, float s, float y, bool fast, float q,
-                                          uint32_t* c) {
+                                          uint32_t* c, bool finite = false) {
+  if (finite) {  // screened unit: no overflow guard, no NaN
+#pragma unroll
+    for (int i = 0; i < V; ++i) c[i] = fq_code_bits_fast_finite(v[i], s, y, q);
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < V; ++i) {
     if (fast) {
@@ -66,6 +71,16 @@ __device__ __forceinline__ void code_unit(const float* v, float s, float y, bool
       c[i] = (uint32_t)(uint8_t)fq_code(v[i], s, q);
     }
   }
+}
+
+// f32 unit screen: every |x| < thr = s * 2^100 (false for NaN and inf, and
+// thr = 0 when the scale is outside the shortcut's range).
+template <int V>
+__device__ __forceinline__ bool screen_f32(const float* v, float thr) {
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i < V; ++i) ok = ok && fabsf(v[i]) < thr;
+  return ok;
 }
 
 // Store V codes (low bytes of c) at unit u of an int8 output (V bytes).
@@ -314,6 +329,7 @@ __global__ void __launch_bounds__(kEwThreads, (kChain ? 6 : 10) / kFwdStages)
     // row changes.
     uint32_t last_row = 0xffffffffu;
     float sc[2] = {1.0f, 1.0f}, rc[2] = {1.0f, 1.0f};
+    float thr[2] = {0.0f, 0.0f};  // f32 screen: |x| < s * 2^100 keeps |x * y| < 2^100
     bool fast[2] = {true, true};
     for (uint32_t k = tid; k < r.units; k += kEwThreads) {
       const uint32_t u = r.u0 + k;
@@ -327,6 +343,7 @@ __global__ void __launch_bounds__(kEwThreads, (kChain ? 6 : 10) / kFwdStages)
             sc[j] = __ldg(d.s[j] + ch);
             fast[j] = fast_div_ok(sc[j]);
             rc[j] = fast[j] ? __frcp_rn(sc[j]) : 1.0f;
+            thr[j] = fast[j] ? __fmul_rn(sc[j], 0x1p100f) : 0.0f;
           }
         }
       }
@@ -379,7 +396,8 @@ __global__ void __launch_bounds__(kEwThreads, (kChain ? 6 : 10) / kFwdStages)
         for (int j = 0; j < 2; ++j) {
           if (j >= QFB_NOUT) break;
           uint32_t c[V];
-          code_unit<V>(v, sc[j], rc[j], fast[j], qv, c);
+          code_unit<V>(v, sc[j], rc[j], fast[j], qv, c,
+                       sizeof(T) == 4 && kFwdStages < 4 && screen_f32<V>(v, thr[j]));
           store_codes<V>(d.y[j], u, c);
         }
         continue;
@@ -388,8 +406,13 @@ __global__ void __launch_bounds__(kEwThreads, (kChain ? 6 : 10) / kFwdStages)
       for (int j = 0; j < 2; ++j) {
         if (j >= QFB_NOUT) break;
         float o[V];
-        if (sizeof(T) == 2 && !special && fast[j] && sc[j] >= 0x1p-80f) {
-          // binary16 unit without inf/NaN: |x / s| < 2^96, no guards needed
+        // (the 4-stage f32 ring, used for long memory-bound launches, keeps
+        // the guarded path: its extra registers cost it 1.5 %)
+        const bool finite = sizeof(T) == 2 ? (!special && fast[j] && sc[j] >= 0x1p-80f)
+                                           : (kFwdStages < 4 && screen_f32<V>(v, thr[j]));
+        if (finite) {
+          // binary16 unit without inf/NaN (|x / s| < 2^96) or an f32 unit
+          // passing the screen: no guards needed
 #pragma unroll
           for (int i = 0; i < V; ++i) o[i] = fq_value_fast_finite(v[i], sc[j], rc[j], qv);
         } else if (fast[j]) {

@@ -15,6 +15,9 @@
 //    log-uniform in [1e-6, 64], specials, all-ones significands), the full
 //    FQ result of the fast path equals the IEEE-division FQ (covers zeros,
 //    subnormals, infinities, NaN, overflow and underflow regions).
+//  Test 2b: within test 2, every x passing the f32 screen |x| < s * 2^100
+//    also through fq_value_fast_finite (negated residual, no guard, no
+//    copysign) and fq_code_bits_fast_finite (int8 code), against IEEE.
 //  Test 3 (evidence only): the double analogue with float numerators.
 //
 // Build/run (GPU box):  nvcc -O3 -gencode arch=compute_100a,code=sm_100a \
@@ -68,6 +71,14 @@ __global__ void fq_all_x_kernel(const float* scales, int ns, uint64_t base) {
     const float a = fq_value(x, s, 127.0f);
     const float b = fq_value_fast(x, s, y, 127.0f);
     if (__float_as_uint(a) != __float_as_uint(b)) ++bad;
+    // test 2b: the screened f32 paths (|x| < s * 2^100): FQ value without
+    // guards / copysign, and the int8 code bits
+    if (fast_div_ok(s) && fabsf(x) < __fmul_rn(s, 0x1p100f)) {
+      const float c = fq_value_fast_finite(x, s, y, 127.0f);
+      if (__float_as_uint(a) != __float_as_uint(c)) ++bad;
+      const uint32_t cb = fq_code_bits_fast_finite(x, s, y, 127.0f) & 0xffu;
+      if (cb != (uint32_t)(uint8_t)fq_code(x, s, 127.0f)) ++bad;
+    }
   }
   if (bad) {
     const unsigned long long i = atomicAdd(&g_bad, bad);
@@ -154,7 +165,7 @@ int main(int argc, char** argv) {
   cudaEventSynchronize(e1);
   cudaEventElapsedTime(&ms_t, e0, e1);
   const unsigned long long bad2 = read_bad();
-  printf("test2 FQ fast vs IEEE: all 2^32 x patterns x %d scales, mismatches = %llu (%.1f s)\n", NS,
+  printf("test2 FQ fast (+2b: screened finite value and int8 code) vs IEEE: all 2^32 x patterns x %d scales, mismatches = %llu (%.1f s)\n", NS,
          bad2, ms_t / 1000);
 
   // ---- Test 3: double analogue (evidence) ----
