@@ -239,9 +239,9 @@ def test_gelu_portable_bitwise(qfb, orc, cuda):
     want = np.array([orc.gelu(float(t)) for t in v], dtype=np.float32)
     outs, pre = qfb.fq_chain(to_dev(v, cuda), None, scales=(), act=2, preact=True)
     assert np.array_equal(bits32(host(pre)), bits32(want))
-    # sanity: close to the erf GELU
+    # the definition is the erf GELU to within 2.1e-6 (degree-12 polynomial Phi)
     ref = 0.5 * v.astype(np.float64) * (1 + np.vectorize(__import__("math").erf)(v / np.sqrt(2)))
-    assert np.max(np.abs(want[:100_000] - ref[:100_000])) < 2e-3
+    assert np.max(np.abs(want[:101_000] - ref[:101_000])) < 5e-6
 
 
 # --------------------------------------------------------- per-op ---
