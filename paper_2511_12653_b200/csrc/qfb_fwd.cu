@@ -397,7 +397,8 @@ __global__ void __launch_bounds__(kEwThreads, (kChain ? 6 : 10) / kFwdStages)
           if (j >= QFB_NOUT) break;
           uint32_t c[V];
           code_unit<V>(v, sc[j], rc[j], fast[j], qv, c,
-                       sizeof(T) == 4 && kFwdStages < 4 && screen_f32<V>(v, thr[j]));
+                       sizeof(T) == 2 ? (!special && fast[j] && sc[j] >= 0x1p-80f)
+                                      : (kFwdStages < 4 && screen_f32<V>(v, thr[j])));
           store_codes<V>(d.y[j], u, c);
         }
         continue;
