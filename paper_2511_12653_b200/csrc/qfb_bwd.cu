@@ -313,6 +313,29 @@ __device__ __forceinline__ double fast_term(float xv, float uv, const DivCtx& dc
   return __dmul_rn(d_ds, (double)uv);
 }
 
+// binary16 operands: converted straight to double (one F2F.F64.F16 each,
+// exact) and d_input written from up's storage bits (mask ? up : +-0 with
+// up's sign, exact for finite up; non-finite up is fixed per group as for
+// f32). Same values as fast_term on the widened floats.
+__device__ __forceinline__ double h2d(__half h) {
+  double d;
+  asm("cvt.f64.f16 %0, %1;" : "=d"(d) : "h"(__half_as_ushort(h)));
+  return d;
+}
+__device__ __forceinline__ double fast_term_h(__half xh, __half uh, const DivCtx& dc, double q,
+                                              __half* dx) {
+  const double xd = h2d(xh);
+  const double z = markstein2_div(xd, dc);
+  const bool mask = fabs(z) <= q;
+  const double sat = xd > 0.0 ? q : -q;
+  const double d_ds = mask ? __dadd_rn(rint(z), -z) : sat;
+  if (dx) {
+    const unsigned short b = __half_as_ushort(uh);
+    *dx = __ushort_as_half(mask ? b : (unsigned short)(b & 0x8000u));
+  }
+  return __dmul_rn(d_ds, h2d(uh));
+}
+
 // d_input of the group's non-finite upstream values (rare): the fast path
 // stored up (mask) or +-0 (masked out); masked_upstream gives the
 // reference's value from that mask.
@@ -337,14 +360,20 @@ __device__ __forceinline__ double group_sum_lr_u(T* sx, const T* su, int h, cons
 #pragma unroll
   for (int k = 0; k < LR; ++k) {
     const bool l0 = k < LR - 1 || lv;  // left slot k valid
-    const float x0 = l0 ? to_f<T>(sx[k]) : 0.0f, u0 = l0 ? to_f<T>(su[k]) : 0.0f;
-    const float x2 = to_f<T>(rx[k]), u2 = to_f<T>(ru[k]);
-    float d0, d2;
-    const double t0 = fast_term(x0, u0, dc, q, d0);
-    const double t2 = fast_term(x2, u2, dc, q, d2);
-    if (kDx) {
-      if (l0) sx[k] = from_f<T>(d0);
-      rx[k] = from_f<T>(d2);
+    double t0, t2;
+    if constexpr (sizeof(T) == 2) {
+      t0 = l0 ? fast_term_h(sx[k], su[k], dc, q, kDx ? sx + k : nullptr) : 0.0;
+      t2 = fast_term_h(rx[k], ru[k], dc, q, kDx ? rx + k : nullptr);
+    } else {
+      const float x0 = l0 ? to_f<T>(sx[k]) : 0.0f, u0 = l0 ? to_f<T>(su[k]) : 0.0f;
+      const float x2 = to_f<T>(rx[k]), u2 = to_f<T>(ru[k]);
+      float d0, d2;
+      t0 = fast_term(x0, u0, dc, q, d0);
+      t2 = fast_term(x2, u2, dc, q, d2);
+      if (kDx) {
+        if (l0) sx[k] = from_f<T>(d0);
+        rx[k] = from_f<T>(d2);
+      }
     }
     if (l0) acc_l = __dadd_rn(acc_l, t0);
     acc_r = __dadd_rn(acc_r, t2);
