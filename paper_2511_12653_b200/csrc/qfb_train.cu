@@ -247,7 +247,7 @@ cudaError_t halve_all(uint32_t depth, uint32_t nb, double div, double* res, uint
 // One thread per (pair, location): the channel loops are sequential in the
 // reference order; the loads of a channel step are independent of the
 // accumulations, so unrolling keeps several in flight.
-__global__ void cosine_kernel(const float* __restrict__ s, const float* __restrict__ t,
+__global__ void __launch_bounds__(256, 4) cosine_kernel(const float* __restrict__ s, const float* __restrict__ t,
                               float* __restrict__ ds, uint64_t c, uint64_t hw, double w,
                               double gscale, double n, double* __restrict__ cos_loc) {
   const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -258,7 +258,7 @@ __global__ void cosine_kernel(const float* __restrict__ s, const float* __restri
   ds += pair * c * hw;
   cos_loc += pair * hw;
   double dot = 0.0, na2 = 0.0, nb2 = 0.0;
-#pragma unroll 8
+#pragma unroll 16
   for (uint64_t ch = 0; ch < c; ++ch) {
     const double a = (double)__ldg(s + ch * hw + p);
     const double b = (double)__ldg(t + ch * hw + p);
@@ -284,7 +284,7 @@ __global__ void cosine_kernel(const float* __restrict__ s, const float* __restri
   da.s = zero ? 1.0 : na2;
   da.y = __drcp_rn(da.s);
   cos_loc[p] = cosv;
-#pragma unroll 4
+#pragma unroll 8
   for (uint64_t ch = 0; ch < c; ++ch) {
     const uint64_t i = ch * hw + p;
     const double a = (double)__ldg(s + i);
