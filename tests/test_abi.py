@@ -171,3 +171,42 @@ def test_nccl_loads_at_run_time():
     deps = subprocess.run(["readelf", "-d", LIB_PATH], capture_output=True, text=True).stdout
     assert "nccl" not in deps.lower()
     assert nccl_available()
+
+
+def test_plain_c_client(tmp_path):
+    """include/qfb.h is a C header: a C11 program compiled with gcc links
+    against libqfb.so and calls the host entry points (scale math, error
+    taxonomy, QSIM serialization) — the binding an FFI (cgo, ctypes, JNI
+    shim) would generate. No GPU needed."""
+    import subprocess
+    from paper_2511_12653_b200 import LIB_PATH
+    src = tmp_path / "client.c"
+    src.write_text(r'''
+#include <stdio.h>
+#include <string.h>
+#include "qfb.h"
+int main(void) {
+  qfb_quant_config cfg;
+  qfb_quant_config_default(&cfg);
+  if (qfb_quant_config_validate(&cfg) != QFB_OK || qfb_q_max(&cfg) != 127) return 1;
+  double ls[3] = {-4.0, 0.0, 2.0}, s[3];
+  if (qfb_resolve_scales(ls, 3, &cfg, QFB_PREC_FULL, s) != QFB_OK) return 2;
+  if (!(s[0] > 0.0 && s[1] > s[0] && s[2] > s[1])) return 3;
+  double bad = 0.0 / 0.0;
+  if (qfb_resolve_scales(&bad, 1, &cfg, QFB_PREC_FULL, s) != QFB_ERR_NONFINITE) return 4;
+  if (strlen(qfb_last_error()) == 0) return 5;
+  float data[6] = {1, 2, 3, 4, 5, 6};
+  int64_t shape[2] = {2, 3};
+  size_t n = 0;
+  if (qfb_qsim_serialize(data, 2, shape, 0, NULL, 0, &n) != QFB_OK || n != 13 + 16 + 24) return 6;
+  printf("ok %s\n", qfb_build_info());
+  return 0;
+}
+''')
+    exe = tmp_path / "client"
+    libdir = os.path.dirname(LIB_PATH)
+    subprocess.run(["gcc", "-std=c11", "-Wall", "-Werror", "-O1", f"-I{ROOT}/include", str(src), "-o", str(exe),
+                    f"-L{libdir}", "-lqfb", f"-Wl,-rpath,{libdir}"], check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, (r.returncode, r.stdout, r.stderr)
+    assert r.stdout.startswith("ok ")
