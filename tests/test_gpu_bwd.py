@@ -354,3 +354,19 @@ def test_scales_outside_fast_range(qfb, orc, cuda):
     _, dx, dls = orc.fq_backward(x, up, ls, 1, C, HW, cfg=ocfg)
     assert np.array_equal(bits32(host(g.d_input).ravel()), bits32(dx))
     assert np.asarray(g.d_log_scale).tobytes() == dls.tobytes()
+
+
+@pytest.mark.parametrize("n", [128 * 120 * 160, 11_000_000])
+def test_long_rows_finisher_paths(qfb, orc, cuda, n):
+    """Per-tensor backward over one long row: 2.46 M elements (config 1's
+    map: 1,024 tiles per row -> the shared-memory finisher) and 11 M
+    elements (> 4,096 tiles -> its in-place global path). d_input and
+    d_log_s bitwise."""
+    rng = np.random.default_rng(n % 1000)
+    x = rng.normal(0, 1, n).astype(np.float32)
+    up = rng.normal(0, 1, n).astype(np.float32)
+    ls = -3.2
+    g = qfb.fake_quantize_backward(to_dev(x, cuda), ls, None, to_dev(up, cuda))
+    _, dx, dls = orc.fq_backward(x, up, [ls], 1, 1, n)
+    assert np.array_equal(bits32(host(g.d_input)), bits32(dx))
+    check_grads(g.d_log_scale, dls, TOL_F32)
