@@ -50,8 +50,10 @@ constexpr int kProbeNoCompute = 8;
 constexpr int kProbeNoLoads = 16;
 
 constexpr int kWinPad = 32;                // window slack: 16-byte rounding at both ends
-constexpr size_t kRingBudget = 72 * 1024;  // default per-CTA ring + sums: 3 CTAs per SM
-constexpr size_t kRedBytes = kBwdThreads * sizeof(double);  // group sums of one stage
+constexpr size_t kRingBudget = 76 * 1024;  // default per-CTA ring + sums: 3 CTAs per SM
+// group sums of one stage use, double-buffered per stage (the producer reads
+// use u's sums after it has already refilled the stage for use u + 1)
+constexpr size_t kRedBytes = 2 * kBwdThreads * sizeof(double);
 constexpr size_t kSmemMax = 220 * 1024;    // dynamic smem attribute (ring + sums; + static <= 227 KB)
 
 // Descend `levels` levels of the reference split from node (lo, m) along
@@ -533,7 +535,8 @@ __global__ void __launch_bounds__(kBwdCtaThreads, 3) bwd_kernel(const __grid_con
   __shared__ TileRef refs[kMaxStages];
   const int nst = bt.nstages;
   const uint32_t se = bt.stage_elems;
-  // per-stage group sums of a tile, after the ring
+  // per-stage group sums of a tile, after the ring: red[2 * s + parity of
+  // the stage's use] (the parity is the stage's full/done phase bit)
   double(*red)[kBwdThreads] = reinterpret_cast<double(*)[kBwdThreads]>(
       smem_raw + (size_t)nst * 2 * se * sizeof(T));
   const int tid = threadIdx.x;
@@ -588,18 +591,21 @@ __global__ void __launch_bounds__(kBwdCtaThreads, 3) bwd_kernel(const __grid_con
       const uint32_t nid = j_id + (uint32_t)nst * gridDim.x;
       TileRef nr;
       if (nid < total) nr = ref_of(k + (uint32_t)nst);
-      mbar_wait(&done[s], (done_phase >> s) & 1u);
+      const uint32_t par = (done_phase >> s) & 1u;
+      mbar_wait(&done[s], par);
       done_phase ^= 1u << s;
       Stage<T> st = stage_at<T>(smem_raw, se, s);
       const TileRef cur = refs[s];
       const BwdDesc& d = bt.d[cur.di];
-      const double part = lane_subtree(d, red[s], lane);
       if constexpr ((V & kProbeNoLoads) == 0) {
         store_dx<T>(d, cur, st, lane);
         if (lane == 0) bulk_wait_read_all();  // the store has read the stage
       }
       __syncwarp();
       if (nid < total) produce<T, V>(bt, nr, st, &refs[s], &full[s], lane, true);
+      // the tile's sums are read after the refill was issued (the next use
+      // of this stage writes the other buffer)
+      const double part = lane_subtree(d, red[2 * s + par], lane);
       tile_sum(d, cur, part);
       s = s + 1 == nst ? 0 : s + 1;
     }
@@ -612,7 +618,8 @@ __global__ void __launch_bounds__(kBwdCtaThreads, 3) bwd_kernel(const __grid_con
   GroupCache gc;
   int s = 0;
   for (uint32_t tile_id = blockIdx.x; tile_id < total; tile_id += gridDim.x) {
-    mbar_wait(&full[s], (full_phase >> s) & 1u);
+    const uint32_t par = (full_phase >> s) & 1u;
+    mbar_wait(&full[s], par);
     full_phase ^= 1u << s;
     Stage<T> st = stage_at<T>(smem_raw, se, s);
     const TileRef cur = refs[s];
@@ -630,7 +637,7 @@ __global__ void __launch_bounds__(kBwdCtaThreads, 3) bwd_kernel(const __grid_con
     double v = (V & kProbeNoCompute) ? 0.0
              : (d.dx != nullptr && !(V & kProbeNoLoads)) ? group_sum_any<T, true>(sx, su, glen, dc, q)
                                                           : group_sum_any<T, false>(sx, su, glen, dc, q);
-    red[s][tid] = v;  // the producer runs the tile's tree reduction
+    red[2 * s + par][tid] = v;  // the producer runs the tile's tree reduction
     __syncwarp();     // the warp's d_input and group sums are written
     if (lane == 0) mbar_arrive(&done[s]);
     s = s + 1 == nst ? 0 : s + 1;
