@@ -280,7 +280,13 @@ qfb_status plan_ew(int dtype, const EwJob& j, std::vector<EwDesc>& out) {
 // element-rate bound and want the most CTAs (2 stages).
 int tma_stages(const qfb_ctx* ctx, int dtype, bool chain, bool int8_out, uint64_t chunks) {
   if (ctx->tma_stages_env) return ctx->tma_stages_env;
-  if (chain || dtype != 0 || int8_out) return 2;
+  if (chain || int8_out) return 2;
+  if (dtype != 0) {
+    // f16 plain: 3 stages for medium launches (one frame: 36.3 -> 35.8 us),
+    // 2 for long ones (8 frames: 0.222 vs 0.226 ms) and tiny ones
+    const uint64_t ctas2h = (uint64_t)ctx->sm_count * (uint64_t)std::max(1, ctx->tma_blocks_per_sm[dtype][0][2]);
+    return (chunks >= 2 * ctas2h && chunks < 32 * ctas2h) ? 3 : 2;
+  }
   // short launches (about one chunk per CTA, e.g. one 128x120x160 map): the
   // 2-stage ring's extra CTAs beat depth (6.5 -> 6.0 us per call; with PDL
   // on these launches the early-scheduled dependents take those CTA slots
