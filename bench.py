@@ -33,11 +33,12 @@ sys.path.insert(0, ROOT)
 
 METRIC = "fake-quant GB/s (% of HBM peak) and front-end frames/sec at 1/2/4/8 B200 vs CPU ref"
 UNIT = "frames/s"
+DATA = "synthetic: standard-normal activations and upstream, per-channel scales log-uniform [1e-3, 0.1]"
 WORKLOAD = ("BASELINE config 2: per-channel fake-quant fwd + scale-only LSQ/STE bwd over the 22 "
             "DPVO encoder activation quant points of one 480x640 frame (41,164,800 quant-point elems)")
 
 
-def parse():
+def parse(argv=None):
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=1000)
@@ -53,10 +54,15 @@ def parse():
                    help="gloo: exercise the N>1 path with ranks sharing one GPU (tests only)")
     p.add_argument("--graph-steps", type=int, default=8,
                    help="consecutive steps captured in one CUDA graph (N=1)")
-    p.add_argument("--cpu-seconds", type=float, default=15.0)
+    p.add_argument("--no-single-thread", action="store_true",
+                   help="reference arm: skip the one-thread sample")
     p.add_argument("--no-secondary", action="store_true",
                    help="skip the config-3 chain window and config-5 forward-throughput lines")
-    return p.parse_args()
+    return p.parse_args(argv)
+
+
+def parse_args_list(argv):
+    return parse(argv)
 
 
 # ------------------------------------------------------------- helpers --
@@ -255,17 +261,40 @@ def host_threads():
         return os.cpu_count() or 1
 
 
+def bench_config(args, ws):
+    """The `config` object of the JSON line — one function for both arms,
+    so the reference arm and ours describe the identical workload (same
+    dict, byte for byte)."""
+    from paper_2511_12653_b200.shapes import dpvo_quant_points, frame_bytes
+    pts = dpvo_quant_points()
+    esize = 4 if args.dtype == "f32" else 2
+    b = frame_bytes(pts, esize)
+    step_bytes = b["fwd"] + b["bwd"]
+    return {"workload": WORKLOAD, "frames_per_step_per_gpu": 1,
+            "quant_points": sum(len(p.consumers) for p in pts), "tensors": len(pts),
+            "scales": "per-channel, log-uniform [1e-3, 0.1]",
+            "l2_policy": f"inputs > L2: {max(1, args.sets)} rotating frame sets, "
+                         f"{step_bytes / 1e6:.0f} MB moved per step vs 126 MB L2",
+            "parallelism": (f"frames sharded over {ws} GPUs (one process each); per step one "
+                            f"exchange of the per-frame scale-gradient rows: NCCL all-gather + "
+                            f"frame-order fold through the C-ABI (qfb_gather_fold_scale_grads)"
+                            if ws > 1 else "1 GPU")}
+
+
 def run_reference_arm(args):
     """--impl reference: the reference CPU implementation on the host cores,
-    same metric/unit/config; each step a bounded sample of the workload."""
+    same metric/unit/config; each step a bounded sample of the workload.
+    This process maps no native code of the package (shapes is pure
+    Python); the timed code is the reference's, compiled from its sources
+    (oracle/_ref/libqfref.so)."""
     import oracle
+    from paper_2511_12653_b200.shapes import dpvo_quant_points
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
     if not oracle.reference_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libqfref.so missing"}))
         return 0
-    from paper_2511_12653_b200.frontend import dpvo_quant_points
     pts = dpvo_quant_points()
     consumers = [(p, c) for p in pts for c in p.consumers]
     threads = host_threads()
@@ -279,59 +308,127 @@ def run_reference_arm(args):
         tot_s += s
         tot_f += f
     fps = tot_f / tot_s
+    cpu = {"value": fps, "unit": UNIT, "cores": threads, "kind": "reference",
+           "sample": "per step: " + w.describe(tot_s / args.steps, tot_f / args.steps),
+           "host": host_cpu_info()}
+    if not args.no_single_thread:
+        # the reference at threads = 0 (sequential) as well
+        w1 = RefCpuWorkload(consumers, 1, args.dtype).size(3.0)
+        s1, f1 = w1.run()
+        cpu["single_thread"] = {"value": f1 / s1, "unit": UNIT, "cores": 1, "sample": w1.describe(s1, f1)}
     line = {"metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1000.0 / fps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-            "config": {"workload": WORKLOAD, "host_threads": threads},
+            "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": DATA,
+            "data_generator": "numpy default_rng standard normal on the host",
+            "config": bench_config(args, ws),
             "impl": "reference",
-            "cpu_baseline": {"value": fps, "unit": UNIT, "cores": threads, "kind": "reference",
-                             "sample": "per step: " + w.describe(tot_s / args.steps,
-                                                                 tot_f / args.steps)},
+            "cpu_baseline": cpu,
             "e2e": {"value": fps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
 
 
+def reference_arm_subprocess(args, steps=8, warmup=2):
+    """cpu_baseline of our arm: the reference arm itself (`bench.py --impl
+    reference`), run as a fresh process with the same dtype, so the two
+    numbers are the same code under the same conditions."""
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    cmd = [sys.executable, os.path.abspath(__file__), "--impl", "reference", "--steps", str(steps),
+           "--warmup", str(warmup), "--dtype", args.dtype, "--sets", str(args.sets)]
+    out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=600)
+    for ln in out.stdout.splitlines()[::-1]:
+        ln = ln.strip()
+        if ln.startswith("{"):
+            d = json.loads(ln)
+            if "unavailable" in d:
+                return None
+            cpu = dict(d["cpu_baseline"])
+            cpu["sample"] = (f"`bench.py --impl reference --steps {steps} --warmup {warmup}` in a fresh "
+                             f"process: " + cpu["sample"])
+            return cpu
+    raise RuntimeError(f"reference arm failed: rc={out.returncode} {out.stderr[-400:]}")
+
+
 # --------------------------------------------------------- our arm (GPU) --
 
-def run_qfb(args):
-    import ctypes
+class Plumbing:
+    """N > 1 process plumbing. torch.distributed runs on gloo for control
+    only (the NCCL id broadcast, barriers, the max over ranks of the timed
+    region); the data exchange of the QAT step — the per-frame scale-gradient
+    rows, all-gathered and folded in global frame order — goes through the
+    library's C-ABI on NCCL (qfb_nccl_comm_init_rank +
+    qfb_gather_fold_scale_grads, captured in the step's CUDA graph).
+    --dist-backend gloo (tests: ranks sharing one GPU, where NCCL refuses
+    to run) exchanges the rows through gloo instead, eagerly."""
 
-    import numpy as np
+    def __init__(self, args, q, ws, rank, gpu):
+        import torch.distributed as dist
+        self.ws, self.rank, self.gpu, self.dist = ws, rank, gpu, dist
+        self.nccl = args.dist_backend == "nccl"
+        dist.init_process_group("gloo")
+        self.comm = None
+        if self.nccl:
+            box = [q.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(box, src=0)
+            self.comm = q.NcclRankComm(box[0], ws, rank, gpu)
+
+    def exchange(self, ctx, rows_per_rank, n, device):
+        from paper_2511_12653_b200.frontend import GlooGatherFold, NcclGatherFold
+        if self.nccl:
+            return NcclGatherFold(ctx, self.comm, rows_per_rank, n, device=device)
+        return GlooGatherFold(ctx)
+
+    def barrier(self):
+        self.dist.barrier()
+
+    def max(self, v: float) -> float:
+        import torch
+        t = torch.tensor([float(v)], dtype=torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.comm is not None:
+            self.comm.close()
+        self.dist.barrier()
+        self.dist.destroy_process_group()
+
+
+def run_qfb(args):
     import torch
 
     import paper_2511_12653_b200 as q
-    from paper_2511_12653_b200.dist import gather_fold
     from paper_2511_12653_b200.frontend import FrontendQuantPass
 
     ws, rank, local = dist_env()
-    local = local % max(1, torch.cuda.device_count())
     # --dist-backend gloo (test only): ranks may share a GPU, so the device is
     # local % device_count; with NCCL (the default) every rank owns a GPU
     gpu = local % max(1, torch.cuda.device_count()) if args.dist_backend == "gloo" else local
     torch.cuda.set_device(gpu)
     dev = torch.device("cuda", gpu)
-    pg = None
-    if ws > 1:
-        import torch.distributed as dist
-        if args.dist_backend == "gloo":
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=dev)
-        pg = dist
+    pg = Plumbing(args, q, ws, rank, gpu) if ws > 1 else None
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
-    ctx = q.Context(local, stream.cuda_stream)
-    fp = FrontendQuantPass(ctx, frames=1, dtype=args.dtype, sets=max(1, args.sets),
-                           seed=1 + 7919 * rank, device=dev)
+    ctx = q.Context(gpu, stream.cuda_stream)
+    # at N > 1 the step's backward leaves this rank's frame row for the
+    # exchange; every rank holds distinct frames (frame_offset = rank)
+    rows = None
+    if ws > 1:
+        from paper_2511_12653_b200.shapes import dpvo_quant_points
+        n_grad = sum(p.channels * len(p.consumers) for p in dpvo_quant_points())
+        rows = torch.zeros((1, n_grad), dtype=torch.float64, device=dev)
+    fp = FrontendQuantPass(ctx, frames=1, dtype=args.dtype, sets=max(1, args.sets), seed=1, device=dev,
+                           rows_out=rows, frame_offset=rank)
     grads = fp.scale_grads()
     nsets = len(fp.sets)
+    ex = pg.exchange(ctx, 1, fp.n_grad, dev) if pg is not None else None
 
     def exchange():
-        if pg is not None:
-            # QAT exchange: per-frame scale-gradient rows, all-gathered and
-            # folded in frame order (bit-identical at any GPU count)
-            gather_fold(fp.dls_flat.unsqueeze(0))
+        if ex is not None:
+            # QAT exchange: the step's frame rows of all ranks, folded in
+            # frame order into the gradient vector (bit-identical at any N)
+            ex(rows, grads)
 
     def eager_step(i, ev=None):
         si = i % nsets
@@ -345,18 +442,18 @@ def run_qfb(args):
             ev[2].record(stream)
         exchange()
 
-    # warm up eagerly (sizes the workspaces), then capture one CUDA graph per
-    # input set: the step is 1 forward + 2 backward launches
+    # warm up eagerly (sizes the workspaces), then capture the step as CUDA
+    # graphs: 1 forward + 2 backward launches (+ the NCCL exchange at N > 1)
     for i in range(max(1, args.warmup)):
         eager_step(i)
     ctx.sync()
-    use_graph = not args.no_graph
+    capturable = pg is None or pg.nccl
+    use_graph = not args.no_graph and capturable
     graphs = []
     launches_per_step = 3
     # steps per graph replay: G consecutive steps (sets alternating) in one
-    # graph, so the per-replay launch gap is paid once per G steps; at N > 1
-    # every step ends in the NCCL exchange, launched outside the graph (G = 1)
-    G = max(1, args.graph_steps) if ws == 1 else 1
+    # graph, so the per-replay launch gap is paid once per G steps
+    G = max(1, args.graph_steps)
     G = G - G % nsets if G >= nsets else G
     big = None
     if use_graph:
@@ -367,6 +464,7 @@ def run_qfb(args):
                 with torch.cuda.graph(g, stream=stream):
                     fp.forward(si)
                     fp.backward(si)
+                    exchange()
                 graphs.append(g)
             launches_per_step = (ctx.launch_count - c0) // nsets
             if G > 1:
@@ -375,15 +473,19 @@ def run_qfb(args):
                     for k in range(G):
                         fp.forward(k % nsets)
                         fp.backward(k % nsets)
+                        exchange()
         except Exception as exc:  # pragma: no cover - fall back to eager timing
             print(f"graph capture failed ({exc}); timing eager launches", file=sys.stderr)
             use_graph = False
             big = None
+    elif pg is not None:
+        c0 = ctx.launch_count
+        eager_step(0)
+        launches_per_step = ctx.launch_count - c0
 
     def step(i):
         if use_graph:
             graphs[i % nsets].replay()
-            exchange()
         else:
             eager_step(i)
 
@@ -433,9 +535,7 @@ def run_qfb(args):
     fwd_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / k_att
     bwd_ms = sum(e[1].elapsed_time(e[2]) for e in evs) / k_att
     if pg is not None:
-        t = torch.tensor([ms_total], device=dev)
-        pg.all_reduce(t, op=pg.ReduceOp.MAX)
-        ms_total = t.item()
+        ms_total = pg.max(ms_total)
         pg.barrier()
     ms_step = ms_total / args.steps
     frames_total = ws * args.steps * fp.frames
@@ -453,7 +553,8 @@ def run_qfb(args):
                 "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": b["bwd"],
                 "traffic": (traffic or {}).get(args.dtype, {}).get("bwd_bytes_per_launch"),
-                "fwd_kernel": {"kernel": "qfb::ew_kernel (fused multi-point forward)",
+                "fwd_kernel": {"kernel": "qfb::ew_tma_kernel<T, false, NS> (fused multi-point forward; "
+                                         "NS = tma_stages(): 3 for one f32 frame)",
                                "achieved": fwd_gbps, "frac": fwd_gbps / peak,
                                "algorithmic_bytes_per_launch": b["fwd"],
                                "traffic": (traffic or {}).get(args.dtype, {}).get("fwd_bytes_per_launch")},
@@ -462,17 +563,16 @@ def run_qfb(args):
     # ---------------------------------------------------- e2e (host API) --
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, q, ctx, fp, stream, dev, pg, ws)
+        e2e = run_e2e(args, q, ctx, fp, stream, dev, pg, ws, rank)
 
     secondary = None
     if not args.no_secondary:
-        secondary = run_secondary(args, ctx, stream, dev, peak, rank, ws)
+        secondary = run_secondary(args, ctx, stream, dev, peak, rank, ws, pg)
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
-        cons = [(p, c) for p in fp.points for c in p.consumers]
         try:
-            cpu = cpu_reference_frames_per_s(cons, args.cpu_seconds, host_threads(), args.dtype)
+            cpu = reference_arm_subprocess(args)
         except Exception as exc:  # pragma: no cover
             cpu = {"value": None, "unit": UNIT, "cores": host_threads(), "kind": "reference",
                    "sample": f"failed: {exc}"}
@@ -481,30 +581,24 @@ def run_qfb(args):
         line = {"metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
-                "data": "synthetic (CounterRng normal, rng.hpp:24-50, generated on device)",
-                "config": {"workload": WORKLOAD, "frames_per_step_per_gpu": fp.frames,
-                           "quant_points": len(fp.consumers), "tensors": len(fp.points),
-                           "scales": "per-channel, log-uniform [1e-3, 0.1]",
-                           "l2_policy": f"inputs > L2: {nsets} rotating frame sets, "
-                                        f"{step_bytes / 1e6:.0f} MB moved per step vs 126 MB L2",
-                           "parallelism": f"frames sharded over {ws} GPU(s); NCCL all-gather + frame-order fold "
-                                          f"of {int(grads.numel())} fp64 scale grads per step" if ws > 1
-                           else "1 GPU"},
+                "data": DATA,
+                "data_generator": "CounterRng normal (rng.hpp:24-50), generated on the device",
+                "config": bench_config(args, ws),
                 "gbps": gbps, "hbm_frac": (gbps / ws) / peak,
                 "kernel_ms": {"fwd": fwd_ms, "bwd": bwd_ms},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clocks, "secondary": secondary,
                 "timing": (f"value: CUDA-graph replays of {G} consecutive steps each (fwd + bwd + finisher "
-                           "launches per step, serial on the library stream) between CUDA events"
+                           "launches per step" + (" + the NCCL gather-fold exchange" if ws > 1 else "") +
+                           ", serial on the library stream) between CUDA events, max over ranks"
                            if use_graph else
                            "value: eager launches between CUDA events on the library stream") +
                           f"; roofline: per-kernel CUDA events over {k_att} eager steps",
                 "wall_ms_per_step": (wall1 - wall0) * 1000.0 / args.steps}
         print(json.dumps(line))
-    if pg is not None:
-        pg.barrier()
-        pg.destroy_process_group()
     ctx.close()
+    if pg is not None:
+        pg.close()
     return 0
 
 
@@ -524,12 +618,38 @@ def time_device(fn, stream, reps, warmup=2):
     return t0.elapsed_time(t1) / reps
 
 
-def run_secondary(args, ctx, stream, dev, peak, rank, ws):
-    """BASELINE configs 3 and 5 on this GPU (reported beside the headline):
-    c3 = fused quant->act->quant chains over every quant point of a 15-frame
-    window + its patch/update-operator inputs (ReLU and GELU variants);
-    c5 = the fused multi-point forward alone (inference front-end), 8 frames
-    per launch, frames/s, with the reference's forward timed on the host."""
+def time_aggregate(fn, n_calls, stream, pg, warmup=2):
+    """ms for n_calls calls of fn() on this rank (CUDA events on `stream`),
+    the whole job's time = the max over ranks, barrier + synchronize on both
+    sides."""
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    if pg is not None:
+        pg.barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(n_calls):
+        fn()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    if pg is not None:
+        ms = pg.max(ms)
+        pg.barrier()
+    return ms
+
+
+def run_secondary(args, ctx, stream, dev, peak, rank, ws, pg):
+    """BASELINE configs 3, 5, 4 and 1 on this GPU (reported beside the
+    headline): c3 = fused quant->act->quant chains over every quant point of
+    a 15-frame window + its patch/update-operator inputs (ReLU and GELU);
+    c5 = the throughput sweep as specified: 32 sequences x 1000 frames
+    through the fused forward, sequences split over the ranks, 8 frames per
+    launch, timed as one aggregate (max over ranks); c4 = the 64-frame QAT
+    step; c1 = the per-tensor map."""
     import torch
     from paper_2511_12653_b200.frontend import FrontendQuantPass, WindowChainPass
     out = {}
@@ -542,54 +662,51 @@ def run_secondary(args, ctx, stream, dev, peak, rank, ws):
             "bytes_per_window": wp.bytes_per_run(), "quant_points": len(wp.points),
             "launches_per_window": 1,
             "workload": "15-frame window: 22 encoder quant points x 15 frames + gmap/imap (96 patches x "
-                        "15) + corr/net/inp (21,600 edges), relu(a [+ b]) or gelu -> K fake-quant outputs"}
+                        "15) + corr/net/inp (21,600 edges), relu(a [+ b]) or gelu -> K fake-quant outputs" +
+                        ("; GELU is defined by this build (the reference has none: parity unpinned, "
+                         "oracle and kernel share include/qfb_portable.h)" if gelu else "")}
         del wp
         torch.cuda.empty_cache()
-    fp = FrontendQuantPass(ctx, frames=8, dtype=args.dtype, sets=2, seed=11 + rank, device=dev)
-    k = [0]
+    for int8 in (False, True):
+        fp = FrontendQuantPass(ctx, frames=8, dtype=args.dtype, sets=2, seed=11, device=dev, int8_out=int8,
+                               frame_offset=8 * rank)
+        k = [0]
 
-    def fwd():
-        fp.forward(k[0] % 2)
-        k[0] += 1
-    ms = time_device(fwd, stream, reps=50)
-    fps = fp.frames / (ms / 1e3)
-    gb = fp.bytes_per_step()["fwd"] / (ms / 1e3) / 1e9
-    c5 = {"value": ws * fps, "unit": "frames/s", "per_gpu_frames_per_s": fps, "gbps": gb,
-          "hbm_frac": gb / peak, "frames_per_launch": fp.frames,
-          "seconds_for_32x1000_frames": 32000.0 / (ws * fps),
-          "workload": "BASELINE config 5: fused multi-point fake-quant forward of the 22 DPVO "
-                      "activation quant points (inference front-end), 8 frames per launch; weights "
-                      "are fake-quantized once (cache_weights, exec.hpp:59-60), not per frame"}
-    if rank == 0 and ws == 1 and not args.no_cpu:
-        cons = [(p, c) for p in fp.points for c in p.consumers]
-        try:
-            c5["cpu_baseline"] = cpu_reference_frames_per_s(cons, 5.0, host_threads(), args.dtype,
-                                                            do_bwd=False)
-        except Exception as exc:  # pragma: no cover
-            c5["cpu_baseline"] = {"value": None, "sample": f"failed: {exc}"}
-    out["c5_forward_throughput"] = c5
-    del fp
-    torch.cuda.empty_cache()
-    out["c4_qat_step"] = run_qat_step(args, ctx, stream, dev, peak, rank, ws)
+        def fwd():
+            fp.forward(k[0] % 2)
+            k[0] += 1
+        total = 32 * 1000
+        per_rank = total // ws
+        launches = (per_rank + fp.frames - 1) // fp.frames
+        ms = time_aggregate(fwd, launches, stream, pg)
+        fps = ws * launches * fp.frames / (ms / 1e3)
+        key = "fwd_int8" if int8 else "fwd"
+        gb = ws * launches * fp.bytes_per_step()[key] / (ms / 1e3) / 1e9
+        line = {"value": fps, "unit": "frames/s", "seconds_for_32x1000_frames": ms / 1e3,
+                "gbps_per_gpu": gb / ws, "hbm_frac": gb / ws / peak, "frames_per_launch": fp.frames,
+                "launches_per_rank": launches, "n_gpus": ws,
+                "timing": "all 32,000 frames (32 sequences x 1000) split over the ranks; CUDA events around "
+                          "each rank's launches, barrier + synchronize both sides, max over ranks"}
+        if int8:
+            line["workload"] = ("config 5 forward emitting int8 codes (QFB_FLAG_INT8_OUT, SURVEY §8 f2): "
+                                "input read once, 1 byte written per quant-point element")
+            out["c5_forward_int8_codes"] = line
+        else:
+            line["workload"] = ("BASELINE config 5: fused multi-point fake-quant forward of the 22 DPVO "
+                                "activation quant points (inference front-end) over 32 x 1000 frames, 8 frames "
+                                "per launch; weights are fake-quantized once (cache_weights, exec.hpp:59-60)")
+            if rank == 0 and ws == 1 and not args.no_cpu:
+                cons = [(p, c) for p in fp.points for c in p.consumers]
+                try:
+                    line["cpu_baseline"] = cpu_reference_frames_per_s(cons, 5.0, host_threads(), args.dtype,
+                                                                      do_bwd=False)
+                except Exception as exc:  # pragma: no cover
+                    line["cpu_baseline"] = {"value": None, "sample": f"failed: {exc}"}
+            out["c5_forward_throughput"] = line
+        del fp
+        torch.cuda.empty_cache()
+    out["c4_qat_step"] = run_qat_step(args, ctx, stream, dev, peak, rank, ws, pg)
     out["c1_per_tensor_fwd"] = run_c1(args, ctx, stream, dev, peak, rank, ws)
-    # f2: the same forward emitting int8 codes (1 byte per quant-point element)
-    fq = FrontendQuantPass(ctx, frames=8, dtype=args.dtype, sets=2, seed=11 + rank, device=dev,
-                           int8_out=True)
-    k[0] = 0
-
-    def fwd8():
-        fq.forward(k[0] % 2)
-        k[0] += 1
-    ms = time_device(fwd8, stream, reps=50)
-    fps = fq.frames / (ms / 1e3)
-    gb = fq.bytes_per_step()["fwd_int8"] / (ms / 1e3) / 1e9
-    out["c5_forward_int8_codes"] = {
-        "value": ws * fps, "unit": "frames/s", "per_gpu_frames_per_s": fps, "gbps": gb,
-        "hbm_frac": gb / peak, "frames_per_launch": fq.frames,
-        "workload": "config 5 forward emitting int8 codes (QFB_FLAG_INT8_OUT, SURVEY §8 f2): "
-                    "input read once, 1 byte written per quant-point element"}
-    del fq
-    torch.cuda.empty_cache()
     return out
 
 
@@ -664,46 +781,47 @@ def run_c1(args, ctx, stream, dev, peak, rank, ws):
     return res
 
 
-def run_qat_step(args, ctx, stream, dev, peak, rank, ws):
-    """BASELINE config 4: one scale-only QAT step over 64 frames (64 / N per
-    rank): fused fake-quant forward, per-frame distillation loss (fnet and
-    inet pairs), scale-only backward (frame rows accumulated in order), Adam
-    on the 1,494 scales (+ at N > 1 the gather-fold of the scale gradients).
-    Convolutions excluded (cuDNN); features and upstream are synthetic. The
-    step's ~260 launches replay as one CUDA graph."""
+def run_qat_step(args, ctx, stream, dev, peak, rank, ws, pg):
+    """BASELINE config 4: one scale-only QAT step over 64 frames, sharded
+    64 / N per rank: fused fake-quant forward, per-frame distillation loss
+    (fnet and inet pairs), scale-only backward leaving one gradient row per
+    frame, the rows of all ranks gathered and folded in frame order (NCCL
+    through the C-ABI at N > 1), then Adam (device step counter) — replicas
+    stay bitwise equal. Scales are resolved on the device from the current
+    log scales each step. Convolutions excluded (cuDNN); features and
+    upstream are synthetic. The step replays as one CUDA graph."""
     import torch
-    from paper_2511_12653_b200.dist import gather_fold
     from paper_2511_12653_b200.frontend import QatStep
     frames = max(1, 64 // ws)
-    qs = QatStep(ctx, frames=frames, dtype=args.dtype, seed=21 + rank, device=dev)
-    for _ in range(2):
-        qs.run()
+    qs = QatStep(ctx, frames=frames, dtype=args.dtype, seed=21, device=dev, frame_offset=rank * frames,
+                 total_frames=frames * ws, resolve="device")
+    if pg is not None:
+        qs.exchange_fn = pg.exchange(ctx, frames, qs.n_act, dev)
+    qs.run()  # sizes the scratch (growth is refused under capture)
     torch.cuda.synchronize(dev)
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g, stream=stream):
-        qs.run()
-
-    def step():
-        g.replay()
-        if ws > 1:
-            gather_fold(qs.grads.unsqueeze(0))
-    ms = time_device(step, stream, reps=5, warmup=1)
-    if ws > 1:
-        t = torch.tensor([ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = t.item()
-    gb = qs.bytes_per_step() / (ms / 1e3) / 1e9
-    res = {"ms_per_step": ms, "frames_per_step": 64, "frames_per_s": 64 / (ms / 1e3),
-           "gbps_per_gpu": gb, "hbm_frac": gb / peak, "scaling": "strong (64 frames over N GPUs)",
-           "workload": "BASELINE config 4: scale-only QAT step over 64 frames (fwd FQ 22 points, "
-                       "distill loss fnet+inet per frame, bwd FQ with frame-ordered accumulation, "
-                       "Adam on 1,494 scales); convolutions excluded"}
-    del qs, g
+    runner = qs.run
+    graph = pg is None or pg.nccl
+    if graph:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            qs.run()
+        runner = g.replay
+    ms = time_aggregate(runner, 5, stream, pg, warmup=1)
+    gb = qs.bytes_per_step() / (ms / 5 / 1e3) / 1e9
+    res = {"ms_per_step": ms / 5, "frames_per_step": frames * ws, "frames_per_s": frames * ws / (ms / 5 / 1e3),
+           "gbps_per_gpu": gb, "hbm_frac": gb / peak, "n_gpus": ws,
+           "scaling": "strong (64 frames over N GPUs)", "graph": graph,
+           "workload": "BASELINE config 4: scale-only QAT step over 64 frames (device scale resolve, fwd FQ "
+                       "22 points, distill loss fnet+inet per frame, bwd FQ with per-frame rows, frame-order "
+                       "gather-fold of the rows over all ranks, Adam on 1,494 scales); convolutions excluded"}
+    del qs
+    if graph:
+        del g
     torch.cuda.empty_cache()
     return res
 
 
-def run_e2e(args, q, ctx, fp, stream, dev, pg, ws):
+def run_e2e(args, q, ctx, fp, stream, dev, pg, ws, rank):
     """Same workload end to end through the public host C-ABI: one
     qfb_quant_pass_host_submit / _wait pair per frame (pinned host float32
     buffers in: every quant-point tensor + every upstream; host buffers out:
@@ -745,10 +863,24 @@ def run_e2e(args, q, ctx, fp, stream, dev, pg, ws):
     tables = [build(0), build(1)]
     prec = 1 if args.dtype == "f16" else 0
 
+    n_grad = sum(p.channels for (p, _c) in fp.consumers)
+    if pg is not None:
+        # the frame's gradient row up, the gather-fold over all ranks, the
+        # folded vector down (pinned buffers, the library's stream)
+        ex = pg.exchange(ctx, 1, n_grad, dev)
+        row_h = torch.empty((1, n_grad), dtype=torch.float64).pin_memory()
+        row_d = torch.empty((1, n_grad), dtype=torch.float64, device=dev)
+        fold_d = torch.empty(n_grad, dtype=torch.float64, device=dev)
+        fold_h = torch.empty(n_grad, dtype=torch.float64).pin_memory()
+
     def exchange(grad_arrays):
         if pg is not None:
-            from paper_2511_12653_b200.dist import gather_fold
-            gather_fold(torch.from_numpy(np.concatenate(grad_arrays)).to(dev).unsqueeze(0))
+            row_h[0].numpy()[:] = np.concatenate(grad_arrays)
+            with torch.cuda.stream(stream):
+                row_d.copy_(row_h, non_blocking=True)
+                ex(row_d, fold_d)
+                fold_h.copy_(fold_d, non_blocking=True)
+            stream.synchronize()
 
     def submit(i):
         t, n, _g = tables[i % 2]
@@ -775,18 +907,22 @@ def run_e2e(args, q, ctx, fp, stream, dev, pg, ws):
     torch.cuda.synchronize(dev)
     ms = (time.perf_counter() - t0) * 1e3
     if pg is not None:
-        t = torch.tensor([ms], device=dev)
-        pg.all_reduce(t, op=pg.ReduceOp.MAX)
-        ms = t.item()
+        ms = pg.max(ms)
     h2d = sum(p.numel * 4 for p in fp.points) + sum(p.numel * 4 for (p, _c) in fp.consumers)
     d2h = sum(p.numel * 4 * 2 + p.channels * 8 for (p, _c) in fp.consumers)
+    if pg is not None:
+        h2d += 8 * n_grad
+        d2h += 8 * n_grad
     return {"value": ws * k / (ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "steps": k,
             "timing": "host wall clock around the submit/wait calls (the pass is synchronous per "
                       "frame: wait returns when the outputs are in host memory), max over ranks",
             "api": "qfb_quant_pass_host_submit/_wait (one pair per frame: 19 tensors, 22 quant points; "
-                   "float32 pinned host buffers; H2D/compute/D2H pipelined per point, two frames in "
-                   "flight)"}
+                   "float32 pinned host buffers" + ("; EmulatedHalf precision: values on the binary16 grid, "
+                                                    "half-grid FQ outputs" if args.dtype == "f16" else "") +
+                   "; H2D/compute/D2H pipelined per point, two frames in flight" +
+                   ("; + per frame the gradient row exchange (up, NCCL gather-fold, down)" if pg is not None
+                    else "") + ")"}
 
 
 def main():

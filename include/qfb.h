@@ -176,8 +176,15 @@ qfb_status qfb_int8_codes(qfb_ctx* ctx, qfb_dtype dtype, const void* x,
  *  d_log_s: device double[channels]. Row (o,c) yields
  *    r[o][c] = pairwise_sum(d_ds * up over the row) * chain[c].
  *  accumulate == 0: d_log_s[c] = ((r[0][c] + r[1][c]) + ...)
- *  accumulate != 0: d_log_s[c] = ((d_log_s[c] + r[0][c]) + r[1][c]) + ...
- *    (the trainer's `g += grad` accumulation, frontend.hpp:222-228). */
+ *  accumulate == 1: d_log_s[c] = ((d_log_s[c] + r[0][c]) + r[1][c]) + ...
+ *    (the trainer's `g += grad` accumulation, frontend.hpp:222-228).
+ *  accumulate == QFB_BWD_ROWS (2): one result per row, no fold:
+ *    d_log_s[o * row_stride + c] = r[o][c] (row_stride = channels here,
+ *    settable per entry in qfb_bwd_desc). The rows of frames sharded over
+ *    GPUs are gathered and folded in frame order by
+ *    qfb_gather_fold_scale_grads / qfb_fold_rows, which reproduces the
+ *    single-process fold bit for bit. */
+#define QFB_BWD_ROWS 2
 qfb_status qfb_fq_bwd(qfb_ctx* ctx, qfb_dtype dtype, const void* x,
                       const void* up, void* dx, int64_t outer,
                       int64_t channels, int64_t inner, const double* scale64,
@@ -243,11 +250,18 @@ typedef struct qfb_bwd_desc {
   double* d_log_s;
   int64_t outer, channels, inner;
   int32_t q_max;
-  int32_t accumulate;
+  int32_t accumulate;       /* 0, 1 or QFB_BWD_ROWS (see qfb_fq_bwd) */
+  int64_t row_stride;       /* QFB_BWD_ROWS: doubles between rows (0: channels) */
 } qfb_bwd_desc;
 
 qfb_status qfb_fq_bwd_multi(qfb_ctx* ctx, qfb_dtype dtype,
                             const qfb_bwd_desc* table, int32_t n);
+/* Size the context's backward workspace for `table` without launching, so
+ * the first call may be made under stream capture (growth during a capture
+ * is refused with QFB_ERR_UNSUPPORTED; buffers a captured graph references
+ * are never freed before qfb_ctx_destroy). */
+qfb_status qfb_fq_bwd_reserve(qfb_ctx* ctx, qfb_dtype dtype,
+                              const qfb_bwd_desc* table, int32_t n);
 
 qfb_status qfb_fq_chain_multi(qfb_ctx* ctx, const qfb_chain_desc* table,
                               int32_t n);
@@ -453,6 +467,13 @@ qfb_status qfb_nccl_available(void);
 /* ncclCommInitAll: one communicator per device, single process, one      */
 /* stream per GPU (the process model of SURVEY §8e; no launcher needed).  */
 qfb_status qfb_nccl_comm_init_all(int ndev, const int* devices, void** comms);
+/* One process per GPU (torchrun / mpirun style): rank 0 creates the id,  */
+/* the launcher's plumbing broadcasts its QFB_NCCL_UNIQUE_ID_BYTES bytes, */
+/* every rank calls ncclCommInitRank on its device.                       */
+#define QFB_NCCL_UNIQUE_ID_BYTES 128
+qfb_status qfb_nccl_get_unique_id(void* id);
+qfb_status qfb_nccl_comm_init_rank(void** comm, int nranks, const void* id, int rank,
+                                   int device);
 qfb_status qfb_nccl_comm_destroy(void* comm);
 /* In-place ncclAllReduce(sum) of n DEVICE doubles on the context stream  */
 /* (the cheap exchange; its bits depend on the GPU count).                */
@@ -469,6 +490,19 @@ qfb_status qfb_adam_bias_corrections(double beta1, double beta2, int64_t t,
 qfb_status qfb_adam_step(qfb_ctx* ctx, double* params, double* m, double* v,
                          const double* grads, int64_t n, double beta1, double beta2,
                          double lr, double eps, double bc1, double bc2, uint32_t* skipped);
+/* Graph-replayable Adam: the step counter lives on the DEVICE.           */
+/* counters (DEVICE int64[3]) = {non-skipped steps, skipped steps,        */
+/* table overflow}; t = counters[0] + 1 (distill.hpp:262-264); bc1/bc2 =  */
+/* bias_table[2(t-1)], [2(t-1)+1] (DEVICE, from qfb_adam_bias_table: the  */
+/* host libm pow, like the reference). The update is skipped (counters[1] */
+/* += 1) when a gradient or one of the n_loss loss values is non-finite   */
+/* (distill.hpp:254-258) or t > t_max; flag (DEVICE u32) = the count.     */
+qfb_status qfb_adam_bias_table(double beta1, double beta2, int64_t t_max, double* table);
+qfb_status qfb_adam_step_dev(qfb_ctx* ctx, double* params, double* m, double* v,
+                             const double* grads, int64_t n, double beta1, double beta2,
+                             double lr, double eps, const double* bias_table, int64_t t_max,
+                             int64_t* counters, const double* loss, int64_t n_loss,
+                             uint32_t* flag);
 
 /* ---------------------------------------------------------------------- */
 /* On-disk formats (host only, no GPU needed) — SURVEY.md §8 f4.           */

@@ -108,23 +108,35 @@ struct qfb_ctx {
     const double* grad_base = nullptr;  // the pinned double block
   } slots[2];
   DevBuf train_ws[4];      // scratch of the trainer ops (qfb_train.cu)
+  // buffers replaced by grow(): a captured graph may still reference them
+  std::vector<void*> retired;
+  // status word the forward kernels latch into: d_status, or a host-pass
+  // slot's own word while that slot's kernels are enqueued
+  uint32_t* cur_status = nullptr;
 };
 
 namespace {
 
+// Grow a workspace buffer. The old buffer is NOT freed: a CUDA graph
+// captured earlier may hold its address (baked into a __grid_constant__
+// descriptor), so it is retired and freed only by qfb_ctx_destroy (growth
+// is geometric, so the retired total stays below the live size). Growth
+// during a stream capture is refused: cudaMalloc is not capturable, and the
+// caller must size the context first (an eager call, or *_reserve).
 qfb_status grow(qfb_ctx* ctx, DevBuf& b, size_t bytes, bool zero) {
   if (b.bytes >= bytes) return QFB_OK;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(ctx->stream, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone)
+    return fail(QFB_ERR_UNSUPPORTED,
+                "workspace must grow to %zu bytes during a stream capture: run the call once eagerly "
+                "(or qfb_fq_bwd_reserve) before capturing", bytes);
   size_t nb = std::max(bytes, b.bytes * 2);
   nb = (nb + 255) & ~size_t(255);
-  if (b.p) {
-    // In-flight kernels may still read the old buffer.
-    QFB_CUDA(cudaStreamSynchronize(ctx->stream));
-    QFB_CUDA(cudaFree(b.p));
-    b.p = nullptr;
-    b.bytes = 0;
-  }
-  QFB_CUDA(cudaMalloc(&b.p, nb));
-  if (zero) QFB_CUDA(cudaMemsetAsync(b.p, 0, nb, ctx->stream));
+  void* np = nullptr;
+  QFB_CUDA(cudaMalloc(&np, nb));
+  if (zero) QFB_CUDA(cudaMemsetAsync(np, 0, nb, ctx->stream));
+  if (b.p) ctx->retired.push_back(b.p);
+  b.p = np;
   b.bytes = nb;
   return QFB_OK;
 }
@@ -321,12 +333,12 @@ qfb_status run_ew(qfb_ctx* ctx, int dtype, const std::vector<EwDesc>& descs, boo
     cudaError_t e;
     if (all_vec) {
       const int grid = (int)std::min<uint64_t>(chunks, (uint64_t)ctx->sm_count * tma_per_sm);
-      e = launch_ew_tma(dtype, chain, stages, b, ctx->d_status, grid, ctx->stream,
+      e = launch_ew_tma(dtype, chain, stages, b, ctx->cur_status, grid, ctx->stream,
                         chunks < 4ull * (uint64_t)grid);
     } else {
       const int grid = (int)std::min<uint64_t>(
           chunks, (uint64_t)ctx->sm_count * ctx->ew_blocks_per_sm[dtype][chain ? 1 : 0]);
-      e = launch_ew(dtype, chain, b, ctx->d_status, grid, ctx->stream);
+      e = launch_ew(dtype, chain, b, ctx->cur_status, grid, ctx->stream);
     }
     if (e != cudaSuccess) return cuda_fail(e, "ew_kernel launch");
     ctx->launches++;
@@ -490,9 +502,11 @@ qfb_status qfb_ctx_create(int32_t device, void* stream, qfb_ctx** out) {
       if (v >= kTmaStagesMin && v <= kTmaStagesMax) c->tma_stages_env = v;
     }
   }
-  if (e == cudaSuccess) e = cudaMalloc(&c->d_status, sizeof(uint32_t));
+  // status words: [0] the context's, [1 + k] host-pass slot k's own
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_status, 3 * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMallocHost(&c->h_status, sizeof(uint32_t));
-  if (e == cudaSuccess) e = cudaMemsetAsync(c->d_status, 0, sizeof(uint32_t), c->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(c->d_status, 0, 3 * sizeof(uint32_t), c->stream);
+  c->cur_status = c->d_status;
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) {
     qfb_ctx_destroy(c);
@@ -513,6 +527,7 @@ qfb_status qfb_ctx_destroy(qfb_ctx* ctx) {
   if (ctx->h_status) cudaFreeHost(ctx->h_status);
   if (ctx->ws_f64.p) cudaFree(ctx->ws_f64.p);
   if (ctx->ws_u32.p) cudaFree(ctx->ws_u32.p);
+  for (void* p : ctx->retired) cudaFree(p);
   for (auto& b : ctx->host_io)
     if (b.p) cudaFree(b.p);
   for (auto& b : ctx->train_ws)
@@ -694,7 +709,7 @@ qfb_status qfb_fq_fwd_perop(qfb_ctx* ctx, qfb_dtype dtype, const void* x, void* 
   for (int op = 0; op < 4; ++op) {
     PerOpDesc d{ins[op], outs[op], scale, n, (uint64_t)inner, (uint64_t)channels, q,
                 flags & kEwHalfGrid};
-    cudaError_t e = launch_perop(dtype, op, d, ctx->d_status, std::max(grid, 1), ctx->stream);
+    cudaError_t e = launch_perop(dtype, op, d, ctx->cur_status, std::max(grid, 1), ctx->stream);
     if (e != cudaSuccess) return cuda_fail(e, "perop_kernel launch");
     ctx->launches++;
   }
@@ -727,7 +742,7 @@ qfb_status qfb_resolve_scales_dev(qfb_ctx* ctx, const double* log_s, int64_t n,
   if (n == 0) return QFB_OK;
   ResolveDesc d{log_s, s32, s64, chain, n, lower_for(cfg, prec), cfg->s_max, cfg->eps};
   DeviceGuard g(ctx->device);
-  cudaError_t e = launch_resolve(d, ctx->d_status, ctx->stream);
+  cudaError_t e = launch_resolve(d, ctx->cur_status, ctx->stream);
   if (e != cudaSuccess) return cuda_fail(e, "resolve launch");
   ctx->launches++;
   return QFB_OK;
@@ -771,7 +786,11 @@ qfb_status plan_bwd(const qfb_bwd_desc& t, BwdPlan& p, int dtype_of_plan) {
   d.depth = leaf_depth((uint64_t)t.inner);
   d.g = std::min<uint32_t>(d.depth, (uint32_t)kBwdGroupsLog);
   d.tps_log = d.depth - d.g;
-  d.accumulate = t.accumulate ? 1 : 0;
+  if (t.accumulate < 0 || t.accumulate > QFB_BWD_ROWS)
+    return fail(QFB_ERR_VALUE, "fake_quantize_backward: accumulate must be 0, 1 or QFB_BWD_ROWS");
+  if (t.row_stride < 0) return fail(QFB_ERR_VALUE, "fake_quantize_backward: negative row_stride");
+  d.accumulate = t.accumulate;
+  d.row_stride = t.row_stride > 0 ? (uint64_t)t.row_stride : (uint64_t)t.channels;
   d.q = (double)t.q_max;
   d.vec = (aligned16(t.x) && aligned16(t.up) && (!t.dx || aligned16(t.dx))) ? 1u : 0u;
   d.total_bytes = (uint64_t)t.outer * (uint64_t)t.channels * (uint64_t)t.inner *
@@ -785,6 +804,32 @@ qfb_status plan_bwd(const qfb_bwd_desc& t, BwdPlan& p, int dtype_of_plan) {
 }
 
 }  // namespace
+
+qfb_status qfb_fq_bwd_reserve(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc* table, int32_t n) {
+  if (qfb_status st = check_ctx(ctx)) return st;
+  if (qfb_status st = check_dtype(dtype)) return st;
+  if (n < 0 || (n > 0 && !table)) return fail(QFB_ERR_VALUE, "fq_bwd_reserve: bad table");
+  size_t need = 1, f64 = 0;
+  int32_t cnt = 0;
+  uint64_t tiles = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    BwdPlan p;
+    if (qfb_status st = plan_bwd(table[i], p, dtype)) return st;
+    // the same batching as qfb_fq_bwd_multi: the largest batch sizes it
+    if (cnt == kMaxBwdDesc || (cnt > 0 && tiles + p.tiles >= (1ull << 31))) {
+      need = std::max(need, f64);
+      f64 = 0;
+      cnt = 0;
+      tiles = 0;
+    }
+    f64 += p.f64_need;
+    tiles += p.tiles;
+    ++cnt;
+  }
+  need = std::max(need, f64);
+  DeviceGuard g(ctx->device);
+  return grow(ctx, ctx->ws_f64, need * 8, false);
+}
 
 qfb_status qfb_fq_bwd_multi(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc* table, int32_t n) {
   if (qfb_status st = check_ctx(ctx)) return st;
@@ -854,7 +899,7 @@ qfb_status qfb_fq_bwd_multi(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc* t
 qfb_status qfb_fq_bwd(qfb_ctx* ctx, qfb_dtype dtype, const void* x, const void* up, void* dx,
                       int64_t outer, int64_t channels, int64_t inner, const double* scale64,
                       const double* chain, int32_t q_max, double* d_log_s, int32_t accumulate) {
-  qfb_bwd_desc t{x, up, dx, scale64, chain, d_log_s, outer, channels, inner, q_max, accumulate};
+  qfb_bwd_desc t{x, up, dx, scale64, chain, d_log_s, outer, channels, inner, q_max, accumulate, 0};
   return qfb_fq_bwd_multi(ctx, dtype, &t, 1);
 }
 
@@ -1091,6 +1136,16 @@ qfb_status qfb_quant_pass_host_submit(qfb_ctx* ctx, qfb_precision prec, const qf
     return v > 0 ? v : 1;  // measured: 1 point per group is best (7.40 ms/frame vs 7.42, 7.73 for 2, 3)
   }();
   const uint32_t flags = prec == QFB_PREC_HALF ? QFB_FLAG_HALF_GRID : 0u;
+  // this slot's kernels latch non-finite results into the slot's own status
+  // word (restored on every exit), copied down and cleared on s_out below,
+  // so a non-finite value is reported by this slot's wait and no other's
+  uint32_t* const slot_status = ctx->d_status + 1 + slot;
+  struct StatusScope {
+    qfb_ctx* c;
+    uint32_t* prev;
+    ~StatusScope() { c->cur_status = prev; }
+  } status_scope{ctx, ctx->cur_status};
+  ctx->cur_status = slot_status;
   std::vector<void*> cdst, csrc;
   std::vector<size_t> csz;
   for (int32_t g0 = 0; g0 < n; g0 += group_pts) {
@@ -1140,7 +1195,7 @@ qfb_status qfb_quant_pass_host_submit(qfb_ctx* ctx, qfb_precision prec, const qf
         if (!p.log_s[k]) continue;
         const double* f = dD + doff[i] + (size_t)k * 3 * p.channels;
         bd[nb] = qfb_bwd_desc{B[0].p, B[1 + k].p, p.dx[k] ? B[5 + k].p : nullptr, f, f + p.channels,
-                              const_cast<double*>(f + 2 * p.channels), p.outer, p.channels, p.inner, q, 0};
+                              const_cast<double*>(f + 2 * p.channels), p.outer, p.channels, p.inner, q, 0, 0};
         ++nb;
       }
       if (nb)
@@ -1172,7 +1227,8 @@ qfb_status qfb_quant_pass_host_submit(qfb_ctx* ctx, qfb_precision prec, const qf
   // the status word of this pass's kernels rides down with the gradients
   QFB_CUDA(cudaEventRecord(sl.ev[2 * n], ctx->stream));
   QFB_CUDA(cudaStreamWaitEvent(ctx->s_out, sl.ev[2 * n], 0));
-  QFB_CUDA(cudaMemcpyAsync(sl.h_status, ctx->d_status, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->s_out));
+  QFB_CUDA(cudaMemcpyAsync(sl.h_status, slot_status, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->s_out));
+  QFB_CUDA(cudaMemsetAsync(slot_status, 0, sizeof(uint32_t), ctx->s_out));
   QFB_CUDA(cudaEventRecord(sl.done, ctx->s_out));
   for (int32_t i = 0; i < n; ++i) {
     const qfb_host_point& p = pts[i];
@@ -1204,11 +1260,10 @@ qfb_status qfb_quant_pass_host_wait(qfb_ctx* ctx, int32_t slot) {
   QFB_CUDA(cudaEventSynchronize(sl.done));
   for (size_t i = 0; i < sl.grads.size(); ++i)
     std::memcpy(sl.grads[i].first, sl.grad_base + sl.grads[i].second, (size_t)sl.grad_len[i] * sizeof(double));
-  if (*sl.h_status != 0) {
-    QFB_CUDA(cudaMemsetAsync(ctx->d_status, 0, sizeof(uint32_t), ctx->stream));
-    QFB_CUDA(cudaStreamSynchronize(ctx->stream));
-    return fail(QFB_ERR_NONFINITE, "demote_half: non-finite value on the binary16 path");
-  }
+  // the slot's word was cleared on s_out after its copy (ordered before
+  // `done`), so nothing is left to reset here
+  if (*sl.h_status != 0)
+    return fail(QFB_ERR_NONFINITE, "demote_half: non-finite value on the binary16 path (slot %d)", slot);
   return QFB_OK;
 }
 

@@ -638,6 +638,10 @@ __global__ void __launch_bounds__(kBwdCtaThreads, 3) bwd_kernel(const __grid_con
              : (d.dx != nullptr && !(V & kProbeNoLoads)) ? group_sum_any<T, true>(sx, su, glen, dc, q)
                                                           : group_sum_any<T, false>(sx, su, glen, dc, q);
     red[2 * s + par][tid] = v;  // the producer runs the tile's tree reduction
+    // d_input was written into the stage with generic stores and leaves it
+    // through a TMA bulk store (async proxy): every writing thread orders
+    // its stores before the handoff (the TMA-store pattern)
+    fence_proxy_async_smem();
     __syncwarp();     // the warp's d_input and group sums are written
     if (lane == 0) mbar_arrive(&done[s]);
     s = s + 1 == nst ? 0 : s + 1;
@@ -693,11 +697,17 @@ __global__ void __launch_bounds__(32) bwd_finish_kernel(const __grid_constant__ 
     }
     for (uint32_t off = 1; off < lanes; off <<= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
     const double r = __dmul_rn(v, chain);
-    // accumulate == 0: ((r0 + r1) + ...); else ((d_log_s + r0) + r1) + ...
-    if (o == 0) acc = d.accumulate ? __dadd_rn(d.d_log_s[c], r) : r;
-    else acc = __dadd_rn(acc, r);
+    // accumulate == 0: ((r0 + r1) + ...); 1: ((d_log_s + r0) + r1) + ...;
+    // QFB_BWD_ROWS: every row's r stored on its own
+    if (d.accumulate == 2) {
+      if (lane == 0) d.d_log_s[(uint64_t)o * d.row_stride + c] = r;
+    } else if (o == 0) {
+      acc = d.accumulate ? __dadd_rn(d.d_log_s[c], r) : r;
+    } else {
+      acc = __dadd_rn(acc, r);
+    }
   }
-  if (lane == 0) d.d_log_s[c] = acc;
+  if (lane == 0 && d.accumulate != 2) d.d_log_s[c] = acc;
   (void)warp_base_mul;
 }
 
@@ -750,7 +760,8 @@ __global__ void __launch_bounds__(32) bwd_finish_reg_kernel(const __grid_constan
   pdl_trigger();
   pdl_wait();
   const double chain = d.chain[c];
-  double acc = d.accumulate ? d.d_log_s[c] : 0.0;
+  const bool rows = d.accumulate == 2;
+  double acc = d.accumulate == 1 ? d.d_log_s[c] : 0.0;
   for (uint32_t o = 0; o < d.outer; o += kFinRows) {
     double v[kFinRows];
 #pragma unroll
@@ -765,12 +776,17 @@ __global__ void __launch_bounds__(32) bwd_finish_reg_kernel(const __grid_constan
         v[j] = __dadd_rn(v[j], __shfl_xor_sync(0xffffffffu, v[j], off));
       if (o + j < d.outer) {
         const double r = __dmul_rn(v[j], chain);
-        // accumulate == 0: ((r0 + r1) + ...); else ((d_log_s + r0) + r1) + ...
-        acc = (o + j == 0 && !d.accumulate) ? r : __dadd_rn(acc, r);
+        // accumulate == 0: ((r0 + r1) + ...); 1: ((d_log_s + r0) + r1) + ...;
+        // QFB_BWD_ROWS: every row's r stored on its own
+        if (rows) {
+          if (lane == 0) d.d_log_s[(uint64_t)(o + j) * d.row_stride + c] = r;
+        } else {
+          acc = (o + j == 0 && d.accumulate == 0) ? r : __dadd_rn(acc, r);
+        }
       }
     }
   }
-  if (lane == 0) d.d_log_s[c] = acc;
+  if (lane == 0 && !rows) d.d_log_s[c] = acc;
 }
 
 }  // namespace

@@ -171,11 +171,12 @@ struct BwdDesc {
   uint32_t tps_log;  // tiles per segment = 2^(depth - g)
   uint32_t depth;    // tree depth of the 16-bounded leaf groups
   uint32_t g;        // tile depth = min(depth, kBwdGroupsLog)
-  int32_t accumulate;
+  int32_t accumulate;  // 0 fold, 1 fold into d_log_s, 2 (QFB_BWD_ROWS) one value per row
   double q;
   uint32_t vec;  // x/up/dx 16-byte aligned: TMA bulk staging
   uint32_t pad;
   uint64_t total_bytes;  // outer * chans * inner * sizeof(T)
+  uint64_t row_stride;   // QFB_BWD_ROWS: d_log_s[o * row_stride + c]
 };
 
 struct BwdBatch {

@@ -16,6 +16,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <cstring>
 #include <mutex>
 #include <string>
 
@@ -30,6 +31,8 @@ struct Nccl {
   ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                              cudaStream_t) = nullptr;
   ncclResult_t (*init_all)(ncclComm_t*, int, const int*) = nullptr;
+  ncclResult_t (*get_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*destroy)(ncclComm_t) = nullptr;
   ncclResult_t (*count)(const ncclComm_t, int*) = nullptr;
   const char* (*err_str)(ncclResult_t) = nullptr;
@@ -56,9 +59,12 @@ const Nccl& nccl() {
     n.all_reduce = reinterpret_cast<decltype(n.all_reduce)>(dlsym(n.h, "ncclAllReduce"));
     n.init_all = reinterpret_cast<decltype(n.init_all)>(dlsym(n.h, "ncclCommInitAll"));
     n.destroy = reinterpret_cast<decltype(n.destroy)>(dlsym(n.h, "ncclCommDestroy"));
+    n.get_id = reinterpret_cast<decltype(n.get_id)>(dlsym(n.h, "ncclGetUniqueId"));
+    n.init_rank = reinterpret_cast<decltype(n.init_rank)>(dlsym(n.h, "ncclCommInitRank"));
     n.count = reinterpret_cast<decltype(n.count)>(dlsym(n.h, "ncclCommCount"));
     n.err_str = reinterpret_cast<decltype(n.err_str)>(dlsym(n.h, "ncclGetErrorString"));
-    if (!n.all_gather || !n.all_reduce || !n.init_all || !n.destroy || !n.count || !n.err_str)
+    if (!n.all_gather || !n.all_reduce || !n.init_all || !n.destroy || !n.count || !n.err_str || !n.get_id ||
+        !n.init_rank)
       n.why = "NCCL library lacks a required symbol";
   });
   return n;
@@ -86,6 +92,31 @@ qfb_status qfb_nccl_comm_init_all(int ndev, const int* devices, void** comms) {
   if (qfb_status s = nccl_ready()) return s;
   ncclResult_t r = nccl().init_all(reinterpret_cast<ncclComm_t*>(comms), ndev, devices);
   if (r != ncclSuccess) return nccl_fail(r, "ncclCommInitAll");
+  return QFB_OK;
+}
+
+static_assert(sizeof(ncclUniqueId) == QFB_NCCL_UNIQUE_ID_BYTES, "ncclUniqueId size");
+
+qfb_status qfb_nccl_get_unique_id(void* id) {
+  if (!id) return qfb::set_error(QFB_ERR_VALUE, "nccl_get_unique_id: null buffer");
+  if (qfb_status s = nccl_ready()) return s;
+  ncclResult_t r = nccl().get_id(static_cast<ncclUniqueId*>(id));
+  if (r != ncclSuccess) return nccl_fail(r, "ncclGetUniqueId");
+  return QFB_OK;
+}
+
+qfb_status qfb_nccl_comm_init_rank(void** comm, int nranks, const void* id, int rank, int device) {
+  if (!comm || !id || nranks < 1 || rank < 0 || rank >= nranks)
+    return qfb::set_error(QFB_ERR_VALUE, "nccl_comm_init_rank: bad arguments");
+  if (qfb_status s = nccl_ready()) return s;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  if (cudaSetDevice(device) != cudaSuccess) return qfb::set_error(QFB_ERR_CUDA, "nccl_comm_init_rank: bad device");
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, sizeof uid);
+  ncclResult_t r = nccl().init_rank(reinterpret_cast<ncclComm_t*>(comm), nranks, uid, rank);
+  if (prev >= 0) cudaSetDevice(prev);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclCommInitRank");
   return QFB_OK;
 }
 

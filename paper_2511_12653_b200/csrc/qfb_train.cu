@@ -322,6 +322,50 @@ __global__ void adam_kernel(double* __restrict__ p, double* __restrict__ m, doub
   }
 }
 
+// Device-stepped Adam for CUDA-graph replays: t = (non-skipped steps so
+// far) + 1 read from counters[0] (distill.hpp:262-264: t = step - skipped),
+// the bias corrections taken from a host-computed table (the host libm pow,
+// bit-identical to the reference's), the skip decided from the gradient and
+// loss non-finite counts in flag[0]. counters[1] counts skipped steps; a
+// step beyond the table is skipped and latched in counters[2].
+__global__ void nonfinite2_kernel(const double* __restrict__ g, int64_t n, const double* __restrict__ loss,
+                                  int64_t n_loss, uint32_t* flag) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n + n_loss; i += stride) {
+    const double v = i < n ? g[i] : loss[i - n];
+    if (!isfinite(v)) atomicAdd(flag, 1u);
+  }
+}
+
+__global__ void adam_dev_kernel(double* __restrict__ p, double* __restrict__ m, double* __restrict__ v,
+                                const double* __restrict__ g, int64_t n, double b1, double b2, double lr,
+                                double eps, const double* __restrict__ bc, int64_t t_max,
+                                const int64_t* __restrict__ counters, const uint32_t* flag) {
+  const int64_t t = counters[0] + 1;
+  if (*flag != 0 || t > t_max) return;
+  const double bc1 = bc[2 * (t - 1)], bc2 = bc[2 * (t - 1) + 1];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double gi = g[i];
+    const double mk = __dadd_rn(__dmul_rn(b1, m[i]), __dmul_rn(__dadd_rn(1.0, -b1), gi));
+    const double vk = __dadd_rn(__dmul_rn(b2, v[i]), __dmul_rn(__dmul_rn(__dadd_rn(1.0, -b2), gi), gi));
+    m[i] = mk;
+    v[i] = vk;
+    const double mhat = __ddiv_rn(mk, bc1);
+    const double vhat = __ddiv_rn(vk, bc2);
+    p[i] = __dadd_rn(p[i], -__ddiv_rn(__dmul_rn(lr, mhat), __dadd_rn(__dsqrt_rn(vhat), eps)));
+  }
+}
+
+__global__ void adam_advance_kernel(int64_t* counters, int64_t t_max, const uint32_t* flag) {
+  const bool over = counters[0] + 1 > t_max;
+  if (*flag != 0 || over) {
+    counters[1] += 1;
+    if (over) counters[2] = 1;
+  } else {
+    counters[0] += 1;
+  }
+}
+
 // Row-order fold of per-frame gradient rows (the multi-GPU exchange's
 // combine step): out[j] = ((into[j] + r0[j]) + r1[j]) + ..., one thread per
 // column, so the bits equal the single-process frame-order accumulation.
@@ -492,6 +536,39 @@ qfb_status qfb_adam_step(qfb_ctx* ctx, double* params, double* m, double* v, con
     e = cudaGetLastError();
   }
   if (e != cudaSuccess) return cuda_error(e, "adam_step");
+  return QFB_OK;
+}
+
+qfb_status qfb_adam_bias_table(double beta1, double beta2, int64_t t_max, double* table) {
+  if (!table || t_max < 1) return err(QFB_ERR_VALUE, "adam_bias_table: bad arguments");
+  for (int64_t t = 1; t <= t_max; ++t)
+    if (qfb_status s = qfb_adam_bias_corrections(beta1, beta2, t, table + 2 * (t - 1), table + 2 * (t - 1) + 1))
+      return s;
+  return QFB_OK;
+}
+
+qfb_status qfb_adam_step_dev(qfb_ctx* ctx, double* params, double* m, double* v, const double* grads,
+                             int64_t n, double beta1, double beta2, double lr, double eps,
+                             const double* bias_table, int64_t t_max, int64_t* counters,
+                             const double* loss, int64_t n_loss, uint32_t* flag) {
+  if (!ctx) return err(QFB_ERR_VALUE, "null qfb_ctx");
+  if (n < 0 || (n > 0 && (!params || !m || !v || !grads)) || !flag || !counters || !bias_table ||
+      t_max < 1 || n_loss < 0 || (n_loss > 0 && !loss))
+    return err(QFB_ERR_VALUE, "adam_step_dev: bad arguments");
+  Guard g(ctx_device(ctx));
+  const cudaStream_t st = ctx_stream(ctx);
+  cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(uint32_t), st);
+  const int64_t work = n + n_loss;
+  const int blocks = (int)((work + 255) / 256 > 1024 ? 1024 : ((work + 255) / 256 > 0 ? (work + 255) / 256 : 1));
+  if (e == cudaSuccess) {
+    nonfinite2_kernel<<<blocks, 256, 0, st>>>(grads, n, loss, n_loss, flag);
+    adam_dev_kernel<<<blocks, 256, 0, st>>>(params, m, v, grads, n, beta1, beta2, lr, eps, bias_table, t_max,
+                                            counters, flag);
+    adam_advance_kernel<<<1, 1, 0, st>>>(counters, t_max, flag);
+    ctx_count_launches(ctx, 3);
+    e = cudaGetLastError();
+  }
+  if (e != cudaSuccess) return cuda_error(e, "adam_step_dev");
   return QFB_OK;
 }
 

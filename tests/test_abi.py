@@ -12,6 +12,7 @@ import ctypes
 import os
 import re
 import subprocess
+import sys
 
 import numpy as np
 import pytest
@@ -210,3 +211,37 @@ int main(void) {
     r = subprocess.run([str(exe)], capture_output=True, text=True)
     assert r.returncode == 0, (r.returncode, r.stdout, r.stderr)
     assert r.stdout.startswith("ok ")
+
+
+def test_reference_arm_maps_no_product_library():
+    """bench.py --impl reference times the reference's own code only: the
+    process maps oracle/_ref/libqfref.so and NOT libqfb.so (the package's
+    binding loads lazily; the arm imports only the pure-Python shapes), and
+    its `config` is the GPU arm's (the same bench_config function)."""
+    import json
+    import oracle
+    if not oracle.reference_available():
+        pytest.skip("reference build absent")
+    code = r"""
+import io, json, sys, contextlib, runpy
+sys.argv = ["bench.py", "--impl", "reference", "--steps", "1", "--warmup", "0", "--no-single-thread"]
+buf = io.StringIO()
+with contextlib.redirect_stdout(buf):
+    try:
+        runpy.run_path("bench.py", run_name="__main__")
+    except SystemExit:
+        pass
+maps = open("/proc/self/maps").read()
+line = [l for l in buf.getvalue().splitlines() if l.startswith("{")][-1]
+print(json.dumps({"line": json.loads(line), "qfb": "libqfb.so" in maps, "ref": "libqfref.so" in maps}))
+"""
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    assert d["ref"] and not d["qfb"]
+    assert d["line"]["impl"] == "reference"
+    sys.path.insert(0, ROOT)
+    import bench
+    args = bench.parse_args_list(["--steps", "1", "--warmup", "0"])
+    assert d["line"]["config"] == bench.bench_config(args, 1)
+    assert d["line"]["data"] == bench.DATA
