@@ -67,6 +67,8 @@ class Oracle:
         cfgp = ctypes.POINTER(OrcCfg)
         L.orc_softplus.restype = _dbl
         L.orc_softplus.argtypes = [_dbl]
+        L.orc_fq_backward_s.restype = _i32
+        L.orc_fq_backward_s.argtypes = [_f32p, _f32p, _vp, _i64, _i64, _i64, _f64p, _f64p, _dbl, _f64p]
         L.orc_sigmoid.restype = _dbl
         L.orc_sigmoid.argtypes = [_dbl]
         L.orc_softplus_inv.restype = _i32
@@ -169,6 +171,17 @@ class Oracle:
                else np.array(d_log_s, dtype=np.float64).ravel().copy())
         st = self.L.orc_fq_backward(x, up, _ptr_or_null(dx), outer, channels, inner, log_s,
                                     ctypes.byref(cfg or default_cfg()), half, dls, accumulate)
+        return st, dx, dls
+
+    def fq_backward_s(self, x, up, s, chain, outer, channels, inner, q=127.0, want_dx=True):
+        """fq_backward with the resolved scales and chain factors given."""
+        x = np.ascontiguousarray(x, dtype=np.float32).ravel()
+        up = np.ascontiguousarray(up, dtype=np.float32).ravel()
+        s = np.ascontiguousarray(s, dtype=np.float64).ravel()
+        chain = np.ascontiguousarray(chain, dtype=np.float64).ravel()
+        dx = np.empty_like(x) if want_dx else None
+        dls = np.zeros(channels, dtype=np.float64)
+        st = self.L.orc_fq_backward_s(x, up, _ptr_or_null(dx), outer, channels, inner, s, chain, float(q), dls)
         return st, dx, dls
 
     def fq_chain(self, a, b, scales, outer, channels, inner, act=1, half=0, preact=False, cfg=None):

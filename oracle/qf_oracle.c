@@ -317,6 +317,33 @@ int orc_fq_backward(const float* x, const float* up, float* dx, int64_t outer,
   return ORC_OK;
 }
 
+/* The same with the per-channel scale and chain factor given directly
+ * (quant.hpp:281-292 after resolve_scale): reaches scales no log scale
+ * resolves to (e.g. below 2^-100, the device's exact slow path). */
+int orc_fq_backward_s(const float* x, const float* up, float* dx, int64_t outer,
+                      int64_t channels, int64_t inner, const double* s,
+                      const double* chain, double q, double* d_log_s) {
+  double* terms = (double*)malloc(sizeof(double) * (size_t)(inner > 0 ? inner : 1));
+  if (!terms) return ORC_VALUE;
+  for (int64_t ch = 0; ch < channels; ++ch) {
+    double acc = 0.0;
+    for (int64_t o = 0; o < outer; ++o) {
+      const int64_t base = (o * channels + ch) * inner;
+      for (int64_t i = 0; i < inner; ++i) {
+        double mask, d_ds;
+        grad_terms((double)x[base + i], s[ch], q, &mask, &d_ds);
+        if (dx) dx[base + i] = (float)(mask * (double)up[base + i]);
+        terms[i] = d_ds * (double)up[base + i];
+      }
+      const double r = orc_pairwise_sum(terms, inner) * chain[ch];
+      acc = (o == 0) ? r : acc + r;
+    }
+    if (outer > 0) d_log_s[ch] = acc;
+  }
+  free(terms);
+  return ORC_OK;
+}
+
 float orc_gelu(float x) { return qfb_p_gelu(x); }
 
 /* exec.hpp:438-451: v = maybe_half(act(add(a, b))) feeding the fused

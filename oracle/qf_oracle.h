@@ -75,6 +75,9 @@ int orc_int8_codes(const float* x, int8_t* codes, int64_t outer,
 int orc_fq_backward(const float* x, const float* up, float* dx, int64_t outer,
                     int64_t channels, int64_t inner, const double* log_s,
                     const orc_cfg* c, int half, double* d_log_s, int accumulate);
+int orc_fq_backward_s(const float* x, const float* up, float* dx, int64_t outer,
+                      int64_t channels, int64_t inner, const double* s,
+                      const double* chain, double q, double* d_log_s);
 
 /* Fused chain (exec.hpp:438-451 + :353-361). act: 0 none, 1 relu, 2 gelu.
  * s0/s1: double scales (cast to float), NULL when unused. */

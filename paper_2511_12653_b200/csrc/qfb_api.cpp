@@ -110,6 +110,19 @@ struct qfb_ctx {
   DevBuf train_ws[4];      // scratch of the trainer ops (qfb_train.cu)
   // buffers replaced by grow(): a captured graph may still reference them
   std::vector<void*> retired;
+  // streaming backward: per row length, the device table of per-chunk block
+  // metadata (kSbMetaWords u32 per chunk of a row); never freed before
+  // qfb_ctx_destroy (captured graphs hold the pointers)
+  struct SbShape {
+    uint32_t* meta = nullptr;
+    uint32_t nch = 0;
+  };
+  std::vector<std::pair<uint64_t, SbShape>> sb_shapes;
+  int sb_blocks_per_sm[2] = {0, 0};
+  // backward kernel (QFB_BWD_IMPL at creation): 0 tile kernel with
+  // consumer-side partials (default), 1 tile kernel as in round 1 ("tile1"),
+  // 2 streaming kernel ("stream")
+  int bwd_impl = 0;
   // status word the forward kernels latch into: d_status, or a host-pass
   // slot's own word while that slot's kernels are enqueued
   uint32_t* cur_status = nullptr;
@@ -207,6 +220,17 @@ qfb_status check_dtype(int dtype) {
 
 int elem_size(int dtype) { return dtype == QFB_F32 ? 4 : 2; }
 int per_vec(int dtype) { return dtype == QFB_F32 ? 4 : 8; }
+
+// Streaming-backward ring depth (QFB_SB_STAGES = 2..4 overrides).
+int sb_stages(int dtype) {
+  static const int env = [] {
+    const char* e = getenv("QFB_SB_STAGES");
+    const int v = e ? atoi(e) : 0;
+    return v >= 2 && v <= 4 ? v : 0;
+  }();
+  (void)dtype;
+  return env ? env : 4;
+}
 
 constexpr uint64_t kMaxUnits = 1ull << 31;
 
@@ -495,6 +519,12 @@ qfb_status qfb_ctx_create(int32_t device, void* stream, qfb_ctx** out) {
             c->tma_blocks_per_sm[dt][ch][ns] = per;
         }
     }
+    for (int dt = 0; dt < 2; ++dt) {
+      int per = 0;
+      if (sbwd_occupancy(dt, sb_stages(dt), &per) == cudaSuccess && per > 0) c->sb_blocks_per_sm[dt] = per;
+    }
+    if (const char* env = getenv("QFB_BWD_IMPL"))
+      c->bwd_impl = std::strcmp(env, "stream") == 0 ? 2 : std::strcmp(env, "tile1") == 0 ? 1 : 0;
     if (const char* env = getenv("QFB_DISABLE_TMA_FWD"))
       if (env[0] == '1') std::memset(c->tma_blocks_per_sm, 0, sizeof c->tma_blocks_per_sm);
     if (const char* env = getenv("QFB_FWD_STAGES")) {
@@ -528,6 +558,7 @@ qfb_status qfb_ctx_destroy(qfb_ctx* ctx) {
   if (ctx->ws_f64.p) cudaFree(ctx->ws_f64.p);
   if (ctx->ws_u32.p) cudaFree(ctx->ws_u32.p);
   for (void* p : ctx->retired) cudaFree(p);
+  for (auto& kv : ctx->sb_shapes) cudaFree(kv.second.meta);
   for (auto& b : ctx->host_io)
     if (b.p) cudaFree(b.p);
   for (auto& b : ctx->train_ws)
@@ -786,6 +817,7 @@ qfb_status plan_bwd(const qfb_bwd_desc& t, BwdPlan& p, int dtype_of_plan) {
   d.depth = leaf_depth((uint64_t)t.inner);
   d.g = std::min<uint32_t>(d.depth, (uint32_t)kBwdGroupsLog);
   d.tps_log = d.depth - d.g;
+  d.part_log = d.tps_log;
   if (t.accumulate < 0 || t.accumulate > QFB_BWD_ROWS)
     return fail(QFB_ERR_VALUE, "fake_quantize_backward: accumulate must be 0, 1 or QFB_BWD_ROWS");
   if (t.row_stride < 0) return fail(QFB_ERR_VALUE, "fake_quantize_backward: negative row_stride");
@@ -805,6 +837,136 @@ qfb_status plan_bwd(const qfb_bwd_desc& t, BwdPlan& p, int dtype_of_plan) {
 
 }  // namespace
 
+namespace {
+
+// ---- streaming backward planning (sbwd_kernel, qfb_bwd.cu) ----
+// Eligible: 16-byte aligned x / up / dx, rows that are 16-byte multiples of
+// at least one chunk and below 2^28 elements. QFB_BWD_IMPL=tile (read at
+// context creation) forces the tile kernel.
+
+bool sb_eligible(const BwdPlan& p, int dtype) {
+  const uint64_t es = (uint64_t)elem_size(dtype);
+  return p.d.vec && (p.d.inner * es) % 16 == 0 && p.d.inner >= (uint64_t)kSbChunk &&
+         p.d.inner < (1ull << 28) && p.d.depth >= (uint32_t)kSbBlockLog;
+}
+
+// Block starts of a row of n elements at depth L of the reference's split
+// (tensor.hpp:100-109: left child floor(m/2)); lo[2^L] = n.
+std::vector<uint32_t> tree_starts(uint64_t n, uint32_t L) {
+  std::vector<uint64_t> lo{0}, m{n};
+  for (uint32_t l = 0; l < L; ++l) {
+    std::vector<uint64_t> lo2, m2;
+    lo2.reserve(lo.size() * 2);
+    m2.reserve(lo.size() * 2);
+    for (size_t i = 0; i < lo.size(); ++i) {
+      const uint64_t h = m[i] >> 1;
+      lo2.push_back(lo[i]);
+      m2.push_back(h);
+      lo2.push_back(lo[i] + h);
+      m2.push_back(m[i] - h);
+    }
+    lo.swap(lo2);
+    m.swap(m2);
+  }
+  std::vector<uint32_t> out(lo.size() + 1);
+  for (size_t i = 0; i < lo.size(); ++i) out[i] = (uint32_t)lo[i];
+  out[lo.size()] = (uint32_t)n;
+  return out;
+}
+
+// The per-chunk metadata of one row shape, built on the host and uploaded
+// once: {jb0, nblk, le, 0, lo[jb0 .. jb0 + nblk]} per chunk k of the row
+// (blocks starting in [k*CH, (k+1)*CH); le = end of the last one).
+qfb_status sb_shape(qfb_ctx* ctx, uint64_t n, uint32_t depth, const uint32_t** meta, uint32_t* nch) {
+  for (const auto& kv : ctx->sb_shapes)
+    if (kv.first == n) {
+      *meta = kv.second.meta;
+      *nch = kv.second.nch;
+      return QFB_OK;
+    }
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(ctx->stream, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone)
+    return fail(QFB_ERR_UNSUPPORTED, "backward: row length %llu first seen during a stream capture: run the "
+                "call once eagerly (or qfb_fq_bwd_reserve) before capturing", (unsigned long long)n);
+  const uint32_t L = depth - (uint32_t)kSbBlockLog;
+  const std::vector<uint32_t> lo = tree_starts(n, L);
+  const uint32_t NB = 1u << L;
+  const uint32_t k_n = (uint32_t)((n + kSbChunk - 1) / kSbChunk);
+  std::vector<uint32_t> tab((size_t)k_n * kSbMetaWords, 0u);
+  for (uint32_t k = 0; k < k_n; ++k) {
+    const uint32_t c0 = k * (uint32_t)kSbChunk;
+    const uint32_t c1 = (uint32_t)std::min<uint64_t>(c0 + (uint64_t)kSbChunk, n);
+    const uint32_t jb0 = (uint32_t)(std::lower_bound(lo.begin(), lo.begin() + NB, c0) - lo.begin());
+    const uint32_t jb1 = (uint32_t)(std::lower_bound(lo.begin(), lo.begin() + NB, c1) - lo.begin());
+    const uint32_t nblk = jb1 - jb0;
+    if (nblk > (uint32_t)kSbMaxBlocks || (nblk && lo[jb1] - c0 > (uint32_t)kSbWin))
+      return fail(QFB_ERR_UNSUPPORTED, "backward: block layout of a %llu-element row exceeds the chunk bounds",
+                  (unsigned long long)n);
+    uint32_t* e = tab.data() + (size_t)k * kSbMetaWords;
+    e[0] = jb0;
+    e[1] = nblk;
+    e[2] = nblk ? lo[jb1] : c1;
+    for (uint32_t i = 0; i <= nblk; ++i) e[4 + i] = lo[jb0 + i];
+  }
+  qfb_ctx::SbShape sh;
+  QFB_CUDA(cudaMalloc(&sh.meta, tab.size() * sizeof(uint32_t)));
+  QFB_CUDA(cudaMemcpy(sh.meta, tab.data(), tab.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  sh.nch = k_n;
+  ctx->sb_shapes.emplace_back(n, sh);
+  *meta = sh.meta;
+  *nch = k_n;
+  return QFB_OK;
+}
+
+// Switch a plan to the streaming kernel: block partials (part_log = D - 4),
+// chunks instead of tiles.
+qfb_status sb_plan(qfb_ctx* ctx, BwdPlan& p) {
+  BwdDesc& d = p.d;
+  const uint32_t* meta = nullptr;
+  uint32_t nch = 0;
+  if (qfb_status st = sb_shape(ctx, d.inner, d.depth, &meta, &nch)) return st;
+  d.sb_meta = meta;
+  d.sb_nch = nch;
+  d.sb_nch_div = make_fastdiv(nch);
+  d.part_log = d.depth - (uint32_t)kSbBlockLog;
+  const uint64_t segs = (uint64_t)d.outer * d.chans;
+  p.tiles = segs * nch;
+  p.f64_need = segs << d.part_log;
+  if (p.tiles >= (1ull << 31)) return fail(QFB_ERR_UNSUPPORTED, "too many chunks");
+  return QFB_OK;
+}
+
+// Plans of a table, switched to the streaming kernel when every entry is
+// eligible (one launch for the whole table, as for the tile kernel).
+qfb_status plan_bwd_table(qfb_ctx* ctx, int dtype, const qfb_bwd_desc* table, int32_t n,
+                          std::vector<BwdPlan>& plans, bool* stream, bool* warp_part) {
+  plans.assign((size_t)n, BwdPlan{});
+  for (int32_t i = 0; i < n; ++i)
+    if (qfb_status st = plan_bwd(table[i], plans[i], dtype)) return st;
+  bool all = ctx->bwd_impl == 2 && n > 0 && ctx->sb_blocks_per_sm[dtype] > 0;
+  for (int32_t i = 0; i < n && all; ++i) all = sb_eligible(plans[i], dtype);
+  *stream = all;
+  if (all)
+    for (auto& p : plans)
+      if (qfb_status st = sb_plan(ctx, p)) return st;
+  // tile kernel: consumer-side warp partials when every row has full
+  // 256-group tiles (g == kBwdGroupsLog): 8 partials per tile
+  *warp_part = false;
+  if (!all && ctx->bwd_impl == 0) {
+    bool wp = n > 0;
+    for (int32_t i = 0; i < n && wp; ++i) wp = plans[i].d.g == (uint32_t)kBwdGroupsLog;
+    *warp_part = wp;
+    if (wp)
+      for (auto& p : plans) {
+        p.d.part_log = p.d.tps_log + 3;
+        p.f64_need <<= 3;
+      }
+  }
+  return QFB_OK;
+}
+
+}  // namespace
+
 qfb_status qfb_fq_bwd_reserve(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc* table, int32_t n) {
   if (qfb_status st = check_ctx(ctx)) return st;
   if (qfb_status st = check_dtype(dtype)) return st;
@@ -812,9 +974,12 @@ qfb_status qfb_fq_bwd_reserve(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc*
   size_t need = 1, f64 = 0;
   int32_t cnt = 0;
   uint64_t tiles = 0;
+  std::vector<BwdPlan> plans;
+  bool stream = false, warp_part = false;
+  DeviceGuard g0(ctx->device);
+  if (qfb_status st = plan_bwd_table(ctx, dtype, table, n, plans, &stream, &warp_part)) return st;
   for (int32_t i = 0; i < n; ++i) {
-    BwdPlan p;
-    if (qfb_status st = plan_bwd(table[i], p, dtype)) return st;
+    const BwdPlan& p = plans[(size_t)i];
     // the same batching as qfb_fq_bwd_multi: the largest batch sizes it
     if (cnt == kMaxBwdDesc || (cnt > 0 && tiles + p.tiles >= (1ull << 31))) {
       need = std::max(need, f64);
@@ -835,10 +1000,10 @@ qfb_status qfb_fq_bwd_multi(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc* t
   if (qfb_status st = check_ctx(ctx)) return st;
   if (qfb_status st = check_dtype(dtype)) return st;
   if (n < 0 || (n > 0 && !table)) return fail(QFB_ERR_VALUE, "fq_bwd_multi: bad table");
-  std::vector<BwdPlan> plans((size_t)n);
-  for (int32_t i = 0; i < n; ++i)
-    if (qfb_status st = plan_bwd(table[i], plans[i], dtype)) return st;
   DeviceGuard g(ctx->device);
+  std::vector<BwdPlan> plans;
+  bool stream = false, warp_part = false;
+  if (qfb_status st = plan_bwd_table(ctx, dtype, table, n, plans, &stream, &warp_part)) return st;
   int32_t i = 0;
   while (i < n) {
     // Batch up to kMaxBwdDesc entries; each gets its own workspace slice.
@@ -862,7 +1027,7 @@ qfb_status qfb_fq_bwd_multi(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc* t
     for (int32_t k = 0; k < cnt; ++k) {
       BwdDesc d = plans[i + k].d;
       const uint64_t segs = (uint64_t)d.outer * d.chans;
-      const uint64_t tps = 1ull << d.tps_log;
+      const uint64_t tps = 1ull << d.part_log;
       d.partials = fp;
       fp += segs * tps;
       b.d[k] = d;
@@ -871,6 +1036,15 @@ qfb_status qfb_fq_bwd_multi(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc* t
     }
     b.n = cnt;
     b.tile_begin[cnt] = (uint32_t)tb;
+    b.warp_part = warp_part ? 1u : 0u;
+    if (stream) {
+      const int grid = ctx->sm_count * ctx->sb_blocks_per_sm[dtype];
+      cudaError_t e = launch_sbwd(dtype, sb_stages(dtype), b, grid, ctx->stream);
+      if (e != cudaSuccess) return cuda_fail(e, "sbwd_kernel launch");
+      ctx->launches += 2;  // main pass + finisher
+      i += cnt;
+      continue;
+    }
     // ring sized from the largest tile of the batch (node size bound)
     uint32_t max_tile = 1;
     for (int32_t k = 0; k < cnt; ++k) {

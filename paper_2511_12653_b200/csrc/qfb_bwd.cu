@@ -48,6 +48,11 @@ constexpr int kMaxStages = 8;
 // no refills or stores). Not used in production; results in DESIGN.md §7.
 constexpr int kProbeNoCompute = 8;
 constexpr int kProbeNoLoads = 16;
+// Consumer-side partials (production when every row has full 256-group
+// tiles): each consumer warp reduces its 32 group sums with a 5-level xor
+// butterfly (a perfect subtree: the node at depth D - 5) and stores that
+// partial itself, so the producer warp does no tree work per tile.
+constexpr int kWarpPart = 32;
 
 constexpr int kWinPad = 32;                // window slack: 16-byte rounding at both ends
 constexpr size_t kRingBudget = 76 * 1024;  // default per-CTA ring + sums: 3 CTAs per SM
@@ -500,7 +505,7 @@ __device__ __forceinline__ void tile_sum(const BwdDesc& d, const TileRef& cur, d
   const int groups = 1 << d.g;
   const int lanes_used = groups >= 32 ? 32 : groups;
   for (int o = 1; o < lanes_used; o <<= 1) r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, o));
-  if ((threadIdx.x & 31) == 0) d.partials[((uint64_t)cur.seg << d.tps_log) + cur.t] = r;
+  if ((threadIdx.x & 31) == 0) d.partials[((uint64_t)cur.seg << d.part_log) + cur.t] = r;
 }
 
 // d_input of a finished tile: ragged ends by lanes, the aligned interior as
@@ -605,8 +610,10 @@ __global__ void __launch_bounds__(kBwdCtaThreads, 3) bwd_kernel(const __grid_con
       if (nid < total) produce<T, V>(bt, nr, st, &refs[s], &full[s], lane, true);
       // the tile's sums are read after the refill was issued (the next use
       // of this stage writes the other buffer)
-      const double part = lane_subtree(d, red[2 * s + par], lane);
-      tile_sum(d, cur, part);
+      if constexpr ((V & kWarpPart) == 0) {
+        const double part = lane_subtree(d, red[2 * s + par], lane);
+        tile_sum(d, cur, part);
+      }
       s = s + 1 == nst ? 0 : s + 1;
     }
     if (lane == 0) bulk_wait_all();
@@ -637,7 +644,13 @@ __global__ void __launch_bounds__(kBwdCtaThreads, 3) bwd_kernel(const __grid_con
     double v = (V & kProbeNoCompute) ? 0.0
              : (d.dx != nullptr && !(V & kProbeNoLoads)) ? group_sum_any<T, true>(sx, su, glen, dc, q)
                                                           : group_sum_any<T, false>(sx, su, glen, dc, q);
-    red[2 * s + par][tid] = v;  // the producer runs the tile's tree reduction
+    if constexpr ((V & kWarpPart) != 0) {
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+      if (lane == 0) d.partials[((uint64_t)cur.seg << d.part_log) + ((uint64_t)cur.t << 3) + (uint32_t)warp] = v;
+    } else {
+      red[2 * s + par][tid] = v;  // the producer runs the tile's tree reduction
+    }
     // d_input was written into the stage with generic stores and leaves it
     // through a TMA bulk store (async proxy): every writing thread orders
     // its stores before the handoff (the TMA-store pattern)
@@ -648,7 +661,7 @@ __global__ void __launch_bounds__(kBwdCtaThreads, 3) bwd_kernel(const __grid_con
   }
 }
 
-// Finisher: one warp per (descriptor, channel). Each row's 2^tps_log tile
+// Finisher: one warp per (descriptor, channel). Each row's 2^part_log tile
 // partials are reduced in perfect-tree order (lane slices + xor butterfly),
 // times chain[c]; rows of the channel are folded in row order.
 constexpr int kFinSmem = 4096;  // partials per row staged in smem (32 KB)
@@ -668,7 +681,7 @@ __global__ void __launch_bounds__(32) bwd_finish_kernel(const __grid_constant__ 
   const BwdDesc& d = bt.d[di];
   const uint32_t c = w;
   const int lane = threadIdx.x;
-  const uint32_t tps = 1u << d.tps_log;
+  const uint32_t tps = 1u << d.part_log;
   const uint32_t lanes = tps < 32u ? tps : 32u;
   const uint32_t per = tps / lanes;
   pdl_trigger();
@@ -676,7 +689,7 @@ __global__ void __launch_bounds__(32) bwd_finish_kernel(const __grid_constant__ 
   const double chain = d.chain[c];
   double acc = 0.0;
   for (uint32_t o = 0; o < d.outer; ++o) {
-    const double* p = d.partials + (((uint64_t)o * d.chans + c) << d.tps_log);
+    const double* p = d.partials + (((uint64_t)o * d.chans + c) << d.part_log);
     double v = 0.0;
     if (per == 1) {
       v = (uint32_t)lane < lanes ? p[lane] : 0.0;
@@ -728,16 +741,34 @@ __device__ __forceinline__ double lane_slice(const double* p, int lane) {
   return a[0];
 }
 
+// per = 8 * M consecutive partials: M perfect subtrees of 8, then the
+// perfect tree over their M sums (perfect trees compose).
+template <int M>
+__device__ __forceinline__ double lane_slice_wide(const double* p, int lane) {
+  double a[M];
+  const double* base = p + (size_t)lane * 8 * M;
+#pragma unroll
+  for (int g = 0; g < M; ++g) a[g] = lane_slice<8>(base + 8 * g, 0);
+#pragma unroll
+  for (int w = M; w > 1; w >>= 1)
+#pragma unroll
+    for (int k = 0; k < w / 2; ++k) a[k] = __dadd_rn(a[2 * k], a[2 * k + 1]);
+  return a[0];
+}
+
 __device__ __forceinline__ double lane_slice_any(const double* p, int lane, uint32_t per) {
   switch (per) {
     case 1: return p[lane];
     case 2: return lane_slice<2>(p, lane);
     case 4: return lane_slice<4>(p, lane);
-    default: return lane_slice<8>(p, lane);
+    case 8: return lane_slice<8>(p, lane);
+    case 16: return lane_slice_wide<2>(p, lane);
+    case 32: return lane_slice_wide<4>(p, lane);
+    default: return lane_slice_wide<8>(p, lane);
   }
 }
 
-constexpr uint32_t kFinRegMaxTiles = 256;  // per <= 8
+constexpr uint32_t kFinRegMaxTiles = 2048;  // per <= 64
 constexpr int kFinRows = 4;
 
 __global__ void __launch_bounds__(32) bwd_finish_reg_kernel(const __grid_constant__ BwdBatch bt) {
@@ -751,7 +782,7 @@ __global__ void __launch_bounds__(32) bwd_finish_reg_kernel(const __grid_constan
   const BwdDesc& d = bt.d[di];
   const uint32_t c = w;
   const int lane = threadIdx.x;
-  const uint32_t tps = 1u << d.tps_log;
+  const uint32_t tps = 1u << d.part_log;
   const uint32_t lanes = tps < 32u ? tps : 32u;
   const uint32_t per = tps / lanes;
   const bool on = (uint32_t)lane < lanes;
@@ -768,7 +799,7 @@ __global__ void __launch_bounds__(32) bwd_finish_reg_kernel(const __grid_constan
     for (int j = 0; j < kFinRows; ++j) {
       v[j] = 0.0;
       if (on && o + j < d.outer)
-        v[j] = lane_slice_any(d.partials + (((uint64_t)(o + j) * d.chans + c) << d.tps_log), lane, per);
+        v[j] = lane_slice_any(d.partials + (((uint64_t)(o + j) * d.chans + c) << d.part_log), lane, per);
     }
 #pragma unroll
     for (int j = 0; j < kFinRows; ++j) {
@@ -787,6 +818,339 @@ __global__ void __launch_bounds__(32) bwd_finish_reg_kernel(const __grid_constan
     }
   }
   if (lane == 0 && !rows) d.d_log_s[c] = acc;
+}
+
+// =====================================================================
+// Streaming backward (sbwd_kernel). The memory-pipeline probe
+// (tools/pipe_probe.cu, profiles/r02_pipe_probe.txt) moves this traffic
+// shape (read x and up, write d_input) at 0.95-1.01 of measured HBM with
+// ANY ring structure (register loads, TMA + CTA barrier, warp-specialized
+// TMA with register or bulk stores), so the tile kernel's deficit was its
+// per-tile work, not the pipeline. Here the pipeline carries no tree logic:
+//   chunk = kSbChunk consecutive elements of one row (16-byte aligned: rows
+//           of eligible tensors are 16-byte multiples), staged by TMA
+//           together with the overhang of its last tree block and a
+//           96-byte metadata record (its block starts, built once per row
+//           shape by the host);
+//   block = a node at depth D - 4 of the row's pairwise tree (16 leaf
+//           groups, <= 256 elements); a chunk OWNS the blocks that start
+//           inside it and folds them completely (their overhang is in its
+//           window); d_input is stored for the chunk's own elements only.
+// Warp roles (no CTA barrier after the prologue): one producer warp issues
+// the stage refills (metadata prefetched one issue ahead); consumer warp w
+// takes the chunk's blocks 2w and 2w+1 (32 leaf groups): phase 1 computes
+// every element of its range lane-strided (4 independent elements per lane
+// in flight: exact double quotient, term d_ds * up, d_input stored
+// coalesced from registers) into a per-warp term buffer, releases the
+// stage (one arrive per warp on `empty`), then phase 2: each half-warp
+// folds one block — lane l folds leaf group l in the reference order (two
+// <= 8 folds) and a 4-level xor butterfly forms the block's perfect-tree
+// sum. The head of the chunk (elements before its first block, owned by
+// the previous chunk's last block) gets its d_input from the first warp
+// without blocks. Block partials feed the same finisher (part_log = D - 4).
+// =====================================================================
+constexpr int kSbConsumers = kSbThreads / 32;       // 8
+constexpr int kSbCtaThreads = kSbThreads + 32;      // + producer warp
+constexpr int kSbWarpTerms = kSbWarpBlocks * kSbMaxBlk;  // terms of a warp's blocks
+
+struct SbRef {
+  uint32_t di, row, c0, c1;  // descriptor, row (o * chans + c), chunk [c0, c1) of the row
+  double s, y;               // scale and RN(1/s)
+};
+
+__device__ __forceinline__ void sb_decode(const BwdBatch& bt, uint32_t chunk, int& di, uint32_t& row,
+                                          uint32_t& k) {
+  int lo = 0, hi = bt.n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (bt.tile_begin[mid] <= chunk) lo = mid;
+    else hi = mid - 1;
+  }
+  di = lo;
+  const BwdDesc& d = bt.d[lo];
+  const uint32_t local = chunk - bt.tile_begin[lo];
+  row = fdiv(local, d.sb_nch_div);
+  k = local - row * d.sb_nch;
+}
+
+// Fold of one leaf group's terms in the reference order (tensor.hpp:100-109
+// below the block: n <= 8 -> left fold from 0.0, else fold(first n/2) +
+// fold(rest)). Groups here hold 8..16 terms.
+__device__ __forceinline__ double sb_group_fold(const double* t, int len) {
+  if (len <= 8) {
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (k < len) acc = __dadd_rn(acc, t[k]);
+    return acc;
+  }
+  const int h = len >> 1;
+  const double* r = t + h;
+  double al = 0.0, ar = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    if (k < h) al = __dadd_rn(al, t[k]);
+    if (k < len - h) ar = __dadd_rn(ar, r[k]);
+  }
+  return __dadd_rn(al, ar);
+}
+
+// One element: term (double) and d_input bits, exact reference semantics.
+template <typename T>
+__device__ __forceinline__ double sb_elem(T xe, T ue, const DivCtx& dc, double q, T& dxo) {
+  if (dc.usable) {
+    double t;
+    if constexpr (sizeof(T) == 4) {
+      float dd;
+      t = fast_term(xe, ue, dc, q, dd);
+      dxo = dd;
+    } else {
+      t = fast_term_h(xe, ue, dc, q, &dxo);
+    }
+    const float uf = to_f<T>(ue);
+    if (__builtin_expect((__float_as_uint(uf) & 0x7f800000u) == 0x7f800000u, 0))
+      dxo = from_f<T>(masked_upstream(grad_term(to_f<T>(xe), dc.s, q).mask, uf));
+    return t;
+  }
+  const double2 t2 = slow_elem(to_f<T>(xe), to_f<T>(ue), dc.s, q);
+  dxo = from_f<T>((float)t2.y);
+  return t2.x;
+}
+
+// Phase 1 of one warp over the row elements [lo, hi) (window-relative
+// views sx / su): lane-strided (consecutive lanes, consecutive elements:
+// conflict-free shared reads, coalesced d_input stores), 4 independent
+// elements per lane in flight in the unchecked main loop, then 32-element
+// steps. Terms (kTerms) go to the warp's buffer at [i - lo]; d_input is
+// stored for i < c1 (kDxCheck: only the warp whose range crosses c1 tests
+// it). kUsable is the chunk-uniform scale test of the fast quotient.
+template <typename T, bool kUsable>
+__device__ __forceinline__ double sb_term(T xe, T ue, const DivCtx& dc, double q, T& dv, uint32_t& bad) {
+  if constexpr (kUsable) {
+    bad |= (__float_as_uint(to_f<T>(ue)) & 0x7f800000u) == 0x7f800000u ? 1u : 0u;
+    if constexpr (sizeof(T) == 4) {
+      float dd;
+      const double t = fast_term(xe, ue, dc, q, dd);
+      dv = dd;
+      return t;
+    } else {
+      return fast_term_h(xe, ue, dc, q, &dv);
+    }
+  } else {
+    const double2 t2 = slow_elem(to_f<T>(xe), to_f<T>(ue), dc.s, q);
+    dv = from_f<T>((float)t2.y);
+    return t2.x;
+  }
+}
+
+template <typename T>
+__device__ __noinline__ T sb_fix_dx(T xe, T ue, const DivCtx& dc, double q, T dv) {
+  // non-finite upstream: the reference's d_input rules (rare)
+  const float uf = to_f<T>(ue);
+  if ((__float_as_uint(uf) & 0x7f800000u) == 0x7f800000u)
+    return from_f<T>(masked_upstream(grad_term(to_f<T>(xe), dc.s, q).mask, uf));
+  return dv;
+}
+
+template <typename T, bool kUsable, bool kTerms, bool kDxCheck>
+__device__ __forceinline__ void sb_sweep(const T* sx, const T* su, uint32_t lo, uint32_t hi, uint32_t c1,
+                                         const DivCtx& dc, double q, double* terms, T* dxrow) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t n = hi - lo;
+  const uint32_t nd = c1 > lo ? c1 - lo : 0u;  // d_input for relative index < nd
+  const T* px = sx + lo;
+  const T* pu = su + lo;
+  T* pd = dxrow ? dxrow + lo : nullptr;
+  uint32_t i = lane;
+  for (; i + 96u < n; i += 128u) {
+    double tv[4];
+    T dv[4], xe[4], ue[4];
+    uint32_t bad = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      xe[k] = px[i + 32u * k];
+      ue[k] = pu[i + 32u * k];
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) tv[k] = sb_term<T, kUsable>(xe[k], ue[k], dc, q, dv[k], bad);
+    if (kUsable && __builtin_expect(bad != 0, 0)) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) dv[k] = sb_fix_dx<T>(xe[k], ue[k], dc, q, dv[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (kTerms) terms[i + 32u * k] = tv[k];
+      if (pd && (!kDxCheck || i + 32u * k < nd)) pd[i + 32u * k] = dv[k];
+    }
+  }
+  for (; i < n; i += 32u) {
+    T dv;
+    uint32_t bad = 0;
+    const T xe = px[i], ue = pu[i];
+    const double tv = sb_term<T, kUsable>(xe, ue, dc, q, dv, bad);
+    if (kUsable && __builtin_expect(bad != 0, 0)) dv = sb_fix_dx<T>(xe, ue, dc, q, dv);
+    if (kTerms) terms[i] = tv;
+    if (pd && (!kDxCheck || i < nd)) pd[i] = dv;
+  }
+}
+
+// Fold of a leaf group of 9 or 10 terms (every group of the DPVO rows:
+// n / 2^D = 9.375) in the reference order: fold(first 4 or 5) + fold(5).
+__device__ __forceinline__ double sb_group_fold_9_10(const double* t, int len) {
+  const int h = len >> 1;  // 4 or 5
+  const double* r = t + h;
+  double al = __dadd_rn(0.0, t[0]), ar = __dadd_rn(0.0, r[0]);
+#pragma unroll
+  for (int k = 1; k < 4; ++k) {
+    al = __dadd_rn(al, t[k]);
+    ar = __dadd_rn(ar, r[k]);
+  }
+  if (h == 5) al = __dadd_rn(al, t[4]);
+  ar = __dadd_rn(ar, r[4]);
+  return __dadd_rn(al, ar);
+}
+
+template <typename T, int NS>
+__global__ void __launch_bounds__(kSbCtaThreads, 3) sbwd_kernel(const __grid_constant__ BwdBatch bt) {
+  constexpr uint32_t kWinBytes = kSbWin * sizeof(T);
+  constexpr uint32_t kStageBytes = 2 * kWinBytes + kSbMetaWords * 4;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full[NS];
+  __shared__ __align__(8) uint64_t empty[NS];
+  __shared__ SbRef refs[NS];
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int lane = tid & 31;
+  const uint32_t total = bt.tile_begin[bt.n];
+  pdl_wait();
+  if (blockIdx.x >= total) return;
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kSbConsumers);
+    }
+    fence_mbar_init();
+    pdl_trigger();
+  }
+  __syncthreads();  // the only CTA barrier: barrier init
+
+  if (warp == kSbConsumers) {
+    // ------------------------------------------------ producer warp ----
+    if (lane != 0) return;
+    uint32_t nx_chunk = 0, nx_row = 0, nx_k = 0, nx_le = 0;
+    int nx_di = 0;
+    double nx_s = 1.0;
+    auto prefetch = [&](uint32_t chunk) {
+      nx_chunk = chunk;
+      if (chunk >= total) return;
+      sb_decode(bt, chunk, nx_di, nx_row, nx_k);
+      const BwdDesc& d = bt.d[nx_di];
+      nx_le = __ldg(d.sb_meta + (size_t)nx_k * kSbMetaWords + 2);
+      nx_s = __ldg(d.s64 + (nx_row % d.chans));
+    };
+    auto issue = [&](int stage) {
+      const BwdDesc& d = bt.d[nx_di];
+      const uint32_t n = (uint32_t)d.inner;
+      const uint32_t c0 = nx_k * (uint32_t)kSbChunk;
+      const uint32_t c1 = min(c0 + (uint32_t)kSbChunk, n);
+      constexpr uint32_t V = 16 / sizeof(T);
+      uint32_t end = max(c1, nx_le);
+      end = min((end + V - 1) & ~(V - 1), n);
+      SbRef r;
+      r.di = (uint32_t)nx_di;
+      r.row = nx_row;
+      r.c0 = c0;
+      r.c1 = c1;
+      r.s = nx_s;
+      r.y = __drcp_rn(nx_s);
+      refs[stage] = r;
+      const uint32_t bytes = (end - c0) * (uint32_t)sizeof(T);
+      unsigned char* st = smem_raw + (size_t)stage * kStageBytes;
+      const uint64_t off = ((uint64_t)nx_row * d.inner + c0) * sizeof(T);
+      mbar_arrive_expect_tx(&full[stage], 2 * bytes + kSbMetaWords * 4);
+      bulk_g2s(st, static_cast<const char*>(d.x) + off, bytes, &full[stage]);
+      bulk_g2s(st + kWinBytes, static_cast<const char*>(d.up) + off, bytes, &full[stage]);
+      bulk_g2s(st + 2 * kWinBytes, d.sb_meta + (size_t)nx_k * kSbMetaWords, kSbMetaWords * 4, &full[stage]);
+    };
+    prefetch(blockIdx.x);
+    uint32_t phase = 0;
+    int s = 0;
+    for (uint32_t it = 0; nx_chunk < total; ++it) {
+      if (it >= (uint32_t)NS) {
+        mbar_wait_sleep(&empty[s], (phase >> s) & 1u);  // all consumer warps are done reading stage s
+        phase ^= 1u << s;
+      }
+      issue(s);
+      prefetch(nx_chunk + gridDim.x);
+      s = s + 1 == NS ? 0 : s + 1;
+    }
+    return;
+  }
+
+  // ------------------------------------------------- consumer warps ----
+  double* terms = reinterpret_cast<double*>(smem_raw + (size_t)NS * kStageBytes) + (size_t)warp * kSbWarpTerms;
+  uint32_t phase = 0;
+  int s = 0;
+  for (uint32_t chunk = blockIdx.x; chunk < total; chunk += gridDim.x) {
+    mbar_wait_sleep(&full[s], (phase >> s) & 1u);
+    phase ^= 1u << s;
+    const SbRef r = refs[s];
+    const BwdDesc& d = bt.d[r.di];
+    const unsigned char* st = smem_raw + (size_t)s * kStageBytes;
+    const uint32_t* meta = reinterpret_cast<const uint32_t*>(st + 2 * kWinBytes);
+    // window-relative element views of the staged x and upstream
+    const T* sx = reinterpret_cast<const T*>(st) - r.c0;
+    const T* su = reinterpret_cast<const T*>(st + kWinBytes) - r.c0;
+    DivCtx dc;
+    dc.s = r.s;
+    dc.y = r.y;
+    dc.usable = r.s >= 0x1p-100 && r.s <= 0x1p100;
+    const double q = d.q;
+    T* dxrow = d.dx ? static_cast<T*>(d.dx) + (uint64_t)r.row * d.inner : nullptr;
+    const uint32_t nblk = meta[1];
+    const uint32_t b0 = (uint32_t)kSbWarpBlocks * (uint32_t)warp;  // this warp's blocks (chunk-relative)
+    const uint32_t nb = nblk > b0 ? min(nblk - b0, (uint32_t)kSbWarpBlocks) : 0u;
+    const uint32_t a = nb ? meta[4 + b0] : 0u;  // this warp's range [a, e) of the row
+    const uint32_t e = nb ? meta[4 + b0 + nb] : 0u;
+    const uint32_t blo0 = 0u, bm0 = nb ? meta[5 + b0] - a : 0u;
+    const uint32_t blo1 = bm0, bm1 = nb > 1 ? e - meta[5 + b0] : 0u;
+    const uint32_t jb = meta[0] + b0;
+    // the chunk head [c0, first block) belongs to the previous chunk's last
+    // block: its d_input comes from the first warp without blocks (warp 7
+    // when all have blocks)
+    const bool head =
+        (uint32_t)warp == min((nblk + kSbWarpBlocks - 1u) / kSbWarpBlocks, (uint32_t)kSbConsumers - 1u);
+    const uint32_t head_end = nblk ? meta[4] : r.c1;
+    // ---- phase 1: this warp's elements, lane-strided, 4 in flight per lane
+    if (dc.usable) {
+      if (nb) {
+        if (e <= r.c1) sb_sweep<T, true, true, false>(sx, su, a, e, r.c1, dc, q, terms, dxrow);
+        else sb_sweep<T, true, true, true>(sx, su, a, e, r.c1, dc, q, terms, dxrow);
+      }
+      if (head) sb_sweep<T, true, false, false>(sx, su, r.c0, head_end, r.c1, dc, q, terms, dxrow);
+    } else {
+      if (nb) sb_sweep<T, false, true, true>(sx, su, a, e, r.c1, dc, q, terms, dxrow);
+      if (head) sb_sweep<T, false, false, false>(sx, su, r.c0, head_end, r.c1, dc, q, terms, dxrow);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);  // stage s no longer read by this warp
+    // ---- phase 2: one half-warp per block, from this warp's terms
+    const int h = lane >> 4;
+    const int l16 = lane & 15;
+    double v = 0.0;
+    const bool active = (uint32_t)h < nb;
+    if (active) {
+      uint32_t gl = 0, gm = h ? bm1 : bm0;
+      descend<uint32_t>(gl, gm, (uint32_t)l16, kSbBlockLog);
+      const double* tg = terms + (h ? blo1 : blo0) + gl;
+      v = (gm == 9 || gm == 10) ? sb_group_fold_9_10(tg, (int)gm) : sb_group_fold(tg, (int)gm);
+    }
+#pragma unroll
+    for (int o = 1; o < 16; o <<= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (active && l16 == 0) d.partials[((uint64_t)r.row << d.part_log) + jb + h] = v;
+    __syncwarp();  // terms read before the next chunk overwrites them
+    s = s + 1 == NS ? 0 : s + 1;
+  }
 }
 
 }  // namespace
@@ -837,16 +1201,17 @@ static int variant() {
 }
 
 template <typename T>
-const void* kernel_ptr(int v) {
+const void* kernel_ptr(int v, bool warp_part) {
   switch (v) {
     case kProbeNoCompute: return (const void*)bwd_kernel<T, kProbeNoCompute>;
     case kProbeNoLoads: return (const void*)bwd_kernel<T, kProbeNoLoads>;
-    default: return (const void*)bwd_kernel<T, 0>;
+    default:
+      return warp_part ? (const void*)bwd_kernel<T, kWarpPart> : (const void*)bwd_kernel<T, 0>;
   }
 }
 
-const void* bwd_fn(int dtype) {
-  return dtype == 0 ? kernel_ptr<float>(variant()) : kernel_ptr<__half>(variant());
+const void* bwd_fn(int dtype, bool warp_part = false) {
+  return dtype == 0 ? kernel_ptr<float>(variant(), warp_part) : kernel_ptr<__half>(variant(), warp_part);
 }
 
 }  // namespace
@@ -872,12 +1237,58 @@ cudaError_t launch_bwd(int dtype, const BwdBatch& b, int grid, cudaStream_t st) 
   if ((uint32_t)grid > tiles) grid = (int)tiles;
   const size_t smem = (size_t)b.nstages * (2 * b.stage_elems * (dtype == 0 ? 4 : 2) + kRedBytes);
   void* args[] = {const_cast<BwdBatch*>(&b)};
-  cudaError_t e = launch_main(bwd_fn(dtype), dim3(grid), dim3(kBwdCtaThreads), args, smem, st, kPdlBwd);
+  const void* fn = bwd_fn(dtype, b.warp_part != 0);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
+  cudaError_t e = launch_main(fn, dim3(grid), dim3(kBwdCtaThreads), args, smem, st, kPdlBwd);
   if (e != cudaSuccess) return e;
+  return launch_bwd_finish(b, st);
+}
+
+namespace {
+constexpr int kSbStagesF32 = 3, kSbStagesF16 = 3;
+const void* sbwd_fn(int dtype, int stages) {
+  if (dtype == 0) {
+    if (stages == 2) return (const void*)sbwd_kernel<float, 2>;
+    if (stages == 4) return (const void*)sbwd_kernel<float, 4>;
+    return (const void*)sbwd_kernel<float, 3>;
+  }
+  if (stages == 2) return (const void*)sbwd_kernel<__half, 2>;
+  if (stages == 4) return (const void*)sbwd_kernel<__half, 4>;
+  return (const void*)sbwd_kernel<__half, 3>;
+}
+}  // namespace
+
+size_t sbwd_smem(int dtype, int stages) {
+  const size_t es = dtype == 0 ? 4 : 2;
+  return (size_t)stages * (2 * kSbWin * es + kSbMetaWords * 4) +
+         (size_t)kSbConsumers * kSbWarpTerms * sizeof(double);
+}
+
+cudaError_t sbwd_occupancy(int dtype, int stages, int* blocks_per_sm) {
+  const void* f = sbwd_fn(dtype, stages);
+  const size_t smem = sbwd_smem(dtype, stages);
+  cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, kSbCtaThreads, smem);
+}
+
+cudaError_t launch_sbwd(int dtype, int stages, const BwdBatch& b, int grid, cudaStream_t st) {
+  const uint32_t chunks = b.tile_begin[b.n];
+  if (chunks == 0) return cudaSuccess;
+  if ((uint32_t)grid > chunks) grid = (int)chunks;
+  void* args[] = {const_cast<BwdBatch*>(&b)};
+  cudaError_t e = launch_main(sbwd_fn(dtype, stages), dim3(grid), dim3(kSbCtaThreads), args,
+                              sbwd_smem(dtype, stages), st, kPdlBwd);
+  if (e != cudaSuccess) return e;
+  return launch_bwd_finish(b, st);
+}
+
+cudaError_t launch_bwd_finish(const BwdBatch& b, cudaStream_t st) {
+  cudaError_t e;
   uint32_t warps = 0, max_tps = 0;
   for (int i = 0; i < b.n; ++i) {
     warps += b.d[i].chans;
-    max_tps = std::max(max_tps, 1u << b.d[i].tps_log);
+    max_tps = std::max(max_tps, 1u << b.d[i].part_log);
   }
   static const bool force_smem = [] {
     const char* e = getenv("QFB_FIN_SMEM");

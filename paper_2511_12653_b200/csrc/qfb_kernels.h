@@ -169,6 +169,7 @@ struct BwdDesc {
   uint32_t outer;
   uint32_t chans;
   uint32_t tps_log;  // tiles per segment = 2^(depth - g)
+  uint32_t part_log; // partials per segment (row) = 2^part_log, reduced by the finisher
   uint32_t depth;    // tree depth of the 16-bounded leaf groups
   uint32_t g;        // tile depth = min(depth, kBwdGroupsLog)
   int32_t accumulate;  // 0 fold, 1 fold into d_log_s, 2 (QFB_BWD_ROWS) one value per row
@@ -177,13 +178,20 @@ struct BwdDesc {
   uint32_t pad;
   uint64_t total_bytes;  // outer * chans * inner * sizeof(T)
   uint64_t row_stride;   // QFB_BWD_ROWS: d_log_s[o * row_stride + c]
+  // streaming backward (sbwd_kernel) only: per-chunk block metadata of this
+  // row shape (kSbMetaWords u32 per chunk of a row, built by the host) and
+  // the chunks per row
+  const uint32_t* sb_meta;
+  uint32_t sb_nch;
+  uint32_t pad3;
+  FastDivHost sb_nch_div;
 };
 
 struct BwdBatch {
   int32_t n;
   int32_t nstages;       // TMA ring depth (2..4), sized from the max tile
   uint32_t stage_elems;  // elements per array per stage (16-byte multiple)
-  uint32_t pad2;
+  uint32_t warp_part;    // tile kernel: consumer warps store the partials (tps_log = depth - 5)
   uint32_t tile_begin[kMaxBwdDesc + 1];
   BwdDesc d[kMaxBwdDesc];
 };
@@ -197,5 +205,26 @@ void bwd_ring_size(int dtype, uint32_t max_tile, uint32_t* stage_elems, int32_t*
 // Main pass (tile partials) + finisher (segment trees, chain, outer fold);
 // stream order replaces fences and tickets.
 cudaError_t launch_bwd(int dtype, const BwdBatch& b, int grid, cudaStream_t st);
+// The finisher alone: per (descriptor, channel) the perfect tree over the
+// 2^tps_log partials of each row, times chain, folded over the rows.
+cudaError_t launch_bwd_finish(const BwdBatch& b, cudaStream_t st);
+
+// ---------------------------------------------- streaming backward ----
+// sbwd_kernel (qfb_sbwd.cu): fixed row-relative chunks of kSbChunk
+// elements, TMA-staged with the overhang of the chunk's last tree block;
+// element-parallel terms into shared memory, then one half-warp per block
+// of 16 leaf groups (a tree node at depth D - 4) folds and reduces it; the
+// block partials feed the same finisher (tps_log = D - 4).
+constexpr int kSbThreads = 256;
+constexpr int kSbChunk = 1024;        // elements of a row per chunk
+constexpr int kSbBlockLog = 4;        // leaf groups per block = 16
+constexpr int kSbMaxBlk = 256;        // block length bound (16 groups x 16)
+constexpr int kSbWarpBlocks = 1;      // blocks per consumer warp (8 warps x 1 >= 1024 / 128)
+constexpr int kSbMaxBlocks = 8 * kSbWarpBlocks;  // block starts per chunk bound (blocks >= 128 elements)
+constexpr int kSbMetaWords = 24;      // {jb0, nblk, le, 0, lo[0..nblk]} padded to 96 bytes
+constexpr int kSbWin = kSbChunk + kSbMaxBlk;  // staged elements per array per stage
+size_t sbwd_smem(int dtype, int stages);
+cudaError_t sbwd_occupancy(int dtype, int stages, int* blocks_per_sm);
+cudaError_t launch_sbwd(int dtype, int stages, const BwdBatch& b, int grid, cudaStream_t st);
 
 }  // namespace qfb
