@@ -949,18 +949,13 @@ qfb_status plan_bwd_table(qfb_ctx* ctx, int dtype, const qfb_bwd_desc* table, in
   if (all)
     for (auto& p : plans)
       if (qfb_status st = sb_plan(ctx, p)) return st;
-  // tile kernel: consumer-side warp partials when every row has full
-  // 256-group tiles (g == kBwdGroupsLog): 8 partials per tile
+  // tile kernel: consumer-side warp sums when every row has full 256-group
+  // tiles (g == kBwdGroupsLog)
   *warp_part = false;
   if (!all && ctx->bwd_impl == 0) {
     bool wp = n > 0;
     for (int32_t i = 0; i < n && wp; ++i) wp = plans[i].d.g == (uint32_t)kBwdGroupsLog;
     *warp_part = wp;
-    if (wp)
-      for (auto& p : plans) {
-        p.d.part_log = p.d.tps_log + 3;
-        p.f64_need <<= 3;
-      }
   }
   return QFB_OK;
 }
@@ -1055,11 +1050,12 @@ qfb_status qfb_fq_bwd_multi(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc* t
     bwd_ring_size(dtype, max_tile, &b.stage_elems, &b.nstages, &smem);
     // cached: keeps steady-state launches free of runtime queries (graph capture)
     int per_sm = 0;
+    const size_t key = smem * 2 + (warp_part ? 1 : 0);
     for (const auto& kv : ctx->bwd_occ[dtype])
-      if (kv.first == smem) per_sm = kv.second;
+      if (kv.first == key) per_sm = kv.second;
     if (per_sm == 0) {
-      if (bwd_occupancy_smem(dtype, smem, &per_sm) != cudaSuccess || per_sm < 1) per_sm = 1;
-      ctx->bwd_occ[dtype].emplace_back(smem, per_sm);
+      if (bwd_occupancy_smem(dtype, smem, &per_sm, warp_part) != cudaSuccess || per_sm < 1) per_sm = 1;
+      ctx->bwd_occ[dtype].emplace_back(key, per_sm);
     }
     const int grid = ctx->sm_count * per_sm;
     cudaError_t e = launch_bwd(dtype, b, grid, ctx->stream);

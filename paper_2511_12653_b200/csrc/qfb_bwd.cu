@@ -48,10 +48,13 @@ constexpr int kMaxStages = 8;
 // no refills or stores). Not used in production; results in DESIGN.md §7.
 constexpr int kProbeNoCompute = 8;
 constexpr int kProbeNoLoads = 16;
-// Consumer-side partials (production when every row has full 256-group
+// Consumer-side tree (production when every row has full 256-group
 // tiles): each consumer warp reduces its 32 group sums with a 5-level xor
-// butterfly (a perfect subtree: the node at depth D - 5) and stores that
-// partial itself, so the producer warp does no tree work per tile.
+// butterfly (a perfect subtree: the node at depth D - 5) and leaves the
+// sum in shared memory; the producer combines the tile's 8 warp sums
+// (3-level butterfly over lanes 0..7) into the tile partial. Before, the
+// producer folded all 256 group sums itself (8 per lane + 5 levels) on the
+// refill path of every tile.
 constexpr int kWarpPart = 32;
 
 constexpr int kWinPad = 32;                // window slack: 16-byte rounding at both ends
@@ -532,8 +535,12 @@ __device__ __forceinline__ void store_dx(const BwdDesc& d, const TileRef& cur, S
   }
 }
 
+// Two CTAs per SM with the registers that frees (more independent
+// elements in flight per consumer lane) and a deeper ring (QFB_BWD_CTAS=2).
+constexpr int kTwoCtas = 128;
+
 template <typename T, int V>
-__global__ void __launch_bounds__(kBwdCtaThreads, 3) bwd_kernel(const __grid_constant__ BwdBatch bt) {
+__global__ void __launch_bounds__(kBwdCtaThreads, (V & kTwoCtas) ? 2 : 3) bwd_kernel(const __grid_constant__ BwdBatch bt) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[kMaxStages];
   __shared__ __align__(8) uint64_t done[kMaxStages];
@@ -613,6 +620,11 @@ __global__ void __launch_bounds__(kBwdCtaThreads, 3) bwd_kernel(const __grid_con
       if constexpr ((V & kWarpPart) == 0) {
         const double part = lane_subtree(d, red[2 * s + par], lane);
         tile_sum(d, cur, part);
+      } else {
+        double w = lane < kConsumerWarps ? red[2 * s + par][lane] : 0.0;
+#pragma unroll
+        for (int o = 1; o < kConsumerWarps; o <<= 1) w = __dadd_rn(w, __shfl_xor_sync(0xffffffffu, w, o));
+        if (lane == 0) d.partials[((uint64_t)cur.seg << d.part_log) + cur.t] = w;
       }
       s = s + 1 == nst ? 0 : s + 1;
     }
@@ -647,13 +659,16 @@ __global__ void __launch_bounds__(kBwdCtaThreads, 3) bwd_kernel(const __grid_con
     if constexpr ((V & kWarpPart) != 0) {
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
-      if (lane == 0) d.partials[((uint64_t)cur.seg << d.part_log) + ((uint64_t)cur.t << 3) + (uint32_t)warp] = v;
+      if (lane == 0) red[2 * s + par][warp] = v;  // the producer combines the 8 warp sums
     } else {
       red[2 * s + par][tid] = v;  // the producer runs the tile's tree reduction
     }
     // d_input was written into the stage with generic stores and leaves it
     // through a TMA bulk store (async proxy): every writing thread orders
-    // its stores before the handoff (the TMA-store pattern)
+    // its stores before the handoff (the TMA-store pattern). Measured:
+    // consumer warps copying their own ranges out instead (coalesced
+    // stores, no producer store) cost 19 M more instructions per frame and
+    // 14 us.
     fence_proxy_async_smem();
     __syncwarp();     // the warp's d_input and group sums are written
     if (lane == 0) mbar_arrive(&done[s]);
@@ -1205,8 +1220,14 @@ const void* kernel_ptr(int v, bool warp_part) {
   switch (v) {
     case kProbeNoCompute: return (const void*)bwd_kernel<T, kProbeNoCompute>;
     case kProbeNoLoads: return (const void*)bwd_kernel<T, kProbeNoLoads>;
-    default:
-      return warp_part ? (const void*)bwd_kernel<T, kWarpPart> : (const void*)bwd_kernel<T, 0>;
+    default: {
+      static const bool two = [] {
+        const char* e = getenv("QFB_BWD_CTAS");
+        return e && e[0] == '2';
+      }();
+      if (!warp_part) return (const void*)bwd_kernel<T, 0>;
+      return two ? (const void*)bwd_kernel<T, kWarpPart | kTwoCtas> : (const void*)bwd_kernel<T, kWarpPart>;
+    }
   }
 }
 
@@ -1224,8 +1245,8 @@ cudaError_t bwd_occupancy(int dtype, int* blocks_per_sm) {
   return bwd_occupancy_smem(dtype, smem, blocks_per_sm);
 }
 
-cudaError_t bwd_occupancy_smem(int dtype, size_t smem, int* blocks_per_sm) {
-  const void* f = bwd_fn(dtype);
+cudaError_t bwd_occupancy_smem(int dtype, size_t smem, int* blocks_per_sm, bool warp_part) {
+  const void* f = bwd_fn(dtype, warp_part);
   cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
   if (e != cudaSuccess) return e;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, kBwdCtaThreads, smem);

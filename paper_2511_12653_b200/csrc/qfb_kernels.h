@@ -197,7 +197,7 @@ struct BwdBatch {
 };
 
 cudaError_t bwd_occupancy(int dtype, int* blocks_per_sm);  // at the default ring size
-cudaError_t bwd_occupancy_smem(int dtype, size_t smem, int* blocks_per_sm);
+cudaError_t bwd_occupancy_smem(int dtype, size_t smem, int* blocks_per_sm, bool warp_part = false);
 // Ring sizing: stage_elems / nstages / dynamic smem for a batch whose
 // largest tile has max_tile elements.
 void bwd_ring_size(int dtype, uint32_t max_tile, uint32_t* stage_elems, int32_t* nstages,
