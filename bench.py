@@ -160,10 +160,12 @@ class RefCpuWorkload:
     A bounded sample (a fixed subset of blocks, sized to `budget_s`) is
     timed and converted to frames/s = frames-worth of elements / seconds."""
 
-    def __init__(self, consumers, threads, dtype="f32", seed=7, do_bwd=True):
+    def __init__(self, consumers, threads, dtype="f32", seed=7, do_bwd=True, mode="blocks", lib=None):
         import numpy as np
         import oracle
-        self.ref = oracle.Reference()
+        self.ref = oracle.Reference(lib) if lib else oracle.Reference()
+        self.lib = os.path.basename(lib) if lib else "libqfref.so"
+        self.mode = mode  # "blocks": 4-channel blocks over a pool; "sweeps": the reference's schedule
         self.threads = threads
         self.do_bwd = 1 if do_bwd else 0
         self.reps = 1
@@ -178,8 +180,9 @@ class RefCpuWorkload:
             x = xs[p.name]
             up = rng.standard_normal((p.channels, p.inner), dtype=np.float32)
             ls = np.log(np.expm1(np.exp(rng.uniform(np.log(1e-3), np.log(0.1), p.channels))))
-            for c0 in range(0, p.channels, 4):
-                c1 = min(c0 + 4, p.channels)
+            step = 4 if mode == "blocks" else p.channels
+            for c0 in range(0, p.channels, step):
+                c1 = min(c0 + step, p.channels)
                 self.items.append((np.ascontiguousarray(x[c0:c1]), np.ascontiguousarray(up[c0:c1]),
                                    c1 - c0, p.inner, np.ascontiguousarray(ls[c0:c1])))
         order = list(range(len(self.items)))
@@ -189,17 +192,23 @@ class RefCpuWorkload:
 
     def _run(self, idx, reps=1):
         sel = [self.items[i] for i in idx]
-        st, secs, _ = self.ref.bench_points([s[0] for s in sel], [s[1] for s in sel],
-                                            [s[2] for s in sel], [s[3] for s in sel],
-                                            [s[4] for s in sel], half=self.half,
-                                            do_bwd=self.do_bwd, threads=self.threads, reps=reps)
+        if self.mode == "sweeps":
+            st, secs, _ = self.ref.bench_sweeps([s[0] for s in sel], [s[1] for s in sel],
+                                                [s[2] for s in sel], [s[3] for s in sel],
+                                                [s[4] for s in sel], half=self.half,
+                                                do_bwd=self.do_bwd, threads=self.threads, reps=reps)
+        else:
+            st, secs, _ = self.ref.bench_points([s[0] for s in sel], [s[1] for s in sel],
+                                                [s[2] for s in sel], [s[3] for s in sel],
+                                                [s[4] for s in sel], half=self.half,
+                                                do_bwd=self.do_bwd, threads=self.threads, reps=reps)
         assert st == 0, f"reference bench failed: {st}"
         return secs, reps * sum(s[2] * s[3] for s in sel)
 
     def size(self, budget_s):
         """Pick the sample: a subset of one frame's blocks when a frame takes
         longer than the budget, else whole frames repeated (reps) to fill it."""
-        probe = self.order[:max(2 * self.threads, 8)]
+        probe = self.order[:max(2 * self.threads, 8)] if self.mode == "blocks" else self.order[:2]
         secs, elems = self._run(probe)
         want = elems / max(secs, 1e-9) * budget_s
         self.reps = 1
@@ -221,10 +230,37 @@ class RefCpuWorkload:
         return secs, elems / self.frame_elems
 
     def describe(self, secs, frames):
+        if self.mode == "sweeps":
+            return (f"{frames:.3f} frames-worth of quant-point elements ({len(self.sel)} of "
+                    f"{len(self.items)} quant points x {self.reps} reps) in {secs:.2f} s; the reference's own "
+                    f"schedule: scale pass + fused sweep through qf::Dispatcher({self.threads}) (exec.hpp:127-146, "
+                    f"248-259, 363-375) + sequential fake_quantize_backward (frontend.hpp:226-229); {self.lib}")
         ops = "fake_quantize + fake_quantize_backward" if self.do_bwd else "fake_quantize"
         return (f"{frames:.3f} frames-worth of quant-point elements ({len(self.sel)} of "
                 f"{len(self.items)} 4-channel blocks x {self.reps} reps) in {secs:.2f} s on "
-                f"{self.threads} threads; reference quant.hpp {ops}, -O3 from its sources")
+                f"{self.threads} threads; reference quant.hpp {ops}, -O3 from its sources ({self.lib})")
+
+
+def reference_variants(consumers, threads, dtype, budget_s=3.0):
+    """The other CPU lines BASELINE.md §3 names, each a bounded sample:
+    the reference's own schedule (ExecutionPlan.threads = all host threads
+    and 0) and the channel-block pool built for x86-64-v3 (the -march=native
+    line; FMA contraction may change bits, timing only)."""
+    import oracle
+    out = {}
+    for key, th in (("reference_schedule_threads_all", threads), ("reference_schedule_threads_0", 0)):
+        w = RefCpuWorkload(consumers, th, dtype, mode="sweeps").size(budget_s)
+        s_, f_ = w.run()
+        out[key] = {"value": f_ / s_, "unit": UNIT, "cores": max(th, 1), "sample": w.describe(s_, f_)}
+    if os.path.exists(oracle.REF_V3_PATH):
+        try:
+            w = RefCpuWorkload(consumers, threads, dtype, lib=oracle.REF_V3_PATH).size(budget_s)
+            s_, f_ = w.run()
+            out["march_x86_64_v3"] = {"value": f_ / s_, "unit": UNIT, "cores": threads,
+                                      "sample": w.describe(s_, f_)}
+        except OSError as e:  # a host CPU without AVX2/FMA
+            out["march_x86_64_v3"] = {"unavailable": str(e)}
+    return out
 
 
 def cpu_reference_frames_per_s(consumers, budget_s, threads, dtype="f32", do_bwd=True):
@@ -316,6 +352,7 @@ def run_reference_arm(args):
         w1 = RefCpuWorkload(consumers, 1, args.dtype).size(3.0)
         s1, f1 = w1.run()
         cpu["single_thread"] = {"value": f1 / s1, "unit": UNIT, "cores": 1, "sample": w1.describe(s1, f1)}
+        cpu.update(reference_variants(consumers, threads, args.dtype))
     line = {"metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1000.0 / fps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": DATA,

@@ -26,6 +26,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORC_PATH = os.path.join(HERE, "liborc.so")
 REF_PATH = os.path.join(HERE, "_ref", "libqfref.so")
+REF_V3_PATH = os.path.join(HERE, "_ref", "libqfref_v3.so")  # -march=x86-64-v3, timing only
 
 _f32p = np.ctypeslib.ndpointer(dtype=np.float32, flags="C_CONTIGUOUS")
 _f64p = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
@@ -281,6 +282,10 @@ class Reference:
         L.ref_bench_points.argtypes = [_i32, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i64p, _i64p,
                                        ctypes.POINTER(_vp), _i32, _i32, _i32, _i32, _i32,
                                        ctypes.POINTER(_dbl), ctypes.POINTER(_dbl)]
+        L.ref_bench_sweeps.restype = _i32
+        L.ref_bench_sweeps.argtypes = [_i32, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i64p, _i64p,
+                                       ctypes.POINTER(_vp), _i32, _i32, _i32, _i32,
+                                       ctypes.POINTER(_dbl), ctypes.POINTER(_dbl)]
 
         _sz = ctypes.c_size_t
         L.ref_serialize_tensor.restype = _i32
@@ -473,6 +478,18 @@ class Reference:
         st = self.L.ref_bench_points(n, arr(xs), arr(ups), np.array(channels, dtype=np.int64),
                                      np.array(inners, dtype=np.int64), arr(log_ss), half, do_fwd,
                                      do_bwd, threads, reps, ctypes.byref(secs), ctypes.byref(cs))
+        return st, secs.value, cs.value
+
+    def bench_sweeps(self, xs, ups, channels, inners, log_ss, half=0, do_bwd=1, threads=0, reps=1):
+        """Time the reference's own schedule: scale pass + Dispatcher sweep
+        (exec.hpp:127-146, 248-259, 363-375) + sequential backward per point."""
+        n = len(xs)
+        arr = lambda lst: (_vp * n)(*[a.ctypes.data_as(_vp) for a in lst])  # noqa: E731
+        secs = _dbl()
+        cs = _dbl()
+        st = self.L.ref_bench_sweeps(n, arr(xs), arr(ups), np.array(channels, dtype=np.int64),
+                                     np.array(inners, dtype=np.int64), arr(log_ss), half, do_bwd,
+                                     threads, reps, ctypes.byref(secs), ctypes.byref(cs))
         return st, secs.value, cs.value
 
 

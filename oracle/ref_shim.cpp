@@ -254,6 +254,67 @@ int ref_bench_points(int32_t npoints, const float* const* x,
 }
 
 // ---------------------------------------------------------------------
+// Reference CPU arm with the reference's OWN parallel schedule: per quant
+// point the operator's scale pass (exec.hpp:248-259: resolve_scale per
+// channel, cast to float), its fused quantization sweep through the
+// engine's qf::Dispatcher (exec.hpp:127-146: `threads` workers, contiguous
+// parts, sequential below 4096 elements; the sweep body is the per-channel
+// form of exec.hpp:371-375, + round_to_half under HalfActivations as
+// exec.hpp:365-367), then the trainer's backward call fake_quantize_backward
+// (frontend.hpp:226-229), which the reference runs sequentially. threads =
+// 0 is ExecutionPlan{threads = 0}. Output buffers are allocated before the
+// clock starts, as the engine's arena would hold them.
+// ---------------------------------------------------------------------
+int ref_bench_sweeps(int32_t npoints, const float* const* x, const float* const* up,
+                     const int64_t* channels, const int64_t* inner, const double* const* log_s,
+                     int half, int do_bwd, int32_t threads, int32_t reps, double* seconds,
+                     double* checksum) {
+  return guarded([&] {
+    const qf::QuantConfig cfg;
+    const float q = static_cast<float>(cfg.q_max());
+    std::vector<qf::Tensor> tx, tu;
+    std::vector<std::vector<float>> qa;
+    for (int32_t p = 0; p < npoints; ++p) {
+      const int64_t n = channels[p] * inner[p];
+      tx.emplace_back(std::vector<int64_t>{channels[p], inner[p]},
+                      std::vector<float>(x[p], x[p] + n), prec_of(half));
+      tu.emplace_back(std::vector<int64_t>{channels[p], inner[p]},
+                      std::vector<float>(up[p], up[p] + n));
+      qa.emplace_back(static_cast<size_t>(n));
+    }
+    qf::Dispatcher disp(threads);
+    double cs = 0.0;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int32_t r = 0; r < reps; ++r) {
+      for (int32_t p = 0; p < npoints; ++p) {
+        const int64_t C = channels[p], per = inner[p], n = C * per;
+        std::vector<float> sw(static_cast<size_t>(C));
+        for (int64_t c = 0; c < C; ++c)
+          sw[static_cast<size_t>(c)] = static_cast<float>(qf::resolve_scale(log_s[p][c], cfg, prec_of(half)));
+        const float* xi = tx[p].data.data();
+        float* out = qa[p].data();
+        disp.sweep(n, [&](int64_t lo, int64_t hi) {
+          for (int64_t i = lo; i < hi; ++i) {
+            float v = qf::fake_quantize_value(xi[i], sw[static_cast<size_t>(i / per)], q);
+            if (half) v = qf::round_to_half(v);
+            out[i] = v;
+          }
+        });
+        cs += out[0];
+        if (do_bwd) {
+          qf::FakeQuantGrad g = qf::fake_quantize_backward(
+              tx[p], std::span<const double>(log_s[p], static_cast<size_t>(C)), cfg, tu[p], prec_of(half));
+          cs += g.d_log_scale[0];
+        }
+      }
+    }
+    const auto t1 = std::chrono::steady_clock::now();
+    *seconds = std::chrono::duration<double>(t1 - t0).count();
+    if (checksum) *checksum = cs;
+  });
+}
+
+// ---------------------------------------------------------------------
 // Formats (tensor_io.hpp, distill.hpp:287-362) and the distillation loss
 // (distill.hpp:66-141), for the f3/f4 parity tests and golden fixtures.
 // ---------------------------------------------------------------------

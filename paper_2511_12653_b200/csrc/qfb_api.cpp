@@ -123,6 +123,8 @@ struct qfb_ctx {
   // consumer-side partials (default), 1 tile kernel as in round 1 ("tile1"),
   // 2 streaming kernel ("stream")
   int bwd_impl = 0;
+  // consumer layout of the full-tile kernel (QFB_BWD_IMPL=tile[q][m][d] at creation)
+  uint32_t bwd_layout = kBwdLayoutDD;  // measured best (r02)
   // status word the forward kernels latch into: d_status, or a host-pass
   // slot's own word while that slot's kernels are enqueued
   uint32_t* cur_status = nullptr;
@@ -523,8 +525,17 @@ qfb_status qfb_ctx_create(int32_t device, void* stream, qfb_ctx** out) {
       int per = 0;
       if (sbwd_occupancy(dt, sb_stages(dt), &per) == cudaSuccess && per > 0) c->sb_blocks_per_sm[dt] = per;
     }
-    if (const char* env = getenv("QFB_BWD_IMPL"))
+    if (const char* env = getenv("QFB_BWD_IMPL")) {
       c->bwd_impl = std::strcmp(env, "stream") == 0 ? 2 : std::strcmp(env, "tile1") == 0 ? 1 : 0;
+      // consumer layout of the full-tile kernel (A/B runs and per-layout
+      // tests): "tile" + any of q (quad), m (magic rint), d (dd quotient)
+      if (std::strncmp(env, "tile", 4) == 0 && env[4] != '1') {
+        uint32_t l = 0;
+        for (const char* p = env + 4; *p; ++p)
+          l |= *p == 'q' ? kBwdLayoutQuad : *p == 'm' ? kBwdLayoutMagic : *p == 'd' ? kBwdLayoutDD : 0u;
+        c->bwd_layout = l;
+      }
+    }
     if (const char* env = getenv("QFB_DISABLE_TMA_FWD"))
       if (env[0] == '1') std::memset(c->tma_blocks_per_sm, 0, sizeof c->tma_blocks_per_sm);
     if (const char* env = getenv("QFB_FWD_STAGES")) {
@@ -1032,6 +1043,7 @@ qfb_status qfb_fq_bwd_multi(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc* t
     b.n = cnt;
     b.tile_begin[cnt] = (uint32_t)tb;
     b.warp_part = warp_part ? 1u : 0u;
+    b.layout = ctx->bwd_layout;
     if (stream) {
       const int grid = ctx->sm_count * ctx->sb_blocks_per_sm[dtype];
       cudaError_t e = launch_sbwd(dtype, sb_stages(dtype), b, grid, ctx->stream);
@@ -1050,11 +1062,11 @@ qfb_status qfb_fq_bwd_multi(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc* t
     bwd_ring_size(dtype, max_tile, &b.stage_elems, &b.nstages, &smem);
     // cached: keeps steady-state launches free of runtime queries (graph capture)
     int per_sm = 0;
-    const size_t key = smem * 2 + (warp_part ? 1 : 0);
+    const size_t key = (smem * 2 + (warp_part ? 1 : 0)) * 4 + b.layout;
     for (const auto& kv : ctx->bwd_occ[dtype])
       if (kv.first == key) per_sm = kv.second;
     if (per_sm == 0) {
-      if (bwd_occupancy_smem(dtype, smem, &per_sm, warp_part) != cudaSuccess || per_sm < 1) per_sm = 1;
+      if (bwd_occupancy_smem(dtype, smem, &per_sm, warp_part, b.layout) != cudaSuccess || per_sm < 1) per_sm = 1;
       ctx->bwd_occ[dtype].emplace_back(key, per_sm);
     }
     const int grid = ctx->sm_count * per_sm;

@@ -313,12 +313,33 @@ __device__ __forceinline__ double group_sum(T* sx, const T* su, int glen, const 
 //    and such an element makes the group sum non-finite (term = inf or
 //    NaN; a finite term is < 2^136), so one test per group finds it and
 //    fix_nonfinite_up rewrites those d_input values.
+// rint(z) for |z| < 2^51 (every z with |z| <= q): RN(z + 1.5*2^52) lies in
+// (2^52, 2^53) where the spacing is 1, so the add rounds z to the nearest
+// integer, ties to even, and the subtraction is exact. Two DADDs on the
+// FP64 pipe instead of FRND.F64 on the quarter-rate XU pipe; identical bits
+// to rint(z) - z, including the +0 of integer z.
+__device__ __forceinline__ double rint_small(double z) {
+  return __dadd_rn(__dadd_rn(z, 0x1.8p52), -0x1.8p52);
+}
+
+// Arithmetic options of the fast path (template M): kMathMagic = rint by
+// rint_small, kMathDD = quotient by markstein_dd. Bit-identical results.
+constexpr int kMathMagic = 1;
+constexpr int kMathDD = 2;
+
+template <int M>
+__device__ __forceinline__ double quotient(double x, const DivCtx& dc) {
+  return (M & kMathDD) ? markstein_dd(x, dc) : markstein2_div(x, dc);
+}
+
+template <int M = 0>
 __device__ __forceinline__ double fast_term(float xv, float uv, const DivCtx& dc, double q,
                                             float& dx) {
-  const double z = markstein2_div((double)xv, dc);
+  const double z = quotient<M>((double)xv, dc);
   const bool mask = fabs(z) <= q;
   const double sat = xv > 0.0f ? q : -q;
-  const double d_ds = mask ? __dadd_rn(rint(z), -z) : sat;
+  const double r = (M & kMathMagic) ? rint_small(z) : rint(z);
+  const double d_ds = mask ? __dadd_rn(r, -z) : sat;
   dx = mask ? uv : __uint_as_float(__float_as_uint(uv) & 0x80000000u);
   return __dmul_rn(d_ds, (double)uv);
 }
@@ -332,13 +353,15 @@ __device__ __forceinline__ double h2d(__half h) {
   asm("cvt.f64.f16 %0, %1;" : "=d"(d) : "h"(__half_as_ushort(h)));
   return d;
 }
+template <int M = 0>
 __device__ __forceinline__ double fast_term_h(__half xh, __half uh, const DivCtx& dc, double q,
                                               __half* dx) {
   const double xd = h2d(xh);
-  const double z = markstein2_div(xd, dc);
+  const double z = quotient<M>(xd, dc);
   const bool mask = fabs(z) <= q;
   const double sat = xd > 0.0 ? q : -q;
-  const double d_ds = mask ? __dadd_rn(rint(z), -z) : sat;
+  const double r = (M & kMathMagic) ? rint_small(z) : rint(z);
+  const double d_ds = mask ? __dadd_rn(r, -z) : sat;
   if (dx) {
     const unsigned short b = __half_as_ushort(uh);
     *dx = __ushort_as_half(mask ? b : (unsigned short)(b & 0x8000u));
@@ -360,7 +383,7 @@ static __device__ __noinline__ void fix_nonfinite_up(T* sx, const T* su, int gle
   }
 }
 
-template <typename T, bool kDx, int LR>
+template <typename T, bool kDx, int LR, int M = 0>
 __device__ __forceinline__ double group_sum_lr_u(T* sx, const T* su, int h, const DivCtx& dc,
                                                  double q) {
   T* rx = sx + h;
@@ -372,14 +395,14 @@ __device__ __forceinline__ double group_sum_lr_u(T* sx, const T* su, int h, cons
     const bool l0 = k < LR - 1 || lv;  // left slot k valid
     double t0, t2;
     if constexpr (sizeof(T) == 2) {
-      t0 = l0 ? fast_term_h(sx[k], su[k], dc, q, kDx ? sx + k : nullptr) : 0.0;
-      t2 = fast_term_h(rx[k], ru[k], dc, q, kDx ? rx + k : nullptr);
+      t0 = l0 ? fast_term_h<M>(sx[k], su[k], dc, q, kDx ? sx + k : nullptr) : 0.0;
+      t2 = fast_term_h<M>(rx[k], ru[k], dc, q, kDx ? rx + k : nullptr);
     } else {
       const float x0 = l0 ? to_f<T>(sx[k]) : 0.0f, u0 = l0 ? to_f<T>(su[k]) : 0.0f;
       const float x2 = to_f<T>(rx[k]), u2 = to_f<T>(ru[k]);
       float d0, d2;
-      t0 = fast_term(x0, u0, dc, q, d0);
-      t2 = fast_term(x2, u2, dc, q, d2);
+      t0 = fast_term<M>(x0, u0, dc, q, d0);
+      t2 = fast_term<M>(x2, u2, dc, q, d2);
       if (kDx) {
         if (l0) sx[k] = from_f<T>(d0);
         rx[k] = from_f<T>(d2);
@@ -396,19 +419,124 @@ __device__ __forceinline__ double group_sum_lr_u(T* sx, const T* su, int h, cons
 
 // Dispatch on the right-half length (groups of 9..16 elements, the only
 // sizes of rows with >= 16 * 2^g elements); other sizes take the generic loop.
-template <typename T, bool kDx>
+template <typename T, bool kDx, int M = 0>
 __device__ __forceinline__ double group_sum_any(T* sx, const T* su, int glen, const DivCtx& dc,
                                                 double q) {
   if (glen >= 9 && dc.usable) {
     const int lr = (glen + 1) >> 1, h = glen >> 1;
     switch (lr) {
-      case 5: return group_sum_lr_u<T, kDx, 5>(sx, su, h, dc, q);
-      case 6: return group_sum_lr_u<T, kDx, 6>(sx, su, h, dc, q);
-      case 7: return group_sum_lr_u<T, kDx, 7>(sx, su, h, dc, q);
-      default: return group_sum_lr_u<T, kDx, 8>(sx, su, h, dc, q);
+      case 5: return group_sum_lr_u<T, kDx, 5, M>(sx, su, h, dc, q);
+      case 6: return group_sum_lr_u<T, kDx, 6, M>(sx, su, h, dc, q);
+      case 7: return group_sum_lr_u<T, kDx, 7, M>(sx, su, h, dc, q);
+      default: return group_sum_lr_u<T, kDx, 8, M>(sx, su, h, dc, q);
     }
   }
   return group_sum<T, kDx>(sx, su, glen, dc, q);  // short groups / unusable scales: checked
+}
+
+// ---------------------------------------------------------------------
+// Quad consumer (kQuad): 4 consumer warps, each lane owns TWO adjacent leaf
+// groups of the tile (2t, 2t+1: the children of node t at depth g - 1), so
+// four fold chains (left/right half of each group) run interleaved per lane
+// and the per-tile work of a warp (barrier wait, descriptor reads, tree
+// butterfly, handoff) is spread over twice the elements. The lane's two
+// group sums form their parent node (A + B); a 5-level xor butterfly gives
+// the warp's 64-group subtree, and the producer combines the 4 warp sums.
+// ---------------------------------------------------------------------
+struct PairCache {
+  int k0 = -1, lo0 = 0, m0 = 0;
+  int k1 = -1, lo1 = 0, m1 = 0;
+  // parent node of lane pair t (path t, g - 1 levels) in a tile of m elements
+  __device__ __forceinline__ void get(int m, int g, int t, int& plo, int& pm) {
+    const int k = m | (g << 16);
+    if (k0 == k) {
+      plo = lo0;
+      pm = m0;
+      return;
+    }
+    if (k1 == k) {
+      plo = lo1;
+      pm = m1;
+      return;
+    }
+    int l = 0, mm = m;
+    descend<int>(l, mm, (uint32_t)t, g - 1);
+    k1 = k0;
+    lo1 = lo0;
+    m1 = m0;
+    k0 = k;
+    lo0 = l;
+    m0 = mm;
+    plo = l;
+    pm = mm;
+  }
+};
+
+// One fold slot of a half-group: term of element k (predicated on `on`),
+// d_input written back in place when kDx.
+template <typename T, bool kDx, int M>
+__device__ __forceinline__ void quad_slot(T* px, const T* pu, int k, bool on, const DivCtx& dc, double q,
+                                          double& acc) {
+  double t;
+  if constexpr (sizeof(T) == 2) {
+    t = fast_term_h<M>(px[k], pu[k], dc, q, (kDx && on) ? px + k : nullptr);
+  } else {
+    float d;
+    t = fast_term<M>(on ? px[k] : 0.0f, on ? pu[k] : 0.0f, dc, q, d);
+    if (kDx && on) px[k] = d;
+  }
+  if (on) acc = __dadd_rn(acc, t);
+}
+
+// Sums of two sibling leaf groups A = [0, la), B = [la, la + lb) (9..16
+// elements each, lb - la in {0, 1}) in the reference order, four chains
+// interleaved: fold(A left) + fold(A right), fold(B left) + fold(B right).
+// LR = the longest half; only the last two slots can be short.
+template <typename T, bool kDx, int M, int LR>
+__device__ __forceinline__ double quad_sum_u(T* sx, const T* su, int la, int lb, const DivCtx& dc, double q) {
+  const int ha = la >> 1, hb = lb >> 1;
+  const int ra = la - ha, rb = lb - hb;
+  T* ax = sx;
+  T* arx = sx + ha;
+  T* bx = sx + la;
+  T* brx = sx + la + hb;
+  const T* au = su;
+  const T* aru = su + ha;
+  const T* bu = su + la;
+  const T* bru = su + la + hb;
+  double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+  for (int k = 0; k < LR; ++k) {
+    const bool tail = k >= LR - 2;
+    quad_slot<T, kDx, M>(ax, au, k, !tail || k < ha, dc, q, a0);
+    quad_slot<T, kDx, M>(arx, aru, k, !tail || k < ra, dc, q, a1);
+    quad_slot<T, kDx, M>(bx, bu, k, !tail || k < hb, dc, q, b0);
+    quad_slot<T, kDx, M>(brx, bru, k, !tail || k < rb, dc, q, b1);
+  }
+  const double va = __dadd_rn(a0, a1);
+  const double vb = __dadd_rn(b0, b1);
+  if (kDx && __builtin_expect((__double2hiint(va) & 0x7ff00000) == 0x7ff00000, 0)) fix_nonfinite_up<T>(sx, su, la);
+  if (kDx && __builtin_expect((__double2hiint(vb) & 0x7ff00000) == 0x7ff00000, 0))
+    fix_nonfinite_up<T>(sx + la, su + la, lb);
+  return __dadd_rn(va, vb);
+}
+
+template <typename T, bool kDx, int M>
+__device__ __forceinline__ double quad_sum(T* sx, const T* su, int pm, const DivCtx& dc, double q) {
+  const int la = pm >> 1, lb = pm - la;
+  if (la >= 9 && dc.usable) {
+    const int lr = ((lb + 1) >> 1) > ((la + 1) >> 1) ? ((lb + 1) >> 1) : ((la + 1) >> 1);
+    switch (lr) {
+      case 5: return quad_sum_u<T, kDx, M, 5>(sx, su, la, lb, dc, q);
+      case 6: return quad_sum_u<T, kDx, M, 6>(sx, su, la, lb, dc, q);
+      case 7: return quad_sum_u<T, kDx, M, 7>(sx, su, la, lb, dc, q);
+      default: return quad_sum_u<T, kDx, M, 8>(sx, su, la, lb, dc, q);
+    }
+  }
+  // short groups / unusable scales: the checked per-group path
+  const double va = group_sum<T, kDx>(sx, su, la, dc, q);
+  const double vb = group_sum<T, kDx>(sx + la, su + la, lb, dc, q);
+  return __dadd_rn(va, vb);
 }
 
 // ---------------------------------------------------------------------
@@ -423,7 +551,17 @@ __device__ __forceinline__ double group_sum_any(T* sx, const T* su, int glen, co
 // Consumers never execute a CTA-wide barrier.
 // ---------------------------------------------------------------------
 constexpr int kConsumerWarps = kBwdThreads / 32;      // 8
-constexpr int kBwdCtaThreads = kBwdThreads + 32;     // + producer warp
+constexpr int kQuad = 64;         // 4 consumer warps x 2 leaf groups per lane (see quad_sum)
+constexpr int kMagicRint = 256;   // rint via rint_small (FP64 pipe) instead of FRND (XU pipe)
+constexpr int kDDiv = 2048;       // quotient via markstein_dd (4 FP64 ops) instead of markstein2_div (5)
+template <int V>
+__host__ __device__ constexpr int math_of() {
+  return ((V & kMagicRint) ? kMathMagic : 0) | ((V & kDDiv) ? kMathDD : 0);
+}
+template <int V>
+__host__ __device__ constexpr int cons_warps() { return (V & kQuad) ? 4 : kConsumerWarps; }
+template <int V>
+__host__ __device__ constexpr int cta_threads() { return cons_warps<V>() * 32 + 32; }
 
 __device__ __forceinline__ TileRef shfl_ref(const TileRef& r, int src) {
   constexpr unsigned kAll = 0xffffffffu;
@@ -540,7 +678,8 @@ __device__ __forceinline__ void store_dx(const BwdDesc& d, const TileRef& cur, S
 constexpr int kTwoCtas = 128;
 
 template <typename T, int V>
-__global__ void __launch_bounds__(kBwdCtaThreads, (V & kTwoCtas) ? 2 : 3) bwd_kernel(const __grid_constant__ BwdBatch bt) {
+__global__ void __launch_bounds__(cta_threads<V>(), (V & kTwoCtas) ? 2 : 3) bwd_kernel(const __grid_constant__ BwdBatch bt) {
+  constexpr int CW = cons_warps<V>();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[kMaxStages];
   __shared__ __align__(8) uint64_t done[kMaxStages];
@@ -561,7 +700,7 @@ __global__ void __launch_bounds__(kBwdCtaThreads, (V & kTwoCtas) ? 2 : 3) bwd_ke
   if (tid == 0) {
     for (int s = 0; s < nst; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&done[s], kConsumerWarps);
+      mbar_init(&done[s], CW);
     }
     fence_mbar_init();
     // the finisher (launched as a programmatic dependent) may be scheduled
@@ -571,7 +710,7 @@ __global__ void __launch_bounds__(kBwdCtaThreads, (V & kTwoCtas) ? 2 : 3) bwd_ke
   }
   __syncthreads();  // the only CTA barrier: barrier init
 
-  if (warp == kConsumerWarps) {
+  if (warp == CW) {
     // ----------------------------- producer warp -----------------------
     // TileRefs are located 32 at a time (lane i: the CTA's tile ordinal
     // 32*b + i) and broadcast when needed, so the scale load in locate_full
@@ -621,9 +760,9 @@ __global__ void __launch_bounds__(kBwdCtaThreads, (V & kTwoCtas) ? 2 : 3) bwd_ke
         const double part = lane_subtree(d, red[2 * s + par], lane);
         tile_sum(d, cur, part);
       } else {
-        double w = lane < kConsumerWarps ? red[2 * s + par][lane] : 0.0;
+        double w = lane < CW ? red[2 * s + par][lane] : 0.0;
 #pragma unroll
-        for (int o = 1; o < kConsumerWarps; o <<= 1) w = __dadd_rn(w, __shfl_xor_sync(0xffffffffu, w, o));
+        for (int o = 1; o < CW; o <<= 1) w = __dadd_rn(w, __shfl_xor_sync(0xffffffffu, w, o));
         if (lane == 0) d.partials[((uint64_t)cur.seg << d.part_log) + cur.t] = w;
       }
       s = s + 1 == nst ? 0 : s + 1;
@@ -635,6 +774,7 @@ __global__ void __launch_bounds__(kBwdCtaThreads, (V & kTwoCtas) ? 2 : 3) bwd_ke
   // ------------------------------- consumer warps ----------------------
   uint32_t full_phase = 0;
   GroupCache gc;
+  PairCache pc;
   int s = 0;
   for (uint32_t tile_id = blockIdx.x; tile_id < total; tile_id += gridDim.x) {
     const uint32_t par = (full_phase >> s) & 1u;
@@ -644,18 +784,32 @@ __global__ void __launch_bounds__(kBwdCtaThreads, (V & kTwoCtas) ? 2 : 3) bwd_ke
     const TileRef cur = refs[s];
     const BwdDesc& d = bt.d[cur.di];
 
-    int glo, glen;
-    gc.get(cur.m, (int)d.g, tid, glo, glen);
     DivCtx dc;
     dc.s = pin(cur.s);
     dc.y = pin(cur.y);
+    dc.ylo = (V & kDDiv) ? pin(recip_lo(cur.s, cur.y)) : 0.0;
     dc.usable = cur.s >= 0x1p-100 && cur.s <= 0x1p100;
     const double q = pin(d.q);
-    T* sx = st.x + cur.off + glo;
-    const T* su = st.up + cur.off + glo;
-    double v = (V & kProbeNoCompute) ? 0.0
-             : (d.dx != nullptr && !(V & kProbeNoLoads)) ? group_sum_any<T, true>(sx, su, glen, dc, q)
-                                                          : group_sum_any<T, false>(sx, su, glen, dc, q);
+    double v;
+    if constexpr ((V & kQuad) != 0) {
+      int plo, pm;
+      pc.get(cur.m, (int)d.g, tid, plo, pm);
+      T* sx = st.x + cur.off + plo;
+      const T* su = st.up + cur.off + plo;
+      constexpr int kM = math_of<V>();
+      v = (V & kProbeNoCompute) ? 0.0
+        : (d.dx != nullptr && !(V & kProbeNoLoads)) ? quad_sum<T, true, kM>(sx, su, pm, dc, q)
+                                                     : quad_sum<T, false, kM>(sx, su, pm, dc, q);
+    } else {
+      int glo, glen;
+      gc.get(cur.m, (int)d.g, tid, glo, glen);
+      T* sx = st.x + cur.off + glo;
+      const T* su = st.up + cur.off + glo;
+      constexpr int kM = math_of<V>();
+      v = (V & kProbeNoCompute) ? 0.0
+        : (d.dx != nullptr && !(V & kProbeNoLoads)) ? group_sum_any<T, true, kM>(sx, su, glen, dc, q)
+                                                     : group_sum_any<T, false, kM>(sx, su, glen, dc, q);
+    }
     if constexpr ((V & kWarpPart) != 0) {
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -1215,24 +1369,52 @@ static int variant() {
   return v;
 }
 
+// A kernel instance and its block size.
+struct BwdFn {
+  const void* fn;
+  int threads;
+};
+template <typename T, int V>
+BwdFn bwd_inst() {
+  return BwdFn{(const void*)bwd_kernel<T, V>, cta_threads<V>()};
+}
+
+// The production instance for a batch: the generic kernel when some row
+// has short tiles, else the full-tile kernel with the batch's consumer
+// layout. QFB_BWD_VARIANT (diagnostics) selects the probes: 8 memory
+// pipeline only, 16 arithmetic only (on the generic kernel, or with
+// kQuad | kMagicRint set: on the quad kernel).
 template <typename T>
-const void* kernel_ptr(int v, bool warp_part) {
+BwdFn kernel_ptr(int v, bool warp_part, uint32_t layout) {
+  constexpr int kQM = kWarpPart | kQuad | kMagicRint;
   switch (v) {
-    case kProbeNoCompute: return (const void*)bwd_kernel<T, kProbeNoCompute>;
-    case kProbeNoLoads: return (const void*)bwd_kernel<T, kProbeNoLoads>;
-    default: {
-      static const bool two = [] {
-        const char* e = getenv("QFB_BWD_CTAS");
-        return e && e[0] == '2';
-      }();
-      if (!warp_part) return (const void*)bwd_kernel<T, 0>;
-      return two ? (const void*)bwd_kernel<T, kWarpPart | kTwoCtas> : (const void*)bwd_kernel<T, kWarpPart>;
-    }
+    case kProbeNoCompute: return bwd_inst<T, kProbeNoCompute>();
+    case kProbeNoLoads: return bwd_inst<T, kProbeNoLoads>();
+    case kQM | kProbeNoCompute: if (warp_part) return bwd_inst<T, kQM | kProbeNoCompute>(); break;
+    case kQM | kProbeNoLoads: if (warp_part) return bwd_inst<T, kQM | kProbeNoLoads>(); break;
+    default: break;
+  }
+  if (!warp_part) return bwd_inst<T, 0>();
+  static const bool two = [] {
+    const char* e = getenv("QFB_BWD_CTAS");
+    return e && e[0] == '2';
+  }();
+  // layout bits: kBwdLayoutMagic | kBwdLayoutQuad | kBwdLayoutDD
+  switch (layout & 7u) {
+    case 1: return bwd_inst<T, kWarpPart | kMagicRint>();
+    case 2: return bwd_inst<T, kWarpPart | kQuad>();
+    case 3: return bwd_inst<T, kWarpPart | kQuad | kMagicRint>();
+    case 4: return bwd_inst<T, kWarpPart | kDDiv>();
+    case 5: return bwd_inst<T, kWarpPart | kMagicRint | kDDiv>();
+    case 6: return bwd_inst<T, kWarpPart | kQuad | kDDiv>();
+    case 7: return bwd_inst<T, kWarpPart | kQuad | kMagicRint | kDDiv>();
+    default: return two ? bwd_inst<T, kWarpPart | kTwoCtas>() : bwd_inst<T, kWarpPart>();
   }
 }
 
-const void* bwd_fn(int dtype, bool warp_part = false) {
-  return dtype == 0 ? kernel_ptr<float>(variant(), warp_part) : kernel_ptr<__half>(variant(), warp_part);
+BwdFn bwd_fn(int dtype, bool warp_part, uint32_t layout) {
+  return dtype == 0 ? kernel_ptr<float>(variant(), warp_part, layout)
+                    : kernel_ptr<__half>(variant(), warp_part, layout);
 }
 
 }  // namespace
@@ -1245,11 +1427,11 @@ cudaError_t bwd_occupancy(int dtype, int* blocks_per_sm) {
   return bwd_occupancy_smem(dtype, smem, blocks_per_sm);
 }
 
-cudaError_t bwd_occupancy_smem(int dtype, size_t smem, int* blocks_per_sm, bool warp_part) {
-  const void* f = bwd_fn(dtype, warp_part);
-  cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
+cudaError_t bwd_occupancy_smem(int dtype, size_t smem, int* blocks_per_sm, bool warp_part, uint32_t layout) {
+  const BwdFn f = bwd_fn(dtype, warp_part, layout);
+  cudaError_t e = cudaFuncSetAttribute(f.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, kBwdCtaThreads, smem);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f.fn, f.threads, smem);
 }
 
 cudaError_t launch_bwd(int dtype, const BwdBatch& b, int grid, cudaStream_t st) {
@@ -1258,9 +1440,9 @@ cudaError_t launch_bwd(int dtype, const BwdBatch& b, int grid, cudaStream_t st) 
   if ((uint32_t)grid > tiles) grid = (int)tiles;
   const size_t smem = (size_t)b.nstages * (2 * b.stage_elems * (dtype == 0 ? 4 : 2) + kRedBytes);
   void* args[] = {const_cast<BwdBatch*>(&b)};
-  const void* fn = bwd_fn(dtype, b.warp_part != 0);
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
-  cudaError_t e = launch_main(fn, dim3(grid), dim3(kBwdCtaThreads), args, smem, st, kPdlBwd);
+  const BwdFn f = bwd_fn(dtype, b.warp_part != 0, b.layout);
+  cudaFuncSetAttribute(f.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
+  cudaError_t e = launch_main(f.fn, dim3(grid), dim3(f.threads), args, smem, st, kPdlBwd);
   if (e != cudaSuccess) return e;
   return launch_bwd_finish(b, st);
 }

@@ -190,6 +190,7 @@ __device__ __forceinline__ GradTerm grad_term(float x, double s, double q) {
 struct DivCtx {
   double s;
   double y;     // RN(1/s)
+  double ylo;   // RN(RN(1 - s*y) * y): y + ylo = 1/s to ~2^-105 (markstein_dd only)
   bool usable;  // s in [2^-100, 2^100]
 };
 
@@ -214,6 +215,23 @@ __device__ __forceinline__ double markstein2_div(double x, const DivCtx& c) {
   const double q0 = __dmul_rn(x, c.y);
   const double z1 = __fma_rn(__fma_rn(-c.s, q0, x), c.y, q0);
   return __fma_rn(__fma_rn(-c.s, z1, x), c.y, z1);
+}
+
+// Low half of the double-double reciprocal: 1 - s*y is exact (FMA residual
+// of the correctly rounded reciprocal), times y ~ (1/s - y).
+__device__ __forceinline__ double recip_lo(double s, double y) { return __dmul_rn(__fma_rn(-s, y, 1.0), y); }
+
+// z = RN(x / s) from the double-double reciprocal (y, ylo) and ONE
+// Markstein correction: q0 = RN(x*y + RN(x*ylo)) is within 1/2 ulp +
+// 2^-103 |x/s| of x/s (faithful), so z = RN(q0 + (x - s*q0)*y) is the
+// correctly rounded quotient (y = RN(1/s), q0 faithful: Markstein's
+// theorem). Four FP64 ops at dependency depth 4 (markstein2_div: five,
+// depth 5). Same domain as markstein2_div (s in [2^-100, 2^100], finite
+// x; inf/NaN x give NaN). Validated against __ddiv_rn for all 2^32 float x
+// and 40,290 scales (tools/verify_ddiv3.cu, profiles/r02_verify_ddiv3.txt).
+__device__ __forceinline__ double markstein_dd(double x, const DivCtx& c) {
+  const double q0 = __fma_rn(x, c.y, __dmul_rn(x, c.ylo));
+  return __fma_rn(__fma_rn(-c.s, q0, x), c.y, q0);
 }
 
 // ------------------------------------------------------ fast divide ---

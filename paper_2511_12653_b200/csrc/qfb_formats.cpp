@@ -19,10 +19,9 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
-#include <fstream>
-#include <iterator>
 #include <map>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/qfb.h"
@@ -33,43 +32,49 @@ namespace {
 using qfb::set_error;
 
 // ------------------------------------------------------------ bytes ---
+// Both formats are little-endian on disk. The host is little-endian (x86-64,
+// aarch64), so scalars are copied as raw bytes; the static_assert keeps a
+// big-endian port from silently writing the wrong byte order.
+static_assert(__BYTE_ORDER__ == __ORDER_LITTLE_ENDIAN__, "qfb formats assume a little-endian host");
+
 template <typename T>
 void put_le(std::string& out, T v) {
-  for (size_t i = 0; i < sizeof(T); ++i) out.push_back(static_cast<char>((static_cast<uint64_t>(v) >> (8 * i)) & 0xff));
+  static_assert(std::is_trivially_copyable<T>::value, "raw scalar");
+  char raw[sizeof(T)];
+  std::memcpy(raw, &v, sizeof(T));
+  out.append(raw, sizeof(T));
 }
 
 template <typename T>
 T get_le(const char* p) {
-  uint64_t v = 0;
-  for (size_t i = 0; i < sizeof(T); ++i) v |= static_cast<uint64_t>(static_cast<unsigned char>(p[i])) << (8 * i);
-  return static_cast<T>(v);
+  T v;
+  std::memcpy(&v, p, sizeof(T));
+  return v;
 }
 
-void put_f32(std::string& out, float f) {
-  uint32_t u;
-  std::memcpy(&u, &f, 4);
-  put_le<uint32_t>(out, u);
-}
-
-float get_f32(const char* p) {
-  const uint32_t u = get_le<uint32_t>(p);
-  float f;
-  std::memcpy(&f, &u, 4);
-  return f;
-}
+// float32 payloads move by bit pattern (NaN payloads and -0 preserved)
+void put_f32(std::string& out, float f) { put_le<float>(out, f); }
+float get_f32(const char* p) { return get_le<float>(p); }
 
 bool read_file(const char* path, std::string& out) {
-  std::ifstream f(path, std::ios::binary);
+  FILE* f = std::fopen(path, "rb");
   if (!f) return false;
-  out.assign((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
-  return true;
+  out.clear();
+  char buf[1 << 16];
+  size_t got;
+  while ((got = std::fread(buf, 1, sizeof buf, f)) > 0) out.append(buf, got);
+  const bool ok = !std::ferror(f);
+  std::fclose(f);
+  return ok;
 }
 
+// IoError texts as the reference's writer reports them (tensor_io.hpp:101-106)
 qfb_status write_file(const char* path, const std::string& bytes) {
-  std::ofstream f(path, std::ios::binary | std::ios::trunc);
+  FILE* f = std::fopen(path, "wb");
   if (!f) return set_error(QFB_ERR_IO, (std::string("cannot open for writing: ") + path).c_str());
-  f.write(bytes.data(), static_cast<std::streamsize>(bytes.size()));
-  if (!f) return set_error(QFB_ERR_IO, (std::string("write failed: ") + path).c_str());
+  const bool ok = std::fwrite(bytes.data(), 1, bytes.size(), f) == bytes.size();
+  const bool closed = std::fclose(f) == 0;
+  if (!ok || !closed) return set_error(QFB_ERR_IO, (std::string("write failed: ") + path).c_str());
   return QFB_OK;
 }
 

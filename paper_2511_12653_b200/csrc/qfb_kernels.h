@@ -192,12 +192,25 @@ struct BwdBatch {
   int32_t nstages;       // TMA ring depth (2..4), sized from the max tile
   uint32_t stage_elems;  // elements per array per stage (16-byte multiple)
   uint32_t warp_part;    // tile kernel: consumer warps store the partials (tps_log = depth - 5)
+  uint32_t layout;       // full-tile consumer layout: kBwdLayout* (warp_part batches only)
+  uint32_t pad0;
   uint32_t tile_begin[kMaxBwdDesc + 1];
   BwdDesc d[kMaxBwdDesc];
 };
 
+// Consumer layouts of the full-tile kernel (BwdBatch::layout), bit flags:
+// 8 warps x 1 leaf group per lane, or (kBwdLayoutQuad) 4 warps x 2 adjacent
+// groups per lane (quad_sum); rint by FRND.F64 or (kBwdLayoutMagic) by the
+// magic-number add (rint_small); the quotient by markstein2_div or
+// (kBwdLayoutDD) markstein_dd. Every layout gives the same bits.
+constexpr uint32_t kBwdLayout8 = 0;
+constexpr uint32_t kBwdLayoutMagic = 1;
+constexpr uint32_t kBwdLayoutQuad = 2;
+constexpr uint32_t kBwdLayoutDD = 4;
+
 cudaError_t bwd_occupancy(int dtype, int* blocks_per_sm);  // at the default ring size
-cudaError_t bwd_occupancy_smem(int dtype, size_t smem, int* blocks_per_sm, bool warp_part = false);
+cudaError_t bwd_occupancy_smem(int dtype, size_t smem, int* blocks_per_sm, bool warp_part = false,
+                               uint32_t layout = kBwdLayout8);
 // Ring sizing: stage_elems / nstages / dynamic smem for a batch whose
 // largest tile has max_tile elements.
 void bwd_ring_size(int dtype, uint32_t max_tile, uint32_t* stage_elems, int32_t* nstages,

@@ -30,5 +30,5 @@ e1.record(stream)
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 200
 b = fp.bytes_per_step()["bwd"]
-print(json.dumps({"dtype": dt, "variant": os.environ.get("QFB_BWD_VARIANT", "0"), "us": ms * 1e3,
+print(json.dumps({"dtype": dt, "variant": os.environ.get("QFB_BWD_VARIANT", "0"), "impl": os.environ.get("QFB_BWD_IMPL", ""), "us": ms * 1e3,
                   "gbps": b / (ms / 1e3) / 1e9, "frac": b / (ms / 1e3) / 1e9 / 6551.0}))
