@@ -58,6 +58,9 @@ def parse(argv=None):
                    help="reference arm: skip the one-thread sample")
     p.add_argument("--no-secondary", action="store_true",
                    help="skip the config-3 chain window and config-5 forward-throughput lines")
+    p.add_argument("--half-fp32-terms", action="store_true",
+                   help="f16: the opt-in float32-term backward (QFB_OPT_BWD_HALF_FP32; d_input bitwise, "
+                        "scale gradients within tolerance instead of bitwise)")
     return p.parse_args(argv)
 
 
@@ -314,7 +317,10 @@ def bench_config(args, ws):
             "parallelism": (f"frames sharded over {ws} GPUs (one process each); per step one "
                             f"exchange of the per-frame scale-gradient rows: NCCL all-gather + "
                             f"frame-order fold through the C-ABI (qfb_gather_fold_scale_grads)"
-                            if ws > 1 else "1 GPU")}
+                            if ws > 1 else "1 GPU"),
+            **({"backward_terms": "float32 (QFB_OPT_BWD_HALF_FP32): d_input bitwise, scale gradients "
+                                  "within the FP16 tolerance, not bitwise"}
+               if getattr(args, "half_fp32_terms", False) else {})}
 
 
 def run_reference_arm(args):
@@ -448,6 +454,8 @@ def run_qfb(args):
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
     ctx = q.Context(gpu, stream.cuda_stream)
+    if args.half_fp32_terms:
+        ctx.set_option(q.OPT_BWD_HALF_FP32, 1)
     # at N > 1 the step's backward leaves this rank's frame row for the
     # exchange; every rank holds distinct frames (frame_offset = rank)
     rows = None

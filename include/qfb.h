@@ -138,6 +138,14 @@ typedef struct qfb_ctx qfb_ctx;
 qfb_status qfb_ctx_create(int32_t device, void* stream, qfb_ctx** out);
 qfb_status qfb_ctx_destroy(qfb_ctx* ctx);
 qfb_status qfb_ctx_set_stream(qfb_ctx* ctx, void* stream);
+/* Context options. QFB_OPT_BWD_HALF_FP32 (value 0/1, default 0): binary16
+ * storage only — the STE/LSQ backward computes its scale-gradient terms in
+ * float32 instead of the reference's binary64 (quant.hpp:217-228). d_input
+ * stays bit-identical (the clip mask is decided exactly); d_log_s agrees
+ * with the reference within the FP16 tolerance (rel 1e-2; measured ~1e-6,
+ * DESIGN.md §2) instead of bitwise. Off: every result is bitwise. */
+#define QFB_OPT_BWD_HALF_FP32 1
+qfb_status qfb_ctx_set_option(qfb_ctx* ctx, int32_t option, int64_t value);
 void* qfb_ctx_stream(qfb_ctx* ctx);
 int32_t qfb_ctx_sm_count(qfb_ctx* ctx);
 /* Synchronize the stream; report (and clear) latched device conditions.

@@ -163,6 +163,8 @@ _sig("qfb_cast_scales_f32", _i32, [_pd, _i64, _pf])
 _sig("qfb_ctx_create", _i32, [_i32, _vp, ctypes.POINTER(_vp)])
 _sig("qfb_ctx_destroy", _i32, [_vp])
 _sig("qfb_ctx_set_stream", _i32, [_vp, _vp])
+_sig("qfb_ctx_set_option", _i32, [_vp, _i32, _i64])
+OPT_BWD_HALF_FP32 = 1  # QFB_OPT_BWD_HALF_FP32
 _sig("qfb_ctx_stream", _vp, [_vp])
 _sig("qfb_ctx_sm_count", _i32, [_vp])
 _sig("qfb_ctx_sync", _i32, [_vp])
@@ -305,6 +307,11 @@ class Context:
 
     def set_stream(self, stream: Optional[int]) -> None:
         check(_lib.qfb_ctx_set_stream(self.handle, _vp(stream or 0)))
+
+    def set_option(self, option: int, value: int) -> None:
+        """qfb_ctx_set_option, e.g. (OPT_BWD_HALF_FP32, 1): float32 terms in
+        the binary16 backward (d_input bitwise, d_log_s within tolerance)."""
+        check(_lib.qfb_ctx_set_option(self.handle, option, value))
 
     def sync(self) -> None:
         check(_lib.qfb_ctx_sync(self.handle))

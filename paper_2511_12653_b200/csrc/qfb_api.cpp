@@ -125,6 +125,7 @@ struct qfb_ctx {
   int bwd_impl = 0;
   // consumer layout of the full-tile kernel (QFB_BWD_IMPL=tile[q][m][d] at creation)
   uint32_t bwd_layout = kBwdLayoutDD;  // measured best (r02)
+  bool bwd_half_fp32 = false;           // QFB_OPT_BWD_HALF_FP32
   // status word the forward kernels latch into: d_status, or a host-pass
   // slot's own word while that slot's kernels are enqueued
   uint32_t* cur_status = nullptr;
@@ -532,7 +533,8 @@ qfb_status qfb_ctx_create(int32_t device, void* stream, qfb_ctx** out) {
       if (std::strncmp(env, "tile", 4) == 0 && env[4] != '1') {
         uint32_t l = 0;
         for (const char* p = env + 4; *p; ++p)
-          l |= *p == 'q' ? kBwdLayoutQuad : *p == 'm' ? kBwdLayoutMagic : *p == 'd' ? kBwdLayoutDD : 0u;
+          l |= *p == 'q' ? kBwdLayoutQuad : *p == 'm' ? kBwdLayoutMagic : *p == 'd' ? kBwdLayoutDD
+             : *p == '2' ? kBwdLayoutTwoCtas : 0u;
         c->bwd_layout = l;
       }
     }
@@ -586,6 +588,18 @@ qfb_status qfb_ctx_destroy(qfb_ctx* ctx) {
   if (ctx->s_out) cudaStreamDestroy(ctx->s_out);
   delete ctx;
   return QFB_OK;
+}
+
+qfb_status qfb_ctx_set_option(qfb_ctx* ctx, int32_t option, int64_t value) {
+  if (qfb_status st = check_ctx(ctx)) return st;
+  switch (option) {
+    case QFB_OPT_BWD_HALF_FP32:
+      if (value != 0 && value != 1) return fail(QFB_ERR_VALUE, "QFB_OPT_BWD_HALF_FP32 takes 0 or 1");
+      ctx->bwd_half_fp32 = value != 0;
+      return QFB_OK;
+    default:
+      return fail(QFB_ERR_VALUE, "unknown context option %d", option);
+  }
 }
 
 qfb_status qfb_ctx_set_stream(qfb_ctx* ctx, void* stream) {
@@ -1043,7 +1057,7 @@ qfb_status qfb_fq_bwd_multi(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc* t
     b.n = cnt;
     b.tile_begin[cnt] = (uint32_t)tb;
     b.warp_part = warp_part ? 1u : 0u;
-    b.layout = ctx->bwd_layout;
+    b.layout = ctx->bwd_layout | ((dtype == QFB_F16 && ctx->bwd_half_fp32) ? kBwdLayoutHalfF32 : 0u);
     if (stream) {
       const int grid = ctx->sm_count * ctx->sb_blocks_per_sm[dtype];
       cudaError_t e = launch_sbwd(dtype, sb_stages(dtype), b, grid, ctx->stream);
@@ -1062,7 +1076,7 @@ qfb_status qfb_fq_bwd_multi(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc* t
     bwd_ring_size(dtype, max_tile, &b.stage_elems, &b.nstages, &smem);
     // cached: keeps steady-state launches free of runtime queries (graph capture)
     int per_sm = 0;
-    const size_t key = (smem * 2 + (warp_part ? 1 : 0)) * 4 + b.layout;
+    const size_t key = (smem * 2 + (warp_part ? 1 : 0)) * 32 + b.layout;
     for (const auto& kv : ctx->bwd_occ[dtype])
       if (kv.first == key) per_sm = kv.second;
     if (per_sm == 0) {

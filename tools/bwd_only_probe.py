@@ -18,6 +18,8 @@ dev = torch.device("cuda:0")
 stream = torch.cuda.Stream(device=dev)
 torch.cuda.set_stream(stream)
 ctx = q.Context(0, stream.cuda_stream)
+if os.environ.get("QFB_HALF_FP32") == "1":
+    ctx.set_option(q.OPT_BWD_HALF_FP32, 1)
 fp = FrontendQuantPass(ctx, frames=1, dtype=dt, sets=2, seed=3, device=dev)
 for i in range(5):
     fp.backward(i % 2)
@@ -30,5 +32,5 @@ e1.record(stream)
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 200
 b = fp.bytes_per_step()["bwd"]
-print(json.dumps({"dtype": dt, "variant": os.environ.get("QFB_BWD_VARIANT", "0"), "impl": os.environ.get("QFB_BWD_IMPL", ""), "us": ms * 1e3,
+print(json.dumps({"dtype": dt, "variant": os.environ.get("QFB_BWD_VARIANT", "0"), "impl": os.environ.get("QFB_BWD_IMPL", "") + ("+h32" if os.environ.get("QFB_HALF_FP32") == "1" else ""), "us": ms * 1e3,
                   "gbps": b / (ms / 1e3) / 1e9, "frac": b / (ms / 1e3) / 1e9 / 6551.0}))
