@@ -597,8 +597,11 @@ __device__ __forceinline__ void h32_slot(__half* px, const __half* pu, int k, bo
   const bool mask = fabsf(x) <= hc.t;
   const float p = __fmul_rn(x, hc.yh);
   const float zl = __fmaf_rn(x, hc.yl, __fmaf_rn(x, hc.yh, -p));
-  float d = __fsub_rn(__fsub_rn(rintf(p), p), zl);
-  d = __fsub_rn(d, rintf(d));
+  // rint by the float magic number 1.5*2^23 (exact for |v| < 2^22, i.e. for
+  // every unclipped p and for d): two FADDs on the FMA pipe, not FRND on XU
+  constexpr float kM = 12582912.0f;
+  float d = __fsub_rn(__fsub_rn(__fsub_rn(__fadd_rn(p, kM), kM), p), zl);
+  d = __fsub_rn(d, __fsub_rn(__fadd_rn(d, kM), kM));
   const float sat = x > 0.0f ? hc.q : -hc.q;
   const float t = __fmul_rn(mask ? d : sat, u);
   if (kDx && on) {
@@ -665,6 +668,7 @@ constexpr int kQuad = 64;         // 4 consumer warps x 2 leaf groups per lane (
 constexpr int kMagicRint = 256;   // rint via rint_small (FP64 pipe) instead of FRND (XU pipe)
 constexpr int kDDiv = 2048;       // quotient via markstein_dd (4 FP64 ops) instead of markstein2_div (5)
 constexpr int kHalfF32 = 4096;    // binary16 storage, float32 terms (quad layout; QFB_OPT_BWD_HALF_FP32)
+constexpr int kL2Pre = 8192;      // producer prefetches the tile after the next refill into L2
 template <int V>
 __host__ __device__ constexpr int math_of() {
   return ((V & kMagicRint) ? kMathMagic : 0) | ((V & kDDiv) ? kMathDD : 0);
@@ -865,6 +869,19 @@ __global__ void __launch_bounds__(cta_threads<V>(), (V & kTwoCtas) ? 2 : 3) bwd_
       }
       __syncwarp();
       if (nid < total) produce<T, V>(bt, nr, st, &refs[s], &full[s], lane, true);
+      if constexpr ((V & kL2Pre) != 0) {
+        // the tile one refill further ahead: into L2 now, so its TMA load
+        // (issued when this stage frees up again) hits L2 instead of DRAM
+        const uint32_t pid = nid + gridDim.x;
+        if (pid < total) {
+          const TileRef pr = ref_of(k + (uint32_t)nst + 1u);
+          if (lane == 0 && pr.w1 > pr.w0) {
+            const BwdDesc& pd = bt.d[pr.di];
+            bulk_prefetch_l2(static_cast<const char*>(pd.x) + pr.w0, (uint32_t)(pr.w1 - pr.w0));
+            bulk_prefetch_l2(static_cast<const char*>(pd.up) + pr.w0, (uint32_t)(pr.w1 - pr.w0));
+          }
+        }
+      }
       // the tile's sums are read after the refill was issued (the next use
       // of this stage writes the other buffer)
       if constexpr ((V & kWarpPart) == 0) {
@@ -1519,6 +1536,8 @@ BwdFn kernel_ptr(int v, bool warp_part, uint32_t layout) {
     if (layout & kBwdLayoutHalfF32) return bwd_inst<T, kWarpPart | kQuad | kDDiv | kHalfF32>();
   const bool two = two_env || (layout & kBwdLayoutTwoCtas) != 0;
   if (two && (layout & ~kBwdLayoutTwoCtas) == kBwdLayoutDD) return bwd_inst<T, kWarpPart | kDDiv | kTwoCtas>();
+  if ((layout & ~kBwdLayoutPrefetch) == kBwdLayoutDD && (layout & kBwdLayoutPrefetch))
+    return bwd_inst<T, kWarpPart | kDDiv | kL2Pre>();
   // layout bits: kBwdLayoutMagic | kBwdLayoutQuad | kBwdLayoutDD
   switch (layout & 7u) {
     case 1: return bwd_inst<T, kWarpPart | kMagicRint>();
