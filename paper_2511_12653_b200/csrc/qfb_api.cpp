@@ -126,6 +126,7 @@ struct qfb_ctx {
   // consumer layout of the full-tile kernel (QFB_BWD_IMPL=tile[q][m][d] at creation)
   uint32_t bwd_layout = kBwdLayoutDD;  // measured best (r02)
   bool bwd_half_fp32 = false;           // QFB_OPT_BWD_HALF_FP32
+  bool bwd_sep_finish = false;          // QFB_BWD_IMPL=tile...f: separate finisher kernel (A/B)
   // status word the forward kernels latch into: d_status, or a host-pass
   // slot's own word while that slot's kernels are enqueued
   uint32_t* cur_status = nullptr;
@@ -532,9 +533,11 @@ qfb_status qfb_ctx_create(int32_t device, void* stream, qfb_ctx** out) {
       // tests): "tile" + any of q (quad), m (magic rint), d (dd quotient)
       if (std::strncmp(env, "tile", 4) == 0 && env[4] != '1') {
         uint32_t l = 0;
-        for (const char* p = env + 4; *p; ++p)
+        for (const char* p = env + 4; *p; ++p) {
+          if (*p == 'f') c->bwd_sep_finish = true;
           l |= *p == 'q' ? kBwdLayoutQuad : *p == 'm' ? kBwdLayoutMagic : *p == 'd' ? kBwdLayoutDD
              : *p == '2' ? kBwdLayoutTwoCtas : *p == 'p' ? kBwdLayoutPrefetch : 0u;
+        }
         c->bwd_layout = l;
       }
     }
@@ -856,7 +859,7 @@ qfb_status plan_bwd(const qfb_bwd_desc& t, BwdPlan& p, int dtype_of_plan) {
   p.tiles = segs * tps;
   if (p.tiles >= (1ull << 31)) return fail(QFB_ERR_UNSUPPORTED, "too many tiles");
   p.f64_need = segs * tps;  // tile partials, reduced by the finisher
-  p.u32_need = 0;
+  p.u32_need = segs;        // per-row tile counters (fused finish)
   return QFB_OK;
 }
 
@@ -961,6 +964,15 @@ qfb_status sb_plan(qfb_ctx* ctx, BwdPlan& p) {
   return QFB_OK;
 }
 
+// QFB_BWD_FUSED_FIN=0 restores the separate finisher kernel (A/B runs).
+bool fused_finish_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("QFB_BWD_FUSED_FIN");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // Plans of a table, switched to the streaming kernel when every entry is
 // eligible (one launch for the whole table, as for the tile kernel).
 qfb_status plan_bwd_table(qfb_ctx* ctx, int dtype, const qfb_bwd_desc* table, int32_t n,
@@ -1012,7 +1024,10 @@ qfb_status qfb_fq_bwd_reserve(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc*
     ++cnt;
   }
   need = std::max(need, f64);
+  size_t rows = 1;
+  for (const auto& p : plans) rows += p.u32_need;
   DeviceGuard g(ctx->device);
+  if (qfb_status st = grow(ctx, ctx->ws_u32, rows * 4, true)) return st;
   return grow(ctx, ctx->ws_f64, need * 8, false);
 }
 
@@ -1038,11 +1053,22 @@ qfb_status qfb_fq_bwd_multi(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc* t
       tiles += p.tiles;
       ++cnt;
     }
-    (void)u32;
     if (qfb_status st = grow(ctx, ctx->ws_f64, std::max<size_t>(f64, 1) * 8, false)) return st;
+    // fused finish: rows complete inside the main pass (the last tile's CTA
+    // reduces them), no finisher launch. Needs full tiles (warp partials)
+    // and no fold over rows (outer == 1 or QFB_BWD_ROWS).
+    bool fused = warp_part && !stream && fused_finish_enabled() && !ctx->bwd_sep_finish;
+    for (int32_t k = 0; k < cnt && fused; ++k) {
+      const BwdDesc& d = plans[i + k].d;
+      fused = (d.outer == 1 || d.accumulate == QFB_BWD_ROWS) && (uint64_t)d.outer * d.chans < (1ull << 26) &&
+              d.part_log <= 11;
+    }
+    if (fused)
+      if (qfb_status st = grow(ctx, ctx->ws_u32, std::max<size_t>(u32, 1) * 4, true)) return st;
     BwdBatch b;
     std::memset(&b, 0, sizeof b);
     double* fp = static_cast<double*>(ctx->ws_f64.p);
+    uint32_t* cp = static_cast<uint32_t*>(ctx->ws_u32.p);
     uint64_t tb = 0;
     for (int32_t k = 0; k < cnt; ++k) {
       BwdDesc d = plans[i + k].d;
@@ -1050,6 +1076,10 @@ qfb_status qfb_fq_bwd_multi(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc* t
       const uint64_t tps = 1ull << d.part_log;
       d.partials = fp;
       fp += segs * tps;
+      if (fused) {
+        d.rowcnt = cp;
+        cp += segs;
+      }
       b.d[k] = d;
       b.tile_begin[k] = (uint32_t)tb;
       tb += plans[i + k].tiles;
@@ -1074,9 +1104,15 @@ qfb_status qfb_fq_bwd_multi(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc* t
     }
     size_t smem = 0;
     bwd_ring_size(dtype, max_tile, &b.stage_elems, &b.nstages, &smem);
+    if (fused) {
+      // rows a CTA completes <= tiles it processes <= ceil(tiles / SMs) (grid >= SMs)
+      b.fused_fin = 1u;
+      b.fin_cap = (uint32_t)((tb + (uint64_t)ctx->sm_count - 1) / (uint64_t)ctx->sm_count) + 2u;
+      smem += (size_t)b.fin_cap * sizeof(uint32_t);
+    }
     // cached: keeps steady-state launches free of runtime queries (graph capture)
     int per_sm = 0;
-    const size_t key = (smem * 2 + (warp_part ? 1 : 0)) * 64 + b.layout;
+    const size_t key = (smem * 2 + (warp_part ? 1 : 0)) * 64 + b.layout;  // smem includes the fused-finish list
     for (const auto& kv : ctx->bwd_occ[dtype])
       if (kv.first == key) per_sm = kv.second;
     if (per_sm == 0) {
@@ -1086,7 +1122,7 @@ qfb_status qfb_fq_bwd_multi(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc* t
     const int grid = ctx->sm_count * per_sm;
     cudaError_t e = launch_bwd(dtype, b, grid, ctx->stream);
     if (e != cudaSuccess) return cuda_fail(e, "bwd_kernel launch");
-    ctx->launches += 2;  // main pass + finisher
+    ctx->launches += fused ? 1 : 2;  // main pass (+ finisher)
     i += cnt;
   }
   return QFB_OK;

@@ -115,6 +115,7 @@ struct TileRef {
   uint64_t w0;  // window [w0, w1) in bytes
   uint64_t w1;
   double s, y;  // scale and RN(1/s)
+  float hthr;   // kHalfF32: binary16 clip threshold (half_clip_threshold), per tile
 };
 
 __device__ __forceinline__ TileRef locate(const BwdBatch& bt, uint32_t tile_id) {
@@ -580,11 +581,12 @@ __device__ __forceinline__ float half_clip_threshold(const DivCtx& dc, double q)
   return __half2float(__ushort_as_half(h));
 }
 
-__device__ __forceinline__ HalfCtx make_half_ctx(const DivCtx& dc, double q) {
+// thr: half_clip_threshold(dc, q), computed per tile by the producer
+__device__ __forceinline__ HalfCtx make_half_ctx(const DivCtx& dc, double q, float thr) {
   HalfCtx h;
   h.yh = (float)dc.y;
   h.yl = (float)(dc.y - (double)h.yh);
-  h.t = half_clip_threshold(dc, q);
+  h.t = thr;
   h.q = (float)q;
   return h;
 }
@@ -692,6 +694,7 @@ __device__ __forceinline__ TileRef shfl_ref(const TileRef& r, int src) {
   o.w1 = __shfl_sync(kAll, (unsigned long long)r.w1, src);
   o.s = __shfl_sync(kAll, r.s, src);
   o.y = __shfl_sync(kAll, r.y, src);
+  o.hthr = __shfl_sync(kAll, r.hthr, src);
   return o;
 }
 
@@ -792,6 +795,27 @@ __device__ __forceinline__ void store_dx(const BwdDesc& d, const TileRef& cur, S
 // elements in flight per consumer lane) and a deeper ring (QFB_BWD_CTAS=2).
 constexpr int kTwoCtas = 128;
 
+// One row's completion inside the main pass (fused finish): the perfect
+// tree over its 2^part_log tile partials (as bwd_finish_reg_kernel), times
+// chain[c], stored per the accumulate rule (outer == 1 or QFB_BWD_ROWS:
+// no fold over rows), and the row counter reset for the next launch.
+// Called by a whole warp after its lane 0 observed the row's last tile.
+__device__ double lane_slice_any(const double* p, int lane, uint32_t per);
+__device__ __noinline__ void finish_row_fused(const BwdDesc& d, uint32_t seg, int lane) {
+  const uint32_t tps = 1u << d.part_log;
+  const uint32_t lanes = tps < 32u ? tps : 32u;
+  const uint32_t per = tps / lanes;
+  const uint32_t c = seg % d.chans, o = seg / d.chans;
+  double v = (uint32_t)lane < lanes ? lane_slice_any(d.partials + ((uint64_t)seg << d.part_log), lane, per) : 0.0;
+  for (uint32_t off = 1; off < lanes; off <<= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+  if (lane == 0) {
+    const double r = __dmul_rn(v, d.chain[c]);
+    if (d.accumulate == 2) d.d_log_s[(uint64_t)o * d.row_stride + c] = r;
+    else d.d_log_s[c] = d.accumulate == 1 ? __dadd_rn(d.d_log_s[c], r) : r;
+    d.rowcnt[seg] = 0u;
+  }
+}
+
 template <typename T, int V>
 __global__ void __launch_bounds__(cta_threads<V>(), (V & kTwoCtas) ? 2 : 3) bwd_kernel(const __grid_constant__ BwdBatch bt) {
   constexpr int CW = cons_warps<V>();
@@ -837,7 +861,18 @@ __global__ void __launch_bounds__(cta_threads<V>(), (V & kTwoCtas) ? 2 : 3) bwd_
       if (b != batch) {
         batch = b;
         const uint32_t id = blockIdx.x + ((b << 5) + (uint32_t)lane) * gridDim.x;
-        if (id < total) mine = locate_full<T>(bt, id);
+        if (id < total) {
+          mine = locate_full<T>(bt, id);
+          if constexpr ((V & kHalfF32) != 0) {
+            // the fp32-term path's exact clip threshold, once per tile
+            DivCtx dc;
+            dc.s = mine.s;
+            dc.y = mine.y;
+            dc.ylo = recip_lo(mine.s, mine.y);
+            dc.usable = mine.s >= 0x1p-100 && mine.s <= 0x1p100;
+            mine.hthr = dc.usable ? half_clip_threshold(dc, bt.d[mine.di].q) : 0.0f;
+          }
+        }
       }
       return shfl_ref(mine, (int)(k & 31u));
     };
@@ -852,6 +887,12 @@ __global__ void __launch_bounds__(cta_threads<V>(), (V & kTwoCtas) ? 2 : 3) bwd_
     }
     uint32_t done_phase = 0;
     int s = 0;
+    // fused finish: the counter value returned for the previous tile (its
+    // atomic completes while the next tile is handled) and the rows this CTA
+    // completes after its last tile (list in shared memory, lane 0)
+    uint32_t pend_old = 0, pend_last = 0, pend_di = 0, pend_seg = 0, nfin = 0;
+    bool pend = false;
+    uint32_t* fin_list = reinterpret_cast<uint32_t*>(smem_raw + (size_t)nst * (2 * se * sizeof(T) + kRedBytes));
     for (uint32_t k = 0; j_id < total; j_id += gridDim.x, ++k) {
       // locate the refill tile while the consumers still work on this one
       const uint32_t nid = j_id + (uint32_t)nst * gridDim.x;
@@ -892,10 +933,30 @@ __global__ void __launch_bounds__(cta_threads<V>(), (V & kTwoCtas) ? 2 : 3) bwd_
 #pragma unroll
         for (int o = 1; o < CW; o <<= 1) w = __dadd_rn(w, __shfl_xor_sync(0xffffffffu, w, o));
         if (lane == 0) d.partials[((uint64_t)cur.seg << d.part_log) + cur.t] = w;
+        if (bt.fused_fin && lane == 0) {
+          // the previous tile's counter: its last tile -> this CTA completes the row
+          if (pend && pend_old == pend_last && nfin < bt.fin_cap) fin_list[nfin++] = (pend_di << 26) | pend_seg;
+          // release orders the partial above before the count; the lane
+          // that brings the count to 2^part_log acquires every partial
+          pend_old = atom_add_acq_rel_gpu(d.rowcnt + cur.seg, 1u);
+          pend_last = (1u << d.part_log) - 1u;
+          pend_di = (uint32_t)cur.di;
+          pend_seg = cur.seg;
+          pend = true;
+        }
       }
       s = s + 1 == nst ? 0 : s + 1;
     }
     if (lane == 0) bulk_wait_all();
+    if (bt.fused_fin) {
+      if (lane == 0 && pend && pend_old == pend_last && nfin < bt.fin_cap) fin_list[nfin++] = (pend_di << 26) | pend_seg;
+      nfin = __shfl_sync(0xffffffffu, nfin, 0);
+      __syncwarp();  // orders lane 0's acquire (and list writes) before the warp's partial loads
+      for (uint32_t i = 0; i < nfin; ++i) {
+        const uint32_t e = fin_list[i];
+        finish_row_fused(bt.d[e >> 26], e & ((1u << 26) - 1u), lane);
+      }
+    }
     return;
   }
 
@@ -926,7 +987,7 @@ __global__ void __launch_bounds__(cta_threads<V>(), (V & kTwoCtas) ? 2 : 3) bwd_
       const T* su = st.up + cur.off + plo;
       constexpr int kM = math_of<V>();
       if constexpr ((V & kHalfF32) != 0 && sizeof(T) == 2) {
-        const HalfCtx hc = make_half_ctx(dc, q);
+        const HalfCtx hc = make_half_ctx(dc, q, cur.hthr);
         v = (d.dx != nullptr) ? quad_sum_h32<true>(sx, su, pm, dc, q, hc) : quad_sum_h32<false>(sx, su, pm, dc, q, hc);
       } else {
         v = (V & kProbeNoCompute) ? 0.0
@@ -1058,7 +1119,7 @@ __device__ __forceinline__ double lane_slice_wide(const double* p, int lane) {
   return a[0];
 }
 
-__device__ __forceinline__ double lane_slice_any(const double* p, int lane, uint32_t per) {
+__device__ double lane_slice_any(const double* p, int lane, uint32_t per) {
   switch (per) {
     case 1: return p[lane];
     case 2: return lane_slice<2>(p, lane);
@@ -1577,12 +1638,19 @@ cudaError_t launch_bwd(int dtype, const BwdBatch& b, int grid, cudaStream_t st) 
   const uint32_t tiles = b.tile_begin[b.n];
   if (tiles == 0) return cudaSuccess;
   if ((uint32_t)grid > tiles) grid = (int)tiles;
-  const size_t smem = (size_t)b.nstages * (2 * b.stage_elems * (dtype == 0 ? 4 : 2) + kRedBytes);
+  const size_t smem = (size_t)b.nstages * (2 * b.stage_elems * (dtype == 0 ? 4 : 2) + kRedBytes) +
+                     (b.fused_fin ? (size_t)b.fin_cap * sizeof(uint32_t) : 0);
   void* args[] = {const_cast<BwdBatch*>(&b)};
   const BwdFn f = bwd_fn(dtype, b.warp_part != 0, b.layout);
   cudaFuncSetAttribute(f.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
   cudaError_t e = launch_main(f.fn, dim3(grid), dim3(f.threads), args, smem, st, kPdlBwd);
   if (e != cudaSuccess) return e;
+  // QFB_DIAG_SKIP_FINISH=1: timing diagnostic only (d_log_s is NOT written)
+  static const bool skip_fin = [] {
+    const char* e = getenv("QFB_DIAG_SKIP_FINISH");
+    return e && e[0] == '1';
+  }();
+  if (skip_fin || b.fused_fin) return cudaSuccess;
   return launch_bwd_finish(b, st);
 }
 

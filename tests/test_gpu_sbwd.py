@@ -48,7 +48,7 @@ def inputs(n, C, outer, dtype, seed):
     return x, up, s64, chain
 
 
-IMPLS = ["default", "stream", "tile1", "tile", "tilem", "tileq", "tileqmd", "tile2d", "tiledp"]
+IMPLS = ["default", "stream", "tile1", "tile", "tilem", "tileq", "tileqmd", "tile2d", "tiledp", "tiledf"]
 
 
 def make_ctx(qfb, impl, monkeypatch):
@@ -62,10 +62,14 @@ def make_ctx(qfb, impl, monkeypatch):
 @pytest.mark.parametrize("impl", IMPLS)
 @pytest.mark.parametrize("dtype", [0, 1])
 @pytest.mark.parametrize("n", LENGTHS)
-def test_backward_variants_match_oracle(qfb, orc, cuda, n, dtype, impl, monkeypatch):
+@pytest.mark.parametrize("outer", [1, 2])
+def test_backward_variants_match_oracle(qfb, orc, cuda, n, dtype, impl, outer, monkeypatch):
+    """outer = 1: rows complete inside the main pass (fused finish) on the
+    full-tile kernels; outer = 2 (frames folded per channel): the finisher
+    kernel."""
     if dtype == 1 and n % 8:
         pytest.skip("f16 rows must be 16-byte multiples")
-    C, outer = 3, 2
+    C = 3
     x, up, s64, chain = inputs(n, C, outer, dtype, n + dtype)
     ctx = make_ctx(qfb, impl, monkeypatch)
     dx, dls = run(qfb, cuda, x, up, s64, chain, outer, C, n, dtype, ctx)

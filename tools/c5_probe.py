@@ -22,7 +22,7 @@ fp = FrontendQuantPass(ctx, frames=F, dtype=dt, sets=2, seed=11, device=dev, int
 for i in range(4):
     fp.forward(i % 2)
 torch.cuda.synchronize()
-R = 40
+R = int(os.environ.get("C5_REPS", "40"))
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(st)
 for i in range(R):
@@ -36,4 +36,4 @@ if int8:  # input read once + 1 byte per quant-point element
     b = sum(p.numel * F * esz + p.numel * F * len(p.consumers) for p in fp.points)
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6551.0
 print(json.dumps({"frames": F, "dtype": dt, "ms": ms, "frames_per_s": F / ms * 1e3, "gbps": b / ms / 1e6,
-                  "frac": b / ms / 1e6 / peak, "int8": int8, "stages_env": os.environ.get("QFB_FWD_STAGES")}))
+                  "frac": b / ms / 1e6 / peak, "int8": int8, "reps": R, "stages_env": os.environ.get("QFB_FWD_STAGES")}))

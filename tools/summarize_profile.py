@@ -96,9 +96,12 @@ def main():
         start = next(i for i, r in enumerate(lr) if r and r[0] == "ID")
         h = lr[start]
         ni, vi = h.index("Kernel Name"), h.index("Metric Value")
+        mi = h.index("Metric Name") if "Metric Name" in h else None
         tot, per = 0.0, {}
         for r in lr[start + 1:]:
-            v = float(r[vi])
+            if mi is not None and r[mi] != "gpu__time_duration.sum":
+                continue  # the launch list may carry DRAM byte counters too
+            v = float(r[vi].replace(",", ""))
             k = kernel_key(r[ni])
             per[k] = per.get(k, 0.0) + v
             tot += v
