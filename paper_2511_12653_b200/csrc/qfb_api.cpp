@@ -88,6 +88,7 @@ struct qfb_ctx {
   uint32_t* h_status = nullptr;  // pinned
   DevBuf ws_f64;                 // partials / segment results
   DevBuf ws_u32;                 // tickets (kept zero between launches)
+  DevBuf ws_fused;               // fused-finish tile partials (all-ones between launches)
   DevBuf host_io[6];             // scratch for the *_host entry points
   int64_t launches = 0;
   // qfb_quant_pass_host: copy streams and, per in-flight slot, events,
@@ -155,6 +156,16 @@ qfb_status grow(qfb_ctx* ctx, DevBuf& b, size_t bytes, bool zero) {
   if (b.p) ctx->retired.push_back(b.p);
   b.p = np;
   b.bytes = nb;
+  return QFB_OK;
+}
+
+// grow() for a buffer whose every byte must hold `byte` between uses: the
+// new buffer is filled on the context stream (growth happens before the
+// launch that needs it, in stream order).
+qfb_status grow_fill(qfb_ctx* ctx, DevBuf& b, size_t bytes, int byte) {
+  if (b.bytes >= bytes) return QFB_OK;
+  if (qfb_status st = grow(ctx, b, bytes, false)) return st;
+  QFB_CUDA(cudaMemsetAsync(b.p, byte, b.bytes, ctx->stream));
   return QFB_OK;
 }
 
@@ -573,6 +584,7 @@ qfb_status qfb_ctx_destroy(qfb_ctx* ctx) {
   if (ctx->h_status) cudaFreeHost(ctx->h_status);
   if (ctx->ws_f64.p) cudaFree(ctx->ws_f64.p);
   if (ctx->ws_u32.p) cudaFree(ctx->ws_u32.p);
+  if (ctx->ws_fused.p) cudaFree(ctx->ws_fused.p);
   for (void* p : ctx->retired) cudaFree(p);
   for (auto& kv : ctx->sb_shapes) cudaFree(kv.second.meta);
   for (auto& b : ctx->host_io)
@@ -859,7 +871,7 @@ qfb_status plan_bwd(const qfb_bwd_desc& t, BwdPlan& p, int dtype_of_plan) {
   p.tiles = segs * tps;
   if (p.tiles >= (1ull << 31)) return fail(QFB_ERR_UNSUPPORTED, "too many tiles");
   p.f64_need = segs * tps;  // tile partials, reduced by the finisher
-  p.u32_need = segs;        // per-row tile counters (fused finish)
+  p.u32_need = 0;
   return QFB_OK;
 }
 
@@ -1024,10 +1036,8 @@ qfb_status qfb_fq_bwd_reserve(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc*
     ++cnt;
   }
   need = std::max(need, f64);
-  size_t rows = 1;
-  for (const auto& p : plans) rows += p.u32_need;
   DeviceGuard g(ctx->device);
-  if (qfb_status st = grow(ctx, ctx->ws_u32, rows * 4, true)) return st;
+  if (qfb_status st = grow_fill(ctx, ctx->ws_fused, need * 8, 0xff)) return st;
   return grow(ctx, ctx->ws_f64, need * 8, false);
 }
 
@@ -1063,12 +1073,13 @@ qfb_status qfb_fq_bwd_multi(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc* t
       fused = (d.outer == 1 || d.accumulate == QFB_BWD_ROWS) && (uint64_t)d.outer * d.chans < (1ull << 26) &&
               d.part_log <= 11;
     }
+    // fused batches use their own partials workspace, all-ones between
+    // launches (finish_row_fused's "unwritten" pattern)
     if (fused)
-      if (qfb_status st = grow(ctx, ctx->ws_u32, std::max<size_t>(u32, 1) * 4, true)) return st;
+      if (qfb_status st = grow_fill(ctx, ctx->ws_fused, std::max<size_t>(f64, 1) * 8, 0xff)) return st;
     BwdBatch b;
     std::memset(&b, 0, sizeof b);
-    double* fp = static_cast<double*>(ctx->ws_f64.p);
-    uint32_t* cp = static_cast<uint32_t*>(ctx->ws_u32.p);
+    double* fp = static_cast<double*>(fused ? ctx->ws_fused.p : ctx->ws_f64.p);
     uint64_t tb = 0;
     for (int32_t k = 0; k < cnt; ++k) {
       BwdDesc d = plans[i + k].d;
@@ -1076,10 +1087,7 @@ qfb_status qfb_fq_bwd_multi(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc* t
       const uint64_t tps = 1ull << d.part_log;
       d.partials = fp;
       fp += segs * tps;
-      if (fused) {
-        d.rowcnt = cp;
-        cp += segs;
-      }
+
       b.d[k] = d;
       b.tile_begin[k] = (uint32_t)tb;
       tb += plans[i + k].tiles;

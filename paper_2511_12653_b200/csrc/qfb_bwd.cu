@@ -795,24 +795,64 @@ __device__ __forceinline__ void store_dx(const BwdDesc& d, const TileRef& cur, S
 // elements in flight per consumer lane) and a deeper ring (QFB_BWD_CTAS=2).
 constexpr int kTwoCtas = 128;
 
-// One row's completion inside the main pass (fused finish): the perfect
-// tree over its 2^part_log tile partials (as bwd_finish_reg_kernel), times
-// chain[c], stored per the accumulate rule (outer == 1 or QFB_BWD_ROWS:
-// no fold over rows), and the row counter reset for the next launch.
-// Called by a whole warp after its lane 0 observed the row's last tile.
-__device__ double lane_slice_any(const double* p, int lane, uint32_t per);
+// One row's completion inside the main pass (fused finish). The fused
+// batches' partials live in a workspace that holds the all-ones pattern
+// (a negative NaN with every payload bit set, which no tile sum can be:
+// terms are products of widened binary32/16 values, whose low 29 payload
+// bits are zero, and generated NaNs are 0x7fff...) between launches, so a
+// partial is "written" exactly when it differs from that pattern: 8-byte
+// aligned stores are single-copy atomic, and no counter, fence or atomic
+// is needed. The CTA that processed a row's last tile (in tile order)
+// polls the row's partials after its own loop (the grid is persistent and
+// fully resident, so every tile is processed by a running CTA), reduces
+// them as bwd_finish_reg_kernel does (perfect tree, times chain[c]), stores
+// the result per the accumulate rule (outer == 1 or QFB_BWD_ROWS: no fold
+// over rows) and puts the pattern back for the next launch.
+constexpr unsigned long long kUnwritten = ~0ull;
+
+__device__ __forceinline__ double ld_relaxed_f64(const double* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return __longlong_as_double((long long)v);
+}
+
+__device__ __forceinline__ void st_relaxed_f64(double* p, double v) {
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"((unsigned long long)__double_as_longlong(v))
+               : "memory");
+}
+
 __device__ __noinline__ void finish_row_fused(const BwdDesc& d, uint32_t seg, int lane) {
   const uint32_t tps = 1u << d.part_log;
+  const uint32_t per = tps < 32u ? 1u : tps >> 5;
   const uint32_t lanes = tps < 32u ? tps : 32u;
-  const uint32_t per = tps / lanes;
   const uint32_t c = seg % d.chans, o = seg / d.chans;
-  double v = (uint32_t)lane < lanes ? lane_slice_any(d.partials + ((uint64_t)seg << d.part_log), lane, per) : 0.0;
+  double* row = d.partials + ((uint64_t)seg << d.part_log);
+  double* mine = row + (uint64_t)lane * per;
+  // wait until every partial of the row is written (bounded: a trap turns
+  // a broken residency assumption into a launch error instead of a hang)
+  for (long long spins = 0;; ++spins) {
+    bool ok = true;
+    if ((uint32_t)lane < lanes)
+      for (uint32_t k = 0; k < per; ++k)
+        ok &= (unsigned long long)__double_as_longlong(ld_relaxed_f64(mine + k)) != kUnwritten;
+    if (__all_sync(0xffffffffu, ok)) break;
+    if (spins > (1ll << 26)) __trap();
+    __nanosleep(64);
+  }
+  double v = 0.0;
+  if ((uint32_t)lane < lanes) {
+    double a[64];
+    for (uint32_t k = 0; k < per; ++k) a[k] = ld_relaxed_f64(mine + k);
+    for (uint32_t w = per; w > 1; w >>= 1)
+      for (uint32_t k = 0; k < w / 2; ++k) a[k] = __dadd_rn(a[2 * k], a[2 * k + 1]);
+    v = a[0];
+    for (uint32_t k = 0; k < per; ++k) mine[k] = __longlong_as_double((long long)kUnwritten);
+  }
   for (uint32_t off = 1; off < lanes; off <<= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
   if (lane == 0) {
     const double r = __dmul_rn(v, d.chain[c]);
     if (d.accumulate == 2) d.d_log_s[(uint64_t)o * d.row_stride + c] = r;
     else d.d_log_s[c] = d.accumulate == 1 ? __dadd_rn(d.d_log_s[c], r) : r;
-    d.rowcnt[seg] = 0u;
   }
 }
 
@@ -887,11 +927,9 @@ __global__ void __launch_bounds__(cta_threads<V>(), (V & kTwoCtas) ? 2 : 3) bwd_
     }
     uint32_t done_phase = 0;
     int s = 0;
-    // fused finish: the counter value returned for the previous tile (its
-    // atomic completes while the next tile is handled) and the rows this CTA
-    // completes after its last tile (list in shared memory, lane 0)
-    uint32_t pend_old = 0, pend_last = 0, pend_di = 0, pend_seg = 0, nfin = 0;
-    bool pend = false;
+    // fused finish: the rows whose last tile this CTA processes, completed
+    // after its loop (list in shared memory, lane 0)
+    uint32_t nfin = 0;
     uint32_t* fin_list = reinterpret_cast<uint32_t*>(smem_raw + (size_t)nst * (2 * se * sizeof(T) + kRedBytes));
     for (uint32_t k = 0; j_id < total; j_id += gridDim.x, ++k) {
       // locate the refill tile while the consumers still work on this one
@@ -932,26 +970,17 @@ __global__ void __launch_bounds__(cta_threads<V>(), (V & kTwoCtas) ? 2 : 3) bwd_
         double w = lane < CW ? red[2 * s + par][lane] : 0.0;
 #pragma unroll
         for (int o = 1; o < CW; o <<= 1) w = __dadd_rn(w, __shfl_xor_sync(0xffffffffu, w, o));
-        if (lane == 0) d.partials[((uint64_t)cur.seg << d.part_log) + cur.t] = w;
-        if (bt.fused_fin && lane == 0) {
-          // the previous tile's counter: its last tile -> this CTA completes the row
-          if (pend && pend_old == pend_last && nfin < bt.fin_cap) fin_list[nfin++] = (pend_di << 26) | pend_seg;
-          // release orders the partial above before the count; the lane
-          // that brings the count to 2^part_log acquires every partial
-          pend_old = atom_add_acq_rel_gpu(d.rowcnt + cur.seg, 1u);
-          pend_last = (1u << d.part_log) - 1u;
-          pend_di = (uint32_t)cur.di;
-          pend_seg = cur.seg;
-          pend = true;
-        }
+        // relaxed (not weak): a fused-finish CTA may poll this word concurrently
+        if (lane == 0) st_relaxed_f64(d.partials + ((uint64_t)cur.seg << d.part_log) + cur.t, w);
+        if (bt.fused_fin && lane == 0 && cur.t == (1u << d.part_log) - 1u && nfin < bt.fin_cap)
+          fin_list[nfin++] = ((uint32_t)cur.di << 26) | cur.seg;
       }
       s = s + 1 == nst ? 0 : s + 1;
     }
     if (lane == 0) bulk_wait_all();
     if (bt.fused_fin) {
-      if (lane == 0 && pend && pend_old == pend_last && nfin < bt.fin_cap) fin_list[nfin++] = (pend_di << 26) | pend_seg;
       nfin = __shfl_sync(0xffffffffu, nfin, 0);
-      __syncwarp();  // orders lane 0's acquire (and list writes) before the warp's partial loads
+      __syncwarp();  // lane 0's list writes
       for (uint32_t i = 0; i < nfin; ++i) {
         const uint32_t e = fin_list[i];
         finish_row_fused(bt.d[e >> 26], e & ((1u << 26) - 1u), lane);
@@ -1119,7 +1148,7 @@ __device__ __forceinline__ double lane_slice_wide(const double* p, int lane) {
   return a[0];
 }
 
-__device__ double lane_slice_any(const double* p, int lane, uint32_t per) {
+__device__ __forceinline__ double lane_slice_any(const double* p, int lane, uint32_t per) {
   switch (per) {
     case 1: return p[lane];
     case 2: return lane_slice<2>(p, lane);

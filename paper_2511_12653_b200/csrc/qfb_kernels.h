@@ -165,7 +165,6 @@ struct BwdDesc {
   const double* chain;
   double* d_log_s;
   double* partials;  // [segments * tps] tile sums, reduced by bwd_finish
-  uint32_t* rowcnt;  // fused finish (BwdBatch::fused_fin): tiles done per row, zero between launches
   uint64_t inner;    // row (segment) length n
   uint32_t outer;
   uint32_t chans;
