@@ -88,7 +88,6 @@ struct qfb_ctx {
   uint32_t* h_status = nullptr;  // pinned
   DevBuf ws_f64;                 // partials / segment results
   DevBuf ws_u32;                 // tickets (kept zero between launches)
-  DevBuf ws_fused;               // fused-finish tile partials (all-ones between launches)
   DevBuf host_io[6];             // scratch for the *_host entry points
   int64_t launches = 0;
   // qfb_quant_pass_host: copy streams and, per in-flight slot, events,
@@ -127,7 +126,6 @@ struct qfb_ctx {
   // consumer layout of the full-tile kernel (QFB_BWD_IMPL=tile[q][m][d] at creation)
   uint32_t bwd_layout = kBwdLayoutDD;  // measured best (r02)
   bool bwd_half_fp32 = false;           // QFB_OPT_BWD_HALF_FP32
-  bool bwd_sep_finish = false;          // QFB_BWD_IMPL=tile...f: separate finisher kernel (A/B)
   // status word the forward kernels latch into: d_status, or a host-pass
   // slot's own word while that slot's kernels are enqueued
   uint32_t* cur_status = nullptr;
@@ -156,16 +154,6 @@ qfb_status grow(qfb_ctx* ctx, DevBuf& b, size_t bytes, bool zero) {
   if (b.p) ctx->retired.push_back(b.p);
   b.p = np;
   b.bytes = nb;
-  return QFB_OK;
-}
-
-// grow() for a buffer whose every byte must hold `byte` between uses: the
-// new buffer is filled on the context stream (growth happens before the
-// launch that needs it, in stream order).
-qfb_status grow_fill(qfb_ctx* ctx, DevBuf& b, size_t bytes, int byte) {
-  if (b.bytes >= bytes) return QFB_OK;
-  if (qfb_status st = grow(ctx, b, bytes, false)) return st;
-  QFB_CUDA(cudaMemsetAsync(b.p, byte, b.bytes, ctx->stream));
   return QFB_OK;
 }
 
@@ -545,7 +533,6 @@ qfb_status qfb_ctx_create(int32_t device, void* stream, qfb_ctx** out) {
       if (std::strncmp(env, "tile", 4) == 0 && env[4] != '1') {
         uint32_t l = 0;
         for (const char* p = env + 4; *p; ++p) {
-          if (*p == 'f') c->bwd_sep_finish = true;
           l |= *p == 'q' ? kBwdLayoutQuad : *p == 'm' ? kBwdLayoutMagic : *p == 'd' ? kBwdLayoutDD
              : *p == '2' ? kBwdLayoutTwoCtas : *p == 'p' ? kBwdLayoutPrefetch : 0u;
         }
@@ -584,7 +571,6 @@ qfb_status qfb_ctx_destroy(qfb_ctx* ctx) {
   if (ctx->h_status) cudaFreeHost(ctx->h_status);
   if (ctx->ws_f64.p) cudaFree(ctx->ws_f64.p);
   if (ctx->ws_u32.p) cudaFree(ctx->ws_u32.p);
-  if (ctx->ws_fused.p) cudaFree(ctx->ws_fused.p);
   for (void* p : ctx->retired) cudaFree(p);
   for (auto& kv : ctx->sb_shapes) cudaFree(kv.second.meta);
   for (auto& b : ctx->host_io)
@@ -976,15 +962,6 @@ qfb_status sb_plan(qfb_ctx* ctx, BwdPlan& p) {
   return QFB_OK;
 }
 
-// QFB_BWD_FUSED_FIN=0 restores the separate finisher kernel (A/B runs).
-bool fused_finish_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("QFB_BWD_FUSED_FIN");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
 // Plans of a table, switched to the streaming kernel when every entry is
 // eligible (one launch for the whole table, as for the tile kernel).
 qfb_status plan_bwd_table(qfb_ctx* ctx, int dtype, const qfb_bwd_desc* table, int32_t n,
@@ -1037,7 +1014,6 @@ qfb_status qfb_fq_bwd_reserve(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc*
   }
   need = std::max(need, f64);
   DeviceGuard g(ctx->device);
-  if (qfb_status st = grow_fill(ctx, ctx->ws_fused, need * 8, 0xff)) return st;
   return grow(ctx, ctx->ws_f64, need * 8, false);
 }
 
@@ -1064,22 +1040,9 @@ qfb_status qfb_fq_bwd_multi(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc* t
       ++cnt;
     }
     if (qfb_status st = grow(ctx, ctx->ws_f64, std::max<size_t>(f64, 1) * 8, false)) return st;
-    // fused finish: rows complete inside the main pass (the last tile's CTA
-    // reduces them), no finisher launch. Needs full tiles (warp partials)
-    // and no fold over rows (outer == 1 or QFB_BWD_ROWS).
-    bool fused = warp_part && !stream && fused_finish_enabled() && !ctx->bwd_sep_finish;
-    for (int32_t k = 0; k < cnt && fused; ++k) {
-      const BwdDesc& d = plans[i + k].d;
-      fused = (d.outer == 1 || d.accumulate == QFB_BWD_ROWS) && (uint64_t)d.outer * d.chans < (1ull << 26) &&
-              d.part_log <= 11;
-    }
-    // fused batches use their own partials workspace, all-ones between
-    // launches (finish_row_fused's "unwritten" pattern)
-    if (fused)
-      if (qfb_status st = grow_fill(ctx, ctx->ws_fused, std::max<size_t>(f64, 1) * 8, 0xff)) return st;
     BwdBatch b;
     std::memset(&b, 0, sizeof b);
-    double* fp = static_cast<double*>(fused ? ctx->ws_fused.p : ctx->ws_f64.p);
+    double* fp = static_cast<double*>(ctx->ws_f64.p);
     uint64_t tb = 0;
     for (int32_t k = 0; k < cnt; ++k) {
       BwdDesc d = plans[i + k].d;
@@ -1112,15 +1075,9 @@ qfb_status qfb_fq_bwd_multi(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc* t
     }
     size_t smem = 0;
     bwd_ring_size(dtype, max_tile, &b.stage_elems, &b.nstages, &smem);
-    if (fused) {
-      // rows a CTA completes <= tiles it processes <= ceil(tiles / SMs) (grid >= SMs)
-      b.fused_fin = 1u;
-      b.fin_cap = (uint32_t)((tb + (uint64_t)ctx->sm_count - 1) / (uint64_t)ctx->sm_count) + 2u;
-      smem += (size_t)b.fin_cap * sizeof(uint32_t);
-    }
     // cached: keeps steady-state launches free of runtime queries (graph capture)
     int per_sm = 0;
-    const size_t key = (smem * 2 + (warp_part ? 1 : 0)) * 64 + b.layout;  // smem includes the fused-finish list
+    const size_t key = (smem * 2 + (warp_part ? 1 : 0)) * 64 + b.layout;
     for (const auto& kv : ctx->bwd_occ[dtype])
       if (kv.first == key) per_sm = kv.second;
     if (per_sm == 0) {
@@ -1130,7 +1087,7 @@ qfb_status qfb_fq_bwd_multi(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc* t
     const int grid = ctx->sm_count * per_sm;
     cudaError_t e = launch_bwd(dtype, b, grid, ctx->stream);
     if (e != cudaSuccess) return cuda_fail(e, "bwd_kernel launch");
-    ctx->launches += fused ? 1 : 2;  // main pass (+ finisher)
+    ctx->launches += 2;  // main pass + finisher
     i += cnt;
   }
   return QFB_OK;

@@ -795,67 +795,6 @@ __device__ __forceinline__ void store_dx(const BwdDesc& d, const TileRef& cur, S
 // elements in flight per consumer lane) and a deeper ring (QFB_BWD_CTAS=2).
 constexpr int kTwoCtas = 128;
 
-// One row's completion inside the main pass (fused finish). The fused
-// batches' partials live in a workspace that holds the all-ones pattern
-// (a negative NaN with every payload bit set, which no tile sum can be:
-// terms are products of widened binary32/16 values, whose low 29 payload
-// bits are zero, and generated NaNs are 0x7fff...) between launches, so a
-// partial is "written" exactly when it differs from that pattern: 8-byte
-// aligned stores are single-copy atomic, and no counter, fence or atomic
-// is needed. The CTA that processed a row's last tile (in tile order)
-// polls the row's partials after its own loop (the grid is persistent and
-// fully resident, so every tile is processed by a running CTA), reduces
-// them as bwd_finish_reg_kernel does (perfect tree, times chain[c]), stores
-// the result per the accumulate rule (outer == 1 or QFB_BWD_ROWS: no fold
-// over rows) and puts the pattern back for the next launch.
-constexpr unsigned long long kUnwritten = ~0ull;
-
-__device__ __forceinline__ double ld_relaxed_f64(const double* p) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return __longlong_as_double((long long)v);
-}
-
-__device__ __forceinline__ void st_relaxed_f64(double* p, double v) {
-  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"((unsigned long long)__double_as_longlong(v))
-               : "memory");
-}
-
-__device__ __noinline__ void finish_row_fused(const BwdDesc& d, uint32_t seg, int lane) {
-  const uint32_t tps = 1u << d.part_log;
-  const uint32_t per = tps < 32u ? 1u : tps >> 5;
-  const uint32_t lanes = tps < 32u ? tps : 32u;
-  const uint32_t c = seg % d.chans, o = seg / d.chans;
-  double* row = d.partials + ((uint64_t)seg << d.part_log);
-  double* mine = row + (uint64_t)lane * per;
-  // wait until every partial of the row is written (bounded: a trap turns
-  // a broken residency assumption into a launch error instead of a hang)
-  for (long long spins = 0;; ++spins) {
-    bool ok = true;
-    if ((uint32_t)lane < lanes)
-      for (uint32_t k = 0; k < per; ++k)
-        ok &= (unsigned long long)__double_as_longlong(ld_relaxed_f64(mine + k)) != kUnwritten;
-    if (__all_sync(0xffffffffu, ok)) break;
-    if (spins > (1ll << 26)) __trap();
-    __nanosleep(64);
-  }
-  double v = 0.0;
-  if ((uint32_t)lane < lanes) {
-    double a[64];
-    for (uint32_t k = 0; k < per; ++k) a[k] = ld_relaxed_f64(mine + k);
-    for (uint32_t w = per; w > 1; w >>= 1)
-      for (uint32_t k = 0; k < w / 2; ++k) a[k] = __dadd_rn(a[2 * k], a[2 * k + 1]);
-    v = a[0];
-    for (uint32_t k = 0; k < per; ++k) mine[k] = __longlong_as_double((long long)kUnwritten);
-  }
-  for (uint32_t off = 1; off < lanes; off <<= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
-  if (lane == 0) {
-    const double r = __dmul_rn(v, d.chain[c]);
-    if (d.accumulate == 2) d.d_log_s[(uint64_t)o * d.row_stride + c] = r;
-    else d.d_log_s[c] = d.accumulate == 1 ? __dadd_rn(d.d_log_s[c], r) : r;
-  }
-}
-
 template <typename T, int V>
 __global__ void __launch_bounds__(cta_threads<V>(), (V & kTwoCtas) ? 2 : 3) bwd_kernel(const __grid_constant__ BwdBatch bt) {
   constexpr int CW = cons_warps<V>();
@@ -927,10 +866,6 @@ __global__ void __launch_bounds__(cta_threads<V>(), (V & kTwoCtas) ? 2 : 3) bwd_
     }
     uint32_t done_phase = 0;
     int s = 0;
-    // fused finish: the rows whose last tile this CTA processes, completed
-    // after its loop (list in shared memory, lane 0)
-    uint32_t nfin = 0;
-    uint32_t* fin_list = reinterpret_cast<uint32_t*>(smem_raw + (size_t)nst * (2 * se * sizeof(T) + kRedBytes));
     for (uint32_t k = 0; j_id < total; j_id += gridDim.x, ++k) {
       // locate the refill tile while the consumers still work on this one
       const uint32_t nid = j_id + (uint32_t)nst * gridDim.x;
@@ -970,22 +905,11 @@ __global__ void __launch_bounds__(cta_threads<V>(), (V & kTwoCtas) ? 2 : 3) bwd_
         double w = lane < CW ? red[2 * s + par][lane] : 0.0;
 #pragma unroll
         for (int o = 1; o < CW; o <<= 1) w = __dadd_rn(w, __shfl_xor_sync(0xffffffffu, w, o));
-        // relaxed (not weak): a fused-finish CTA may poll this word concurrently
-        if (lane == 0) st_relaxed_f64(d.partials + ((uint64_t)cur.seg << d.part_log) + cur.t, w);
-        if (bt.fused_fin && lane == 0 && cur.t == (1u << d.part_log) - 1u && nfin < bt.fin_cap)
-          fin_list[nfin++] = ((uint32_t)cur.di << 26) | cur.seg;
+        if (lane == 0) d.partials[((uint64_t)cur.seg << d.part_log) + cur.t] = w;
       }
       s = s + 1 == nst ? 0 : s + 1;
     }
     if (lane == 0) bulk_wait_all();
-    if (bt.fused_fin) {
-      nfin = __shfl_sync(0xffffffffu, nfin, 0);
-      __syncwarp();  // lane 0's list writes
-      for (uint32_t i = 0; i < nfin; ++i) {
-        const uint32_t e = fin_list[i];
-        finish_row_fused(bt.d[e >> 26], e & ((1u << 26) - 1u), lane);
-      }
-    }
     return;
   }
 
@@ -1667,8 +1591,7 @@ cudaError_t launch_bwd(int dtype, const BwdBatch& b, int grid, cudaStream_t st) 
   const uint32_t tiles = b.tile_begin[b.n];
   if (tiles == 0) return cudaSuccess;
   if ((uint32_t)grid > tiles) grid = (int)tiles;
-  const size_t smem = (size_t)b.nstages * (2 * b.stage_elems * (dtype == 0 ? 4 : 2) + kRedBytes) +
-                     (b.fused_fin ? (size_t)b.fin_cap * sizeof(uint32_t) : 0);
+  const size_t smem = (size_t)b.nstages * (2 * b.stage_elems * (dtype == 0 ? 4 : 2) + kRedBytes);
   void* args[] = {const_cast<BwdBatch*>(&b)};
   const BwdFn f = bwd_fn(dtype, b.warp_part != 0, b.layout);
   cudaFuncSetAttribute(f.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
@@ -1679,7 +1602,7 @@ cudaError_t launch_bwd(int dtype, const BwdBatch& b, int grid, cudaStream_t st) 
     const char* e = getenv("QFB_DIAG_SKIP_FINISH");
     return e && e[0] == '1';
   }();
-  if (skip_fin || b.fused_fin) return cudaSuccess;
+  if (skip_fin) return cudaSuccess;
   return launch_bwd_finish(b, st);
 }
 

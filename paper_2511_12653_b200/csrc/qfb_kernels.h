@@ -193,9 +193,7 @@ struct BwdBatch {
   uint32_t stage_elems;  // elements per array per stage (16-byte multiple)
   uint32_t warp_part;    // tile kernel: consumer warps store the partials (tps_log = depth - 5)
   uint32_t layout;       // full-tile consumer layout: kBwdLayout* (warp_part batches only)
-  uint32_t fused_fin;    // rows finished inside the main pass (no finisher launch)
-  uint32_t fin_cap;      // fused_fin: per-CTA list capacity (rows a CTA may finish)
-  uint32_t pad1;
+  uint32_t pad0;
   uint32_t tile_begin[kMaxBwdDesc + 1];
   BwdDesc d[kMaxBwdDesc];
 };

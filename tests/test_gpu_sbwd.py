@@ -48,7 +48,7 @@ def inputs(n, C, outer, dtype, seed):
     return x, up, s64, chain
 
 
-IMPLS = ["default", "stream", "tile1", "tile", "tilem", "tileq", "tileqmd", "tile2d", "tiledp", "tiledf"]
+IMPLS = ["default", "stream", "tile1", "tile", "tilem", "tileq", "tileqmd", "tile2d", "tiledp"]
 
 
 def make_ctx(qfb, impl, monkeypatch):
