@@ -669,7 +669,7 @@ constexpr int kConsumerWarps = kBwdThreads / 32;      // 8
 constexpr int kQuad = 64;         // 4 consumer warps x 2 leaf groups per lane (see quad_sum)
 constexpr int kMagicRint = 256;   // rint via rint_small (FP64 pipe) instead of FRND (XU pipe)
 constexpr int kDDiv = 2048;       // quotient via markstein_dd (4 FP64 ops) instead of markstein2_div (5)
-constexpr int kHalfF32 = 4096;    // binary16 storage, float32 terms (quad layout; QFB_OPT_BWD_HALF_FP32)
+constexpr int kHalfF32 = 4096;    // binary16 storage, float32 terms (QFB_OPT_BWD_HALF_FP32)
 constexpr int kL2Pre = 8192;      // producer prefetches the tile after the next refill into L2
 template <int V>
 __host__ __device__ constexpr int math_of() {
@@ -1547,6 +1547,8 @@ BwdFn kernel_ptr(int v, bool warp_part, uint32_t layout) {
     return e && e[0] == '2';
   }();
   if constexpr (sizeof(T) == 2)
+    // float32 terms: the quad layout (cheap arithmetic, the faster memory
+    // pipeline of 4 consumer warps: 75 us vs 80 us with 8 warps x 1 group)
     if (layout & kBwdLayoutHalfF32) return bwd_inst<T, kWarpPart | kQuad | kDDiv | kHalfF32>();
   const bool two = two_env || (layout & kBwdLayoutTwoCtas) != 0;
   if (two && (layout & ~kBwdLayoutTwoCtas) == kBwdLayoutDD) return bwd_inst<T, kWarpPart | kDDiv | kTwoCtas>();
