@@ -466,7 +466,7 @@ def fake_quantize_backward(x, log_s, cfg: Optional[QuantConfig], upstream,
     s64, chain = scale_grad_factors(lvals, cfg, precision)
     dev = x.device
     fac = torch.tensor(s64 + chain, dtype=torch.float64, device=dev)
-    dls = torch.zeros(ch, dtype=torch.float64, device=dev)
+    dls = torch.empty(ch, dtype=torch.float64, device=dev)  # accumulate = 0: every entry is written
     x = x.contiguous()
     upstream = upstream.contiguous()
     if upstream.dtype != x.dtype:

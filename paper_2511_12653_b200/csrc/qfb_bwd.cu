@@ -1087,7 +1087,11 @@ __device__ __forceinline__ double lane_slice_any(const double* p, int lane, uint
 constexpr uint32_t kFinRegMaxTiles = 2048;  // per <= 64
 constexpr int kFinRows = 4;
 
-__global__ void __launch_bounds__(32) bwd_finish_reg_kernel(const __grid_constant__ BwdBatch bt) {
+// early_chain: the chain factors were written before the main pass started
+// (the main pass is not itself a programmatic dependent), so they may be
+// read before griddepcontrol.wait, overlapping one load latency with the
+// main pass's tail.
+__global__ void __launch_bounds__(32) bwd_finish_reg_kernel(const __grid_constant__ BwdBatch bt, uint32_t early_chain) {
   uint32_t w = blockIdx.x;
   int di = 0;
   while (di < bt.n && w >= bt.d[di].chans) {
@@ -1105,8 +1109,9 @@ __global__ void __launch_bounds__(32) bwd_finish_reg_kernel(const __grid_constan
   // prologue above overlaps the main pass's tail; d_log_s and the partials
   // are read only after it has completed
   pdl_trigger();
+  double chain = early_chain ? d.chain[c] : 0.0;
   pdl_wait();
-  const double chain = d.chain[c];
+  if (!early_chain) chain = d.chain[c];
   const bool rows = d.accumulate == 2;
   double acc = d.accumulate == 1 ? d.d_log_s[c] : 0.0;
   for (uint32_t o = 0; o < d.outer; o += kFinRows) {
@@ -1660,8 +1665,10 @@ cudaError_t launch_bwd_finish(const BwdBatch& b, cudaStream_t st) {
   }();
   uint32_t zero = 0;
   void* fargs[] = {const_cast<BwdBatch*>(&b), &zero};
+  uint32_t early = pdl_enabled(kPdlBwd) ? 0u : 1u;
+  void* rargs[] = {const_cast<BwdBatch*>(&b), &early};
   if (max_tps <= kFinRegMaxTiles && !force_smem)
-    e = launch_main((const void*)bwd_finish_reg_kernel, dim3(warps), dim3(32), fargs, 0, st, kPdlFin);
+    e = launch_main((const void*)bwd_finish_reg_kernel, dim3(warps), dim3(32), rargs, 0, st, kPdlFin);
   else
     e = launch_main((const void*)bwd_finish_kernel, dim3(warps), dim3(32), fargs, 0, st, kPdlFin);
   if (e != cudaSuccess) return e;

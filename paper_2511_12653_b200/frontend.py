@@ -16,12 +16,19 @@ from __future__ import annotations
 
 import ctypes
 
+import os
+
 import numpy as np
 
 from . import BWD_ROWS, CBwdDesc, CChainDesc, CFqDesc, F16, F32, Context, check, lib, scale_grad_factors
 from .shapes import (ACT_GELU, ACT_NONE, ACT_RELU, H, W, ChainPoint, QuantPoint,  # noqa: F401
                      dpvo_quant_points, frame_bytes, window_chain_points)
 
+
+
+# diagnostic A/B knob: extra QFB_FLAG_* bits on the forward descriptors
+# (e.g. QFB_FWD_EXTRA_FLAGS=2: evict-first loads/stores); results unchanged
+_FWD_EXTRA_FLAGS = int(os.environ.get("QFB_FWD_EXTRA_FLAGS", "0"))
 
 class FrontendQuantPass:
     """Device buffers + C-ABI descriptor tables for `frames` frames of the
@@ -123,7 +130,7 @@ class FrontendQuantPass:
             d = CFqDesc()
             d.x = xs[pi].data_ptr()
             d.outer, d.channels, d.inner = self.frames, p.channels, p.inner
-            d.n_out, d.q_max, d.flags = len(p.consumers), 127, (0x4 if self.int8_out else 0)
+            d.n_out, d.q_max, d.flags = len(p.consumers), 127, (0x4 if self.int8_out else 0) | _FWD_EXTRA_FLAGS
             for k in range(len(p.consumers)):
                 d.y[k] = self.y[ci + k].data_ptr()
                 d.scale[k] = self.s32[ci + k].data_ptr()
