@@ -479,12 +479,16 @@ def run_qfb(args):
         si = i % nsets
         if ev is not None:
             ev[0].record(stream)
+            # the library records ev[3] between the backward's main pass and
+            # its finisher (QFB_OPT_MAIN_PASS_EVENT): the dominant kernel alone
+            ctx.set_option(q.OPT_MAIN_PASS_EVENT, ev[3].cuda_event)
         fp.forward(si)
         if ev is not None:
             ev[1].record(stream)
         fp.backward(si)
         if ev is not None:
             ev[2].record(stream)
+            ctx.set_option(q.OPT_MAIN_PASS_EVENT, 0)
         exchange()
 
     # warm up eagerly (sizes the workspaces), then capture the step as CUDA
@@ -573,12 +577,17 @@ def run_qfb(args):
     # per-kernel attribution for the roofline: the same steps launched
     # eagerly with CUDA events around each kernel on the library's stream
     k_att = min(args.steps, 200)
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(k_att)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(k_att)]
+    for e in evs:
+        e[3].record(stream)  # creates the CUDA event the library records into
+    torch.cuda.synchronize(dev)
     for i in range(k_att):
         eager_step(i, evs[i])
     torch.cuda.synchronize(dev)
     fwd_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / k_att
     bwd_ms = sum(e[1].elapsed_time(e[2]) for e in evs) / k_att
+    bwd_main_ms = sum(e[1].elapsed_time(e[3]) for e in evs) / k_att
+    fin_ms = sum(e[3].elapsed_time(e[2]) for e in evs) / k_att
     if pg is not None:
         ms_total = pg.max(ms_total)
         pg.barrier()
@@ -593,10 +602,19 @@ def run_qfb(args):
     bwd_gbps = b["bwd"] / (bwd_ms / 1000.0) / 1e9
     traffic = load_traffic()
     dominant = "bwd" if b["bwd"] >= b["fwd"] else "fwd"
-    roofline = {"bound": "hbm", "kernel": "qfb::bwd_kernel (scale-only LSQ/STE backward)",
-                "achieved": bwd_gbps, "peak": peak, "unit": "GB/s", "frac": bwd_gbps / peak,
+    bwd_main_gbps = b["bwd"] / (bwd_main_ms / 1000.0) / 1e9
+    roofline = {"bound": "hbm", "kernel": "qfb::bwd_kernel (scale-only LSQ/STE backward, main pass)",
+                "achieved": bwd_main_gbps, "peak": peak, "unit": "GB/s", "frac": bwd_main_gbps / peak,
                 "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": b["bwd"],
+                "launch_us": bwd_main_ms * 1e3,
+                "with_finisher": {"kernels": "bwd_kernel + bwd_finish_reg_kernel (one C-ABI call)",
+                                  "us": bwd_ms * 1e3, "achieved": bwd_gbps, "frac": bwd_gbps / peak,
+                                  "finisher_us": fin_ms * 1e3},
+                "timing": "CUDA events on the library stream around each kernel of 200 eager steps inside "
+                          "the bench (the library records the main-pass event between its two launches, "
+                          "QFB_OPT_MAIN_PASS_EVENT); algorithmic bytes = 3 x 4 B x 41,164,800 quant-point "
+                          "elements (read x and upstream, write d_input)",
                 "traffic": (traffic or {}).get(args.dtype, {}).get("bwd_bytes_per_launch"),
                 "fwd_kernel": {"kernel": "qfb::ew_tma_kernel<T, false, NS> (fused multi-point forward; "
                                          "NS = tma_stages(): 3 for one f32 frame)",
@@ -630,7 +648,7 @@ def run_qfb(args):
                 "data_generator": "CounterRng normal (rng.hpp:24-50), generated on the device",
                 "config": bench_config(args, ws),
                 "gbps": gbps, "hbm_frac": (gbps / ws) / peak,
-                "kernel_ms": {"fwd": fwd_ms, "bwd": bwd_ms},
+                "kernel_ms": {"fwd": fwd_ms, "bwd": bwd_ms, "bwd_main": bwd_main_ms, "bwd_finish": fin_ms},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clocks, "secondary": secondary,
                 "timing": (f"value: CUDA-graph replays of {G} consecutive steps each (fwd + bwd + finisher "

@@ -145,6 +145,11 @@ qfb_status qfb_ctx_set_stream(qfb_ctx* ctx, void* stream);
  * with the reference within the FP16 tolerance (rel 1e-2; measured ~1e-6,
  * DESIGN.md §2) instead of bitwise. Off: every result is bitwise. */
 #define QFB_OPT_BWD_HALF_FP32 1
+/* QFB_OPT_MAIN_PASS_EVENT (value: a cudaEvent_t cast to int64, 0 = off):
+ * profiling hook — each backward call records the event on the context
+ * stream between its main pass and its finisher kernel, so a caller can
+ * time the main pass alone with events (bench.py's roofline). */
+#define QFB_OPT_MAIN_PASS_EVENT 2
 qfb_status qfb_ctx_set_option(qfb_ctx* ctx, int32_t option, int64_t value);
 void* qfb_ctx_stream(qfb_ctx* ctx);
 int32_t qfb_ctx_sm_count(qfb_ctx* ctx);

@@ -165,6 +165,7 @@ _sig("qfb_ctx_destroy", _i32, [_vp])
 _sig("qfb_ctx_set_stream", _i32, [_vp, _vp])
 _sig("qfb_ctx_set_option", _i32, [_vp, _i32, _i64])
 OPT_BWD_HALF_FP32 = 1  # QFB_OPT_BWD_HALF_FP32
+OPT_MAIN_PASS_EVENT = 2  # QFB_OPT_MAIN_PASS_EVENT (profiling hook)
 _sig("qfb_ctx_stream", _vp, [_vp])
 _sig("qfb_ctx_sm_count", _i32, [_vp])
 _sig("qfb_ctx_sync", _i32, [_vp])

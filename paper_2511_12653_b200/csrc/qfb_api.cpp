@@ -126,6 +126,7 @@ struct qfb_ctx {
   // consumer layout of the full-tile kernel (QFB_BWD_IMPL=tile[q][m][d] at creation)
   uint32_t bwd_layout = kBwdLayoutDD;  // measured best (r02)
   bool bwd_half_fp32 = false;           // QFB_OPT_BWD_HALF_FP32
+  cudaEvent_t main_pass_event = nullptr;  // QFB_OPT_MAIN_PASS_EVENT
   // status word the forward kernels latch into: d_status, or a host-pass
   // slot's own word while that slot's kernels are enqueued
   uint32_t* cur_status = nullptr;
@@ -597,6 +598,9 @@ qfb_status qfb_ctx_set_option(qfb_ctx* ctx, int32_t option, int64_t value) {
     case QFB_OPT_BWD_HALF_FP32:
       if (value != 0 && value != 1) return fail(QFB_ERR_VALUE, "QFB_OPT_BWD_HALF_FP32 takes 0 or 1");
       ctx->bwd_half_fp32 = value != 0;
+      return QFB_OK;
+    case QFB_OPT_MAIN_PASS_EVENT:
+      ctx->main_pass_event = reinterpret_cast<cudaEvent_t>(static_cast<intptr_t>(value));
       return QFB_OK;
     default:
       return fail(QFB_ERR_VALUE, "unknown context option %d", option);
@@ -1085,7 +1089,7 @@ qfb_status qfb_fq_bwd_multi(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc* t
       ctx->bwd_occ[dtype].emplace_back(key, per_sm);
     }
     const int grid = ctx->sm_count * per_sm;
-    cudaError_t e = launch_bwd(dtype, b, grid, ctx->stream);
+    cudaError_t e = launch_bwd(dtype, b, grid, ctx->stream, ctx->main_pass_event);
     if (e != cudaSuccess) return cuda_fail(e, "bwd_kernel launch");
     ctx->launches += 2;  // main pass + finisher
     i += cnt;
