@@ -535,7 +535,7 @@ qfb_status qfb_ctx_create(int32_t device, void* stream, qfb_ctx** out) {
         uint32_t l = 0;
         for (const char* p = env + 4; *p; ++p) {
           l |= *p == 'q' ? kBwdLayoutQuad : *p == 'm' ? kBwdLayoutMagic : *p == 'd' ? kBwdLayoutDD
-             : *p == '2' ? kBwdLayoutTwoCtas : *p == 'p' ? kBwdLayoutPrefetch : 0u;
+             : *p == '2' ? kBwdLayoutTwoCtas : *p == 'p' ? kBwdLayoutPrefetch : *p == 'u' ? kBwdLayoutCU : 0u;
         }
         c->bwd_layout = l;
       }
@@ -1081,7 +1081,7 @@ qfb_status qfb_fq_bwd_multi(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc* t
     bwd_ring_size(dtype, max_tile, &b.stage_elems, &b.nstages, &smem);
     // cached: keeps steady-state launches free of runtime queries (graph capture)
     int per_sm = 0;
-    const size_t key = (smem * 2 + (warp_part ? 1 : 0)) * 64 + b.layout;
+    const size_t key = (smem * 2 + (warp_part ? 1 : 0)) * 128 + b.layout;
     for (const auto& kv : ctx->bwd_occ[dtype])
       if (kv.first == key) per_sm = kv.second;
     if (per_sm == 0) {

@@ -977,6 +977,142 @@ __global__ void __launch_bounds__(cta_threads<V>(), (V & kTwoCtas) ? 2 : 3) bwd_
   }
 }
 
+// ---------------------------------------------------------------------
+// CTA-uniform main pass (kCU, QFB_BWD_IMPL=tile...u): the forward chain
+// kernel's pipeline shape for the backward's tree tiles. 8 warps, no
+// producer warp: warp 0 locates tiles (32 at a time) and its lane 0 issues
+// the TMA refill of the stage the previous iteration freed, NS-1 tiles
+// ahead; every warp computes its 32 leaf groups, writes d_input into the
+// stage and its warp sum; ONE CTA barrier per tile; then warp 0 combines
+// the 8 warp sums into the tile partial and sends d_input out (ragged ends
+// by lanes, the aligned interior by one bulk store). A stage is refilled
+// one iteration later, after that store has read it.
+// ---------------------------------------------------------------------
+constexpr int kCU = 16384;
+constexpr int kCuThreadStore = 32768;  // probe: d_input copied out by all threads (no TMA store)
+
+template <typename T, int V>
+__global__ void __launch_bounds__(kBwdThreads, 3) bwd_cu_kernel(const __grid_constant__ BwdBatch bt) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full[kMaxStages];
+  __shared__ TileRef refs[kMaxStages];
+  __shared__ double wsum[kMaxStages][kConsumerWarps];
+  const int nst = bt.nstages;
+  const uint32_t se = bt.stage_elems;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int lane = tid & 31;
+  const uint32_t total = bt.tile_begin[bt.n];
+  pdl_wait();
+  if (blockIdx.x >= total) return;
+  if (tid == 0) {
+    for (int s = 0; s < nst; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+    pdl_trigger();
+  }
+  __syncthreads();
+
+  // warp 0's tile locator (as the warp-specialized producer's)
+  TileRef mine;
+  uint32_t batch = 0xffffffffu;
+  auto ref_of = [&](uint32_t k) -> TileRef {
+    const uint32_t b = k >> 5;
+    if (b != batch) {
+      batch = b;
+      const uint32_t id = blockIdx.x + ((b << 5) + (uint32_t)lane) * gridDim.x;
+      if (id < total) mine = locate_full<T>(bt, id);
+    }
+    return shfl_ref(mine, (int)(k & 31u));
+  };
+  if (warp == 0) {
+    for (int s = 0; s < nst - 1; ++s) {
+      const uint32_t id = blockIdx.x + (uint32_t)s * gridDim.x;
+      if (id < total) {
+        Stage<T> st = stage_at<T>(smem_raw, se, s);
+        produce<T, V>(bt, ref_of((uint32_t)s), st, &refs[s], &full[s], lane);
+      }
+    }
+  }
+  GroupCache gc;
+  uint32_t full_phase = 0;
+  int s = 0;
+  for (uint32_t k = 0, tile_id = blockIdx.x; tile_id < total; tile_id += gridDim.x, ++k) {
+    if (warp == 0) {
+      // refill the stage freed by the previous iteration with tile k+nst-1
+      const uint32_t nid = tile_id + (uint32_t)(nst - 1) * gridDim.x;
+      if (nid < total) {
+        const int rs = (s + nst - 1) % nst;
+        const TileRef nr = ref_of(k + (uint32_t)nst - 1u);
+        if (lane == 0) bulk_wait_read_all();  // that stage's d_input store has read it
+        __syncwarp();
+        Stage<T> st = stage_at<T>(smem_raw, se, rs);
+        produce<T, V>(bt, nr, st, &refs[rs], &full[rs], lane, true);
+      }
+    }
+    const uint32_t par = (full_phase >> s) & 1u;
+    mbar_wait(&full[s], par);
+    full_phase ^= 1u << s;
+    Stage<T> st = stage_at<T>(smem_raw, se, s);
+    const TileRef cur = refs[s];
+    const BwdDesc& d = bt.d[cur.di];
+    double v = 0.0;
+    if constexpr ((V & kProbeNoCompute) == 0) {
+      DivCtx dc;
+      dc.s = pin(cur.s);
+      dc.y = pin(cur.y);
+      dc.ylo = (V & kDDiv) ? pin(recip_lo(cur.s, cur.y)) : 0.0;
+      dc.usable = cur.s >= 0x1p-100 && cur.s <= 0x1p100;
+      const double q = pin(d.q);
+      int glo, glen;
+      gc.get(cur.m, (int)d.g, tid, glo, glen);
+      T* sx = st.x + cur.off + glo;
+      const T* su = st.up + cur.off + glo;
+      constexpr int kM = math_of<V>();
+      v = d.dx != nullptr ? group_sum_any<T, true, kM>(sx, su, glen, dc, q)
+                          : group_sum_any<T, false, kM>(sx, su, glen, dc, q);
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+    }
+    if (lane == 0) wsum[s][warp] = v;
+    fence_proxy_async_smem();  // d_input leaves through the async proxy
+    __syncthreads();           // the tile's d_input and warp sums are in shared memory
+    if constexpr ((V & kCuThreadStore) != 0) {
+      // probe: every thread copies d_input out with 16-byte stores, then a
+      // second barrier frees the stage (no TMA store)
+      if (d.dx != nullptr && d.vec) {
+        const uint64_t b0 = cur.A * sizeof(T), b1 = (cur.A + (uint64_t)cur.m) * sizeof(T);
+        const uint64_t i0 = (b0 + 15) & ~uint64_t(15), i1 = b1 & ~uint64_t(15);
+        for (uint64_t o = i0 + (uint64_t)tid * 16; o < i1; o += 16 * kBwdThreads)
+          *reinterpret_cast<uint4*>(static_cast<char*>(d.dx) + o) =
+              *reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(st.x) + (o - cur.w0));
+        if (warp == 0) {
+          const int head = (int)(((i0 > b1 ? b1 : i0) - b0) / sizeof(T));
+          const int tail0 = i1 > i0 ? (int)((i1 - b0) / sizeof(T)) : head;
+          for (int e = lane; e < head; e += 32) static_cast<T*>(d.dx)[cur.A + e] = st.x[cur.off + e];
+          for (int e = tail0 + lane; e < cur.m; e += 32) static_cast<T*>(d.dx)[cur.A + e] = st.x[cur.off + e];
+        }
+      } else if (warp == 0) {
+        store_dx<T>(d, cur, st, lane);
+      }
+      if (warp == 0) {
+        double w = lane < kConsumerWarps ? wsum[s][lane] : 0.0;
+#pragma unroll
+        for (int o = 1; o < kConsumerWarps; o <<= 1) w = __dadd_rn(w, __shfl_xor_sync(0xffffffffu, w, o));
+        if (lane == 0) d.partials[((uint64_t)cur.seg << d.part_log) + cur.t] = w;
+      }
+      __syncthreads();
+    } else if (warp == 0) {
+      double w = lane < kConsumerWarps ? wsum[s][lane] : 0.0;
+#pragma unroll
+      for (int o = 1; o < kConsumerWarps; o <<= 1) w = __dadd_rn(w, __shfl_xor_sync(0xffffffffu, w, o));
+      if (lane == 0) d.partials[((uint64_t)cur.seg << d.part_log) + cur.t] = w;
+      store_dx<T>(d, cur, st, lane);
+    }
+    s = s + 1 == nst ? 0 : s + 1;
+  }
+  if (warp == 0 && lane == 0) bulk_wait_all();
+}
+
 // Finisher: one warp per (descriptor, channel). Each row's 2^part_log tile
 // partials are reduced in perfect-tree order (lane slices + xor butterfly),
 // times chain[c]; rows of the channel are folded in row order.
@@ -1528,6 +1664,7 @@ struct BwdFn {
 };
 template <typename T, int V>
 BwdFn bwd_inst() {
+  if constexpr ((V & kCU) != 0) return BwdFn{(const void*)bwd_cu_kernel<T, V>, kBwdThreads};
   return BwdFn{(const void*)bwd_kernel<T, V>, cta_threads<V>()};
 }
 
@@ -1559,6 +1696,14 @@ BwdFn kernel_ptr(int v, bool warp_part, uint32_t layout) {
   if (two && (layout & ~kBwdLayoutTwoCtas) == kBwdLayoutDD) return bwd_inst<T, kWarpPart | kDDiv | kTwoCtas>();
   if ((layout & ~kBwdLayoutPrefetch) == kBwdLayoutDD && (layout & kBwdLayoutPrefetch))
     return bwd_inst<T, kWarpPart | kDDiv | kL2Pre>();
+  if (layout & kBwdLayoutCU) {
+    switch (v) {
+      case 9: return bwd_inst<T, kWarpPart | kDDiv | kCU | kProbeNoCompute>();
+      case 10: return bwd_inst<T, kWarpPart | kDDiv | kCU | kProbeNoCompute | kCuThreadStore>();
+      case 11: return bwd_inst<T, kWarpPart | kDDiv | kCU | kCuThreadStore>();
+      default: return bwd_inst<T, kWarpPart | kDDiv | kCU>();
+    }
+  }
   // layout bits: kBwdLayoutMagic | kBwdLayoutQuad | kBwdLayoutDD
   switch (layout & 7u) {
     case 1: return bwd_inst<T, kWarpPart | kMagicRint>();

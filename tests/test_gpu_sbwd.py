@@ -48,7 +48,7 @@ def inputs(n, C, outer, dtype, seed):
     return x, up, s64, chain
 
 
-IMPLS = ["default", "stream", "tile1", "tile", "tilem", "tileq", "tileqmd", "tile2d", "tiledp"]
+IMPLS = ["default", "stream", "tile1", "tile", "tilem", "tileq", "tileqmd", "tile2d", "tiledp", "tiledu"]
 
 
 def make_ctx(qfb, impl, monkeypatch):
