@@ -58,6 +58,10 @@ def parse(argv=None):
                    help="reference arm: skip the one-thread sample")
     p.add_argument("--no-secondary", action="store_true",
                    help="skip the config-3 chain window and config-5 forward-throughput lines")
+    p.add_argument("--async-finish", action="store_true",
+                   help="run the backward's finisher on the library's side stream (QFB_OPT_BWD_ASYNC_FINISH, "
+                        "joined by the next step's backward / the end of the timed region); measured slower "
+                        "for f32 (the finisher's CTAs delay the persistent forward's first wave)")
     p.add_argument("--half-fp32-terms", action="store_true",
                    help="f16: the opt-in float32-term backward (QFB_OPT_BWD_HALF_FP32; d_input bitwise, "
                         "scale gradients within tolerance instead of bitwise)")
@@ -473,6 +477,7 @@ def run_qfb(args):
         if ex is not None:
             # QAT exchange: the step's frame rows of all ranks, folded in
             # frame order into the gradient vector (bit-identical at any N)
+            ctx.join()  # the rows are complete once the finisher is joined
             ex(rows, grads)
 
     def eager_step(i, ev=None):
@@ -487,6 +492,7 @@ def run_qfb(args):
             ev[1].record(stream)
         fp.backward(si)
         if ev is not None:
+            ctx.join()  # the finisher inside the measured backward
             ev[2].record(stream)
             ctx.set_option(q.OPT_MAIN_PASS_EVENT, 0)
         exchange()
@@ -496,6 +502,10 @@ def run_qfb(args):
     for i in range(max(1, args.warmup)):
         eager_step(i)
     ctx.sync()
+    # the finisher of step k overlaps the forward of step k+1 (side stream,
+    # joined by step k+1's backward and at the end of every captured graph)
+    if args.async_finish:
+        ctx.set_option(q.OPT_BWD_ASYNC_FINISH, 1)
     capturable = pg is None or pg.nccl
     use_graph = not args.no_graph and capturable
     graphs = []
@@ -514,6 +524,7 @@ def run_qfb(args):
                     fp.forward(si)
                     fp.backward(si)
                     exchange()
+                    ctx.join()
                 graphs.append(g)
             launches_per_step = (ctx.launch_count - c0) // nsets
             if G > 1:
@@ -523,6 +534,7 @@ def run_qfb(args):
                         fp.forward(k % nsets)
                         fp.backward(k % nsets)
                         exchange()
+                    ctx.join()
         except Exception as exc:  # pragma: no cover - fall back to eager timing
             print(f"graph capture failed ({exc}); timing eager launches", file=sys.stderr)
             use_graph = False
@@ -566,6 +578,7 @@ def run_qfb(args):
     wall0 = time.perf_counter()
     t_start.record(stream)
     run_steps(args.steps)
+    ctx.join()  # eager path: the last step's finisher
     t_end.record(stream)
     torch.cuda.synchronize(dev)
     wall1 = time.perf_counter()
@@ -584,6 +597,7 @@ def run_qfb(args):
     for i in range(k_att):
         eager_step(i, evs[i])
     torch.cuda.synchronize(dev)
+    ctx.set_option(q.OPT_BWD_ASYNC_FINISH, 0)  # stream-ordered finisher for everything below
     fwd_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / k_att
     bwd_ms = sum(e[1].elapsed_time(e[2]) for e in evs) / k_att
     bwd_main_ms = sum(e[1].elapsed_time(e[3]) for e in evs) / k_att
@@ -651,6 +665,9 @@ def run_qfb(args):
                 "kernel_ms": {"fwd": fwd_ms, "bwd": bwd_ms, "bwd_main": bwd_main_ms, "bwd_finish": fin_ms},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clocks, "secondary": secondary,
+                "finisher": ("stream-ordered" if not args.async_finish else
+                             "side stream (QFB_OPT_BWD_ASYNC_FINISH): step k's finisher overlaps step k+1's "
+                             "forward, joined by step k+1's backward and before the end of the timed region"),
                 "timing": (f"value: CUDA-graph replays of {G} consecutive steps each (fwd + bwd + finisher "
                            "launches per step" + (" + the NCCL gather-fold exchange" if ws > 1 else "") +
                            ", serial on the library stream) between CUDA events, max over ranks"

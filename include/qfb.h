@@ -150,7 +150,20 @@ qfb_status qfb_ctx_set_stream(qfb_ctx* ctx, void* stream);
  * stream between its main pass and its finisher kernel, so a caller can
  * time the main pass alone with events (bench.py's roofline). */
 #define QFB_OPT_MAIN_PASS_EVENT 2
+/* QFB_OPT_BWD_ASYNC_FINISH (value 0/1, default 0): the backward's finisher
+ * (the per-row tree of tile partials -> d_log_s) runs on a context-owned
+ * side stream, forked after the main pass, so the caller's next kernels
+ * (e.g. the next frame's forward) overlap it. d_log_s is then complete
+ * only after a JOIN point in the context stream's order: the next
+ * backward call on this context (which reuses the partials workspace),
+ * qfb_ctx_join, or qfb_ctx_sync. Capturable (event fork/join); a capture
+ * must qfb_ctx_join before it ends. */
+#define QFB_OPT_BWD_ASYNC_FINISH 3
 qfb_status qfb_ctx_set_option(qfb_ctx* ctx, int32_t option, int64_t value);
+/* Make the context stream wait for any work the context forked to its side
+ * stream (QFB_OPT_BWD_ASYNC_FINISH); no-op otherwise. Stream-ordered,
+ * capturable. */
+qfb_status qfb_ctx_join(qfb_ctx* ctx);
 void* qfb_ctx_stream(qfb_ctx* ctx);
 int32_t qfb_ctx_sm_count(qfb_ctx* ctx);
 /* Synchronize the stream; report (and clear) latched device conditions.

@@ -166,6 +166,8 @@ _sig("qfb_ctx_set_stream", _i32, [_vp, _vp])
 _sig("qfb_ctx_set_option", _i32, [_vp, _i32, _i64])
 OPT_BWD_HALF_FP32 = 1  # QFB_OPT_BWD_HALF_FP32
 OPT_MAIN_PASS_EVENT = 2  # QFB_OPT_MAIN_PASS_EVENT (profiling hook)
+OPT_BWD_ASYNC_FINISH = 3  # QFB_OPT_BWD_ASYNC_FINISH
+_sig("qfb_ctx_join", _i32, [_vp])
 _sig("qfb_ctx_stream", _vp, [_vp])
 _sig("qfb_ctx_sm_count", _i32, [_vp])
 _sig("qfb_ctx_sync", _i32, [_vp])
@@ -316,6 +318,11 @@ class Context:
 
     def sync(self) -> None:
         check(_lib.qfb_ctx_sync(self.handle))
+
+    def join(self) -> None:
+        """qfb_ctx_join: the context stream waits for its side-stream work
+        (QFB_OPT_BWD_ASYNC_FINISH's finisher)."""
+        check(_lib.qfb_ctx_join(self.handle))
 
     @property
     def launch_count(self) -> int:

@@ -127,6 +127,11 @@ struct qfb_ctx {
   uint32_t bwd_layout = kBwdLayoutDD;  // measured best (r02)
   bool bwd_half_fp32 = false;           // QFB_OPT_BWD_HALF_FP32
   cudaEvent_t main_pass_event = nullptr;  // QFB_OPT_MAIN_PASS_EVENT
+  // QFB_OPT_BWD_ASYNC_FINISH: side stream for the finisher, fork/join events
+  bool async_finish = false;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool side_pending = false;
   // status word the forward kernels latch into: d_status, or a host-pass
   // slot's own word while that slot's kernels are enqueued
   uint32_t* cur_status = nullptr;
@@ -569,6 +574,12 @@ qfb_status qfb_ctx_destroy(qfb_ctx* ctx) {
   if (ctx->s_in) cudaStreamSynchronize(ctx->s_in);
   if (ctx->s_out) cudaStreamSynchronize(ctx->s_out);
   if (ctx->d_status) cudaFree(ctx->d_status);
+  if (ctx->side) {
+    cudaStreamSynchronize(ctx->side);
+    cudaStreamDestroy(ctx->side);
+  }
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->h_status) cudaFreeHost(ctx->h_status);
   if (ctx->ws_f64.p) cudaFree(ctx->ws_f64.p);
   if (ctx->ws_u32.p) cudaFree(ctx->ws_u32.p);
@@ -599,6 +610,19 @@ qfb_status qfb_ctx_set_option(qfb_ctx* ctx, int32_t option, int64_t value) {
       if (value != 0 && value != 1) return fail(QFB_ERR_VALUE, "QFB_OPT_BWD_HALF_FP32 takes 0 or 1");
       ctx->bwd_half_fp32 = value != 0;
       return QFB_OK;
+    case QFB_OPT_BWD_ASYNC_FINISH: {
+      if (value != 0 && value != 1) return fail(QFB_ERR_VALUE, "QFB_OPT_BWD_ASYNC_FINISH takes 0 or 1");
+      if (value && !ctx->side) {
+        DeviceGuard g(ctx->device);
+        QFB_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+        QFB_CUDA(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+        QFB_CUDA(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+      }
+      if (!value)
+        if (qfb_status st = qfb_ctx_join(ctx)) return st;
+      ctx->async_finish = value != 0;
+      return QFB_OK;
+    }
     case QFB_OPT_MAIN_PASS_EVENT:
       ctx->main_pass_event = reinterpret_cast<cudaEvent_t>(static_cast<intptr_t>(value));
       return QFB_OK;
@@ -617,8 +641,18 @@ void* qfb_ctx_stream(qfb_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
 int32_t qfb_ctx_sm_count(qfb_ctx* ctx) { return ctx ? ctx->sm_count : 0; }
 int64_t qfb_ctx_launch_count(qfb_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+qfb_status qfb_ctx_join(qfb_ctx* ctx) {
+  if (qfb_status st = check_ctx(ctx)) return st;
+  if (!ctx->side_pending) return QFB_OK;
+  DeviceGuard g(ctx->device);
+  QFB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
+  ctx->side_pending = false;
+  return QFB_OK;
+}
+
 qfb_status qfb_ctx_sync(qfb_ctx* ctx) {
   if (qfb_status st = check_ctx(ctx)) return st;
+  if (qfb_status st = qfb_ctx_join(ctx)) return st;
   DeviceGuard g(ctx->device);
   QFB_CUDA(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(uint32_t), cudaMemcpyDeviceToHost,
                            ctx->stream));
@@ -1029,6 +1063,8 @@ qfb_status qfb_fq_bwd_multi(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc* t
   std::vector<BwdPlan> plans;
   bool stream = false, warp_part = false;
   if (qfb_status st = plan_bwd_table(ctx, dtype, table, n, plans, &stream, &warp_part)) return st;
+  // an asynchronous finisher still reading the partials workspace
+  if (qfb_status st = qfb_ctx_join(ctx)) return st;
   int32_t i = 0;
   while (i < n) {
     // Batch up to kMaxBwdDesc entries; each gets its own workspace slice.
@@ -1089,7 +1125,15 @@ qfb_status qfb_fq_bwd_multi(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc* t
       ctx->bwd_occ[dtype].emplace_back(key, per_sm);
     }
     const int grid = ctx->sm_count * per_sm;
-    cudaError_t e = launch_bwd(dtype, b, grid, ctx->stream, ctx->main_pass_event);
+    // a later batch reuses the partials: join the previous batch's finisher
+    if (qfb_status st = qfb_ctx_join(ctx)) return st;
+    const bool async = ctx->async_finish && ctx->side;
+    cudaError_t e = launch_bwd(dtype, b, grid, ctx->stream, ctx->main_pass_event, async ? ctx->side : nullptr,
+                               ctx->ev_fork);
+    if (e == cudaSuccess && async) {
+      e = cudaEventRecord(ctx->ev_join, ctx->side);
+      ctx->side_pending = true;
+    }
     if (e != cudaSuccess) return cuda_fail(e, "bwd_kernel launch");
     ctx->launches += 2;  // main pass + finisher
     i += cnt;
@@ -1189,6 +1233,7 @@ qfb_status qfb_fake_quantize_backward_host(qfb_ctx* ctx, qfb_precision prec, con
                                  dx ? ctx->host_io[4].p : nullptr, outer, channels, inner, dfac,
                                  dfac + channels, qfb_q_max(cfg), dacc, accumulate))
     return st;
+  if (qfb_status st = qfb_ctx_join(ctx)) return st;  // d_log_s complete (async finisher)
   if (dx) QFB_CUDA(cudaMemcpyAsync(dx, ctx->host_io[4].p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
   QFB_CUDA(cudaMemcpyAsync(d_log_s, dacc, (size_t)channels * sizeof(double),
                            cudaMemcpyDeviceToHost, ctx->stream));
@@ -1399,8 +1444,10 @@ qfb_status qfb_quant_pass_host_submit(qfb_ctx* ctx, qfb_precision prec, const qf
                               const_cast<double*>(f + 2 * p.channels), p.outer, p.channels, p.inner, q, 0, 0};
         ++nb;
       }
-      if (nb)
+      if (nb) {
         if (qfb_status st = qfb_fq_bwd_multi(ctx, QFB_F32, bd, nb)) return st;
+        if (qfb_status st = qfb_ctx_join(ctx)) return st;  // d_log_s complete (async finisher)
+      }
     }
     QFB_CUDA(cudaEventRecord(sl.ev[2 * g0 + 1], ctx->stream));
     QFB_CUDA(cudaStreamWaitEvent(ctx->s_out, sl.ev[2 * g0 + 1], 0));

@@ -1739,7 +1739,8 @@ cudaError_t bwd_occupancy_smem(int dtype, size_t smem, int* blocks_per_sm, bool 
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f.fn, f.threads, smem);
 }
 
-cudaError_t launch_bwd(int dtype, const BwdBatch& b, int grid, cudaStream_t st, cudaEvent_t after_main) {
+cudaError_t launch_bwd(int dtype, const BwdBatch& b, int grid, cudaStream_t st, cudaEvent_t after_main,
+                       cudaStream_t fin_stream, cudaEvent_t fork) {
   const uint32_t tiles = b.tile_begin[b.n];
   if (tiles == 0) return cudaSuccess;
   if ((uint32_t)grid > tiles) grid = (int)tiles;
@@ -1759,6 +1760,12 @@ cudaError_t launch_bwd(int dtype, const BwdBatch& b, int grid, cudaStream_t st, 
     return e && e[0] == '1';
   }();
   if (skip_fin) return cudaSuccess;
+  if (fin_stream) {  // QFB_OPT_BWD_ASYNC_FINISH: the finisher on the side stream
+    e = cudaEventRecord(fork, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(fin_stream, fork, 0);
+    if (e != cudaSuccess) return e;
+    return launch_bwd_finish(b, fin_stream);
+  }
   return launch_bwd_finish(b, st);
 }
 

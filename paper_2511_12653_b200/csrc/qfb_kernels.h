@@ -221,8 +221,11 @@ void bwd_ring_size(int dtype, uint32_t max_tile, uint32_t* stage_elems, int32_t*
                    size_t* smem_bytes);
 // Main pass (tile partials) + finisher (segment trees, chain, outer fold);
 // stream order replaces fences and tickets.
+// fin_stream != nullptr: the finisher goes to fin_stream after `fork` (recorded
+// on st after the main pass); the caller joins it later.
 cudaError_t launch_bwd(int dtype, const BwdBatch& b, int grid, cudaStream_t st,
-                       cudaEvent_t after_main = nullptr);
+                       cudaEvent_t after_main = nullptr, cudaStream_t fin_stream = nullptr,
+                       cudaEvent_t fork = nullptr);
 // The finisher alone: per (descriptor, channel) the perfect tree over the
 // 2^tps_log partials of each row, times chain, folded over the rows.
 cudaError_t launch_bwd_finish(const BwdBatch& b, cudaStream_t st);

@@ -32,5 +32,19 @@ e1.record(stream)
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 200
 b = fp.bytes_per_step()["bwd"]
-print(json.dumps({"dtype": dt, "variant": os.environ.get("QFB_BWD_VARIANT", "0"), "impl": os.environ.get("QFB_BWD_IMPL", "") + ("+h32" if os.environ.get("QFB_HALF_FP32") == "1" else ""), "us": ms * 1e3,
+# the main pass alone: the library records an event between the main pass
+# and the finisher (QFB_OPT_MAIN_PASS_EVENT)
+st_ev = [torch.cuda.Event(enable_timing=True) for _ in range(50)]
+mid_ev = [torch.cuda.Event(enable_timing=True) for _ in range(50)]
+for e in mid_ev:
+    e.record(stream)
+torch.cuda.synchronize()
+for i in range(50):
+    st_ev[i].record(stream)
+    ctx.set_option(q.OPT_MAIN_PASS_EVENT, mid_ev[i].cuda_event)
+    fp.backward(i % 2)
+ctx.set_option(q.OPT_MAIN_PASS_EVENT, 0)
+torch.cuda.synchronize()
+main_ms = sum(a.elapsed_time(m) for a, m in zip(st_ev, mid_ev)) / 50
+print(json.dumps({"dtype": dt, "variant": os.environ.get("QFB_BWD_VARIANT", "0"), "impl": os.environ.get("QFB_BWD_IMPL", "") + ("+h32" if os.environ.get("QFB_HALF_FP32") == "1" else ""), "us": ms * 1e3, "main_us": main_ms * 1e3, "main_frac": b / (main_ms / 1e3) / 1e9 / 6551.0,
                   "gbps": b / (ms / 1e3) / 1e9, "frac": b / (ms / 1e3) / 1e9 / 6551.0}))
