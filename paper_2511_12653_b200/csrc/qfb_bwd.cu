@@ -1227,8 +1227,10 @@ constexpr int kFinRows = 4;
 // (the main pass is not itself a programmatic dependent), so they may be
 // read before griddepcontrol.wait, overlapping one load latency with the
 // main pass's tail.
-__global__ void __launch_bounds__(32) bwd_finish_reg_kernel(const __grid_constant__ BwdBatch bt, uint32_t early_chain) {
-  uint32_t w = blockIdx.x;
+template <int WPB>
+__global__ void __launch_bounds__(32 * WPB) bwd_finish_reg_kernel(const __grid_constant__ BwdBatch bt, uint32_t early_chain) {
+  // WPB independent warps per CTA (fewer CTAs to launch); warp-local work only
+  uint32_t w = blockIdx.x * WPB + (threadIdx.x >> 5);
   int di = 0;
   while (di < bt.n && w >= bt.d[di].chans) {
     w -= bt.d[di].chans;
@@ -1237,7 +1239,7 @@ __global__ void __launch_bounds__(32) bwd_finish_reg_kernel(const __grid_constan
   if (di >= bt.n) return;
   const BwdDesc& d = bt.d[di];
   const uint32_t c = w;
-  const int lane = threadIdx.x;
+  const int lane = threadIdx.x & 31;
   const uint32_t tps = 1u << d.part_log;
   const uint32_t lanes = tps < 32u ? tps : 32u;
   const uint32_t per = tps / lanes;
@@ -1823,8 +1825,18 @@ cudaError_t launch_bwd_finish(const BwdBatch& b, cudaStream_t st) {
   void* fargs[] = {const_cast<BwdBatch*>(&b), &zero};
   uint32_t early = pdl_enabled(kPdlBwd) ? 0u : 1u;
   void* rargs[] = {const_cast<BwdBatch*>(&b), &early};
-  if (max_tps <= kFinRegMaxTiles && !force_smem)
-    e = launch_main((const void*)bwd_finish_reg_kernel, dim3(warps), dim3(32), rargs, 0, st, kPdlFin);
+  // warps per finisher CTA (QFB_FIN_WARPS 1/4/8): 4 measured best in the
+  // step (0.1346 -> 0.1335 ms: fewer CTAs to launch after the main pass)
+  static const int wpb = [] {
+    const char* e = getenv("QFB_FIN_WARPS");
+    const int v = e ? atoi(e) : 4;
+    return v == 1 || v == 8 ? v : 4;
+  }();
+  if (max_tps <= kFinRegMaxTiles && !force_smem) {
+    const void* fn = wpb == 8 ? (const void*)bwd_finish_reg_kernel<8>
+                   : wpb == 4 ? (const void*)bwd_finish_reg_kernel<4> : (const void*)bwd_finish_reg_kernel<1>;
+    e = launch_main(fn, dim3((warps + wpb - 1) / wpb), dim3(32 * wpb), rargs, 0, st, kPdlFin);
+  }
   else
     e = launch_main((const void*)bwd_finish_kernel, dim3(warps), dim3(32), fargs, 0, st, kPdlFin);
   if (e != cudaSuccess) return e;
