@@ -1682,6 +1682,12 @@ BwdFn kernel_ptr(int v, bool warp_part, uint32_t layout) {
     case kProbeNoCompute: return bwd_inst<T, kProbeNoCompute>();
     case kProbeNoLoads: return bwd_inst<T, kProbeNoLoads>();
     case kQM | kProbeNoCompute: if (warp_part) return bwd_inst<T, kQM | kProbeNoCompute>(); break;
+    case kWarpPart | kDDiv | kProbeNoCompute:  // the production structure's memory-only probe
+      if (warp_part) return bwd_inst<T, kWarpPart | kDDiv | kProbeNoCompute>();
+      break;
+    case kWarpPart | kDDiv | kProbeNoLoads:  // ... and its arithmetic-only probe
+      if (warp_part) return bwd_inst<T, kWarpPart | kDDiv | kProbeNoLoads>();
+      break;
     case kQM | kProbeNoLoads: if (warp_part) return bwd_inst<T, kQM | kProbeNoLoads>(); break;
     default: break;
   }
