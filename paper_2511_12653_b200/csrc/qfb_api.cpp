@@ -95,7 +95,12 @@ struct qfb_ctx {
   cudaStream_t s_in = nullptr, s_out = nullptr;
   struct PassSlot {
     std::vector<cudaEvent_t> ev;
-    std::vector<DevBuf> bufs;
+    // device buffers of the pass: one input arena (per point: x, then the
+    // consumers' upstreams) and one output arena (per point and consumer:
+    // y, then d_input), laid out in copy order, so a caller whose host
+    // buffers are laid out the same way gets its copies merged
+    DevBuf in_arena, out_arena;
+    std::vector<void*> ptr;  // per point: x, up[2], y[2], dx[2] (7 slots)
     DevBuf params;
     void* pinned = nullptr;  // params up, scale gradients and the status word down
     size_t pinned_bytes = 0;
@@ -590,8 +595,8 @@ qfb_status qfb_ctx_destroy(qfb_ctx* ctx) {
   for (auto& b : ctx->train_ws)
     if (b.p) cudaFree(b.p);
   for (auto& sl : ctx->slots) {
-    for (auto& b : sl.bufs)
-      if (b.p) cudaFree(b.p);
+    if (sl.in_arena.p) cudaFree(sl.in_arena.p);
+    if (sl.out_arena.p) cudaFree(sl.out_arena.p);
     if (sl.params.p) cudaFree(sl.params.p);
     if (sl.pinned) cudaFreeHost(sl.pinned);
     for (auto e : sl.ev) cudaEventDestroy(e);
@@ -1250,6 +1255,28 @@ qfb_status copy_batch(void** dst, void** src, size_t* sz, size_t n, cudaStream_t
     const char* e = getenv("QFB_BATCH_COPY");
     return !(e && e[0] == '0');
   }();
+  // merge runs contiguous on both sides into one copy: each DMA copy costs
+  // ~10-20 us of engine overhead when both directions run
+  // (tools/copy_probe.py); QFB_MERGE_COPY=0 disables (A/B)
+  static const bool merge = [] {
+    const char* e = getenv("QFB_MERGE_COPY");
+    return !(e && e[0] == '0');
+  }();
+  if (merge && n > 1) {
+    size_t m = 0;
+    for (size_t i = 0; i < n; ++i) {
+      if (m > 0 && static_cast<char*>(dst[m - 1]) + sz[m - 1] == dst[i] &&
+          static_cast<char*>(src[m - 1]) + sz[m - 1] == src[i]) {
+        sz[m - 1] += sz[i];
+        continue;
+      }
+      dst[m] = dst[i];
+      src[m] = src[i];
+      sz[m] = sz[i];
+      ++m;
+    }
+    n = m;
+  }
   if (n == 0) return QFB_OK;
   if (!batch || n == 1) {
     for (size_t i = 0; i < n; ++i) QFB_CUDA(cudaMemcpyAsync(dst[i], src[i], sz[i], cudaMemcpyDefault, st));
@@ -1355,20 +1382,39 @@ qfb_status qfb_quant_pass_host_submit(qfb_ctx* ctx, qfb_precision prec, const qf
   QFB_CUDA(cudaStreamWaitEvent(ctx->s_in, sl.ev[2 * n], 0));
   if (timing) QFB_CUDA(cudaEventRecord(te[0], ctx->s_in));
   QFB_CUDA(cudaMemcpyAsync(dF, hF, pbytes, cudaMemcpyHostToDevice, ctx->s_in));
-  // per point: buffers x, up[2], y[2], dx[2]
-  if (sl.bufs.size() < (size_t)n * 7) sl.bufs.resize((size_t)n * 7);
-  for (int32_t i = 0; i < n; ++i) {
-    const qfb_host_point& p = pts[i];
-    const size_t bytes = (size_t)(p.outer * p.channels * p.inner) * sizeof(float);
-    DevBuf* B = &sl.bufs[(size_t)i * 7];
-    if (qfb_status st = grow(ctx, B[0], bytes, false)) return st;
-    for (int k = 0; k < p.n_out; ++k) {
-      if (p.log_s[k])
-        if (qfb_status st = grow(ctx, B[1 + k], bytes, false)) return st;
-      if (p.y[k])
-        if (qfb_status st = grow(ctx, B[3 + k], bytes, false)) return st;
-      if (p.log_s[k] && p.dx[k])
-        if (qfb_status st = grow(ctx, B[5 + k], bytes, false)) return st;
+  // per point: x, up[2], y[2], dx[2] inside the two arenas (copy order;
+  // 16-byte aligned offsets)
+  sl.ptr.assign((size_t)n * 7, nullptr);
+  {
+    std::vector<size_t> off((size_t)n * 7, 0);
+    size_t in_b = 0, out_b = 0;
+    auto take = [](size_t& cur, size_t bytes) {
+      const size_t o = cur;
+      cur += (bytes + 15) & ~size_t(15);
+      return o;
+    };
+    for (int32_t i = 0; i < n; ++i) {
+      const qfb_host_point& p = pts[i];
+      const size_t bytes = (size_t)(p.outer * p.channels * p.inner) * sizeof(float);
+      off[(size_t)i * 7] = take(in_b, bytes);
+      for (int k = 0; k < p.n_out; ++k)
+        if (p.log_s[k]) off[(size_t)i * 7 + 1 + k] = take(in_b, bytes);
+      for (int k = 0; k < p.n_out; ++k) {
+        if (p.y[k]) off[(size_t)i * 7 + 3 + k] = take(out_b, bytes);
+        if (p.log_s[k] && p.dx[k]) off[(size_t)i * 7 + 5 + k] = take(out_b, bytes);
+      }
+    }
+    if (qfb_status st = grow(ctx, sl.in_arena, std::max<size_t>(in_b, 16), false)) return st;
+    if (qfb_status st = grow(ctx, sl.out_arena, std::max<size_t>(out_b, 16), false)) return st;
+    for (int32_t i = 0; i < n; ++i) {
+      const qfb_host_point& p = pts[i];
+      void** P = &sl.ptr[(size_t)i * 7];
+      P[0] = static_cast<char*>(sl.in_arena.p) + off[(size_t)i * 7];
+      for (int k = 0; k < p.n_out; ++k) {
+        if (p.log_s[k]) P[1 + k] = static_cast<char*>(sl.in_arena.p) + off[(size_t)i * 7 + 1 + k];
+        if (p.y[k]) P[3 + k] = static_cast<char*>(sl.out_arena.p) + off[(size_t)i * 7 + 3 + k];
+        if (p.log_s[k] && p.dx[k]) P[5 + k] = static_cast<char*>(sl.out_arena.p) + off[(size_t)i * 7 + 5 + k];
+      }
     }
   }
   // ---- pipeline: H2D (s_in) -> kernels (ctx->stream) -> D2H (s_out), in
@@ -1394,30 +1440,51 @@ qfb_status qfb_quant_pass_host_submit(qfb_ctx* ctx, qfb_precision prec, const qf
   ctx->cur_status = slot_status;
   std::vector<void*> cdst, csrc;
   std::vector<size_t> csz;
-  for (int32_t g0 = 0; g0 < n; g0 += group_pts) {
-    const int32_t g1 = std::min(n, g0 + group_pts);
+  // groups of points by input bytes (default 80 MB: 4 groups per DPVO
+  // frame): with host buffers laid out in copy order, each group's copies
+  // merge into one per direction. Measured (`profiles/r02_aq_*`): 141 ->
+  // 151 frames/s end to end, 98 % of the concurrent H2D + D2H ceiling; the
+  // per-point pipeline with merging alone: 142. QFB_PASS_GROUP_MB=0 restores
+  // per-point groups (QFB_PASS_GROUP points each).
+  static const double group_mb = [] {
+    const char* e = getenv("QFB_PASS_GROUP_MB");
+    return e ? atof(e) : 80.0;
+  }();
+  for (int32_t g0 = 0, g1 = 0; g0 < n; g0 = g1) {
+    g1 = std::min(n, g0 + group_pts);
+    if (group_mb > 0.0) {
+      double mb = 0.0;
+      g1 = g0;
+      while (g1 < n && (g1 == g0 || mb < group_mb)) {
+        const qfb_host_point& p = pts[g1];
+        int nin = 1;
+        for (int k = 0; k < p.n_out; ++k) nin += p.log_s[k] ? 1 : 0;
+        mb += (double)(p.outer * p.channels * p.inner) * sizeof(float) * nin / 1e6;
+        ++g1;
+      }
+    }
     cdst.clear();
     csrc.clear();
     csz.clear();
     for (int32_t i = g0; i < g1; ++i) {
       const qfb_host_point& p = pts[i];
       const size_t bytes = (size_t)(p.outer * p.channels * p.inner) * sizeof(float);
-      DevBuf* B = &sl.bufs[(size_t)i * 7];
-      cdst.push_back(B[0].p), csrc.push_back(const_cast<float*>(p.x)), csz.push_back(bytes);
+      void* const* B = &sl.ptr[(size_t)i * 7];
+      cdst.push_back(B[0]), csrc.push_back(const_cast<float*>(p.x)), csz.push_back(bytes);
       for (int k = 0; k < p.n_out; ++k)
         if (p.log_s[k])
-          cdst.push_back(B[1 + k].p), csrc.push_back(const_cast<float*>(p.up[k])), csz.push_back(bytes);
+          cdst.push_back(B[1 + k]), csrc.push_back(const_cast<float*>(p.up[k])), csz.push_back(bytes);
     }
     if (qfb_status st = copy_batch(cdst.data(), csrc.data(), csz.data(), cdst.size(), ctx->s_in)) return st;
     QFB_CUDA(cudaEventRecord(sl.ev[2 * g0], ctx->s_in));
     QFB_CUDA(cudaStreamWaitEvent(ctx->stream, sl.ev[2 * g0], 0));
     for (int32_t i = g0; i < g1; ++i) {
       const qfb_host_point& p = pts[i];
-      DevBuf* B = &sl.bufs[(size_t)i * 7];
+      void* const* B = &sl.ptr[(size_t)i * 7];
       // forward: one launch for all consumers of this tensor
       bool any_y = false;
       qfb_fq_desc fd{};
-      fd.x = B[0].p;
+      fd.x = B[0];
       fd.outer = p.outer;
       fd.channels = p.channels;
       fd.inner = p.inner;
@@ -1426,7 +1493,7 @@ qfb_status qfb_quant_pass_host_submit(qfb_ctx* ctx, qfb_precision prec, const qf
       int no = 0;
       for (int k = 0; k < p.n_out; ++k) {
         if (!p.y[k]) continue;
-        fd.y[no] = B[3 + k].p;
+        fd.y[no] = B[3 + k];
         fd.scale[no] = dF + foff[i] + k * p.channels;
         ++no;
         any_y = true;
@@ -1440,7 +1507,7 @@ qfb_status qfb_quant_pass_host_submit(qfb_ctx* ctx, qfb_precision prec, const qf
       for (int k = 0; k < p.n_out; ++k) {
         if (!p.log_s[k]) continue;
         const double* f = dD + doff[i] + (size_t)k * 3 * p.channels;
-        bd[nb] = qfb_bwd_desc{B[0].p, B[1 + k].p, p.dx[k] ? B[5 + k].p : nullptr, f, f + p.channels,
+        bd[nb] = qfb_bwd_desc{B[0], B[1 + k], p.dx[k] ? B[5 + k] : nullptr, f, f + p.channels,
                               const_cast<double*>(f + 2 * p.channels), p.outer, p.channels, p.inner, q, 0, 0};
         ++nb;
       }
@@ -1457,10 +1524,10 @@ qfb_status qfb_quant_pass_host_submit(qfb_ctx* ctx, qfb_precision prec, const qf
     for (int32_t i = g0; i < g1; ++i) {
       const qfb_host_point& p = pts[i];
       const size_t bytes = (size_t)(p.outer * p.channels * p.inner) * sizeof(float);
-      DevBuf* B = &sl.bufs[(size_t)i * 7];
+      void* const* B = &sl.ptr[(size_t)i * 7];
       for (int k = 0; k < p.n_out; ++k) {
-        if (p.y[k]) cdst.push_back(p.y[k]), csrc.push_back(B[3 + k].p), csz.push_back(bytes);
-        if (p.log_s[k] && p.dx[k]) cdst.push_back(p.dx[k]), csrc.push_back(B[5 + k].p), csz.push_back(bytes);
+        if (p.y[k]) cdst.push_back(p.y[k]), csrc.push_back(B[3 + k]), csz.push_back(bytes);
+        if (p.log_s[k] && p.dx[k]) cdst.push_back(p.dx[k]), csrc.push_back(B[5 + k]), csz.push_back(bytes);
       }
     }
     if (qfb_status st = copy_batch(cdst.data(), csrc.data(), csz.data(), cdst.size(), ctx->s_out)) return st;

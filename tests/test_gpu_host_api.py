@@ -157,3 +157,68 @@ def test_quant_pass_two_slots_in_flight(qfb, ref, cuda):
                 assert np.array_equal(bits32(dx.numpy()), bits32(wdx))
                 assert dls.tobytes() == wdls.tobytes()
     ctx.close()
+
+
+def _pass_table_arena(qfb, rng, shapes):
+    """The same table with every host buffer carved out of two pinned arenas
+    in the library's copy order (inputs: x, then the upstreams; outputs: y,
+    then d_input, per consumer): the pass merges contiguous copies."""
+    import torch
+    r16 = lambda n: (n + 3) & ~3  # noqa: E731
+    n_in = sum(r16(C * H * W) * (1 + n_out) for C, H, W, n_out in shapes)
+    n_out_t = sum(2 * r16(C * H * W) * n_out for C, H, W, n_out in shapes)
+    a_in = torch.empty(n_in, dtype=torch.float32).pin_memory()
+    a_out = torch.empty(n_out_t, dtype=torch.float32).pin_memory()
+    o_in, o_out = [0], [0]
+
+    def take(a, o, n):
+        t = a[o[0]:o[0] + n]
+        o[0] += r16(n)
+        return t
+
+    keep, pts, checks = [a_in, a_out], [], []
+    for C, H, W, n_out in shapes:
+        x = take(a_in, o_in, C * H * W)
+        x.copy_(torch.from_numpy(rng.normal(0, 1, C * H * W).astype(np.float32)))
+        p = qfb.CHostPoint()
+        p.x = x.data_ptr()
+        p.outer, p.channels, p.inner, p.n_out = 1, C, H * W, n_out
+        for k in range(n_out):
+            s = np.exp(rng.uniform(np.log(1e-3), np.log(0.1), C))
+            ls = np.log(np.expm1(s))
+            up = take(a_in, o_in, C * H * W)
+            up.copy_(torch.from_numpy(rng.normal(0, 1, C * H * W).astype(np.float32)))
+            y = take(a_out, o_out, C * H * W)
+            dx = take(a_out, o_out, C * H * W)
+            dls = np.zeros(C)
+            keep += [s, ls, dls]
+            p.s[k], p.y[k], p.log_s[k] = s.ctypes.data, y.data_ptr(), ls.ctypes.data
+            p.up[k], p.dx[k], p.d_log_s[k] = up.data_ptr(), dx.data_ptr(), dls.ctypes.data
+            checks.append((x.numpy(), s, ls, up.numpy(), y, dx, dls, C, H * W))
+        pts.append(p)
+    return (qfb.CHostPoint * len(pts))(*pts), len(pts), checks, keep
+
+
+def test_quant_pass_merged_copies(qfb, ref, cuda):
+    """Host buffers laid out contiguously in copy order (merged DMA copies,
+    both slots in flight): the same bits as the reference's per-point calls."""
+    rng = np.random.default_rng(23)
+    shapes = [(3, 48, 64, 2), (32, 24, 32, 1), (64, 12, 16, 2), (8, 40, 40, 1)]
+    t0 = _pass_table_arena(qfb, rng, shapes)
+    t1 = _pass_table_arena(qfb, rng, shapes)
+    ctx = qfb.Context(0)
+    cfg = qfb.QuantConfig().to_c()
+    L = qfb.lib()
+    for _ in range(2):
+        qfb.check(L.qfb_quant_pass_host_submit(ctx.handle, 0, t0[0], t0[1], ctypes.byref(cfg), 0))
+        qfb.check(L.qfb_quant_pass_host_submit(ctx.handle, 0, t1[0], t1[1], ctypes.byref(cfg), 1))
+        qfb.check(L.qfb_quant_pass_host_wait(ctx.handle, 0))
+        qfb.check(L.qfb_quant_pass_host_wait(ctx.handle, 1))
+        for checks in (t0[2], t1[2]):
+            for x, s, ls, up, y, dx, dls, C, HW in checks:
+                _, wy = ref.fake_quantize(x, [C, HW], s, per_channel=True)
+                assert np.array_equal(bits32(y.numpy()), bits32(wy))
+                _, wdx, wdls = ref.fq_backward(x, up, [C, HW], ls, per_channel=True)
+                assert np.array_equal(bits32(dx.numpy()), bits32(wdx))
+                assert dls.tobytes() == wdls.tobytes()
+    ctx.close()
