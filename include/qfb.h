@@ -413,10 +413,15 @@ qfb_status qfb_exec_model_layer(const qfb_exec_plan* plan, int64_t n_act, int64_
 /* backward_train (exec.hpp:435-451, frontend.hpp:236-258) for a set of    */
 /* quant points given as HOST float32 buffers. Each input tensor is copied */
 /* once even when it feeds two consumers; host->device copies, kernels and */
-/* device->host copies are pipelined per point over two copy engines and  */
-/* the compute stream. Pinned host buffers get full PCIe bandwidth;        */
-/* pageable ones work too (driver-staged). Synchronous. Results are        */
-/* identical to the per-point *_host calls.                                 */
+/* device->host copies are pipelined over two copy engines and the       */
+/* compute stream, in groups of points (~80 MB of input each). Pinned host */
+/* buffers get full PCIe bandwidth; pageable ones work too (driver-staged).*/
+/* Copies that are contiguous on both sides are merged into one DMA        */
+/* operation, so a caller whose buffers are carved from two pinned arenas  */
+/* in copy order — inputs: per point x, then each consumer's up; outputs:  */
+/* per point and consumer y, then dx (16-byte aligned offsets) — moves a   */
+/* frame in a handful of copies. Synchronous. Results are identical to the */
+/* per-point *_host calls.                                                  */
 /* ---------------------------------------------------------------------- */
 typedef struct qfb_host_point {
   const float* x;                              /* [outer, channels, inner] */
