@@ -245,6 +245,54 @@ __device__ __forceinline__ ChunkRef locate_chunk(const EwBatch& bt, uint32_t chu
   return r;
 }
 
+__constant__ int c_fwd_lean = 1;
+
+// ------------------------------------------------ lean plain forward ---
+// The plain multi-output forward's per-unit work for the common case (f32,
+// no int8 output, no half-grid output, the 3-stage ring), with everything
+// loop-invariant hoisted per chunk and the channel's scales recomputed only
+// when a thread's unit crosses into a new row (rows are thousands of units
+// long). A unit whose values or scales fall outside the shortcut's proven
+// domain (f32: the |x| < s * 2^100 screen; f16: inf/NaN, s < 2^-80, or q*s
+// beyond the binary16 range) takes fwd_unit_general, the full guarded code,
+// out of line. Same bits as the general loop (same functions, same order).
+template <typename T>
+struct UnitVals {
+  float v[Elem<T>::kPerVec];
+};
+
+template <typename T>
+__device__ __noinline__ bool fwd_unit_general(const EwDesc& d, uint32_t u, uint32_t ch, UnitVals<T> uv,
+                                              bool special, bool streaming) {
+  constexpr int V = Elem<T>::kPerVec;
+  bool nf = false;
+  for (int j = 0; j < d.n_out; ++j) {
+    const float sc = __ldg(d.s[j] + ch);
+    const bool fast = fast_div_ok(sc);
+    const float rc = fast ? __frcp_rn(sc) : 1.0f;
+    float o[V];
+    const bool finite = sizeof(T) == 2 ? (!special && fast && sc >= 0x1p-80f)
+                                       : (fast && screen_f32<V>(uv.v, __fmul_rn(sc, 0x1p100f)));
+    if (finite) {
+#pragma unroll
+      for (int i = 0; i < V; ++i) o[i] = fq_value_fast_finite(uv.v[i], sc, rc, d.q);
+    } else if (fast) {
+#pragma unroll
+      for (int i = 0; i < V; ++i) o[i] = fq_value_fast(uv.v[i], sc, rc, d.q);
+    } else {
+#pragma unroll
+      for (int i = 0; i < V; ++i) o[i] = fq_value(uv.v[i], sc, d.q);
+    }
+    const bool plain = sizeof(T) == 2 ? (!special && sc * d.q <= 65504.0f) : true;
+    const uint4 packed = plain ? Elem<T>::pack_in_range(o) : Elem<T>::pack(o, uv.v, false, nf);
+    st_v4(static_cast<uint4*>(d.y[j]) + u, packed, streaming);
+  }
+  return nf;
+}
+
+// QFB_FWD_LEAN=0: the general per-unit loop for every launch (A/B)
+__device__ __forceinline__ bool lean_enabled() { return c_fwd_lean != 0; }
+
 // kChain: quant -> act -> quant chains (a [+ b] staged, K outputs, optional
 // demotion / pre-activation output); 2 arrays per stage, 3 CTAs per SM.
 template <typename T, bool kChain, int kFwdStages>
@@ -324,6 +372,72 @@ __global__ void __launch_bounds__(kEwThreads, (kChain ? 6 : 10) / kFwdStages)
     const bool half_out = (QFB_FLAGS & kEwHalfGrid) != 0;
     const float qv = pin_f(d.q);
     const uint4* src = ring + s * kArrays * kEwChunk;
+    // (f32, 3-stage ring only: the one-frame launches; its registers cost the
+    // f16 and the 2/4-stage instances occupancy — measured, r02_as)
+    if constexpr (!kChain && kFwdStages == 3 && sizeof(T) == 4) {
+      if (lean_enabled() && (QFB_FLAGS & (kEwInt8Out | kEwHalfGrid)) == 0) {
+        // ---- lean loop: loop-invariant descriptor fields in registers
+        const int nout = (int)pin_u((uint32_t)d.n_out);
+        const uint32_t nch = pin_u(d.chans.d);
+        FastDivHost inner;
+        inner.d = pin_u(d.inner_u.d);
+        inner.m = pin_u(d.inner_u.m);
+        inner.s = pin_u(d.inner_u.s);
+        FastDivHost chans;
+        chans.d = nch;
+        chans.m = pin_u(d.chans.m);
+        chans.s = pin_u(d.chans.s);
+        uint4* const y0 = static_cast<uint4*>(d.y[0]);
+        uint4* const y1 = static_cast<uint4*>(d.y[1]);
+        const float* const s0p = d.s[0];
+        const float* const s1p = d.s[1];
+        uint32_t row_end = 0, ch = 0;
+        float s0 = 1.0f, s1 = 1.0f, r0 = 1.0f, r1 = 1.0f, t0 = 0.0f, t1 = 0.0f;
+        bool ok0 = false, ok1 = false;
+        for (uint32_t k = tid; k < r.units; k += kEwThreads) {
+          const uint32_t u = r.u0 + k;
+          if (u >= row_end) {  // first unit of the chunk or a new row
+            const uint32_t row = nch == 1 ? 0u : fdiv(u, inner);
+            ch = nch == 1 ? 0u : row - fdiv(row, chans) * nch;
+            row_end = nch == 1 ? 0xffffffffu : (row + 1u) * inner.d;
+            s0 = __ldg(s0p + ch);
+            const bool f0 = fast_div_ok(s0);
+            r0 = f0 ? __frcp_rn(s0) : 1.0f;
+            t0 = f0 ? __fmul_rn(s0, 0x1p100f) : 0.0f;
+            ok0 = f0 && (sizeof(T) == 4 || (s0 >= 0x1p-80f && s0 * qv <= 65504.0f));
+            if (nout > 1) {
+              s1 = __ldg(s1p + ch);
+              const bool f1 = fast_div_ok(s1);
+              r1 = f1 ? __frcp_rn(s1) : 1.0f;
+              t1 = f1 ? __fmul_rn(s1, 0x1p100f) : 0.0f;
+              ok1 = f1 && (sizeof(T) == 4 || (s1 >= 0x1p-80f && s1 * qv <= 65504.0f));
+            } else {
+              ok1 = true;
+              t1 = 0x1p127f;
+            }
+          }
+          UnitVals<T> uv;
+          const bool special = Elem<T>::unpack_flag(src[k], uv.v);
+          const bool fin = sizeof(T) == 2 ? (!special && ok0 && ok1)
+                                          : (ok0 && ok1 && screen_f32<V>(uv.v, t0) && screen_f32<V>(uv.v, t1));
+          if (fin) {
+            float o[V];
+#pragma unroll
+            for (int i = 0; i < V; ++i) o[i] = fq_value_fast_finite(uv.v[i], s0, r0, qv);
+            st_v4(y0 + u, Elem<T>::pack_in_range(o), streaming);
+            if (nout > 1) {
+#pragma unroll
+              for (int i = 0; i < V; ++i) o[i] = fq_value_fast_finite(uv.v[i], s1, r1, qv);
+              st_v4(y1 + u, Elem<T>::pack_in_range(o), streaming);
+            }
+          } else {
+            nf |= fwd_unit_general<T>(d, u, ch, uv, special, streaming);
+          }
+        }
+        __syncthreads();  // stage s free for the producer
+        continue;
+      }
+    }
     // Per-thread scale cache: units of a chunk mostly share a channel, so
     // the channel, its scales and reciprocals are recomputed only when the
     // row changes.
@@ -596,6 +710,13 @@ cudaError_t ew_tma_occupancy(int dtype, bool chain, int stages, int* blocks_per_
 
 cudaError_t launch_ew_tma(int dtype, bool chain, int stages, const EwBatch& b, uint32_t* status,
                           int grid, cudaStream_t st, bool small) {
+  static const cudaError_t lean_set = [] {
+    const char* e = getenv("QFB_FWD_LEAN");
+    if (!(e && e[0] == '0')) return cudaSuccess;
+    const int off = 0;
+    return cudaMemcpyToSymbol(c_fwd_lean, &off, sizeof off);
+  }();
+  if (lean_set != cudaSuccess) return lean_set;
   void* args[] = {const_cast<EwBatch*>(&b), &status};
   return launch_main(tma_fn(dtype, chain, stages), dim3(grid), dim3(kEwThreads), args,
                      ew_tma_smem(chain, stages), st, small ? (kPdlFwd | kPdlFwdSmall) : kPdlFwd);
