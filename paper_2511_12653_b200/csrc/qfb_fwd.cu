@@ -246,6 +246,9 @@ __device__ __forceinline__ ChunkRef locate_chunk(const EwBatch& bt, uint32_t chu
 }
 
 __constant__ int c_fwd_lean = 1;
+// f16 3-stage instance with the lean loop (registers capped at 64): measured
+// slower (one f16 frame 40.6 -> 44.9 us, r02_av), so f16 keeps the general loop
+constexpr bool kLeanHalf = false;
 
 // ------------------------------------------------ lean plain forward ---
 // The plain multi-output forward's per-unit work for the common case (f32,
@@ -296,7 +299,9 @@ __device__ __forceinline__ bool lean_enabled() { return c_fwd_lean != 0; }
 // kChain: quant -> act -> quant chains (a [+ b] staged, K outputs, optional
 // demotion / pre-activation output); 2 arrays per stage, 3 CTAs per SM.
 template <typename T, bool kChain, int kFwdStages>
-__global__ void __launch_bounds__(kEwThreads, (kChain ? 6 : 10) / kFwdStages)
+__global__ void __launch_bounds__(kEwThreads, (!kChain && kFwdStages == 3 && sizeof(T) == 2 && kLeanHalf)
+                                                   ? 4
+                                                   : (kChain ? 6 : 10) / kFwdStages)
     ew_tma_kernel(const __grid_constant__ EwBatch bt, uint32_t* __restrict__ status) {
   constexpr int V = Elem<T>::kPerVec;
   constexpr int kArrays = kChain ? 2 : 1;  // a [, b] per stage
@@ -374,7 +379,7 @@ __global__ void __launch_bounds__(kEwThreads, (kChain ? 6 : 10) / kFwdStages)
     const uint4* src = ring + s * kArrays * kEwChunk;
     // (f32, 3-stage ring only: the one-frame launches; its registers cost the
     // f16 and the 2/4-stage instances occupancy — measured, r02_as)
-    if constexpr (!kChain && kFwdStages == 3 && sizeof(T) == 4) {
+    if constexpr (!kChain && kFwdStages == 3 && (sizeof(T) == 4 || kLeanHalf)) {
       if (lean_enabled() && (QFB_FLAGS & (kEwInt8Out | kEwHalfGrid)) == 0) {
         // ---- lean loop: loop-invariant descriptor fields in registers
         const int nout = (int)pin_u((uint32_t)d.n_out);
