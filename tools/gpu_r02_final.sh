@@ -1,6 +1,6 @@
 # round-2 final record run (lean outputs). Outputs -> gpurun_out/
 set -x
-T=r02f
+T=r02g
 O=gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $O/${T}_gpu.txt
 timeout 1800 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/${T}_pytest_gpu.log 2>&1; echo rc=$? >> $O/${T}_pytest_gpu.log
