@@ -174,6 +174,50 @@ Tensor run_quant_conv(ExecutionContext& ectx, const ConvLayer& layer, int layer_
   return out;
 }
 
+}  // namespace qf
+
+// The qfb side of the device-view hooks: x, y, upstream, d_input and the
+// scale vectors in device memory, the async qfb::DeviceView overloads on
+// the context stream, one sync, results copied back.
+qf::Tensor dropin_dv_fq(const qf::Tensor& x, std::span<const double> s, const qf::QuantConfig& cfg) {
+  const int64_t C = x.shape[0], n = x.numel();
+  std::vector<float> s32((size_t)C);
+  qfb::check(qfb_cast_scales_f32(s.data(), C, s32.data()));
+  DevBuf dx((size_t)n), dy((size_t)n), ds((size_t)C);
+  cuda_check(cudaMemcpy(dx.p, x.data.data(), n * 4, cudaMemcpyHostToDevice), "H2D x");
+  cuda_check(cudaMemcpy(ds.p, s32.data(), C * 4, cudaMemcpyHostToDevice), "H2D s");
+  qfb::fake_quantize(ctx(), qfb::DeviceView{dx.p, QFB_F32, 1, C, n / C}, dy.p, ds.p, cfg.q_max());
+  qfb::check(qfb_ctx_sync(ctx().get()));
+  qf::Tensor y = x;
+  cuda_check(cudaMemcpy(y.data.data(), dy.p, n * 4, cudaMemcpyDeviceToHost), "D2H y");
+  return y;
+}
+
+qf::FakeQuantGrad dropin_dv_bwd(const qf::Tensor& x, std::span<const double> log_s, const qf::QuantConfig& cfg,
+                                const qf::Tensor& up) {
+  const int64_t C = x.shape[0], n = x.numel();
+  const qfb_quant_config c = qfb::to_c(cfg);
+  std::vector<double> fac((size_t)(2 * C));
+  qfb::check(qfb_scale_grad_factors(log_s.data(), C, &c, QFB_PREC_FULL, fac.data(), fac.data() + C));
+  DevBuf dx((size_t)n), du((size_t)n), dd((size_t)n), df((size_t)(4 * C)), dl((size_t)(2 * C));
+  cuda_check(cudaMemcpy(dx.p, x.data.data(), n * 4, cudaMemcpyHostToDevice), "H2D x");
+  cuda_check(cudaMemcpy(du.p, up.data.data(), n * 4, cudaMemcpyHostToDevice), "H2D up");
+  double* f64 = reinterpret_cast<double*>(df.p);
+  double* dls = reinterpret_cast<double*>(dl.p);
+  cuda_check(cudaMemcpy(f64, fac.data(), 2 * C * 8, cudaMemcpyHostToDevice), "H2D factors");
+  qfb::fake_quantize_backward(ctx(), qfb::DeviceView{dx.p, QFB_F32, 1, C, n / C}, du.p, dd.p, f64, f64 + C, dls,
+                              false, cfg.q_max());
+  qfb::check(qfb_ctx_sync(ctx().get()));
+  qf::FakeQuantGrad g;
+  g.d_input = qf::Tensor::zeros(x.shape);
+  g.d_log_scale.resize((size_t)C);
+  cuda_check(cudaMemcpy(g.d_input.data.data(), dd.p, n * 4, cudaMemcpyDeviceToHost), "D2H dx");
+  cuda_check(cudaMemcpy(g.d_log_scale.data(), dls, C * 8, cudaMemcpyDeviceToHost), "D2H d_log_s");
+  return g;
+}
+
+namespace qf {
+
 // distill.hpp:125-141 on the GPU (qfb_distill_loss_host, bit-identical).
 DistillLoss distill_loss(const Tensor& f_s, const Tensor& f_t, const Tensor& i_s, const Tensor& i_t,
                          double lambda_cos) {

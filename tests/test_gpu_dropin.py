@@ -31,6 +31,9 @@ def test_reference_call_sites_with_qfb_are_bit_identical():
     res = json.loads(line)
     assert r.returncode == 0 and res["ok"], res
     assert res["mismatched"] == 0 and res["blobs"] > 200, res
+    # include/qfb.hpp's DeviceView overloads (device buffers, async on the
+    # context stream) reproduce the reference's per-channel calls bitwise
+    assert res["device_view_blobs"] == 12, res
     calls = res["calls"]
     # every substituted entry point was reached through the reference's code
     assert calls["fake_quantize"] > 0 and calls["fake_quantize_backward"] > 0
