@@ -246,9 +246,6 @@ __device__ __forceinline__ ChunkRef locate_chunk(const EwBatch& bt, uint32_t chu
 }
 
 __constant__ int c_fwd_lean = 1;
-// f16 3-stage instance with the lean loop (registers capped at 64): measured
-// slower (one f16 frame 40.6 -> 44.9 us, r02_av), so f16 keeps the general loop
-constexpr bool kLeanHalf = false;
 
 // ------------------------------------------------ lean plain forward ---
 // The plain multi-output forward's per-unit work for the common case (f32,
@@ -265,11 +262,12 @@ struct UnitVals {
 };
 
 template <typename T>
-__device__ __noinline__ bool fwd_unit_general(const EwDesc& d, uint32_t u, uint32_t ch, UnitVals<T> uv,
-                                              bool special, bool streaming) {
+__device__ __forceinline__ bool fwd_unit_general_body(const EwDesc& d, uint32_t u, uint32_t ch,
+                                                      const UnitVals<T>& uv, bool special, bool streaming,
+                                                      int jb, int je) {
   constexpr int V = Elem<T>::kPerVec;
   bool nf = false;
-  for (int j = 0; j < d.n_out; ++j) {
+  for (int j = jb; j < je; ++j) {
     const float sc = __ldg(d.s[j] + ch);
     const bool fast = fast_div_ok(sc);
     const float rc = fast ? __frcp_rn(sc) : 1.0f;
@@ -292,6 +290,13 @@ __device__ __noinline__ bool fwd_unit_general(const EwDesc& d, uint32_t u, uint3
   }
   return nf;
 }
+// out of line for the f32 lean loop; the binary16 lean loop inlines the
+// body (a call there raises the kernel's registers from 56 to 76)
+template <typename T>
+__device__ __noinline__ bool fwd_unit_general(const EwDesc& d, uint32_t u, uint32_t ch, UnitVals<T> uv,
+                                              bool special, bool streaming, int jb, int je) {
+  return fwd_unit_general_body<T>(d, u, ch, uv, special, streaming, jb, je);
+}
 
 // QFB_FWD_LEAN=0: the general per-unit loop for every launch (A/B)
 __device__ __forceinline__ bool lean_enabled() { return c_fwd_lean != 0; }
@@ -299,9 +304,7 @@ __device__ __forceinline__ bool lean_enabled() { return c_fwd_lean != 0; }
 // kChain: quant -> act -> quant chains (a [+ b] staged, K outputs, optional
 // demotion / pre-activation output); 2 arrays per stage, 3 CTAs per SM.
 template <typename T, bool kChain, int kFwdStages>
-__global__ void __launch_bounds__(kEwThreads, (!kChain && kFwdStages == 3 && sizeof(T) == 2 && kLeanHalf)
-                                                   ? 4
-                                                   : (kChain ? 6 : 10) / kFwdStages)
+__global__ void __launch_bounds__(kEwThreads, (kChain ? 6 : 10) / kFwdStages)
     ew_tma_kernel(const __grid_constant__ EwBatch bt, uint32_t* __restrict__ status) {
   constexpr int V = Elem<T>::kPerVec;
   constexpr int kArrays = kChain ? 2 : 1;  // a [, b] per stage
@@ -379,7 +382,56 @@ __global__ void __launch_bounds__(kEwThreads, (!kChain && kFwdStages == 3 && siz
     const uint4* src = ring + s * kArrays * kEwChunk;
     // (f32, 3-stage ring only: the one-frame launches; its registers cost the
     // f16 and the 2/4-stage instances occupancy — measured, r02_as)
-    if constexpr (!kChain && kFwdStages == 3 && (sizeof(T) == 4 || kLeanHalf)) {
+    if constexpr (!kChain && sizeof(T) == 2) {
+      if (lean_enabled() && (QFB_FLAGS & (kEwInt8Out | kEwHalfGrid)) == 0) {
+        // ---- lean binary16 loop, one output at a time (the outputs of a
+        // two-consumer point re-read the staged unit: a single output's
+        // state keeps the loop inside the general loop's registers). A unit
+        // with inf/NaN, or a row whose scale is outside the shortcut's
+        // domain (s < 2^-80, q*s beyond the binary16 range), takes
+        // fwd_unit_general for that output.
+        FastDivHost inner;
+        inner.d = pin_inner.d;
+        inner.m = pin_inner.m;
+        inner.s = pin_inner.s;
+        FastDivHost chans;
+        chans.d = pin_nch;
+        chans.m = pin_u(d.chans.m);
+        chans.s = pin_u(d.chans.s);
+        for (int j = 0; j < (int)pin_nout; ++j) {
+          uint4* const y = static_cast<uint4*>(d.y[j]);
+          const float* const sp = d.s[j];
+          uint32_t row_end = 0, ch = 0;
+          float sj = 1.0f, rj = 1.0f;
+          bool ok = false;
+#pragma unroll 1
+          for (uint32_t k = tid; k < r.units; k += kEwThreads) {
+            const uint32_t u = r.u0 + k;
+            if (u >= row_end) {  // first unit of the chunk or a new row
+              const uint32_t row = pin_nch == 1 ? 0u : fdiv(u, inner);
+              ch = pin_nch == 1 ? 0u : row - fdiv(row, chans) * pin_nch;
+              row_end = pin_nch == 1 ? 0xffffffffu : (row + 1u) * inner.d;
+              sj = __ldg(sp + ch);
+              ok = fast_div_ok(sj) && sj >= 0x1p-80f && sj * qv <= 65504.0f;
+              rj = ok ? __frcp_rn(sj) : 1.0f;
+            }
+            UnitVals<T> uv;
+            const bool special = Elem<T>::unpack_flag(src[k], uv.v);
+            if (ok && !special) {
+              float o[V];
+#pragma unroll
+              for (int i = 0; i < V; ++i) o[i] = fq_value_fast_finite(uv.v[i], sj, rj, qv);
+              st_v4(y + u, Elem<T>::pack_in_range(o), streaming);
+            } else {
+              nf |= fwd_unit_general_body<T>(d, u, ch, uv, special, streaming, j, j + 1);
+            }
+          }
+        }
+        __syncthreads();  // stage s free for the producer
+        continue;
+      }
+    }
+    if constexpr (!kChain && kFwdStages == 3 && sizeof(T) == 4) {
       if (lean_enabled() && (QFB_FLAGS & (kEwInt8Out | kEwHalfGrid)) == 0) {
         // ---- lean loop: loop-invariant descriptor fields in registers
         const int nout = (int)pin_u((uint32_t)d.n_out);
@@ -436,7 +488,7 @@ __global__ void __launch_bounds__(kEwThreads, (!kChain && kFwdStages == 3 && siz
               st_v4(y1 + u, Elem<T>::pack_in_range(o), streaming);
             }
           } else {
-            nf |= fwd_unit_general<T>(d, u, ch, uv, special, streaming);
+            nf |= fwd_unit_general<T>(d, u, ch, uv, special, streaming, 0, nout);
           }
         }
         __syncthreads();  // stage s free for the producer
