@@ -42,10 +42,9 @@
  * coefficients, Horner with FMAs); beyond |x| > 5, Phi is 1 or 0 exactly.
  * Within 2.1e-6 of the erf GELU. NaN passes through; +inf -> +inf,
  * -inf -> -0. FMAs, one multiply and one add: identical bits on both sides. */
-QFB_HD float qfb_p_gelu(float x) {
-  if (!(x == x)) return x;
-  if (x > 5.0f) return x;
-  if (x < -5.0f) return -0.0f;
+/* x * Phi(x) from the polynomial, for -5 <= x <= 5 (qfb_p_gelu's middle
+ * branch; the device's branch-free form selects around it). */
+QFB_HD float qfb_p_gelu_core(float x) {
   const float t = x < 0.0f ? -x : x;
   const float u = QFB_P_FMA(t, 0.4f, -1.0f);
   float h = 0.010865055f;
@@ -63,6 +62,13 @@ QFB_HD float qfb_p_gelu(float x) {
   h = QFB_P_FMA(h, u, 0.49378976f);
   const float phi = QFB_P_ADD(0.5f, x < 0.0f ? -h : h);
   return QFB_P_MUL(x, phi);
+}
+
+QFB_HD float qfb_p_gelu(float x) {
+  if (!(x == x)) return x;
+  if (x > 5.0f) return x;
+  if (x < -5.0f) return -0.0f;
+  return qfb_p_gelu_core(x);
 }
 
 #endif /* QFB_PORTABLE_H_ */

@@ -245,7 +245,14 @@ __device__ __forceinline__ ChunkRef locate_chunk(const EwBatch& bt, uint32_t chu
   return r;
 }
 
-__constant__ int c_fwd_lean = 1;
+// lean loops enabled (QFB_FWD_LEAN=<mask>, A/B): 1 plain forward, 2 f32
+// chains with ReLU / no activation, 4 chains with GELU, 8 binary16 chains
+// with ReLU / no activation. Default: all but 2 — the f32 ReLU window is
+// memory-bound at 0.95 of HBM on the general loop and the lean loop's
+// screens cost it 3-4 % (r02bc); GELU gains 0.73 -> 0.90 (f32), binary16
+// ReLU 0.69 -> 0.81 and GELU 0.42 -> 0.54.
+constexpr int kLeanPlain = 1, kLeanChain = 2, kLeanChainGelu = 4, kLeanChainHalf = 8;
+__constant__ int c_fwd_lean = kLeanPlain | kLeanChainGelu | kLeanChainHalf;
 
 // ------------------------------------------------ lean plain forward ---
 // The plain multi-output forward's per-unit work for the common case (f32,
@@ -298,8 +305,76 @@ __device__ __noinline__ bool fwd_unit_general(const EwDesc& d, uint32_t u, uint3
   return fwd_unit_general_body<T>(d, u, ch, uv, special, streaming, jb, je);
 }
 
-// QFB_FWD_LEAN=0: the general per-unit loop for every launch (A/B)
-__device__ __forceinline__ bool lean_enabled() { return c_fwd_lean != 0; }
+// ------------------------------------------------ lean chain loop ---
+// Any inf/NaN among a unit's staged values (exponent all ones; the carry
+// trick reaches the sign bit of each lane exactly then).
+template <typename T>
+__device__ __forceinline__ bool nonfinite_unit(const uint4& r) {
+  constexpr uint32_t kE = sizeof(T) == 2 ? 0x7c007c00u : 0x7f800000u;
+  constexpr uint32_t kOne = sizeof(T) == 2 ? 0x04000400u : 0x00800000u;
+  constexpr uint32_t kTop = sizeof(T) == 2 ? 0x80008000u : 0x80000000u;
+  return ((((r.x & kE) + kOne) | ((r.y & kE) + kOne) | ((r.z & kE) + kOne) | ((r.w & kE) + kOne)) & kTop) != 0;
+}
+
+// qfb_p_gelu for a non-NaN x without branches: the polynomial for every
+// element, then the two saturated ranges selected around it (identical
+// bits: the middle range runs the same qfb_p_gelu_core).
+__device__ __forceinline__ float gelu_nonnan(float x) {
+  const float g = qfb_p_gelu_core(x);
+  return x > 5.0f ? x : (x < -5.0f ? -0.0f : g);
+}
+
+// One chain unit through the general code (x86 NaN propagation, guarded
+// quotient, checked binary16 pack): units of the lean chain loop with
+// inf/NaN inputs or values outside the screened domain.
+template <typename T>
+__device__ __noinline__ bool chain_unit_general(const EwDesc& d, uint32_t u, uint32_t ch, uint4 ra, uint4 rb,
+                                                bool streaming) {
+  constexpr int V = Elem<T>::kPerVec;
+  bool nf = false;
+  float v[V];
+  bool special = Elem<T>::unpack_flag(ra, v);
+  if (d.b != nullptr) {
+    float w[V];
+    special |= Elem<T>::unpack_flag(rb, w);
+    if (sizeof(T) == 2 && !special) {
+#pragma unroll
+      for (int i = 0; i < V; ++i) v[i] = __fadd_rn(v[i], w[i]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < V; ++i) v[i] = x86_add(v[i], w[i]);  // tensor.hpp:126-134
+    }
+  }
+  if (d.act != 0) {
+#pragma unroll
+    for (int i = 0; i < V; ++i) v[i] = apply_act(v[i], d.act);
+  }
+  if (d.flags & kEwDemoteIn) {  // binary16 storage only (the lean loop's domain)
+    if (!special) {
+#pragma unroll
+      for (int i = 0; i < V; i += 2) {
+        const float2 f = __half22float2(__floats2half2_rn(fminf(fmaxf(v[i], -65504.0f), 65504.0f),
+                                                          fminf(fmaxf(v[i + 1], -65504.0f), 65504.0f)));
+        v[i] = f.x;
+        v[i + 1] = f.y;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < V; ++i) v[i] = half_grid(v[i], v[i], nf);  // tensor.hpp:159-170
+    }
+  }
+  for (int j = 0; j < d.n_out; ++j) {
+    const float sc = __ldg(d.s[j] + ch);
+    float o[V];
+    fq_unit<V>(v, sc, d.q, o);
+    const bool plain = sizeof(T) == 2 ? (!special && sc * d.q <= 65504.0f) : true;
+    const uint4 packed = plain ? Elem<T>::pack_in_range(o) : Elem<T>::pack(o, v, false, nf);
+    st_v4(static_cast<uint4*>(d.y[j]) + u, packed, streaming);
+  }
+  return nf;
+}
+
+__device__ __forceinline__ bool lean_enabled(int bit) { return (c_fwd_lean & bit) != 0; }
 
 // kChain: quant -> act -> quant chains (a [+ b] staged, K outputs, optional
 // demotion / pre-activation output); 2 arrays per stage, 3 CTAs per SM.
@@ -382,8 +457,113 @@ __global__ void __launch_bounds__(kEwThreads, (kChain ? 6 : 10) / kFwdStages)
     const uint4* src = ring + s * kArrays * kEwChunk;
     // (f32, 3-stage ring only: the one-frame launches; its registers cost the
     // f16 and the 2/4-stage instances occupancy — measured, r02_as)
+    if constexpr (kChain) {
+      if (lean_enabled(d.act == 2 ? kLeanChainGelu : sizeof(T) == 2 ? kLeanChainHalf : kLeanChain) &&
+          (QFB_FLAGS & (kEwInt8Out | kEwHalfGrid | (sizeof(T) == 2 ? 0u : kEwDemoteIn))) == 0 &&
+          d.preact == nullptr) {
+        // ---- lean chain loop (no pre-activation output; demotion on
+        // binary16 storage only): descriptor fields hoisted, scales
+        // reloaded on row crossings, a unit of finite inputs takes the plain
+        // add, a branch-free activation, the packed clamped demotion and the
+        // screened quotient; anything else goes through chain_unit_general
+        // (same functions as the general loop).
+        const bool demote = (QFB_FLAGS & kEwDemoteIn) != 0;
+        const int nout = (int)pin_u((uint32_t)d.n_out);
+        const int act = (int)pin_u((uint32_t)d.act);
+        const bool has_b = d.b != nullptr;
+        const uint32_t nch = pin_u(d.chans.d);
+        FastDivHost inner;
+        inner.d = pin_u(d.inner_u.d);
+        inner.m = pin_u(d.inner_u.m);
+        inner.s = pin_u(d.inner_u.s);
+        FastDivHost chans;
+        chans.d = nch;
+        chans.m = pin_u(d.chans.m);
+        chans.s = pin_u(d.chans.s);
+        uint4* const y0 = static_cast<uint4*>(d.y[0]);
+        uint4* const y1 = static_cast<uint4*>(d.y[1]);
+        const float* const s0p = d.s[0];
+        const float* const s1p = d.s[1];
+        uint32_t row_end = 0, ch = 0;
+        float s0 = 1.0f, s1 = 1.0f, r0 = 1.0f, r1 = 1.0f, t0 = 0.0f, t1 = 0.0f;
+        bool ok0 = false, ok1 = false;
+        for (uint32_t k = tid; k < r.units; k += kEwThreads) {
+          const uint32_t u = r.u0 + k;
+          if (u >= row_end) {
+            const uint32_t row = nch == 1 ? 0u : fdiv(u, inner);
+            ch = nch == 1 ? 0u : row - fdiv(row, chans) * nch;
+            row_end = nch == 1 ? 0xffffffffu : (row + 1u) * inner.d;
+            s0 = __ldg(s0p + ch);
+            const bool f0 = fast_div_ok(s0);
+            r0 = f0 ? __frcp_rn(s0) : 1.0f;
+            t0 = f0 ? __fmul_rn(s0, 0x1p100f) : 0.0f;
+            ok0 = f0 && (sizeof(T) == 4 || (s0 >= 0x1p-80f && s0 * qv <= 65504.0f));
+            if (nout > 1) {
+              s1 = __ldg(s1p + ch);
+              const bool f1 = fast_div_ok(s1);
+              r1 = f1 ? __frcp_rn(s1) : 1.0f;
+              t1 = f1 ? __fmul_rn(s1, 0x1p100f) : 0.0f;
+              ok1 = f1 && (sizeof(T) == 4 || (s1 >= 0x1p-80f && s1 * qv <= 65504.0f));
+            } else {
+              ok1 = true;
+              t1 = 0x1p127f;
+            }
+          }
+          const uint4 ra = src[k];
+          const uint4 rb = has_b ? src[kEwChunk + k] : make_uint4(0u, 0u, 0u, 0u);
+          bool done = false;
+          if (!nonfinite_unit<T>(ra) && !(has_b && nonfinite_unit<T>(rb))) {
+            float v[V];
+            Elem<T>::unpack(ra, v);
+            if (has_b) {
+              float w[V];
+              Elem<T>::unpack(rb, w);
+#pragma unroll
+              for (int i = 0; i < V; ++i) v[i] = __fadd_rn(v[i], w[i]);  // finite operands: no NaN to propagate
+            }
+            if (act == 1) {
+#pragma unroll
+              for (int i = 0; i < V; ++i) v[i] = v[i] > 0.0f ? v[i] : 0.0f;
+            } else if (act == 2) {
+#pragma unroll
+              for (int i = 0; i < V; ++i) v[i] = gelu_nonnan(v[i]);
+            }
+            if (sizeof(T) == 2 && demote) {
+              // finite values: round_to_half is the clamped RNE conversion
+              // (half.hpp:17-39), two elements per conversion (general loop)
+#pragma unroll
+              for (int i = 0; i < V; i += 2) {
+                const float2 f = __half22float2(__floats2half2_rn(fminf(fmaxf(v[i], -65504.0f), 65504.0f),
+                                                                  fminf(fmaxf(v[i + 1], -65504.0f), 65504.0f)));
+                v[i] = f.x;
+                v[i + 1] = f.y;
+              }
+            }
+            // binary16: the sum of finite halves and its activation stay
+            // finite (|a + b| <= 131008), as in the general loop's screen
+            const bool fin = sizeof(T) == 2 ? (ok0 && ok1)
+                                            : (ok0 && ok1 && screen_f32<V>(v, t0) && screen_f32<V>(v, t1));
+            if (fin) {
+              float o[V];
+#pragma unroll
+              for (int i = 0; i < V; ++i) o[i] = fq_value_fast_finite(v[i], s0, r0, qv);
+              st_v4(y0 + u, Elem<T>::pack_in_range(o), streaming);
+              if (nout > 1) {
+#pragma unroll
+                for (int i = 0; i < V; ++i) o[i] = fq_value_fast_finite(v[i], s1, r1, qv);
+                st_v4(y1 + u, Elem<T>::pack_in_range(o), streaming);
+              }
+              done = true;
+            }
+          }
+          if (!done) nf |= chain_unit_general<T>(d, u, ch, ra, rb, streaming);
+        }
+        __syncthreads();  // stage s free for the producer
+        continue;
+      }
+    }
     if constexpr (!kChain && sizeof(T) == 2) {
-      if (lean_enabled() && (QFB_FLAGS & (kEwInt8Out | kEwHalfGrid)) == 0) {
+      if (lean_enabled(kLeanPlain) && (QFB_FLAGS & (kEwInt8Out | kEwHalfGrid)) == 0) {
         // ---- lean binary16 loop, one output at a time (the outputs of a
         // two-consumer point re-read the staged unit: a single output's
         // state keeps the loop inside the general loop's registers). A unit
@@ -432,7 +612,7 @@ __global__ void __launch_bounds__(kEwThreads, (kChain ? 6 : 10) / kFwdStages)
       }
     }
     if constexpr (!kChain && kFwdStages == 3 && sizeof(T) == 4) {
-      if (lean_enabled() && (QFB_FLAGS & (kEwInt8Out | kEwHalfGrid)) == 0) {
+      if (lean_enabled(kLeanPlain) && (QFB_FLAGS & (kEwInt8Out | kEwHalfGrid)) == 0) {
         // ---- lean loop: loop-invariant descriptor fields in registers
         const int nout = (int)pin_u((uint32_t)d.n_out);
         const uint32_t nch = pin_u(d.chans.d);
@@ -769,9 +949,9 @@ cudaError_t launch_ew_tma(int dtype, bool chain, int stages, const EwBatch& b, u
                           int grid, cudaStream_t st, bool small) {
   static const cudaError_t lean_set = [] {
     const char* e = getenv("QFB_FWD_LEAN");
-    if (!(e && e[0] == '0')) return cudaSuccess;
-    const int off = 0;
-    return cudaMemcpyToSymbol(c_fwd_lean, &off, sizeof off);
+    if (!(e && e[0])) return cudaSuccess;
+    const int mask = (int)strtol(e, nullptr, 0) & (kLeanPlain | kLeanChain | kLeanChainGelu | kLeanChainHalf);
+    return cudaMemcpyToSymbol(c_fwd_lean, &mask, sizeof mask);
   }();
   if (lean_set != cudaSuccess) return lean_set;
   void* args[] = {const_cast<EwBatch*>(&b), &status};

@@ -231,6 +231,69 @@ def test_chain(qfb, orc, cuda, act, half):
     assert np.array_equal(bits32(host(outs[0]).ravel()), bits32(ys[0]))
 
 
+@pytest.mark.parametrize("act", [0, 1, 2])
+@pytest.mark.parametrize("dtype", ["f32", "f16"])
+def test_chain_lean_paths(qfb, orc, cuda, act, dtype):
+    """The lean chain loop (no demotion, no pre-activation output: the
+    config-3 shape) and its exits to the general code: inf/NaN in a or b,
+    a + b overflowing float32, |v| beyond the f32 screen, scales outside the
+    shortcut's range (1e-30) and large ones (30), GELU at and around +-5,
+    signed zeros; two per-channel outputs over rows of 280 / 140 units so
+    chunks cross rows."""
+    import torch
+    rng = np.random.default_rng(50 + act)
+    C, H, W = 6, 20, 56
+    f16 = dtype == "f16"
+    a = rng.normal(0, 3, (C, H, W)).astype(np.float32)
+    b = rng.normal(0, 3, (C, H, W)).astype(np.float32)
+    a[0, 0, :10] = [5.0, -5.0, np.nextafter(np.float32(5), np.float32(6)), np.nextafter(np.float32(-5), np.float32(-6)),
+                    np.nextafter(np.float32(5), np.float32(0)), np.nextafter(np.float32(-5), np.float32(0)),
+                    0.0, -0.0, 40.0, -40.0]
+    b[0, 0, :10] = 0.0
+    a[1, 0, :4] = [np.inf, -np.inf, np.nan, 0.0]
+    b[2, 0, :3] = [np.nan, np.inf, -0.0]
+    if f16:
+        # binary16 storage demotes act(a + b): an inf/NaN operand is the
+        # reference's non-finite error (checked below), so finite values here
+        a[1, 0, :3] = [65504.0, -65504.0, 0.0]
+        b[2, 0, :2] = [-65504.0, 65504.0]
+        a[3, 0, :2] = [60000.0, -60000.0]
+        b[3, 0, :2] = [60000.0, -60000.0]
+        a, b = a.astype(np.float16).astype(np.float32), b.astype(np.float16).astype(np.float32)
+    else:
+        a[3, 0, :2] = [3e38, -3e38]
+        b[3, 0, :2] = [3e38, -3e38]
+        a[3, 1, :2] = [1e30, -1e30]
+    s0 = np.exp(rng.uniform(-6, -2, C))
+    s1 = np.exp(rng.uniform(-6, -2, C))
+    s1[4] = 1e-30
+    s1[5] = 30.0
+    st, want, _ = orc.fq_chain(a, b, [s0, s1], 1, C, H * W, act=act, half=int(f16))
+    dt = torch.float16 if f16 else torch.float32
+    assert st == 0
+    outs, _ = qfb.fq_chain(to_dev(a, cuda, dt), to_dev(b, cuda, dt), scales=(s0.tolist(), s1.tolist()), act=act,
+                           half=False, channel_axis=0)
+    for y, w in zip(outs, want):
+        if f16:  # NaN payloads do not survive torch's half -> float widening
+            same_bits_or_both_nan(host(y).ravel(), w)
+        else:
+            assert np.array_equal(bits32(host(y).ravel()), bits32(w))
+    # and with one output, no b (the lean loop's other shape)
+    st, want, _ = orc.fq_chain(a, None, [s1], 1, C, H * W, act=act, half=int(f16))
+    outs, _ = qfb.fq_chain(to_dev(a, cuda, dt), None, scales=(s1.tolist(),), act=act, half=False, channel_axis=0)
+    if f16:
+        same_bits_or_both_nan(host(outs[0]).ravel(), want[0])
+        # an infinity in a: the oracle and the device both report non-finite
+        a[1, 0, 2] = np.inf
+        st, _, _ = orc.fq_chain(a, b, [s0], 1, C, H * W, act=act, half=1)
+        assert st != 0
+        with pytest.raises(qfb.NonFiniteError):
+            qfb.fq_chain(to_dev(a, cuda, dt), to_dev(b, cuda, dt), scales=(s0.tolist(),), act=act, half=False,
+                         channel_axis=0)
+    else:
+        assert np.array_equal(bits32(host(outs[0]).ravel()), bits32(want[0]))
+
+
 def test_gelu_portable_bitwise(qfb, orc, cuda):
     import torch
     rng = np.random.default_rng(4)
