@@ -251,8 +251,10 @@ __device__ __forceinline__ ChunkRef locate_chunk(const EwBatch& bt, uint32_t chu
 // memory-bound at 0.95 of HBM on the general loop and the lean loop's
 // screens cost it 3-4 % (r02bc); GELU gains 0.73 -> 0.90 (f32), binary16
 // ReLU 0.69 -> 0.81 and GELU 0.42 -> 0.54.
-constexpr int kLeanPlain = 1, kLeanChain = 2, kLeanChainGelu = 4, kLeanChainHalf = 8;
-__constant__ int c_fwd_lean = kLeanPlain | kLeanChainGelu | kLeanChainHalf;
+// 16: int8 code emission.
+constexpr int kLeanPlain = 1, kLeanChain = 2, kLeanChainGelu = 4, kLeanChainHalf = 8, kLeanInt8 = 16;
+constexpr int kLeanAll = kLeanPlain | kLeanChain | kLeanChainGelu | kLeanChainHalf | kLeanInt8;
+__constant__ int c_fwd_lean = kLeanPlain | kLeanChainGelu | kLeanChainHalf | kLeanInt8;
 
 // ------------------------------------------------ lean plain forward ---
 // The plain multi-output forward's per-unit work for the common case (f32,
@@ -557,6 +559,53 @@ __global__ void __launch_bounds__(kEwThreads, (kChain ? 6 : 10) / kFwdStages)
             }
           }
           if (!done) nf |= chain_unit_general<T>(d, u, ch, ra, rb, streaming);
+        }
+        __syncthreads();  // stage s free for the producer
+        continue;
+      }
+    }
+    if constexpr (!kChain) {
+      if (lean_enabled(kLeanInt8) && (QFB_FLAGS & (kEwInt8Out | kEwHalfGrid)) == kEwInt8Out) {
+        // ---- lean int8 code emission, one output at a time: a unit whose
+        // values pass the screen (f32: |x| < s * 2^100; f16: no inf/NaN and
+        // s >= 2^-80) takes the magic-number codes, others code_unit's
+        // guarded per-element path (NaN -> 0) — the general loop's functions.
+        FastDivHost inner;
+        inner.d = pin_u(d.inner_u.d);
+        inner.m = pin_u(d.inner_u.m);
+        inner.s = pin_u(d.inner_u.s);
+        const uint32_t nch = pin_u(d.chans.d);
+        FastDivHost chans;
+        chans.d = nch;
+        chans.m = pin_u(d.chans.m);
+        chans.s = pin_u(d.chans.s);
+        const int nout = (int)pin_u((uint32_t)d.n_out);
+        for (int j = 0; j < nout; ++j) {
+          void* const y = d.y[j];
+          const float* const sp = d.s[j];
+          uint32_t row_end = 0, ch = 0;
+          float sj = 1.0f, rj = 1.0f, tj = 0.0f;
+          bool fj = false, okj = false;
+#pragma unroll 1
+          for (uint32_t k = tid; k < r.units; k += kEwThreads) {
+            const uint32_t u = r.u0 + k;
+            if (u >= row_end) {
+              const uint32_t row = nch == 1 ? 0u : fdiv(u, inner);
+              ch = nch == 1 ? 0u : row - fdiv(row, chans) * nch;
+              row_end = nch == 1 ? 0xffffffffu : (row + 1u) * inner.d;
+              sj = __ldg(sp + ch);
+              fj = fast_div_ok(sj);
+              rj = fj ? __frcp_rn(sj) : 1.0f;
+              tj = fj ? __fmul_rn(sj, 0x1p100f) : 0.0f;
+              okj = fj && (sizeof(T) == 4 || sj >= 0x1p-80f);
+            }
+            float v[V];
+            const bool special = Elem<T>::unpack_flag(src[k], v);
+            const bool fin = sizeof(T) == 2 ? (okj && !special) : screen_f32<V>(v, tj);
+            uint32_t c[V];
+            code_unit<V>(v, sj, rj, fj, qv, c, fin);
+            store_codes<V>(y, u, c);
+          }
         }
         __syncthreads();  // stage s free for the producer
         continue;
@@ -950,7 +999,7 @@ cudaError_t launch_ew_tma(int dtype, bool chain, int stages, const EwBatch& b, u
   static const cudaError_t lean_set = [] {
     const char* e = getenv("QFB_FWD_LEAN");
     if (!(e && e[0])) return cudaSuccess;
-    const int mask = (int)strtol(e, nullptr, 0) & (kLeanPlain | kLeanChain | kLeanChainGelu | kLeanChainHalf);
+    const int mask = (int)strtol(e, nullptr, 0) & kLeanAll;
     return cudaMemcpyToSymbol(c_fwd_lean, &mask, sizeof mask);
   }();
   if (lean_set != cudaSuccess) return lean_set;
