@@ -15,5 +15,5 @@ def t(fn, n=5):
 def distill():
     for k, (c, s, tt, d) in enumerate(qs.feat):
         hw = s.shape[2] * s.shape[3]
-        check(_lib.qfb_distill_batch(ctx.handle, _vp(s.data_ptr()), _vp(tt.data_ptr()), 64, c, hw, 1.0, 1/64, _vp(d.data_ptr()), _vp(qs.loss_k[k].data_ptr())))
+        check(_lib.qfb_distill_batch(ctx.handle, _vp(s.data_ptr()), _vp(tt.data_ptr()), 64, c, hw, 1.0, 1/64, _vp(d.data_ptr()), _vp(qs.loss_flat[k].data_ptr())))
 print(json.dumps({"fwd": t(lambda: qs.fp.forward(0)), "bwd": t(lambda: qs.fp.backward(0)), "distill": t(distill), "step": t(qs.run)}))
