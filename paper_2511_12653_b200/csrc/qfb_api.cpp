@@ -130,6 +130,11 @@ struct qfb_ctx {
   int bwd_impl = 0;
   // consumer layout of the full-tile kernel (QFB_BWD_IMPL=tile[q][m][d] at creation)
   uint32_t bwd_layout = kBwdLayoutDD;  // measured best (r02)
+  // tile order of the full-tile kernel (QFB_BWD_ORDER=rev|fwd at creation):
+  // last tile first by default — in a forward/backward step the backward
+  // then starts on the points whose inputs the forward read last (partly
+  // still in L2): f32 step 0.1326 -> 0.1311 ms (r02bg)
+  uint32_t bwd_order = kBwdLayoutReverse;
   bool bwd_half_fp32 = false;           // QFB_OPT_BWD_HALF_FP32
   cudaEvent_t main_pass_event = nullptr;  // QFB_OPT_MAIN_PASS_EVENT
   // QFB_OPT_BWD_ASYNC_FINISH: side stream for the finisher, fork/join events
@@ -550,6 +555,7 @@ qfb_status qfb_ctx_create(int32_t device, void* stream, qfb_ctx** out) {
         c->bwd_layout = l;
       }
     }
+    if (const char* env = getenv("QFB_BWD_ORDER")) c->bwd_order = std::strcmp(env, "fwd") == 0 ? 0u : kBwdLayoutReverse;
     if (const char* env = getenv("QFB_DISABLE_TMA_FWD"))
       if (env[0] == '1') std::memset(c->tma_blocks_per_sm, 0, sizeof c->tma_blocks_per_sm);
     if (const char* env = getenv("QFB_FWD_STAGES")) {
@@ -1103,7 +1109,7 @@ qfb_status qfb_fq_bwd_multi(qfb_ctx* ctx, qfb_dtype dtype, const qfb_bwd_desc* t
     b.n = cnt;
     b.tile_begin[cnt] = (uint32_t)tb;
     b.warp_part = warp_part ? 1u : 0u;
-    b.layout = ctx->bwd_layout | ((dtype == QFB_F16 && ctx->bwd_half_fp32) ? kBwdLayoutHalfF32 : 0u);
+    b.layout = ctx->bwd_layout | ctx->bwd_order | ((dtype == QFB_F16 && ctx->bwd_half_fp32) ? kBwdLayoutHalfF32 : 0u);
     if (stream) {
       const int grid = ctx->sm_count * ctx->sb_blocks_per_sm[dtype];
       cudaError_t e = launch_sbwd(dtype, sb_stages(dtype), b, grid, ctx->stream);

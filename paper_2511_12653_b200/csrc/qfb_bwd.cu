@@ -839,8 +839,9 @@ __global__ void __launch_bounds__(cta_threads<V>(), (V & kTwoCtas) ? 2 : 3) bwd_
       const uint32_t b = k >> 5;
       if (b != batch) {
         batch = b;
-        const uint32_t id = blockIdx.x + ((b << 5) + (uint32_t)lane) * gridDim.x;
-        if (id < total) {
+        const uint32_t id0 = blockIdx.x + ((b << 5) + (uint32_t)lane) * gridDim.x;
+        if (id0 < total) {
+          const uint32_t id = (bt.layout & kBwdLayoutReverse) ? total - 1u - id0 : id0;
           mine = locate_full<T>(bt, id);
           if constexpr ((V & kHalfF32) != 0) {
             // the fp32-term path's exact clip threshold, once per tile
@@ -1677,6 +1678,7 @@ BwdFn bwd_inst() {
 // kQuad | kMagicRint set: on the quad kernel).
 template <typename T>
 BwdFn kernel_ptr(int v, bool warp_part, uint32_t layout) {
+  layout &= ~kBwdLayoutReverse;  // a runtime bit, not an instance
   constexpr int kQM = kWarpPart | kQuad | kMagicRint;
   switch (v) {
     case kProbeNoCompute: return bwd_inst<T, kProbeNoCompute>();

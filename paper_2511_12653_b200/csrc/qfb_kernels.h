@@ -211,6 +211,10 @@ constexpr uint32_t kBwdLayoutTwoCtas = 8;  // 2 CTAs per SM (up to 112 registers
 constexpr uint32_t kBwdLayoutHalfF32 = 16; // binary16 storage: float32 terms (QFB_OPT_BWD_HALF_FP32)
 constexpr uint32_t kBwdLayoutPrefetch = 32; // producer L2 prefetch one tile beyond the ring
 constexpr uint32_t kBwdLayoutCU = 64;       // CTA-uniform main pass (bwd_cu_kernel)
+// tiles visited last to first (runtime bit of the warp-specialized kernel,
+// not a kernel instance): the step's backward starts on the quant points
+// the forward touched last, whose inputs may still sit in L2
+constexpr uint32_t kBwdLayoutReverse = 128;
 
 cudaError_t bwd_occupancy(int dtype, int* blocks_per_sm);  // at the default ring size
 cudaError_t bwd_occupancy_smem(int dtype, size_t smem, int* blocks_per_sm, bool warp_part = false,

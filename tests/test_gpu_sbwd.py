@@ -120,6 +120,18 @@ def test_variants_agree_on_dpvo_table(qfb, cuda, dtype, monkeypatch):
         out.append(([t.cpu() for t in fp.dx], fp.scale_grads().cpu()))
         ctx.close()
         monkeypatch.delenv("QFB_BWD_IMPL", raising=False)
+    # the default kernel with its tiles visited first to last (QFB_BWD_ORDER=fwd;
+    # the default visits them last to first)
+    monkeypatch.setenv("QFB_BWD_ORDER", "fwd")
+    stream = torch.cuda.Stream(device=cuda)
+    ctx = qfb.Context(0, stream.cuda_stream)
+    fp = FrontendQuantPass(ctx, frames=2, dtype="f32" if dtype == 0 else "f16", sets=1, seed=3, device=cuda,
+                           h=240, w=320)
+    fp.backward(0)
+    ctx.sync()
+    out.append(([t.cpu() for t in fp.dx], fp.scale_grads().cpu()))
+    ctx.close()
+    monkeypatch.delenv("QFB_BWD_ORDER", raising=False)
     (dxa, ga) = out[0]
     for (dxb, gb) in out[1:]:
         assert torch.equal(ga.view(torch.int64), gb.view(torch.int64))
