@@ -172,6 +172,10 @@ __device__ __forceinline__ void window(const BwdDesc& d, const TileRef& r, uint6
 }
 
 // Thread 0: arm the stage's mbarrier and launch the two bulk copies.
+// L2 hints (QFB_L2_HINTS mask, A/B): 2 = x loads evict_last, 4 = upstream
+// loads evict_first, 8 = d_input stores evict_first
+__constant__ int c_bwd_l2_hints = 0;
+
 template <typename T>
 __device__ __forceinline__ void issue_tile(const BwdDesc& d, const TileRef& r, Stage<T>& st,
                                            uint64_t* bar) {
@@ -179,8 +183,11 @@ __device__ __forceinline__ void issue_tile(const BwdDesc& d, const TileRef& r, S
   fence_proxy_async_smem();
   mbar_arrive_expect_tx(bar, 2 * bytes);
   if (bytes) {
-    bulk_g2s(st.x, static_cast<const char*>(d.x) + r.w0, bytes, bar);
-    bulk_g2s(st.up, static_cast<const char*>(d.up) + r.w0, bytes, bar);
+    const int h = c_bwd_l2_hints;
+    if (h & 2) bulk_g2s_hint(st.x, static_cast<const char*>(d.x) + r.w0, bytes, bar, l2_evict_last());
+    else bulk_g2s(st.x, static_cast<const char*>(d.x) + r.w0, bytes, bar);
+    if (h & 4) bulk_g2s_hint(st.up, static_cast<const char*>(d.up) + r.w0, bytes, bar, l2_evict_first());
+    else bulk_g2s(st.up, static_cast<const char*>(d.up) + r.w0, bytes, bar);
   }
 }
 
@@ -785,8 +792,12 @@ __device__ __forceinline__ void store_dx(const BwdDesc& d, const TileRef& cur, S
   for (int e = tail0 + lane; e < cur.m; e += 32) static_cast<T*>(d.dx)[cur.A + e] = st.x[cur.off + e];
   if (lane == 0 && i1 > i0) {
     fence_proxy_async_smem();
-    bulk_s2g(static_cast<char*>(d.dx) + i0, reinterpret_cast<const char*>(st.x) + (i0 - cur.w0),
-             (uint32_t)(i1 - i0));
+    if (c_bwd_l2_hints & 8)
+      bulk_s2g_hint(static_cast<char*>(d.dx) + i0, reinterpret_cast<const char*>(st.x) + (i0 - cur.w0),
+                    (uint32_t)(i1 - i0), l2_evict_first());
+    else
+      bulk_s2g(static_cast<char*>(d.dx) + i0, reinterpret_cast<const char*>(st.x) + (i0 - cur.w0),
+               (uint32_t)(i1 - i0));
     bulk_commit();
   }
 }
@@ -1756,6 +1767,13 @@ cudaError_t launch_bwd(int dtype, const BwdBatch& b, int grid, cudaStream_t st, 
   if ((uint32_t)grid > tiles) grid = (int)tiles;
   const size_t smem = (size_t)b.nstages * (2 * b.stage_elems * (dtype == 0 ? 4 : 2) + kRedBytes);
   void* args[] = {const_cast<BwdBatch*>(&b)};
+  static const cudaError_t hints_set = [] {
+    const char* e = getenv("QFB_L2_HINTS");
+    if (!(e && e[0])) return cudaSuccess;
+    const int mask = (int)strtol(e, nullptr, 0);
+    return cudaMemcpyToSymbol(c_bwd_l2_hints, &mask, sizeof mask);
+  }();
+  if (hints_set != cudaSuccess) return hints_set;
   const BwdFn f = bwd_fn(dtype, b.warp_part != 0, b.layout);
   cudaFuncSetAttribute(f.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
   cudaError_t e = launch_main(f.fn, dim3(grid), dim3(f.threads), args, smem, st, kPdlBwd);

@@ -376,6 +376,9 @@ __device__ __noinline__ bool chain_unit_general(const EwDesc& d, uint32_t u, uin
   return nf;
 }
 
+// L2 hints (QFB_L2_HINTS mask, A/B): 1 = forward input loads evict_last
+__constant__ int c_l2_hints = 0;
+
 __device__ __forceinline__ bool lean_enabled(int bit) { return (c_fwd_lean & bit) != 0; }
 
 // kChain: quant -> act -> quant chains (a [+ b] staged, K outputs, optional
@@ -406,7 +409,10 @@ __global__ void __launch_bounds__(kEwThreads, (kChain ? 6 : 10) / kFwdStages)
     fence_proxy_async_smem();
     mbar_arrive_expect_tx(&bars[s], r.units * 16u * (has_b ? 2u : 1u));
     uint4* st = ring + s * kArrays * kEwChunk;
-    bulk_g2s(st, static_cast<const uint4*>(d.a) + r.u0, r.units * 16u, &bars[s]);
+    if (c_l2_hints & 1)  // keep the forward's inputs in L2 for the backward that follows
+      bulk_g2s_hint(st, static_cast<const uint4*>(d.a) + r.u0, r.units * 16u, &bars[s], l2_evict_last());
+    else
+      bulk_g2s(st, static_cast<const uint4*>(d.a) + r.u0, r.units * 16u, &bars[s]);
     if (has_b) bulk_g2s(st + kEwChunk, static_cast<const uint4*>(d.b) + r.u0, r.units * 16u, &bars[s]);
   };
   if (tid == 0) {
@@ -1003,6 +1009,13 @@ cudaError_t launch_ew_tma(int dtype, bool chain, int stages, const EwBatch& b, u
     return cudaMemcpyToSymbol(c_fwd_lean, &mask, sizeof mask);
   }();
   if (lean_set != cudaSuccess) return lean_set;
+  static const cudaError_t hints_set = [] {
+    const char* e = getenv("QFB_L2_HINTS");
+    if (!(e && e[0])) return cudaSuccess;
+    const int mask = (int)strtol(e, nullptr, 0);
+    return cudaMemcpyToSymbol(c_l2_hints, &mask, sizeof mask);
+  }();
+  if (hints_set != cudaSuccess) return hints_set;
   void* args[] = {const_cast<EwBatch*>(&b), &status};
   return launch_main(tma_fn(dtype, chain, stages), dim3(grid), dim3(kEwThreads), args,
                      ew_tma_smem(chain, stages), st, small ? (kPdlFwd | kPdlFwdSmall) : kPdlFwd);
