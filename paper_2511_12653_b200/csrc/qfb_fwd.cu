@@ -376,6 +376,14 @@ __device__ __noinline__ bool chain_unit_general(const EwDesc& d, uint32_t u, uin
   return nf;
 }
 
+// The one-output-at-a-time lean loop for an f32 instance: measured on the
+// 2-stage ring (short launches: config-1 map 6.50 -> 5.94 us per call);
+// the 3-stage ring keeps its two-output loop (0.1342 vs 0.1349 ms step) and
+// the 4-stage ring the general loop (8-frame launches 20.3 k vs 18.5 k
+// frames/s with this loop), r02bn.
+template <int kFwdStages>
+__host__ __device__ constexpr bool one_output_f32() { return kFwdStages == 2; }
+
 // L2 hints (QFB_L2_HINTS mask, A/B): 1 = forward input loads evict_last
 __constant__ int c_l2_hints = 0;
 
@@ -617,42 +625,45 @@ __global__ void __launch_bounds__(kEwThreads, (kChain ? 6 : 10) / kFwdStages)
         continue;
       }
     }
-    if constexpr (!kChain && sizeof(T) == 2) {
+    if constexpr (!kChain && (sizeof(T) == 2 || one_output_f32<kFwdStages>())) {
       if (lean_enabled(kLeanPlain) && (QFB_FLAGS & (kEwInt8Out | kEwHalfGrid)) == 0) {
-        // ---- lean binary16 loop, one output at a time (the outputs of a
-        // two-consumer point re-read the staged unit: a single output's
-        // state keeps the loop inside the general loop's registers). A unit
-        // with inf/NaN, or a row whose scale is outside the shortcut's
-        // domain (s < 2^-80, q*s beyond the binary16 range), takes
-        // fwd_unit_general for that output.
+        // ---- lean loop, one output at a time (binary16, and f32 on the
+        // 2-stage ring; the outputs of a two-consumer point re-read the
+        // staged unit: a single output's state keeps the loop inside the
+        // general loop's registers). A unit outside the shortcut's domain
+        // (f32: the |x| < s * 2^100 screen; f16: inf/NaN, s < 2^-80, q*s
+        // beyond the binary16 range) takes the general code for that output.
+        const uint32_t lnch = pin_u(d.chans.d);
         FastDivHost inner;
-        inner.d = pin_inner.d;
-        inner.m = pin_inner.m;
-        inner.s = pin_inner.s;
+        inner.d = pin_u(d.inner_u.d);
+        inner.m = pin_u(d.inner_u.m);
+        inner.s = pin_u(d.inner_u.s);
         FastDivHost chans;
-        chans.d = pin_nch;
+        chans.d = lnch;
         chans.m = pin_u(d.chans.m);
         chans.s = pin_u(d.chans.s);
-        for (int j = 0; j < (int)pin_nout; ++j) {
+        const int lnout = (int)pin_u((uint32_t)d.n_out);
+        for (int j = 0; j < lnout; ++j) {
           uint4* const y = static_cast<uint4*>(d.y[j]);
           const float* const sp = d.s[j];
           uint32_t row_end = 0, ch = 0;
-          float sj = 1.0f, rj = 1.0f;
+          float sj = 1.0f, rj = 1.0f, tj = 0.0f;
           bool ok = false;
 #pragma unroll 1
           for (uint32_t k = tid; k < r.units; k += kEwThreads) {
             const uint32_t u = r.u0 + k;
             if (u >= row_end) {  // first unit of the chunk or a new row
-              const uint32_t row = pin_nch == 1 ? 0u : fdiv(u, inner);
-              ch = pin_nch == 1 ? 0u : row - fdiv(row, chans) * pin_nch;
-              row_end = pin_nch == 1 ? 0xffffffffu : (row + 1u) * inner.d;
+              const uint32_t row = lnch == 1 ? 0u : fdiv(u, inner);
+              ch = lnch == 1 ? 0u : row - fdiv(row, chans) * lnch;
+              row_end = lnch == 1 ? 0xffffffffu : (row + 1u) * inner.d;
               sj = __ldg(sp + ch);
-              ok = fast_div_ok(sj) && sj >= 0x1p-80f && sj * qv <= 65504.0f;
+              ok = fast_div_ok(sj) && (sizeof(T) == 4 || (sj >= 0x1p-80f && sj * qv <= 65504.0f));
               rj = ok ? __frcp_rn(sj) : 1.0f;
+              tj = ok ? __fmul_rn(sj, 0x1p100f) : 0.0f;
             }
             UnitVals<T> uv;
             const bool special = Elem<T>::unpack_flag(src[k], uv.v);
-            if (ok && !special) {
+            if (sizeof(T) == 2 ? (ok && !special) : screen_f32<V>(uv.v, tj)) {
               float o[V];
 #pragma unroll
               for (int i = 0; i < V; ++i) o[i] = fq_value_fast_finite(uv.v[i], sj, rj, qv);
