@@ -42,24 +42,23 @@
  * coefficients, Horner with FMAs); beyond |x| > 5, Phi is 1 or 0 exactly.
  * Within 2.1e-6 of the erf GELU. NaN passes through; +inf -> +inf,
  * -inf -> -0. FMAs, one multiply and one add: identical bits on both sides. */
+/* The Horner coefficients of h, highest degree first (shared by the scalar
+ * form below and the device's packed two-lane form). */
+#define QFB_P_GELU_C0 0.010865055f
+#define QFB_P_GELU_HORNER(STEP)                                                 \
+  STEP(-0.013859635f) STEP(-0.041010167f) STEP(0.07832172f) STEP(0.025033878f) \
+  STEP(-0.16348906f) STEP(0.13090801f) STEP(0.0655948f) STEP(-0.23270182f)     \
+  STEP(0.23961057f) STEP(-0.13688436f) STEP(0.043821268f) STEP(0.49378976f)
+
 /* x * Phi(x) from the polynomial, for -5 <= x <= 5 (qfb_p_gelu's middle
  * branch; the device's branch-free form selects around it). */
 QFB_HD float qfb_p_gelu_core(float x) {
   const float t = x < 0.0f ? -x : x;
   const float u = QFB_P_FMA(t, 0.4f, -1.0f);
-  float h = 0.010865055f;
-  h = QFB_P_FMA(h, u, -0.013859635f);
-  h = QFB_P_FMA(h, u, -0.041010167f);
-  h = QFB_P_FMA(h, u, 0.07832172f);
-  h = QFB_P_FMA(h, u, 0.025033878f);
-  h = QFB_P_FMA(h, u, -0.16348906f);
-  h = QFB_P_FMA(h, u, 0.13090801f);
-  h = QFB_P_FMA(h, u, 0.0655948f);
-  h = QFB_P_FMA(h, u, -0.23270182f);
-  h = QFB_P_FMA(h, u, 0.23961057f);
-  h = QFB_P_FMA(h, u, -0.13688436f);
-  h = QFB_P_FMA(h, u, 0.043821268f);
-  h = QFB_P_FMA(h, u, 0.49378976f);
+  float h = QFB_P_GELU_C0;
+#define QFB_P_GELU_STEP(c) h = QFB_P_FMA(h, u, c);
+  QFB_P_GELU_HORNER(QFB_P_GELU_STEP)
+#undef QFB_P_GELU_STEP
   const float phi = QFB_P_ADD(0.5f, x < 0.0f ? -h : h);
   return QFB_P_MUL(x, phi);
 }

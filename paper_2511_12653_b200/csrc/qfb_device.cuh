@@ -106,6 +106,50 @@ __device__ __forceinline__ float fq_value_fast_finite(float x, float s, float y,
   return __fmul_rn(s, rintf(z));
 }
 
+// Packed f32x2 arithmetic (sm_100 FMUL2 / FFMA2: two IEEE round-to-nearest
+// float operations per instruction, denormals kept — no .ftz).
+__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2_unpack(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t f2_mul(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
+// fq_value_fast_finite on two values at once, from their NEGATIONS nx = -x
+// (free in the binary16 unpack: a sign flip of the packed word): with
+// NY = (-y, -y) and S = (s, s), q0 = RN(nx * -y) = RN(x*y), r' = RN(s*q0 +
+// nx) = RN(s*q0 - x), z = RN(r' * -y + q0) = RN(q0 - r'*y) — operation for
+// operation the scalar function's values (x = +-0 included), then the
+// clamp and rint per lane and the product s * rint(z) packed again.
+__device__ __forceinline__ uint64_t fq2_fast_finite_neg(uint64_t nx, uint64_t S, uint64_t NY, float q) {
+  const uint64_t q0 = f2_mul(nx, NY);
+  const uint64_t r = f2_fma(S, q0, nx);
+  const uint64_t z = f2_fma(r, NY, q0);
+  float z0, z1;
+  f2_unpack(z, z0, z1);
+  z0 = rintf(fminf(fmaxf(z0, -q), q));
+  z1 = rintf(fminf(fmaxf(z1, -q), q));
+  return f2_mul(S, f2_pack(z0, z1));
+}
+
 // int8 code bits (low byte) of a screened finite x (|x| < s * 2^100, no
 // NaN): negated-residual quotient, clip, and round-to-nearest-even into the
 // low byte by adding 1.5 * 2^23 (|z| <= q). Equals fq_code

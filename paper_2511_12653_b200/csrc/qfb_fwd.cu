@@ -326,6 +326,25 @@ __device__ __forceinline__ float gelu_nonnan(float x) {
   return x > 5.0f ? x : (x < -5.0f ? -0.0f : g);
 }
 
+// gelu_nonnan on two lanes with packed f32x2 FMAs for the polynomial: each
+// lane runs qfb_p_gelu_core's operations in the same order (IEEE RN per
+// lane), the sign selects and the saturated ranges per lane.
+__device__ __forceinline__ void gelu2_nonnan(float& a, float& b) {
+  const uint64_t u = f2_fma(f2_pack(a < 0.0f ? -a : a, b < 0.0f ? -b : b), f2_pack(0.4f, 0.4f),
+                            f2_pack(-1.0f, -1.0f));
+  uint64_t h = f2_pack(QFB_P_GELU_C0, QFB_P_GELU_C0);
+#define QFB_GELU2_STEP(c) h = f2_fma(h, u, f2_pack(c, c));
+  QFB_P_GELU_HORNER(QFB_GELU2_STEP)
+#undef QFB_GELU2_STEP
+  float ha, hb;
+  f2_unpack(h, ha, hb);
+  const uint64_t phi = f2_add(f2_pack(0.5f, 0.5f), f2_pack(a < 0.0f ? -ha : ha, b < 0.0f ? -hb : hb));
+  float ga, gb;
+  f2_unpack(f2_mul(f2_pack(a, b), phi), ga, gb);
+  a = a > 5.0f ? a : (a < -5.0f ? -0.0f : ga);
+  b = b > 5.0f ? b : (b < -5.0f ? -0.0f : gb);
+}
+
 // One chain unit through the general code (x86 NaN propagation, guarded
 // quotient, checked binary16 pack): units of the lean chain loop with
 // inf/NaN inputs or values outside the screened domain.
@@ -388,6 +407,23 @@ __host__ __device__ constexpr bool one_output_f32() { return kFwdStages == 2; }
 // 16 = only those of the launch's last 4096 chunks (default: one f32 frame
 // step 0.1348-0.1351 -> 0.1338-0.1346 ms, forward 53.3 -> 52.7 us, r02bp)
 __constant__ int c_l2_hints = 16;
+
+// packed f32x2 FQ arithmetic in the binary16 lean loop (QFB_FQ2=0: scalar, A/B)
+__constant__ int c_fq2 = 1;
+
+// V screened values through fq_value_fast_finite, two per FMUL2 / FFMA2
+// from their negations (a sign flip each; see fq2_fast_finite_neg)
+template <int V>
+__device__ __forceinline__ void fq_unit_fast_finite(const float* v, float s, float y, float q, float* o) {
+  if (c_fq2) {
+    const uint64_t S = f2_pack(s, s), NY = f2_pack(-y, -y);
+#pragma unroll
+    for (int i = 0; i < V; i += 2) f2_unpack(fq2_fast_finite_neg(f2_pack(-v[i], -v[i + 1]), S, NY, q), o[i], o[i + 1]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < V; ++i) o[i] = fq_value_fast_finite(v[i], s, y, q);
+  }
+}
 
 __device__ __forceinline__ bool lean_enabled(int bit) { return (c_fwd_lean & bit) != 0; }
 
@@ -546,8 +582,13 @@ __global__ void __launch_bounds__(kEwThreads, (kChain ? 6 : 10) / kFwdStages)
 #pragma unroll
               for (int i = 0; i < V; ++i) v[i] = v[i] > 0.0f ? v[i] : 0.0f;
             } else if (act == 2) {
+              if (c_fq2) {
 #pragma unroll
-              for (int i = 0; i < V; ++i) v[i] = gelu_nonnan(v[i]);
+                for (int i = 0; i < V; i += 2) gelu2_nonnan(v[i], v[i + 1]);
+              } else {
+#pragma unroll
+                for (int i = 0; i < V; ++i) v[i] = gelu_nonnan(v[i]);
+              }
             }
             if (sizeof(T) == 2 && demote) {
               // finite values: round_to_half is the clamped RNE conversion
@@ -566,12 +607,10 @@ __global__ void __launch_bounds__(kEwThreads, (kChain ? 6 : 10) / kFwdStages)
                                             : (ok0 && ok1 && screen_f32<V>(v, t0) && screen_f32<V>(v, t1));
             if (fin) {
               float o[V];
-#pragma unroll
-              for (int i = 0; i < V; ++i) o[i] = fq_value_fast_finite(v[i], s0, r0, qv);
+              fq_unit_fast_finite<V>(v, s0, r0, qv, o);
               st_v4(y0 + u, Elem<T>::pack_in_range(o), streaming);
               if (nout > 1) {
-#pragma unroll
-                for (int i = 0; i < V; ++i) o[i] = fq_value_fast_finite(v[i], s1, r1, qv);
+                fq_unit_fast_finite<V>(v, s1, r1, qv, o);
                 st_v4(y1 + u, Elem<T>::pack_in_range(o), streaming);
               }
               done = true;
@@ -667,11 +706,27 @@ __global__ void __launch_bounds__(kEwThreads, (kChain ? 6 : 10) / kFwdStages)
               tj = ok ? __fmul_rn(sj, 0x1p100f) : 0.0f;
             }
             UnitVals<T> uv;
-            const bool special = Elem<T>::unpack_flag(src[k], uv.v);
-            if (sizeof(T) == 2 ? (ok && !special) : screen_f32<V>(uv.v, tj)) {
-              float o[V];
+            const uint4 raw = src[k];
+            const bool special = Elem<T>::unpack_flag(raw, uv.v);
+            if (sizeof(T) == 2 && c_fq2 && ok && !special) {
+              // packed f32x2 quotient from the negated halves (sign flip of
+              // the staged words), two elements per FMUL2 / FFMA2
+              const uint64_t S = f2_pack(sj, sj), NY = f2_pack(-rj, -rj);
+              const uint32_t w[4] = {raw.x ^ 0x80008000u, raw.y ^ 0x80008000u, raw.z ^ 0x80008000u,
+                                     raw.w ^ 0x80008000u};
+              uint32_t ow[4];
 #pragma unroll
-              for (int i = 0; i < V; ++i) o[i] = fq_value_fast_finite(uv.v[i], sj, rj, qv);
+              for (int i = 0; i < 4; ++i) {
+                const float2 nx = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
+                float o0, o1;
+                f2_unpack(fq2_fast_finite_neg(f2_pack(nx.x, nx.y), S, NY, qv), o0, o1);
+                const __half2 h = __floats2half2_rn(o0, o1);
+                ow[i] = *reinterpret_cast<const uint32_t*>(&h);
+              }
+              st_v4(y + u, make_uint4(ow[0], ow[1], ow[2], ow[3]), streaming);
+            } else if (sizeof(T) == 2 ? (ok && !special) : screen_f32<V>(uv.v, tj)) {
+              float o[V];
+              fq_unit_fast_finite<V>(uv.v, sj, rj, qv, o);
               st_v4(y + u, Elem<T>::pack_in_range(o), streaming);
             } else {
               nf |= fwd_unit_general_body<T>(d, u, ch, uv, special, streaming, j, j + 1);
@@ -730,12 +785,10 @@ __global__ void __launch_bounds__(kEwThreads, (kChain ? 6 : 10) / kFwdStages)
                                           : (ok0 && ok1 && screen_f32<V>(uv.v, t0) && screen_f32<V>(uv.v, t1));
           if (fin) {
             float o[V];
-#pragma unroll
-            for (int i = 0; i < V; ++i) o[i] = fq_value_fast_finite(uv.v[i], s0, r0, qv);
+            fq_unit_fast_finite<V>(uv.v, s0, r0, qv, o);
             st_v4(y0 + u, Elem<T>::pack_in_range(o), streaming);
             if (nout > 1) {
-#pragma unroll
-              for (int i = 0; i < V; ++i) o[i] = fq_value_fast_finite(uv.v[i], s1, r1, qv);
+              fq_unit_fast_finite<V>(uv.v, s1, r1, qv, o);
               st_v4(y1 + u, Elem<T>::pack_in_range(o), streaming);
             }
           } else {
@@ -1032,6 +1085,13 @@ cudaError_t launch_ew_tma(int dtype, bool chain, int stages, const EwBatch& b, u
     return cudaMemcpyToSymbol(c_l2_hints, &mask, sizeof mask);
   }();
   if (hints_set != cudaSuccess) return hints_set;
+  static const cudaError_t fq2_set = [] {
+    const char* e = getenv("QFB_FQ2");
+    if (!(e && e[0] == '0')) return cudaSuccess;
+    const int off = 0;
+    return cudaMemcpyToSymbol(c_fq2, &off, sizeof off);
+  }();
+  if (fq2_set != cudaSuccess) return fq2_set;
   void* args[] = {const_cast<EwBatch*>(&b), &status};
   return launch_main(tma_fn(dtype, chain, stages), dim3(grid), dim3(kEwThreads), args,
                      ew_tma_smem(chain, stages), st, small ? (kPdlFwd | kPdlFwdSmall) : kPdlFwd);
