@@ -150,6 +150,23 @@ __device__ __forceinline__ uint64_t fq2_fast_finite_neg(uint64_t nx, uint64_t S,
   return f2_mul(S, f2_pack(z0, z1));
 }
 
+// fq_code_bits_fast_finite on two values from their negations (the
+// quotient as in fq2_fast_finite_neg, clamp per lane, the magic-number
+// round into the low byte as one packed add).
+__device__ __forceinline__ void code2_fast_finite_neg(uint64_t nx, uint64_t S, uint64_t NY, float q, uint32_t& c0,
+                                                      uint32_t& c1) {
+  const uint64_t q0 = f2_mul(nx, NY);
+  const uint64_t r = f2_fma(S, q0, nx);
+  float z0, z1;
+  f2_unpack(f2_fma(r, NY, q0), z0, z1);
+  z0 = fminf(fmaxf(z0, -q), q);
+  z1 = fminf(fmaxf(z1, -q), q);
+  float b0, b1;
+  f2_unpack(f2_add(f2_pack(z0, z1), f2_pack(12582912.0f, 12582912.0f)), b0, b1);
+  c0 = __float_as_uint(b0);
+  c1 = __float_as_uint(b1);
+}
+
 // int8 code bits (low byte) of a screened finite x (|x| < s * 2^100, no
 // NaN): negated-residual quotient, clip, and round-to-nearest-even into the
 // low byte by adding 1.5 * 2^23 (|z| <= q). Equals fq_code

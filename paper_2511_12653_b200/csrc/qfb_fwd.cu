@@ -661,7 +661,13 @@ __global__ void __launch_bounds__(kEwThreads, (kChain ? 6 : 10) / kFwdStages)
             const bool special = Elem<T>::unpack_flag(src[k], v);
             const bool fin = sizeof(T) == 2 ? (okj && !special) : screen_f32<V>(v, tj);
             uint32_t c[V];
-            code_unit<V>(v, sj, rj, fj, qv, c, fin);
+            if (fin && c_fq2) {
+              const uint64_t S = f2_pack(sj, sj), NY = f2_pack(-rj, -rj);
+#pragma unroll
+              for (int i = 0; i < V; i += 2) code2_fast_finite_neg(f2_pack(-v[i], -v[i + 1]), S, NY, qv, c[i], c[i + 1]);
+            } else {
+              code_unit<V>(v, sj, rj, fj, qv, c, fin);
+            }
             store_codes<V>(y, u, c);
           }
         }
