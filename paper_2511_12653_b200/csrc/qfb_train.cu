@@ -119,7 +119,21 @@ __global__ void __launch_bounds__(kMseWarps * 32) mse_leaf_kernel(const float* _
   const uint32_t groups = 1u << depth;
   const uint32_t g = (blockIdx.x * kMseWarps + warp) * 32u + (uint32_t)lane;
   uint64_t lo = 0, m = 0;
-  if (g < groups) node_of(n, g, depth, lo, m);
+  if (g < groups) {
+    if (n < (1ull << 32)) {  // the descent in 32-bit arithmetic (same values)
+      uint32_t lo32 = 0, m32 = (uint32_t)n;
+      for (int l = (int)depth - 1; l >= 0; --l) {
+        const uint32_t h = m32 >> 1;
+        const bool right = (g >> l) & 1u;
+        lo32 += right ? h : 0u;
+        m32 = right ? m32 - h : h;
+      }
+      lo = lo32;
+      m = m32;
+    } else {
+      node_of(n, g, depth, lo, m);
+    }
+  }
   // the warp's element range [w0, w1)
   const uint64_t w0 = __shfl_sync(0xffffffffu, lo, 0);
   const uint32_t last = min(31u, groups > (g - lane) ? groups - (g - lane) - 1u : 0u);
@@ -130,10 +144,26 @@ __global__ void __launch_bounds__(kMseWarps * 32) mse_leaf_kernel(const float* _
   if ((((uintptr_t)s | (uintptr_t)t) & 15u) == 0) {
     a0 = e0 & ~uint64_t(3);
     const uint64_t v1 = e1 & ~uint64_t(3);  // [a0, v1) by float4, [v1, e1) scalar
-    const int nv = (int)((v1 - a0) >> 2);
-    for (int i = lane; i < nv; i += 32) {
-      reinterpret_cast<float4*>(ss[warp][0])[i] = __ldg(reinterpret_cast<const float4*>(s + a0) + i);
-      reinterpret_cast<float4*>(ss[warp][1])[i] = __ldg(reinterpret_cast<const float4*>(t + a0) + i);
+    const int nv = (int)((v1 - a0) >> 2);  // <= (32 * kLeaf + 3) / 4 + 1 = 129
+    // every load of the warp's range issued before any is stored (the
+    // range is at most 5 float4 per lane and array)
+    constexpr int kPer = (32 * kLeaf / 4 + 2 + 31) / 32;
+    float4 va[kPer], vb[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int i = lane + 32 * j;
+      if (i < nv) {
+        va[j] = __ldg(reinterpret_cast<const float4*>(s + a0) + i);
+        vb[j] = __ldg(reinterpret_cast<const float4*>(t + a0) + i);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int i = lane + 32 * j;
+      if (i < nv) {
+        reinterpret_cast<float4*>(ss[warp][0])[i] = va[j];
+        reinterpret_cast<float4*>(ss[warp][1])[i] = vb[j];
+      }
     }
     const int tail = (int)(e1 - v1);
     if (lane < tail) {
