@@ -403,6 +403,40 @@ def test_chain_f16_extremes(qfb, orc, cuda, act):
     assert np.array_equal(bits32(host(y).ravel()), bits32(want))
 
 
+@pytest.mark.parametrize("frames", [1, 800])
+def test_f32_lean_packed_paths_edge_values(qfb, orc, cuda, frames):
+    """The f32 lean loops with packed f32x2 arithmetic (2-stage ring for a
+    short launch, 3-stage for a longer one): per-channel rows of ties
+    (k + 1/2) * s and their float neighbours, subnormal and tiny x (q0 and
+    the residual subnormal), +-0, values at the clip boundary and beyond the
+    |x| < s * 2^100 screen, inf/NaN, over scales from 1e-6 to 64 — bitwise
+    against the oracle."""
+    import torch
+    rng = np.random.default_rng(91)
+    sp = np.array([1e-6, 1e-4, 0.0315, 0.5, 1.0, 3.0, 64.0, 2.0 ** -100, 2.0 ** 100], dtype=np.float32)
+    C = sp.size
+    rows = []
+    for sv in sp:
+        v = []
+        for k in list(range(-130, 130)):
+            t = np.float32(k + 0.5) * sv
+            v += [t, np.nextafter(t, np.float32(np.inf)), np.nextafter(t, np.float32(-np.inf))]
+        v += [0.0, -0.0, 1e-45, -1e-45, 1.1754944e-38, -1.1754944e-38, 3e-39, -3e-39, 1e-30, -1e-30,
+              np.float32(127) * sv, -np.float32(127) * sv, np.float32(1e30), -np.float32(1e30),
+              3.4028235e38, -3.4028235e38, np.inf, -np.inf, np.nan]
+        v += list(rng.normal(0, 50, 64) * sv)
+        rows.append(np.array(v, dtype=np.float32))
+    inner = max(r.size for r in rows)
+    inner = (inner + 3) // 4 * 4
+    x = np.zeros((C, inner), dtype=np.float32)
+    for c, r in enumerate(rows):
+        x[c, :r.size] = r
+    x = np.tile(x[None], (frames, 1, 1))
+    y = qfb.fake_quantize(torch.from_numpy(x).to(cuda), sp.astype(np.float64).tolist(), channel_axis=1)
+    _, want = orc.fake_quantize(x.ravel(), sp.astype(np.float64), frames, C, inner)
+    assert np.array_equal(bits32(host(y).ravel()), bits32(want))
+
+
 def test_half_fast_path_all_values(qfb, orc, cuda):
     """Every finite binary16 value through the f16 TMA forward (screened
     fast path: negated-residual quotient without copysign) on 64 per-channel
