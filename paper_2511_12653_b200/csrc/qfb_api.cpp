@@ -83,6 +83,7 @@ struct qfb_ctx {
   int bwd_blocks_per_sm[2] = {4, 4};
   int tma_blocks_per_sm[2][2][kTmaStagesMax + 1] = {};  // [dtype][chain][stages]; 0: unavailable
   int tma_stages_env = 0;  // QFB_FWD_STAGES: fixed ring depth (tuning sweeps)
+  uint32_t fwd_chunk_units = 0;  // QFB_FWD_CHUNK: TMA chunk size in 16-byte units (0: kEwChunk)
   std::vector<std::pair<size_t, int>> bwd_occ[2];  // (smem, blocks/SM) cache
   uint32_t* d_status = nullptr;
   uint32_t* h_status = nullptr;  // pinned
@@ -366,6 +367,7 @@ qfb_status run_ew(qfb_ctx* ctx, int dtype, const std::vector<EwDesc>& descs, boo
     }
     b.n = n;
     b.chunk_begin[n] = chunks;
+    b.chunk_units = (uint32_t)kEwChunk;
     if (chunks == 0) continue;
     bool int8_out = false;
     for (int k = 0; k < n; ++k) int8_out = int8_out || (b.d[k].flags & kEwInt8Out) != 0;
@@ -374,6 +376,17 @@ qfb_status run_ew(qfb_ctx* ctx, int dtype, const std::vector<EwDesc>& descs, boo
     bool all_vec = tma_per_sm > 0;
     for (int k = 0; k < n && all_vec; ++k) all_vec = b.d[k].vec > 1;
     cudaError_t e;
+    if (all_vec && ctx->fwd_chunk_units > 0 && ctx->fwd_chunk_units < (uint32_t)kEwChunk) {
+      // smaller TMA chunks (QFB_FWD_CHUNK): the table in those units
+      const uint32_t cu = ctx->fwd_chunk_units;
+      b.chunk_units = cu;
+      chunks = 0;
+      for (int k = 0; k < n; ++k) {
+        b.chunk_begin[k] = chunks;
+        chunks += (b.d[k].nunits + cu - 1) / cu;
+      }
+      b.chunk_begin[n] = chunks;
+    }
     if (all_vec) {
       const int grid = (int)std::min<uint64_t>(chunks, (uint64_t)ctx->sm_count * tma_per_sm);
       e = launch_ew_tma(dtype, chain, stages, b, ctx->cur_status, grid, ctx->stream,
@@ -558,6 +571,10 @@ qfb_status qfb_ctx_create(int32_t device, void* stream, qfb_ctx** out) {
     if (const char* env = getenv("QFB_BWD_ORDER")) c->bwd_order = std::strcmp(env, "fwd") == 0 ? 0u : kBwdLayoutReverse;
     if (const char* env = getenv("QFB_DISABLE_TMA_FWD"))
       if (env[0] == '1') std::memset(c->tma_blocks_per_sm, 0, sizeof c->tma_blocks_per_sm);
+    if (const char* env = getenv("QFB_FWD_CHUNK")) {
+      const int v = atoi(env);
+      if (v >= 256 && v <= kEwChunk) c->fwd_chunk_units = (uint32_t)v;
+    }
     if (const char* env = getenv("QFB_FWD_STAGES")) {
       const int v = atoi(env);
       if (v >= kTmaStagesMin && v <= kTmaStagesMax) c->tma_stages_env = v;

@@ -239,9 +239,10 @@ __device__ __forceinline__ ChunkRef locate_chunk(const EwBatch& bt, uint32_t chu
   }
   ChunkRef r;
   r.di = lo;
-  r.u0 = (chunk - bt.chunk_begin[lo]) * kEwChunk;
+  const uint32_t cu = bt.chunk_units;
+  r.u0 = (chunk - bt.chunk_begin[lo]) * cu;
   const uint32_t left = bt.d[lo].nunits - r.u0;
-  r.units = left < (uint32_t)kEwChunk ? left : (uint32_t)kEwChunk;
+  r.units = left < cu ? left : cu;
   return r;
 }
 

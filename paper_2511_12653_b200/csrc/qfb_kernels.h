@@ -88,7 +88,7 @@ struct EwDesc {
 
 struct EwBatch {
   int32_t n;
-  int32_t pad;
+  uint32_t chunk_units;  // TMA path: units per chunk (<= kEwChunk); the register path uses kEwChunk
   uint32_t chunk_begin[kMaxEwDesc + 1];
   EwDesc d[kMaxEwDesc];
 };
