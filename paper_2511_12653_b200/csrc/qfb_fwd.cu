@@ -426,6 +426,14 @@ __device__ __forceinline__ void fq_unit_fast_finite(const float* v, float s, flo
   }
 }
 
+// The 4-stage ring's general loop takes the screened fast path too, with
+// the packed f32x2 quotient: slower in short bursts (8-frame launches
+// 20.2 k -> 18.9 k frames/s over 40 launches) but faster in the sustained,
+// power-capped run config 5 specifies (32 x 1000 frames: 18.8 k -> 19.8 k),
+// where fewer instructions per byte leave more of the power budget to the
+// memory system (r02cj, r02ck).
+constexpr bool kScreen4 = true;
+
 __device__ __forceinline__ bool lean_enabled(int bit) { return (c_fwd_lean & bit) != 0; }
 
 // kChain: quant -> act -> quant chains (a [+ b] staged, K outputs, optional
@@ -889,15 +897,17 @@ __global__ void __launch_bounds__(kEwThreads, (kChain ? 6 : 10) / kFwdStages)
       for (int j = 0; j < 2; ++j) {
         if (j >= QFB_NOUT) break;
         float o[V];
-        // (the 4-stage f32 ring, used for long memory-bound launches, keeps
-        // the guarded path: its extra registers cost it 1.5 %)
         const bool finite = sizeof(T) == 2 ? (!special && fast[j] && sc[j] >= 0x1p-80f)
-                                           : (kFwdStages < 4 && screen_f32<V>(v, thr[j]));
+                                           : ((kFwdStages < 4 || kScreen4) && screen_f32<V>(v, thr[j]));
         if (finite) {
           // binary16 unit without inf/NaN (|x / s| < 2^96) or an f32 unit
           // passing the screen: no guards needed
+          if constexpr (kScreen4 && kFwdStages == 4) {
+            fq_unit_fast_finite<V>(v, sc[j], rc[j], qv, o);
+          } else {
 #pragma unroll
-          for (int i = 0; i < V; ++i) o[i] = fq_value_fast_finite(v[i], sc[j], rc[j], qv);
+            for (int i = 0; i < V; ++i) o[i] = fq_value_fast_finite(v[i], sc[j], rc[j], qv);
+          }
         } else if (fast[j]) {
 #pragma unroll
           for (int i = 0; i < V; ++i) o[i] = fq_value_fast(v[i], sc[j], rc[j], qv);
